@@ -1,0 +1,171 @@
+/*
+ * hgks.h -- C-ABI of the B200-native HGKS hot path (libhgks.so).
+ *
+ * The library advances the high-order gas-kinetic scheme of Wang, Cao & Pan,
+ * arXiv 2407.00656 (PAPER.md, cited "P:n"), on tetrahedral and hexahedral
+ * unstructured meshes, on one CUDA device per process:
+ *   - third-order WENO reconstruction per cell      (Eqs. polys/weno)
+ *   - BGK gas-kinetic flux per face Gauss point      (Eqs. flux-G/flux)
+ *   - two-stage fourth-order update + CFL minimum    (Alg. 2)
+ *   - halo exchange of 3 ghost layers + min(dt), NCCL
+ * Readings of points where the paper is silent are DESIGN.md R1-R26.
+ *
+ * Conventions for every call:
+ *   - Return value: HGKS_OK (0) or an error code below; nothing throws or
+ *     aborts across this ABI.  hgks_last_error() returns a thread-local,
+ *     NUL-terminated message naming the offending cell/face when relevant.
+ *   - Host pointers are plain caller-owned arrays; the library deep-copies
+ *     what it keeps.  Device memory is owned by the CALLER: it allocates a
+ *     workspace of hgks_workspace_size() bytes (e.g. a torch uint8 CUDA
+ *     tensor) and passes its pointer to hgks_init; the library carves all its
+ *     device arrays from it and never calls cudaMalloc on the hot path.
+ *   - `stream` is a cudaStream_t of the current device (NULL = legacy
+ *     default stream).  All kernels run on it; calls return once the work is
+ *     enqueued unless they must read a device value (documented per call).
+ *   - Conserved variables are Q = (rho, rhoU, rhoV, rhoW, rhoE),
+ *     host layout [n][5] row-major (AoS), fp64.
+ */
+#ifndef HGKS_H_
+#define HGKS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t hgks_status;
+#define HGKS_OK 0
+#define HGKS_E_ARG 1        /* invalid argument / call order */
+#define HGKS_E_MESH 2       /* degenerate cell, non-manifold face, unsupported element, unmatched face */
+#define HGKS_E_STENCIL 3    /* rank-deficient least-squares stencil */
+#define HGKS_E_CUDA 4       /* CUDA runtime error */
+#define HGKS_E_NCCL 5       /* NCCL error or NCCL unavailable for n_ranks > 1 */
+#define HGKS_E_POSITIVITY 6 /* non-positive density or pressure after an update */
+#define HGKS_E_STATE 7      /* dt <= 0 / non-finite state */
+
+#define HGKS_TET 4
+#define HGKS_HEX 8
+#define HGKS_BC_WALL 1      /* no-slip adiabatic wall (R25) */
+#define HGKS_BC_FARFIELD 2  /* Riemann-invariant inlet/outlet (R25) */
+
+typedef struct hgks_mesh hgks_mesh;
+typedef struct hgks_solver hgks_solver;
+
+/* Mesh description.  All arrays are read during hgks_mesh_create only. */
+typedef struct {
+  const double* xyz;          /* [n_nodes][3] node coordinates */
+  int64_t n_nodes;
+  const int8_t* cell_type;    /* [n_cells] HGKS_TET or HGKS_HEX */
+  const int64_t* cell_nodes;  /* [n_cells][8], -1 padded; tet: 4 nodes, face p opposite node p
+                                 (P:541-549); hex: VTK order, faces 0/5 = (0123)/(4567) (R17) */
+  int64_t n_cells;
+  double periodic_origin[3];  /* periodic box; length 0 along an axis = not periodic (R23) */
+  double periodic_length[3];
+  const int64_t* bface_nodes; /* [n_bfaces][4], -1 padded: physical boundary faces */
+  const int32_t* bface_tag;   /* [n_bfaces] HGKS_BC_WALL / HGKS_BC_FARFIELD */
+  int64_t n_bfaces;
+  int32_t n_ranks;            /* >= 1; > 1 builds the k-way partition + 3 ghost layers */
+  const int32_t* cell_part;   /* optional [n_cells] rank of every cell (external partition), or NULL */
+} hgks_mesh_desc;
+
+/* Solver configuration (readings R4, R6, R7, R13, R14, R24). */
+typedef struct {
+  double gamma;        /* specific-heat ratio (K = (5-3 gamma)/(gamma-1)) */
+  double cfl;          /* dt = cfl * min_i h_i / (|U_i| + c_i + 2 nu_i / h_i)  (R6) */
+  double fixed_dt;     /* > 0: use this dt every step instead of the CFL rule */
+  int32_t tau_mode;    /* 0: tau = 0 (smooth flows); 1: tau = mu/p + c1 |pl-pr|/(pl+pr) dt */
+  double c1;
+  double mu_inf, t_inf, mu_exp;  /* mu = mu_inf (T / t_inf)^mu_exp, T = p/rho */
+  double eps;          /* WENO epsilon */
+  int32_t omega_pow;   /* 1 (as printed) or 2 */
+  double freestream[5];/* rho, U, V, W, p for farfield faces */
+} hgks_config;
+
+/* Distributed context: one process per GPU. */
+typedef struct {
+  int32_t rank, n_ranks;
+  int32_t device;            /* CUDA ordinal used by this rank */
+  uint8_t nccl_id[128];      /* ncclUniqueId created by rank 0, broadcast by the caller */
+} hgks_dist;
+
+typedef struct {
+  int64_t n_cells_global;
+  int64_t n_owned;           /* cells updated by this rank */
+  int64_t n_ghost;           /* partition ghosts (3 layers) */
+  int64_t ghost_layer[3];
+  int64_t n_bghost;          /* boundary-condition ghosts (one per wall/farfield face) */
+  int64_t n_faces;           /* faces whose flux this rank computes */
+  int64_t n_faces_bc;        /* ... of which wall/farfield faces */
+  int32_t stencil_min, stencil_max;  /* big stencil sizes over owned cells (self excluded) */
+  int32_t n_sub;             /* sub-stencils per cell (4 tet, 8 hex) */
+  int32_t n_peers;           /* ranks this rank exchanges ghosts with */
+  int64_t send_cells, recv_cells;    /* per stage */
+  int64_t edge_cut;          /* faces between different ranks (global) */
+} hgks_mesh_stats;
+
+typedef struct {
+  int64_t steps_done;        /* steps with dt > 0 performed by this call */
+  double t;                  /* simulation time after the call */
+  double last_dt;
+  int64_t fallbacks;         /* cumulative positivity fallbacks at Gauss points (R21) */
+} hgks_step_info;
+
+/* Build geometry, faces, periodic pairing, stencils (Alg. 1), least-squares
+ * operators, locality (Morton) renumbering and, for n_ranks > 1, the
+ * partition with 3 ghost layers and per-peer send/receive plans.  Host only. */
+hgks_status hgks_mesh_create(const hgks_mesh_desc* desc, hgks_mesh** out);
+hgks_status hgks_mesh_destroy(hgks_mesh* mesh);
+hgks_status hgks_mesh_info(const hgks_mesh* mesh, int32_t rank, hgks_mesh_stats* out);
+
+/* Device bytes rank `rank` needs for `cfg`. */
+hgks_status hgks_workspace_size(const hgks_mesh* mesh, const hgks_config* cfg, int32_t rank, size_t* bytes);
+
+/* Upload the mesh data of this rank into the caller's workspace and set the
+ * initial state h_Q0 ([n_cells_global][5], caller's cell order; each rank
+ * takes its own cells).  dist may be NULL for a single process.  Synchronous
+ * with respect to `stream` (returns after the uploads completed). */
+hgks_status hgks_init(const hgks_mesh* mesh, const hgks_config* cfg, const hgks_dist* dist, void* d_workspace,
+                      size_t workspace_bytes, void* stream, const double* h_Q0, hgks_solver** out);
+hgks_status hgks_destroy(hgks_solver* solver);
+
+/* Advance up to n_steps S2O4 steps (Alg. 2).  If t_stop > 0 the last step is
+ * clipped to land exactly on t_stop and no step starts at t >= t_stop.  The
+ * time step is kept on the device (no host synchronisation) unless `info` is
+ * non-NULL, in which case the call synchronises and fills it; positivity
+ * failures are reported only then (HGKS_E_POSITIVITY, cell id in the message). */
+hgks_status hgks_step(hgks_solver* solver, int32_t n_steps, double t_stop, hgks_step_info* info);
+
+/* Replace the state (host [n_cells_global][5], caller order) and time.  Used
+ * for restart and for end-to-end timing.  Asynchronous on the stream (the host
+ * buffer must stay valid until the stream reaches this point; pinned memory
+ * recommended). */
+hgks_status hgks_set_state(hgks_solver* solver, const double* h_Q, double t);
+
+/* Copy this rank's owned cells into h_Q ([n_owned][5]) in the caller's input
+ * order (ascending global id); h_gid (optional, [n_owned]) receives the global
+ * ids; t (optional) the time.  Synchronises the stream. */
+hgks_status hgks_get_state(const hgks_solver* solver, double* h_Q, int64_t* h_gid, double* t);
+
+/* Parity intermediates (single rank): L(Q) and d_t L(Q)
+ * for state h_Q at step dt, [n_cells][5] caller order each.  Synchronous. */
+hgks_status hgks_debug_residual(hgks_solver* solver, const double* h_Q, double dt, double* h_L, double* h_dL);
+
+/* Per-kernel device time: when enabled, every kernel launch is bracketed by
+ * CUDA events on the solver stream.  hgks_kernel_times fills up to `cap`
+ * entries of (name, launches, total milliseconds) and returns the count in *n.
+ * Synchronises the stream. */
+hgks_status hgks_set_profiling(hgks_solver* solver, int32_t enabled);
+hgks_status hgks_kernel_times(hgks_solver* solver, int32_t cap, char (*names)[32], int64_t* launches,
+                              double* total_ms, int32_t* n);
+/* Number of kernels launched by this solver so far (all kinds). */
+hgks_status hgks_launch_count(const hgks_solver* solver, int64_t* launches);
+
+const char* hgks_last_error(void);
+const char* hgks_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HGKS_H_ */

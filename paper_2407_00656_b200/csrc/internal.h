@@ -1,0 +1,113 @@
+// Internal data model of libhgks (not part of the C-ABI).
+//
+// Host setup (setup.cpp) turns the caller's node/cell arrays into a
+// GlobalMesh (geometry, faces, stencils, least-squares operators) and one
+// RankPlan per rank (partition, 3 ghost layers, renumbered device arrays).
+// The device runtime (solver.cu) uploads a RankPlan into the caller's
+// workspace and runs the kernels (kernels.cuh).
+#pragma once
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace hgks {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+constexpr int kMaxStencil = 40;  // big-stencil capacity (tet 14-16, hex interior 24)
+
+// Sizes of the per-cell device records for one mesh kind.
+struct Layout {
+  int cell_type = 4;   // 4 tet, 8 hex (meshes are single-kind)
+  int nfaces = 4;      // faces per cell
+  int ngp = 3;         // Gauss points per face (R10)
+  int nv = 3;          // vertices per face
+  int K = 14;          // padded big-stencil width
+  int M = 4;           // sub-stencils per cell
+  int NM = 6;          // padded members per sub-stencil
+  int op_entries() const { return 9 * K + M * 3 * NM; }
+};
+
+struct GlobalMesh {
+  int64_t nc = 0;
+  std::vector<int8_t> type;
+  Layout lay;
+  double per_len[3] = {0, 0, 0};
+  // cell geometry: V, centroid, second central moments (xx,yy,zz,xy,xz,yz)
+  std::vector<double> V, C, M2, h_dt;
+  // faces (owner = lower input cell id, normal out of the owner, R19)
+  int64_t nf = 0;
+  std::vector<int64_t> f_owner, f_nb;   // f_nb = -1 for physical boundary faces
+  std::vector<int32_t> f_bc, f_ghost;
+  std::vector<double> f_shift;          // [nf][3] neighbour image = neighbour + shift
+  std::vector<double> f_vert;           // [nf][4][3] vertices, oriented out of the owner
+  std::vector<double> f_area;
+  std::vector<int64_t> cell_face;       // [nc][6]
+  // boundary-condition ghosts (one per wall/farfield face)
+  int64_t ng = 0;
+  std::vector<int64_t> g_cell, g_face;
+  std::vector<int32_t> g_bc;
+  std::vector<double> gV, gC, gM2, g_normal;
+  // stencils: ids >= nc are ghosts (nc + g)
+  std::vector<int64_t> nbr_id;          // [nc][6]
+  std::vector<double> nbr_shift;        // [nc][6][3]
+  std::vector<int64_t> big_off, big_id; // CSR
+  std::vector<double> big_shift;
+  std::vector<int8_t> sub_slot;         // [nc][M][NM] slot into big stencil, -1 pad
+  // least-squares operators per cell, [nc][op_entries]: A0+ (9 x K, row d,
+  // column k) then A_m+ (M x 3 x NM); physical units (R20)
+  std::vector<double> op;
+  // partition
+  int32_t n_ranks = 1;
+  std::vector<int32_t> part;
+  int64_t edge_cut = 0;
+};
+
+// One rank's device-ready arrays.  Local cell order:
+//   [ owned (Morton order) | partition ghosts grouped by owner rank |
+//     boundary ghosts ]
+struct RankPlan {
+  int rank = 0;
+  int64_t n_owned = 0, n_pghost = 0, n_bghost = 0;
+  int64_t ghost_layer[3] = {0, 0, 0};
+  int64_t n_local() const { return n_owned + n_pghost + n_bghost; }
+  std::vector<int64_t> l2g;             // [n_owned + n_pghost] global ids
+  // reconstruction set: owned cells then layer-1 ghosts
+  int64_t n_recon = 0;
+  std::vector<int32_t> recon_cell;      // [n_recon] local cell id
+  std::vector<int32_t> st_id;           // [K][n_recon] local ids (entry-major)
+  std::vector<uint8_t> sub_slot;        // [M*NM][n_recon]
+  std::vector<double> op;               // [op_entries][n_recon]
+  std::vector<double> geo;              // [8][n_recon]: V^{2/3}, V^{4/3}, M2 (xx,yy,zz,xy,xz,yz)
+  // faces: interior [0, n_if), wall [n_if, n_if + n_wf), farfield after
+  int64_t n_faces = 0, n_if = 0, n_wf = 0, n_ff = 0;
+  std::vector<int32_t> f_cells;         // [n_faces][2] local owner / neighbour (bc faces: ghost id)
+  std::vector<double> f_geo;            // [n_faces][FG]: nv vertices rel. owner centroid, then d (3)
+  int f_geo_stride = 12;
+  // update: owned cells
+  std::vector<int32_t> cf;              // [nfaces][n_owned] local face id, ~id when not the owner
+  std::vector<double> inv_v, h_dt;      // [n_owned]
+  // boundary ghosts
+  std::vector<int32_t> bg_cell, bg_bc;  // [n_bghost]
+  std::vector<double> bg_normal;        // [n_bghost][3]
+  // exchange plan (per peer)
+  std::vector<int32_t> peers;
+  std::vector<int64_t> send_off, send_cnt;  // into send_list
+  std::vector<int32_t> send_list;           // local owned ids, grouped by peer, global-id order
+  std::vector<int64_t> recv_off, recv_cnt;  // local ghost range [recv_off, recv_off + recv_cnt)
+  int32_t stencil_min = 0, stencil_max = 0;
+};
+
+struct MeshDescCopy;
+
+GlobalMesh build_global_mesh(const double* xyz, int64_t n_nodes, const int8_t* type, const int64_t* cell_nodes,
+                             int64_t n_cells, const double* per_origin, const double* per_len,
+                             const int64_t* bface_nodes, const int32_t* bface_tag, int64_t n_bf, int32_t n_ranks,
+                             const int32_t* cell_part);
+RankPlan build_rank_plan(const GlobalMesh& gm, int rank);
+
+}  // namespace hgks

@@ -1,0 +1,664 @@
+// sm_100a fp64 kernels of the HGKS hot path.
+//
+//   k_bc_ghosts   a6  boundary-condition ghost states (wall mirror / farfield)
+//   k_recon       a7  WENO reconstruction: LSQ apply, beta, weights, collapse
+//                     to ONE effective quadratic per cell (50 doubles)
+//   k_flux_tau0   a8+a9 per Gauss point: evaluate both polynomials, local
+//                     frame, Q0 by kinetic upwinding, F and d_t F of f = g0(1+A t)
+//                     via the Euler-chain identity, face quadrature sum
+//   k_update1/2   a10 L, d_t L assembly in local-face order + S2O4 stages;
+//                     stage 2 fuses the per-cell CFL bound and its min (a4)
+//
+// No tensor cores: there is no dense contraction on this path.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hgks {
+
+struct Ctrl {
+  double t;          // time at the start of the current step
+  double dt;         // step size of the current step
+  double t_next;     // time after the current step
+  unsigned long long dtmin_bits;  // min over cells of h/(|U|+c+2nu/h), as ordered bits
+  long long steps;   // steps with dt > 0
+  long long fallbacks;
+  int bad_cell;      // first cell with non-positive rho/p (INT_MAX if none)
+  int pad;
+};
+
+struct GasParams {
+  double gamma, K, cfl, fixed_dt, eps, omega_pow;
+  int tau_mode;
+  double c1, mu_inf, t_inf, mu_exp;
+  double fs[5];
+};
+
+// ----------------------------------------------------------------------------
+// a6: boundary ghost states (R25).  Wall: velocity reversed.  Farfield: 1-D
+// Riemann invariants along the face normal.
+// ----------------------------------------------------------------------------
+__device__ inline void farfield_riemann(const double qi[5], const double n[3], const GasParams& gp, double qb[5]) {
+  const double g = gp.gamma;
+  double rho_i = qi[0];
+  double ui[3] = {qi[1] / rho_i, qi[2] / rho_i, qi[3] / rho_i};
+  double p_i = (g - 1.0) * (qi[4] - 0.5 * (qi[1] * ui[0] + qi[2] * ui[1] + qi[3] * ui[2]));
+  double c_i = sqrt(g * p_i / rho_i);
+  double rho_f = gp.fs[0], p_f = gp.fs[4];
+  double uf[3] = {gp.fs[1], gp.fs[2], gp.fs[3]};
+  double c_f = sqrt(g * p_f / rho_f);
+  double un_i = ui[0] * n[0] + ui[1] * n[1] + ui[2] * n[2];
+  double un_f = uf[0] * n[0] + uf[1] * n[1] + uf[2] * n[2];
+  double Rp = un_i + 2.0 * c_i / (g - 1.0), Rm = un_f - 2.0 * c_f / (g - 1.0);
+  if (un_f + c_f < 0.0) Rp = un_f + 2.0 * c_f / (g - 1.0);
+  if (un_i - c_i > 0.0) Rm = un_i - 2.0 * c_i / (g - 1.0);
+  double un = 0.5 * (Rp + Rm), c = 0.25 * (g - 1.0) * (Rp - Rm);
+  double ut[3], s;
+  if (un > 0.0) {
+    for (int a = 0; a < 3; ++a) ut[a] = ui[a] - un_i * n[a];
+    s = p_i / pow(rho_i, g);
+  } else {
+    for (int a = 0; a < 3; ++a) ut[a] = uf[a] - un_f * n[a];
+    s = p_f / pow(rho_f, g);
+  }
+  double rho = pow(c * c / (g * s), 1.0 / (g - 1.0));
+  double p = rho * c * c / g;
+  double u[3] = {ut[0] + un * n[0], ut[1] + un * n[1], ut[2] + un * n[2]};
+  qb[0] = rho;
+  qb[1] = rho * u[0];
+  qb[2] = rho * u[1];
+  qb[3] = rho * u[2];
+  qb[4] = p / (g - 1.0) + 0.5 * rho * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+}
+
+__global__ void k_bc_ghosts(double* __restrict__ Q, int ldq, int first, int n, const int* __restrict__ bg_cell,
+                            const int* __restrict__ bg_bc, const double* __restrict__ bg_normal, GasParams gp) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  int c = bg_cell[k];
+  double qi[5];
+#pragma unroll
+  for (int v = 0; v < 5; ++v) qi[v] = Q[v * ldq + c];
+  double qb[5];
+  if (bg_bc[k] == 1) {
+    qb[0] = qi[0]; qb[1] = -qi[1]; qb[2] = -qi[2]; qb[3] = -qi[3]; qb[4] = qi[4];
+  } else {
+    double n3[3] = {bg_normal[3 * k], bg_normal[3 * k + 1], bg_normal[3 * k + 2]};
+    farfield_riemann(qi, n3, gp, qb);
+  }
+#pragma unroll
+  for (int v = 0; v < 5; ++v) Q[v * ldq + first + k] = qb[v];
+}
+
+// ----------------------------------------------------------------------------
+// a7: WENO reconstruction, one thread per reconstructed cell.
+// Output record per local cell (50 doubles): [const(5) | lin x,y,z (3x5) |
+// quad xx,yy,zz,xy,xz,yz (6x5)], so that at X = x - c_i
+//   Q(x) = const + sum_a lin_a X_a + quad . (X_a X_b)       (Eq. weno collapsed)
+// ----------------------------------------------------------------------------
+constexpr int kRec = 50;
+
+struct ReconArgs {
+  const double* __restrict__ Q;  // [5][ldq]
+  int ldq;
+  int n_recon;
+  const int* __restrict__ recon_cell;
+  const int* __restrict__ st_id;        // [K][n_recon]
+  const uint8_t* __restrict__ sub_slot; // [M*NM][n_recon]
+  const double* __restrict__ op;        // [E][n_recon]
+  const double* __restrict__ geo;       // [8][n_recon]
+  double* __restrict__ ceff;            // [n_cells_local][50]
+  double eps;
+  int omega_pow;
+};
+
+template <int K, int M, int NM, int BLOCK>
+__global__ void __launch_bounds__(BLOCK) k_recon(ReconArgs a) {
+  extern __shared__ double sb[];  // [M*15][BLOCK] sub-stencil slopes
+  const int r = blockIdx.x * BLOCK + threadIdx.x;
+  if (r >= a.n_recon) return;
+  const int R = a.n_recon;
+  const int ci = a.recon_cell[r];
+  const double* __restrict__ Q = a.Q;
+  const int ldq = a.ldq;
+  double qi[5];
+#pragma unroll
+  for (int v = 0; v < 5; ++v) qi[v] = Q[v * ldq + ci];
+  // ---- P_0: c[d][v] = sum_k A0+[d][k] (Q_k - Q_i)[v] ----
+  double c[9][5];
+#pragma unroll
+  for (int d = 0; d < 9; ++d)
+#pragma unroll
+    for (int v = 0; v < 5; ++v) c[d][v] = 0.0;
+  const double* __restrict__ op = a.op + r;
+#pragma unroll 2
+  for (int k = 0; k < K; ++k) {
+    const int id = a.st_id[k * R + r];
+    double dq[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) dq[v] = __ldg(Q + v * ldq + id) - qi[v];
+#pragma unroll
+    for (int d = 0; d < 9; ++d) {
+      const double w = __ldcs(op + (size_t)(d * K + k) * R);
+#pragma unroll
+      for (int v = 0; v < 5; ++v) c[d][v] = fma(w, dq[v], c[d][v]);
+    }
+  }
+  const double V23 = a.geo[0 * R + r], V43 = a.geo[1 * R + r];
+  double m2[6];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) m2[q] = a.geo[(2 + q) * R + r];
+  // ---- beta_0 closed form ----
+  double beta0[5];
+#pragma unroll
+  for (int v = 0; v < 5; ++v) {
+    const double cx = c[0][v], cy = c[1][v], cz = c[2][v];
+    const double cxx = c[3][v], cyy = c[4][v], czz = c[5][v], cxy = c[6][v], cxz = c[7][v], cyz = c[8][v];
+    // gradient d_a P0 = c_a + g_a . X ; g_x = (2cxx, cxy, cxz) ...
+    const double gx[3] = {2.0 * cxx, cxy, cxz}, gy[3] = {cxy, 2.0 * cyy, cyz}, gz[3] = {cxz, cyz, 2.0 * czz};
+    auto quadf = [&](const double g[3]) {
+      return m2[0] * g[0] * g[0] + m2[1] * g[1] * g[1] + m2[2] * g[2] * g[2] +
+             2.0 * (m2[3] * g[0] * g[1] + m2[4] * g[0] * g[2] + m2[5] * g[1] * g[2]);
+    };
+    const double s1 = cx * cx + cy * cy + cz * cz + quadf(gx) + quadf(gy) + quadf(gz);
+    const double s2 = 4.0 * (cxx * cxx + cyy * cyy + czz * czz) + cxy * cxy + cxz * cxz + cyz * cyz;
+    beta0[v] = V23 * s1 + V43 * s2;
+  }
+  // ---- P_m: b[d][v] over the sub-stencils, beta_m ----
+  double betam[M][5];
+  const double* __restrict__ opm = op + (size_t)(9 * K) * R;
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    double b[3][5];
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int v = 0; v < 5; ++v) b[d][v] = 0.0;
+#pragma unroll
+    for (int j = 0; j < NM; ++j) {
+      const int s = a.sub_slot[(m * NM + j) * R + r];
+      const int id = a.st_id[s * R + r];
+      double dq[5];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) dq[v] = __ldg(Q + v * ldq + id) - qi[v];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double w = __ldcs(opm + (size_t)((m * 3 + d) * NM + j) * R);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) b[d][v] = fma(w, dq[v], b[d][v]);
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      betam[m][v] = V23 * (b[0][v] * b[0][v] + b[1][v] * b[1][v] + b[2][v] * b[2][v]);
+#pragma unroll
+      for (int d = 0; d < 3; ++d) sb[((m * 3 + d) * 5 + v) * BLOCK + threadIdx.x] = b[d][v];
+    }
+  }
+  // ---- nonlinear weights and collapse ----
+  const double gm = 0.025, g0 = 1.0 - 0.025 * M;
+  double* __restrict__ out = a.ceff + (size_t)ci * kRec;
+#pragma unroll
+  for (int v = 0; v < 5; ++v) {
+    double tz = 0.0;
+#pragma unroll
+    for (int m = 0; m < M; ++m) tz += fabs(beta0[v] - betam[m][v]);
+    tz *= (1.0 / M);
+    double r0 = tz / (beta0[v] + a.eps);
+    double w0 = g0 * (1.0 + (a.omega_pow == 2 ? r0 * r0 : r0));
+    double wm[M], sum = w0;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      double rm = tz / (betam[m][v] + a.eps);
+      wm[m] = gm * (1.0 + (a.omega_pow == 2 ? rm * rm : rm));
+      sum += wm[m];
+    }
+    const double inv = 1.0 / sum;
+    const double al0 = w0 * inv / g0;  // omega-bar_0 / gamma_0
+    double lin[3] = {al0 * c[0][v], al0 * c[1][v], al0 * c[2][v]};
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const double alm = wm[m] * inv - al0 * gm;  // omega-bar_m - omega-bar_0 gamma_m / gamma_0
+#pragma unroll
+      for (int d = 0; d < 3; ++d) lin[d] = fma(alm, sb[((m * 3 + d) * 5 + v) * BLOCK + threadIdx.x], lin[d]);
+    }
+    double quad[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) quad[q] = al0 * c[3 + q][v];
+    double cst = qi[v] - (quad[0] * m2[0] + quad[1] * m2[1] + quad[2] * m2[2] + quad[3] * m2[3] + quad[4] * m2[4] +
+                          quad[5] * m2[5]);
+    out[v] = cst;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) out[5 + d * 5 + v] = lin[d];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) out[20 + q * 5 + v] = quad[q];
+  }
+}
+
+// ----------------------------------------------------------------------------
+// a8 + a9: face flux for tau = 0, one thread per Gauss point.
+// ----------------------------------------------------------------------------
+struct FluxArgs {
+  const double* __restrict__ Q;
+  int ldq;
+  const double* __restrict__ ceff;
+  const int* __restrict__ f_cells;  // [n][2]
+  const double* __restrict__ f_geo; // [n][stride]
+  int f_stride;
+  int n_faces;                      // faces in this launch
+  int face0;                        // first face index
+  double* __restrict__ F1;          // stage 1: [n_faces][10] (F*S, dF*S)
+  double* __restrict__ F2;          // stage 2: [n_faces][5]  (dF*S)
+  Ctrl* ctrl;
+  double gamma, K;
+};
+
+// evaluate the effective polynomial of a cell at X (relative to its centroid)
+__device__ __forceinline__ void eval_poly(const double* __restrict__ rec, const double X[3], double val[5],
+                                          double grad[5][3]) {
+  const double xx = X[0] * X[0], yy = X[1] * X[1], zz = X[2] * X[2];
+  const double xy = X[0] * X[1], xz = X[0] * X[2], yz = X[1] * X[2];
+#pragma unroll
+  for (int v = 0; v < 5; ++v) {
+    const double c0 = __ldg(rec + v);
+    const double lx = __ldg(rec + 5 + v), ly = __ldg(rec + 10 + v), lz = __ldg(rec + 15 + v);
+    const double qxx = __ldg(rec + 20 + v), qyy = __ldg(rec + 25 + v), qzz = __ldg(rec + 30 + v);
+    const double qxy = __ldg(rec + 35 + v), qxz = __ldg(rec + 40 + v), qyz = __ldg(rec + 45 + v);
+    val[v] = c0 + lx * X[0] + ly * X[1] + lz * X[2] + qxx * xx + qyy * yy + qzz * zz + qxy * xy + qxz * xz + qyz * yz;
+    grad[v][0] = lx + 2.0 * qxx * X[0] + qxy * X[1] + qxz * X[2];
+    grad[v][1] = ly + 2.0 * qyy * X[1] + qxy * X[0] + qyz * X[2];
+    grad[v][2] = lz + 2.0 * qzz * X[2] + qxz * X[0] + qyz * X[1];
+  }
+}
+
+// Gauss point g of a face from its vertices (relative to the owner centroid), R10
+template <int NV>
+__device__ __forceinline__ void face_gp(const double* __restrict__ fg, int g, double x[3], double n[3], double& wS) {
+  if (NV == 3) {
+    double p[3][3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) p[q][a] = __ldg(fg + 3 * q + a);
+    const double e1[3] = {p[1][0] - p[0][0], p[1][1] - p[0][1], p[1][2] - p[0][2]};
+    const double e2[3] = {p[2][0] - p[0][0], p[2][1] - p[0][1], p[2][2] - p[0][2]};
+    double nn[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
+    const double a2 = sqrt(nn[0] * nn[0] + nn[1] * nn[1] + nn[2] * nn[2]);
+    const double l0 = g == 0 ? 2.0 / 3.0 : 1.0 / 6.0, l1 = g == 1 ? 2.0 / 3.0 : 1.0 / 6.0,
+                 l2 = g == 2 ? 2.0 / 3.0 : 1.0 / 6.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      x[a] = l0 * p[0][a] + l1 * p[1][a] + l2 * p[2][a];
+      n[a] = nn[a] / a2;
+    }
+    wS = a2 / 6.0;
+  } else {
+    double p[4][3];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) p[q][a] = __ldg(fg + 3 * q + a);
+    const double h = 0.28867513459481287;  // 1/(2 sqrt 3)
+    const double s = (g & 1) ? 0.5 + h : 0.5 - h, t = (g >> 1) ? 0.5 + h : 0.5 - h;
+    double ds[3], dt[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      x[a] = (1 - s) * (1 - t) * p[0][a] + s * (1 - t) * p[1][a] + s * t * p[2][a] + (1 - s) * t * p[3][a];
+      ds[a] = (1 - t) * (p[1][a] - p[0][a]) + t * (p[2][a] - p[3][a]);
+      dt[a] = (1 - s) * (p[3][a] - p[0][a]) + s * (p[2][a] - p[1][a]);
+    }
+    double nn[3] = {ds[1] * dt[2] - ds[2] * dt[1], ds[2] * dt[0] - ds[0] * dt[2], ds[0] * dt[1] - ds[1] * dt[0]};
+    const double an = sqrt(nn[0] * nn[0] + nn[1] * nn[1] + nn[2] * nn[2]);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) n[a] = nn[a] / an;
+    wS = 0.25 * an;
+  }
+}
+
+// local frame (R11): t1 = normalize(n x e*), e* the axis with the smallest |n.e|
+__device__ __forceinline__ void frame(const double n[3], double t1[3], double t2[3]) {
+  int k = 0;
+  if (fabs(n[1]) < fabs(n[k])) k = 1;
+  if (fabs(n[2]) < fabs(n[k])) k = 2;
+  double e[3] = {0.0, 0.0, 0.0};
+  e[k] = 1.0;
+  double c[3] = {n[1] * e[2] - n[2] * e[1], n[2] * e[0] - n[0] * e[2], n[0] * e[1] - n[1] * e[0]};
+  double inv = 1.0 / sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) t1[a] = c[a] * inv;
+  t2[0] = n[1] * t1[2] - n[2] * t1[1];
+  t2[1] = n[2] * t1[0] - n[0] * t1[2];
+  t2[2] = n[0] * t1[1] - n[1] * t1[0];
+}
+
+// rotate value + gradient (global) into the local frame: q[5], dq[3][5] (derivative along n, t1, t2)
+__device__ __forceinline__ void to_local(const double val[5], const double grad[5][3], const double n[3],
+                                         const double t1[3], const double t2[3], double q[5], double dq[3][5]) {
+  q[0] = val[0];
+  q[4] = val[4];
+  q[1] = val[1] * n[0] + val[2] * n[1] + val[3] * n[2];
+  q[2] = val[1] * t1[0] + val[2] * t1[1] + val[3] * t1[2];
+  q[3] = val[1] * t2[0] + val[2] * t2[1] + val[3] * t2[2];
+  const double* dirs[3] = {n, t1, t2};
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const double* e = dirs[j];
+    double d[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) d[v] = grad[v][0] * e[0] + grad[v][1] * e[1] + grad[v][2] * e[2];
+    dq[j][0] = d[0];
+    dq[j][4] = d[4];
+    dq[j][1] = d[1] * n[0] + d[2] * n[1] + d[3] * n[2];
+    dq[j][2] = d[1] * t1[0] + d[2] * t1[1] + d[3] * t1[2];
+    dq[j][3] = d[1] * t2[0] + d[2] * t2[1] + d[3] * t2[2];
+  }
+}
+
+// Euler-flux Jacobian-vector product along local axis j: dF_j = (dF_j/dQ) dq
+__device__ __forceinline__ void euler_jvp(int j, const double Q[5], const double dq[5], double gm1, double out[5]) {
+  const double rho = Q[0];
+  const double inv = 1.0 / rho;
+  const double u[3] = {Q[1] * inv, Q[2] * inv, Q[3] * inv};
+  const double p = gm1 * (Q[4] - 0.5 * (Q[1] * u[0] + Q[2] * u[1] + Q[3] * u[2]));
+  const double du[3] = {(dq[1] - u[0] * dq[0]) * inv, (dq[2] - u[1] * dq[0]) * inv, (dq[3] - u[2] * dq[0]) * inv};
+  const double dp = gm1 * (dq[4] - (u[0] * dq[1] + u[1] * dq[2] + u[2] * dq[3]) +
+                           0.5 * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]) * dq[0]);
+  out[0] = dq[1 + j];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) out[1 + k] = dq[1 + j] * u[k] + Q[1 + j] * du[k] + (k == j ? dp : 0.0);
+  out[4] = du[j] * (Q[4] + p) + u[j] * (dq[4] + dp);
+}
+
+template <int NV, int STAGE>
+__global__ void __launch_bounds__(NV == 3 ? 96 : 128) k_flux_tau0(FluxArgs a) {
+  constexpr int NGP = NV == 3 ? 3 : 4;
+  constexpr int BLOCK = NV == 3 ? 96 : 128;
+  constexpr int NOUT = STAGE == 1 ? 10 : 5;
+  __shared__ double red[NOUT][BLOCK];
+  const int t = blockIdx.x * BLOCK + threadIdx.x;
+  const int lf = t / NGP, g = t - lf * NGP;
+  const bool active = lf < a.n_faces;
+  double out[NOUT];
+#pragma unroll
+  for (int k = 0; k < NOUT; ++k) out[k] = 0.0;
+  if (active) {
+    const int f = a.face0 + lf;
+    const int co = __ldg(a.f_cells + 2 * f), cn = __ldg(a.f_cells + 2 * f + 1);
+    const double* fg = a.f_geo + (size_t)f * a.f_stride;
+    double x[3], n[3], wS;
+    face_gp<NV>(fg, g, x, n, wS);
+    const double xr[3] = {x[0] + __ldg(fg + 3 * NV), x[1] + __ldg(fg + 3 * NV + 1), x[2] + __ldg(fg + 3 * NV + 2)};
+    double t1[3], t2[3];
+    frame(n, t1, t2);
+    const double gm1 = a.gamma - 1.0;
+    double ql[5], dql[3][5], qr[5], dqr[3][5];
+    {
+      double val[5], grad[5][3];
+      eval_poly(a.ceff + (size_t)co * kRec, x, val, grad);
+      double pl = gm1 * (val[4] - 0.5 * (val[1] * val[1] + val[2] * val[2] + val[3] * val[3]) / val[0]);
+      if (!(val[0] > 0.0) || !(pl > 0.0)) {  // R21 positivity fallback
+        atomicAdd((unsigned long long*)&a.ctrl->fallbacks, 1ull);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+          val[v] = a.Q[v * a.ldq + co];
+          grad[v][0] = grad[v][1] = grad[v][2] = 0.0;
+        }
+      }
+      to_local(val, grad, n, t1, t2, ql, dql);
+    }
+    {
+      double val[5], grad[5][3];
+      eval_poly(a.ceff + (size_t)cn * kRec, xr, val, grad);
+      double pr = gm1 * (val[4] - 0.5 * (val[1] * val[1] + val[2] * val[2] + val[3] * val[3]) / val[0]);
+      if (!(val[0] > 0.0) || !(pr > 0.0)) {
+        atomicAdd((unsigned long long*)&a.ctrl->fallbacks, 1ull);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+          val[v] = a.Q[v * a.ldq + cn];
+          grad[v][0] = grad[v][1] = grad[v][2] = 0.0;
+        }
+      }
+      to_local(val, grad, n, t1, t2, qr, dqr);
+    }
+    // ---- Q0 = int_{u>0} psi g_l + int_{u<0} psi g_r ----
+    double Q0[5];
+    {
+      const double K = a.K;
+      const double rpi = 0.56418958354775628;  // 1/sqrt(pi)
+      // left, u > 0
+      double rl = ql[0], Ul = ql[1] / rl, Vl = ql[2] / rl, Wl = ql[3] / rl;
+      double laml = (K + 3.0) * rl / (4.0 * (ql[4] - 0.5 * rl * (Ul * Ul + Vl * Vl + Wl * Wl)));
+      double sl = sqrt(laml);
+      double a0 = 0.5 * erfc(-sl * Ul);
+      double a1 = Ul * a0 + 0.5 * exp(-laml * Ul * Ul) * rpi / sl;
+      double a2 = Ul * a1 + a0 / (2.0 * laml);
+      // right, u < 0
+      double rr = qr[0], Ur = qr[1] / rr, Vr = qr[2] / rr, Wr = qr[3] / rr;
+      double lamr = (K + 3.0) * rr / (4.0 * (qr[4] - 0.5 * rr * (Ur * Ur + Vr * Vr + Wr * Wr)));
+      double sr = sqrt(lamr);
+      double b0 = 0.5 * erfc(sr * Ur);
+      double b1 = Ur * b0 - 0.5 * exp(-lamr * Ur * Ur) * rpi / sr;
+      double b2 = Ur * b1 + b0 / (2.0 * lamr);
+      Q0[0] = rl * a0 + rr * b0;
+      Q0[1] = rl * a1 + rr * b1;
+      Q0[2] = rl * a0 * Vl + rr * b0 * Vr;
+      Q0[3] = rl * a0 * Wl + rr * b0 * Wr;
+      Q0[4] = 0.5 * rl * (a2 + a0 * (Vl * Vl + Wl * Wl + (K + 2.0) / (2.0 * laml))) +
+              0.5 * rr * (b2 + b0 * (Vr * Vr + Wr * Wr + (K + 2.0) / (2.0 * lamr)));
+    }
+    // ---- tau = 0: f = g0 (1 + A t).  F = Euler flux of Q0 and
+    //      d_t F = A_n(Q0) d_t Q0, d_t Q0 = -sum_j A_j(Q0) d_j Q0, with
+    //      d_j Q0 = (d_j Q_l + d_j Q_r)/2 (R9) ----
+    double dtQ0[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      double d0[5], jv[5];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) d0[v] = 0.5 * (dql[j][v] + dqr[j][v]);
+      euler_jvp(j, Q0, d0, gm1, jv);
+#pragma unroll
+      for (int v = 0; v < 5; ++v) dtQ0[v] -= jv[v];
+    }
+    double dF[5];
+    euler_jvp(0, Q0, dtQ0, gm1, dF);
+    // rotate back and weight by omega_G S
+    if (STAGE == 1) {
+      const double u0 = Q0[1] / Q0[0];
+      const double p0 = gm1 * (Q0[4] - 0.5 * (Q0[1] * Q0[1] + Q0[2] * Q0[2] + Q0[3] * Q0[3]) / Q0[0]);
+      const double F[5] = {Q0[1], Q0[1] * u0 + p0, Q0[2] * u0, Q0[3] * u0, u0 * (Q0[4] + p0)};
+      out[0] = wS * F[0];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) out[1 + c] = wS * (F[1] * n[c] + F[2] * t1[c] + F[3] * t2[c]);
+      out[4] = wS * F[4];
+      out[5] = wS * dF[0];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) out[6 + c] = wS * (dF[1] * n[c] + dF[2] * t1[c] + dF[3] * t2[c]);
+      out[9] = wS * dF[4];
+    } else {
+      out[0] = wS * dF[0];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) out[1 + c] = wS * (dF[1] * n[c] + dF[2] * t1[c] + dF[3] * t2[c]);
+      out[4] = wS * dF[4];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NOUT; ++k) red[k][threadIdx.x] = out[k];
+  __syncthreads();
+  // face quadrature sum in Gauss-point order (deterministic); NOUT-wide store
+  const int faces_in_block = BLOCK / NGP;
+  for (int e = threadIdx.x; e < faces_in_block * NOUT; e += BLOCK) {
+    const int fl = e / NOUT, k = e - fl * NOUT;
+    const int face = blockIdx.x * faces_in_block + fl;
+    if (face < a.n_faces) {
+      double s = red[k][fl * NGP];
+#pragma unroll
+      for (int q = 1; q < NGP; ++q) s += red[k][fl * NGP + q];
+      double* dst = STAGE == 1 ? a.F1 : a.F2;
+      dst[(size_t)(a.face0 + face) * NOUT + k] = s;
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// a10: L, d_t L and the S2O4 stages
+// ----------------------------------------------------------------------------
+struct UpdateArgs {
+  double* __restrict__ Q;  // [5][ldq]  (stage 1: Q^n -> Q*, stage 2: -> Q^{n+1})
+  int ldq;
+  double* __restrict__ R;  // [5][n_owned]
+  const double* __restrict__ F1;
+  const double* __restrict__ F2;
+  const int* __restrict__ cf;  // [NF][n_owned]
+  const double* __restrict__ inv_v;
+  const double* __restrict__ h_dt;
+  int n_owned;
+  Ctrl* ctrl;
+  GasParams gp;
+};
+
+template <int NF>
+__global__ void __launch_bounds__(256) k_update1(UpdateArgs a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n_owned) return;
+  double L[5] = {0, 0, 0, 0, 0}, dL[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+  for (int p = 0; p < NF; ++p) {  // local-face order (deterministic, partition independent)
+    const int e = a.cf[p * a.n_owned + i];
+    const int f = e >= 0 ? e : ~e;
+    const double* F = a.F1 + (size_t)f * 10;
+    if (e >= 0) {
+#pragma unroll
+      for (int v = 0; v < 5; ++v) { L[v] -= F[v]; dL[v] -= F[5 + v]; }
+    } else {
+#pragma unroll
+      for (int v = 0; v < 5; ++v) { L[v] += F[v]; dL[v] += F[5 + v]; }
+    }
+  }
+  const double iv = a.inv_v[i];
+  const double dt = a.ctrl->dt;
+#pragma unroll
+  for (int v = 0; v < 5; ++v) {
+    const double l = L[v] * iv, dl = dL[v] * iv;
+    const double q = a.Q[v * a.ldq + i];
+    a.Q[v * a.ldq + i] = q + 0.5 * dt * l + 0.125 * dt * dt * dl;
+    a.R[v * a.n_owned + i] = q + dt * l + dt * dt / 6.0 * dl;
+  }
+}
+
+__device__ __forceinline__ double cell_dt_bound(const double q[5], double h, const GasParams& gp) {
+  const double rho = q[0];
+  const double u = q[1] / rho, v = q[2] / rho, w = q[3] / rho;
+  const double p = (gp.gamma - 1.0) * (q[4] - 0.5 * rho * (u * u + v * v + w * w));
+  const double c = sqrt(gp.gamma * p / rho);
+  double nu = 0.0;
+  if (gp.tau_mode == 1) nu = gp.mu_inf * pow((p / rho) / gp.t_inf, gp.mu_exp) / rho;
+  return h / (sqrt(u * u + v * v + w * w) + c + 2.0 * nu / h);
+}
+
+__device__ __forceinline__ void block_min_dt(double local, Ctrl* ctrl) {
+  // warp shuffle min, then one atomic per warp on the ordered bits of a positive double
+  unsigned long long bits = __double_as_longlong(local);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long ob = __shfl_xor_sync(0xffffffffu, bits, o);
+    bits = ob < bits ? ob : bits;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMin(&ctrl->dtmin_bits, bits);
+}
+
+template <int NF>
+__global__ void __launch_bounds__(256) k_update2(UpdateArgs a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double bound = 1e300;
+  if (i < a.n_owned) {
+    double dL[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+    for (int p = 0; p < NF; ++p) {
+      const int e = a.cf[p * a.n_owned + i];
+      const int f = e >= 0 ? e : ~e;
+      const double* F = a.F2 + (size_t)f * 5;
+      if (e >= 0) {
+#pragma unroll
+        for (int v = 0; v < 5; ++v) dL[v] -= F[v];
+      } else {
+#pragma unroll
+        for (int v = 0; v < 5; ++v) dL[v] += F[v];
+      }
+    }
+    const double iv = a.inv_v[i];
+    const double dt = a.ctrl->dt;
+    double q[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      q[v] = a.R[v * a.n_owned + i] + dt * dt / 6.0 * 2.0 * (dL[v] * iv);
+      a.Q[v * a.ldq + i] = q[v];
+    }
+    const double p = (a.gp.gamma - 1.0) * (q[4] - 0.5 * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3]) / q[0]);
+    if (!(q[0] > 0.0) || !(p > 0.0)) atomicMin(&a.ctrl->bad_cell, i);
+    else bound = cell_dt_bound(q, a.h_dt[i], a.gp);
+  }
+  block_min_dt(bound, a.ctrl);
+}
+
+__global__ void __launch_bounds__(256) k_dt_init(const double* __restrict__ Q, int ldq, const double* __restrict__ h_dt,
+                                                 int n, Ctrl* ctrl, GasParams gp) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double bound = 1e300;
+  if (i < n) {
+    double q[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) q[v] = Q[v * ldq + i];
+    bound = cell_dt_bound(q, h_dt[i], gp);
+  }
+  block_min_dt(bound, ctrl);
+}
+
+// one thread: advance the time bookkeeping and choose this step's dt
+__global__ void k_step_begin(Ctrl* ctrl, double cfl, double fixed_dt, double t_stop) {
+  double t = ctrl->t_next;
+  double raw = fixed_dt > 0.0 ? fixed_dt : cfl * __longlong_as_double((long long)ctrl->dtmin_bits);
+  double dt = raw, tn = t + raw;
+  if (t_stop > 0.0) {
+    if (t >= t_stop) {
+      dt = 0.0;
+      tn = t;
+    } else if (t + raw > t_stop) {
+      dt = t_stop - t;
+      tn = t_stop;
+    }
+  }
+  ctrl->t = t;
+  ctrl->dt = dt;
+  ctrl->t_next = tn;
+  if (dt > 0.0) ctrl->steps += 1;
+  ctrl->dtmin_bits = 0x7fefffffffffffffull;  // +max finite, reset for this step's accumulation
+}
+
+// state layout conversions for set/get_state: AoS [n][5] in caller order <-> SoA local
+__global__ void k_scatter_state(const double* __restrict__ in, const int64_t* __restrict__ row, int n,
+                                double* __restrict__ Q, int ldq) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t r = row[i];
+#pragma unroll
+  for (int v = 0; v < 5; ++v) Q[v * ldq + i] = in[r * 5 + v];
+}
+__global__ void k_gather_state(const double* __restrict__ Q, int ldq, const int* __restrict__ local_of_out, int n,
+                               double* __restrict__ out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int i = local_of_out[k];
+#pragma unroll
+  for (int v = 0; v < 5; ++v) out[(size_t)k * 5 + v] = Q[v * ldq + i];
+}
+// halo pack: SoA send buffer [5][n_send]
+__global__ void k_pack(const double* __restrict__ Q, int ldq, const int* __restrict__ list, int n,
+                       double* __restrict__ buf) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int i = list[k];
+#pragma unroll
+  for (int v = 0; v < 5; ++v) buf[v * n + k] = Q[v * ldq + i];
+}
+
+}  // namespace hgks

@@ -1,0 +1,916 @@
+// Host setup of libhgks: geometry, faces, periodic
+// pairing, Alg. 1 stencils, least-squares operators, k-way partition with 3
+// ghost layers, Morton renumbering.  Runs once per mesh; never on the hot path.
+//
+// Independent of oracle/ (shares no code): faces are matched by bucketing on
+// the smallest node id, periodic faces by sorted canonical keys, least squares
+// by Gram-Schmidt QR with re-orthogonalisation to an explicit pseudo-inverse.
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <unordered_map>
+
+#include "internal.h"
+
+namespace hgks {
+namespace {
+
+struct P3 {
+  double x, y, z;
+};
+inline P3 operator+(P3 a, P3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+inline P3 operator-(P3 a, P3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+inline P3 operator*(double s, P3 a) { return {s * a.x, s * a.y, s * a.z}; }
+inline double dotp(P3 a, P3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+inline P3 crossp(P3 a, P3 b) { return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x}; }
+inline double len(P3 a) { return std::sqrt(dotp(a, a)); }
+
+// tet face p = nodes other than p; hex faces, VTK order (R17)
+const int kTetF[4][3] = {{1, 2, 3}, {0, 2, 3}, {0, 1, 3}, {0, 1, 2}};
+const int kHexF[6][4] = {{0, 1, 2, 3}, {0, 1, 5, 4}, {1, 2, 6, 5}, {2, 3, 7, 6}, {3, 0, 4, 7}, {4, 5, 6, 7}};
+
+// --- cell geometry (a0) ------------------------------------------------------
+void tet_geometry(const P3 v[4], double& V, P3& c, double m2[6]) {
+  P3 a = v[1] - v[0], b = v[2] - v[0], d = v[3] - v[0];
+  V = std::fabs(dotp(a, crossp(b, d))) / 6.0;
+  c = 0.25 * (((v[0] + v[1]) + v[2]) + v[3]);
+  for (int k = 0; k < 6; ++k) m2[k] = 0;
+  for (int k = 0; k < 4; ++k) {
+    P3 e = v[k] - c;
+    m2[0] += e.x * e.x; m2[1] += e.y * e.y; m2[2] += e.z * e.z;
+    m2[3] += e.x * e.y; m2[4] += e.x * e.z; m2[5] += e.y * e.z;
+  }
+  for (int k = 0; k < 6; ++k) m2[k] *= 0.05;  // mean of (x-c)(x-c)^T over a tet = (1/20) sum_k e_k e_k^T
+}
+
+void hex_geometry(const P3 v[8], double& V, P3& c, double m2[6]) {
+  // trilinear map on [0,1]^3, tensor 3-point Gauss (exact for these integrands)
+  const double s = std::sqrt(0.15);
+  const double gx[3] = {0.5 - s, 0.5, 0.5 + s}, gw[3] = {5.0 / 18.0, 4.0 / 9.0, 5.0 / 18.0};
+  P3 X[27];
+  double W[27];
+  int q = 0;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      for (int k = 0; k < 3; ++k, ++q) {
+        double r = gx[i], t = gx[j], u = gx[k];
+        double Nr[2] = {1 - r, r}, Nt[2] = {1 - t, t}, Nu[2] = {1 - u, u};
+        // VTK corner (a,b,c) offsets
+        const int off[8][3] = {{0, 0, 0}, {1, 0, 0}, {1, 1, 0}, {0, 1, 0}, {0, 0, 1}, {1, 0, 1}, {1, 1, 1}, {0, 1, 1}};
+        P3 x{0, 0, 0}, dr{0, 0, 0}, dt{0, 0, 0}, du{0, 0, 0};
+        for (int n = 0; n < 8; ++n) {
+          int a = off[n][0], b = off[n][1], cc = off[n][2];
+          double sa = a ? 1.0 : -1.0, sb = b ? 1.0 : -1.0, sc = cc ? 1.0 : -1.0;
+          x = x + (Nr[a] * Nt[b] * Nu[cc]) * v[n];
+          dr = dr + (sa * Nt[b] * Nu[cc]) * v[n];
+          dt = dt + (Nr[a] * sb * Nu[cc]) * v[n];
+          du = du + (Nr[a] * Nt[b] * sc) * v[n];
+        }
+        X[q] = x;
+        W[q] = gw[i] * gw[j] * gw[k] * std::fabs(dotp(dr, crossp(dt, du)));
+      }
+  V = 0;
+  P3 acc{0, 0, 0};
+  for (int k = 0; k < 27; ++k) {
+    V += W[k];
+    acc = acc + W[k] * X[k];
+  }
+  c = (1.0 / V) * acc;
+  for (int k = 0; k < 6; ++k) m2[k] = 0;
+  for (int k = 0; k < 27; ++k) {
+    P3 e = X[k] - c;
+    double w = W[k] / V;
+    m2[0] += w * e.x * e.x; m2[1] += w * e.y * e.y; m2[2] += w * e.z * e.z;
+    m2[3] += w * e.x * e.y; m2[4] += w * e.x * e.z; m2[5] += w * e.y * e.z;
+  }
+}
+
+// Face Gauss points (R10): positions, unit normals along the vertex order's
+// right-hand rule, and weight*area.
+int face_gps(int nv, const P3* p, P3* x, P3* n, double* wS) {
+  if (nv == 3) {
+    P3 nn = crossp(p[1] - p[0], p[2] - p[0]);
+    double a2 = len(nn);
+    for (int g = 0; g < 3; ++g) {
+      double l[3] = {1.0 / 6.0, 1.0 / 6.0, 1.0 / 6.0};
+      l[g] = 2.0 / 3.0;
+      x[g] = (l[0] * p[0] + l[1] * p[1]) + l[2] * p[2];
+      n[g] = (1.0 / a2) * nn;
+      wS[g] = a2 / 6.0;
+    }
+    return 3;
+  }
+  const double h = 0.5 / std::sqrt(3.0);
+  const double q[2] = {0.5 - h, 0.5 + h};
+  for (int g = 0; g < 4; ++g) {
+    double s = q[g & 1], t = q[g >> 1];
+    x[g] = ((1 - s) * (1 - t)) * p[0] + (s * (1 - t)) * p[1] + (s * t) * p[2] + ((1 - s) * t) * p[3];
+    P3 ds = (1 - t) * (p[1] - p[0]) + t * (p[2] - p[3]);
+    P3 dt = (1 - s) * (p[3] - p[0]) + s * (p[2] - p[1]);
+    P3 nn = crossp(ds, dt);
+    double a = len(nn);
+    n[g] = (1.0 / a) * nn;
+    wS[g] = 0.25 * a;
+  }
+  return 4;
+}
+
+// --- least squares (a2): pseudo-inverse by Gram-Schmidt QR (CGS2) ----------
+// A is m x n (row-major), returns P (n x m) with P A = I, least-squares sense.
+bool pinv_qr(int m, int n, const double* A, double* P) {
+  std::vector<double> Q(m * n), R(n * n, 0.0);
+  for (int j = 0; j < n; ++j) {
+    for (int i = 0; i < m; ++i) Q[i * n + j] = A[i * n + j];
+    for (int pass = 0; pass < 2; ++pass)
+      for (int k = 0; k < j; ++k) {
+        double r = 0;
+        for (int i = 0; i < m; ++i) r += Q[i * n + k] * Q[i * n + j];
+        R[k * n + j] += r;
+        for (int i = 0; i < m; ++i) Q[i * n + j] -= r * Q[i * n + k];
+      }
+    double nr = 0, na = 0;
+    for (int i = 0; i < m; ++i) {
+      nr += Q[i * n + j] * Q[i * n + j];
+      na += A[i * n + j] * A[i * n + j];
+    }
+    nr = std::sqrt(nr);
+    if (!(nr > 1e-10 * std::sqrt(na)) || na == 0.0) return false;
+    R[j * n + j] = nr;
+    for (int i = 0; i < m; ++i) Q[i * n + j] /= nr;
+  }
+  // P = R^{-1} Q^T : back substitution per column of Q^T
+  for (int i = 0; i < m; ++i)
+    for (int r = n - 1; r >= 0; --r) {
+      double s = Q[i * n + r];
+      for (int k = r + 1; k < n; ++k) s -= R[r * n + k] * P[k * m + i];
+      P[r * m + i] = s / R[r * n + r];
+    }
+  return true;
+}
+
+struct Member {
+  int64_t id;
+  P3 s;
+};
+
+inline bool same_shift(P3 a, P3 b) { return std::fabs(a.x - b.x) + std::fabs(a.y - b.y) + std::fabs(a.z - b.z) < 1e-9; }
+
+// Morton key of a point in [lo, hi]^3 (21 bits per axis)
+uint64_t spread21(uint64_t v) {
+  v &= 0x1fffff;
+  v = (v | v << 32) & 0x1f00000000ffffULL;
+  v = (v | v << 16) & 0x1f0000ff0000ffULL;
+  v = (v | v << 8) & 0x100f00f00f00f00fULL;
+  v = (v | v << 4) & 0x10c30c30c30c30c3ULL;
+  v = (v | v << 2) & 0x1249249249249249ULL;
+  return v;
+}
+
+}  // namespace
+
+// ============================================================================
+GlobalMesh build_global_mesh(const double* xyz, int64_t n_nodes, const int8_t* type, const int64_t* cn,
+                             int64_t n_cells, const double* per_origin, const double* per_len,
+                             const int64_t* bface_nodes, const int32_t* bface_tag, int64_t n_bf, int32_t n_ranks,
+                             const int32_t* cell_part) {
+  GlobalMesh gm;
+  if (n_cells <= 0 || n_nodes <= 0 || !xyz || !type || !cn) throw Error(1, "empty mesh");
+  gm.nc = n_cells;
+  gm.type.assign(type, type + n_cells);
+  const int ct = type[0];
+  if (ct != 4 && ct != 8) throw Error(2, "unsupported element at cell 0");
+  for (int64_t i = 0; i < n_cells; ++i)
+    if (type[i] != ct) throw Error(2, "mixed element kinds are not supported (cell " + std::to_string(i) + ")");
+  Layout& L = gm.lay;
+  L.cell_type = ct;
+  L.nfaces = ct == 4 ? 4 : 6;
+  L.ngp = ct == 4 ? 3 : 4;
+  L.nv = ct == 4 ? 3 : 4;
+  L.M = ct == 4 ? 4 : 8;
+  L.NM = ct == 4 ? 6 : 3;
+  for (int a = 0; a < 3; ++a) gm.per_len[a] = per_len ? per_len[a] : 0.0;
+  const double O[3] = {per_origin ? per_origin[0] : 0.0, per_origin ? per_origin[1] : 0.0,
+                       per_origin ? per_origin[2] : 0.0};
+  auto node = [&](int64_t id) { return P3{xyz[3 * id], xyz[3 * id + 1], xyz[3 * id + 2]}; };
+  const int nfc = L.nfaces, nvf = L.nv;
+  for (int64_t i = 0; i < n_cells; ++i)
+    for (int k = 0; k < ct; ++k) {
+      int64_t v = cn[i * 8 + k];
+      if (v < 0 || v >= n_nodes) throw Error(2, "invalid node id in cell " + std::to_string(i));
+    }
+  // ---------------- geometry ----------------
+  gm.V.resize(n_cells);
+  gm.C.resize(3 * n_cells);
+  gm.M2.resize(6 * n_cells);
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n_cells; ++i) {
+    P3 v[8];
+    for (int k = 0; k < ct; ++k) v[k] = node(cn[i * 8 + k]);
+    double V;
+    P3 c;
+    if (ct == 4) tet_geometry(v, V, c, &gm.M2[6 * i]);
+    else hex_geometry(v, V, c, &gm.M2[6 * i]);
+    gm.V[i] = V;
+    gm.C[3 * i] = c.x; gm.C[3 * i + 1] = c.y; gm.C[3 * i + 2] = c.z;
+  }
+  for (int64_t i = 0; i < n_cells; ++i)
+    if (!(gm.V[i] > 0)) throw Error(2, "degenerate cell " + std::to_string(i));
+  auto centroid = [&](int64_t i) { return P3{gm.C[3 * i], gm.C[3 * i + 1], gm.C[3 * i + 2]}; };
+
+  // ---------------- faces: bucket half-faces by their smallest node ----------
+  const int64_t nh = n_cells * nfc;
+  std::vector<std::array<int64_t, 4>> hkey(nh);
+  for (int64_t i = 0; i < n_cells; ++i)
+    for (int p = 0; p < nfc; ++p) {
+      std::array<int64_t, 4> k{INT64_MAX, INT64_MAX, INT64_MAX, INT64_MAX};
+      for (int q = 0; q < nvf; ++q) k[q] = cn[i * 8 + (ct == 4 ? kTetF[p][q] : kHexF[p][q])];
+      std::sort(k.begin(), k.end());
+      hkey[i * nfc + p] = k;
+    }
+  std::vector<int64_t> bstart(n_nodes + 1, 0), order(nh);
+  for (int64_t h = 0; h < nh; ++h) bstart[hkey[h][0] + 1]++;
+  for (int64_t n = 0; n < n_nodes; ++n) bstart[n + 1] += bstart[n];
+  {
+    std::vector<int64_t> fill(bstart.begin(), bstart.end() - 1);
+    for (int64_t h = 0; h < nh; ++h) order[fill[hkey[h][0]]++] = h;  // stable: ascending h
+  }
+  // boundary tags by key
+  std::unordered_map<std::string, int32_t> btag;
+  auto key_str = [](const std::array<int64_t, 4>& k) { return std::string((const char*)k.data(), sizeof(int64_t) * 4); };
+  for (int64_t b = 0; b < n_bf; ++b) {
+    std::array<int64_t, 4> k{INT64_MAX, INT64_MAX, INT64_MAX, INT64_MAX};
+    int q = 0;
+    for (int j = 0; j < 4; ++j)
+      if (bface_nodes[b * 4 + j] >= 0) k[q++] = bface_nodes[b * 4 + j];
+    std::sort(k.begin(), k.end());
+    btag[key_str(k)] = bface_tag[b];
+  }
+  gm.cell_face.assign(n_cells * 6, -1);
+  std::vector<int64_t> unmatched;
+  struct FaceTmp {
+    int64_t owner, nb, hown;
+    int32_t bc;
+    P3 shift;
+  };
+  std::vector<FaceTmp> ft;
+  ft.reserve(nh / 2 + 16);
+  for (int64_t n = 0; n < n_nodes; ++n) {
+    int64_t b0 = bstart[n], b1 = bstart[n + 1];
+    std::sort(order.begin() + b0, order.begin() + b1, [&](int64_t a, int64_t b) {
+      return hkey[a] != hkey[b] ? hkey[a] < hkey[b] : a < b;
+    });
+    for (int64_t j = b0; j < b1;) {
+      int64_t e = j + 1;
+      while (e < b1 && hkey[order[e]] == hkey[order[j]]) ++e;
+      if (e - j > 2) throw Error(2, "non-manifold face at cell " + std::to_string(order[j] / nfc));
+      if (e - j == 2) {
+        int64_t ha = order[j], hb = order[j + 1];  // ha < hb => lower cell id is the owner (R19)
+        ft.push_back({ha / nfc, hb / nfc, ha, 0, {0, 0, 0}});
+        gm.cell_face[(ha / nfc) * 6 + ha % nfc] = (int64_t)ft.size() - 1;
+        gm.cell_face[(hb / nfc) * 6 + hb % nfc] = (int64_t)ft.size() - 1;
+      } else {
+        int64_t ha = order[j];
+        auto it = btag.find(key_str(hkey[ha]));
+        if (it != btag.end()) {
+          ft.push_back({ha / nfc, -1, ha, it->second, {0, 0, 0}});
+          gm.cell_face[(ha / nfc) * 6 + ha % nfc] = (int64_t)ft.size() - 1;
+        } else {
+          unmatched.push_back(ha);
+        }
+      }
+      j = e;
+    }
+  }
+  // periodic pairing (R23): canonical wrapped vertex coordinates
+  if (!unmatched.empty()) {
+    double Lm = std::max(gm.per_len[0], std::max(gm.per_len[1], gm.per_len[2]));
+    if (!(Lm > 0)) throw Error(2, "open boundary face at cell " + std::to_string(unmatched[0] / nfc));
+    const double tol = 1e-7 * Lm;
+    struct PK {
+      std::array<int64_t, 12> k;
+      int64_t h;
+    };
+    std::vector<PK> pk(unmatched.size());
+    for (size_t u = 0; u < unmatched.size(); ++u) {
+      int64_t h = unmatched[u];
+      std::array<std::array<int64_t, 3>, 4> q;
+      for (int a = 0; a < 4; ++a) q[a] = {INT64_MAX, INT64_MAX, INT64_MAX};
+      for (int v = 0; v < nvf; ++v) {
+        int64_t nd = cn[(h / nfc) * 8 + (ct == 4 ? kTetF[h % nfc][v] : kHexF[h % nfc][v])];
+        double c3[3] = {xyz[3 * nd] - O[0], xyz[3 * nd + 1] - O[1], xyz[3 * nd + 2] - O[2]};
+        for (int a = 0; a < 3; ++a) {
+          double y = c3[a];
+          if (gm.per_len[a] > 0) {
+            y -= gm.per_len[a] * std::floor(y / gm.per_len[a]);
+            if (gm.per_len[a] - y < tol) y = 0.0;
+          }
+          q[v][a] = (int64_t)std::llround(y / tol);
+        }
+      }
+      std::sort(q.begin(), q.end());
+      for (int v = 0; v < 4; ++v)
+        for (int a = 0; a < 3; ++a) pk[u].k[v * 3 + a] = q[v][a];
+      pk[u].h = h;
+    }
+    std::sort(pk.begin(), pk.end(), [](const PK& a, const PK& b) { return a.k != b.k ? a.k < b.k : a.h < b.h; });
+    for (size_t u = 0; u < pk.size(); u += 2) {
+      if (u + 1 >= pk.size() || pk[u].k != pk[u + 1].k || (u + 2 < pk.size() && pk[u + 2].k == pk[u].k))
+        throw Error(2, "unmatched boundary face at cell " + std::to_string(pk[u].h / nfc));
+      int64_t ha = pk[u].h, hb = pk[u + 1].h;
+      if (hb / nfc < ha / nfc) std::swap(ha, hb);
+      if (ha / nfc == hb / nfc) throw Error(2, "self-periodic cell " + std::to_string(ha / nfc));
+      // shift = (owner face centroid) - (neighbour face centroid), snapped to the box lengths
+      P3 ca{0, 0, 0}, cb{0, 0, 0};
+      for (int v = 0; v < nvf; ++v) {
+        ca = ca + (1.0 / nvf) * node(cn[(ha / nfc) * 8 + (ct == 4 ? kTetF[ha % nfc][v] : kHexF[ha % nfc][v])]);
+        cb = cb + (1.0 / nvf) * node(cn[(hb / nfc) * 8 + (ct == 4 ? kTetF[hb % nfc][v] : kHexF[hb % nfc][v])]);
+      }
+      P3 d = ca - cb;
+      double s[3] = {d.x, d.y, d.z};
+      for (int a = 0; a < 3; ++a) s[a] = gm.per_len[a] > 0 ? gm.per_len[a] * std::round(s[a] / gm.per_len[a]) : 0.0;
+      ft.push_back({ha / nfc, hb / nfc, ha, 0, {s[0], s[1], s[2]}});
+      gm.cell_face[(ha / nfc) * 6 + ha % nfc] = (int64_t)ft.size() - 1;
+      gm.cell_face[(hb / nfc) * 6 + hb % nfc] = (int64_t)ft.size() - 1;
+    }
+  }
+  // canonical face order: by (owner, owner-local face index)
+  {
+    std::vector<int64_t> perm(ft.size());
+    std::iota(perm.begin(), perm.end(), 0);
+    std::sort(perm.begin(), perm.end(), [&](int64_t a, int64_t b) { return ft[a].hown < ft[b].hown; });
+    std::vector<int64_t> inv(ft.size());
+    for (size_t k = 0; k < perm.size(); ++k) inv[perm[k]] = (int64_t)k;
+    std::vector<FaceTmp> f2(ft.size());
+    for (size_t k = 0; k < perm.size(); ++k) f2[k] = ft[perm[k]];
+    ft.swap(f2);
+    for (auto& f : gm.cell_face)
+      if (f >= 0) f = inv[f];
+  }
+  gm.nf = (int64_t)ft.size();
+  gm.f_owner.resize(gm.nf);
+  gm.f_nb.resize(gm.nf);
+  gm.f_bc.resize(gm.nf);
+  gm.f_ghost.assign(gm.nf, -1);
+  gm.f_shift.resize(3 * gm.nf);
+  gm.f_vert.assign(12 * gm.nf, 0.0);
+  gm.f_area.resize(gm.nf);
+  for (int64_t f = 0; f < gm.nf; ++f) {
+    const FaceTmp& F = ft[f];
+    gm.f_owner[f] = F.owner;
+    gm.f_nb[f] = F.nb;
+    gm.f_bc[f] = F.bc;
+    gm.f_shift[3 * f] = F.shift.x; gm.f_shift[3 * f + 1] = F.shift.y; gm.f_shift[3 * f + 2] = F.shift.z;
+    int p = (int)(F.hown % nfc);
+    P3 v[4];
+    for (int q = 0; q < nvf; ++q) v[q] = node(cn[F.owner * 8 + (ct == 4 ? kTetF[p][q] : kHexF[p][q])]);
+    // orient out of the owner
+    P3 fc{0, 0, 0};
+    for (int q = 0; q < nvf; ++q) fc = fc + (1.0 / nvf) * v[q];
+    P3 nn = nvf == 3 ? crossp(v[1] - v[0], v[2] - v[0]) : crossp(v[2] - v[0], v[3] - v[1]);
+    if (dotp(nn, fc - centroid(F.owner)) < 0) {
+      if (nvf == 3) std::swap(v[1], v[2]);
+      else std::swap(v[1], v[3]);
+    }
+    for (int q = 0; q < nvf; ++q) {
+      gm.f_vert[12 * f + 3 * q] = v[q].x; gm.f_vert[12 * f + 3 * q + 1] = v[q].y; gm.f_vert[12 * f + 3 * q + 2] = v[q].z;
+    }
+    P3 gx[4], gn[4];
+    double gw[4];
+    int ng = face_gps(nvf, v, gx, gn, gw);
+    double a = 0;
+    for (int g = 0; g < ng; ++g) a += gw[g];
+    gm.f_area[f] = a;
+  }
+  for (int64_t i = 0; i < n_cells; ++i)
+    for (int p = 0; p < nfc; ++p)
+      if (gm.cell_face[i * 6 + p] < 0) throw Error(2, "open face at cell " + std::to_string(i));
+  // ---------------- boundary ghosts (R25) ----------------
+  for (int64_t f = 0; f < gm.nf; ++f) {
+    if (gm.f_nb[f] >= 0) continue;
+    int64_t g = gm.ng++;
+    gm.f_ghost[f] = (int32_t)g;
+    gm.g_cell.push_back(gm.f_owner[f]);
+    gm.g_face.push_back(f);
+    gm.g_bc.push_back(gm.f_bc[f]);
+    P3 v[4];
+    for (int q = 0; q < nvf; ++q) v[q] = {gm.f_vert[12 * f + 3 * q], gm.f_vert[12 * f + 3 * q + 1], gm.f_vert[12 * f + 3 * q + 2]};
+    P3 gx[4], gn[4];
+    double gw[4];
+    int ngp = face_gps(nvf, v, gx, gn, gw);
+    P3 xf{0, 0, 0}, nf{0, 0, 0};
+    for (int q = 0; q < ngp; ++q) {
+      xf = xf + (gw[q] / gm.f_area[f]) * gx[q];
+      nf = nf + gw[q] * gn[q];
+    }
+    nf = (1.0 / len(nf)) * nf;
+    P3 ci = centroid(gm.f_owner[f]);
+    P3 cg = ci - (2.0 * dotp(ci - xf, nf)) * nf;
+    gm.gV.push_back(gm.V[gm.f_owner[f]]);
+    gm.gC.push_back(cg.x); gm.gC.push_back(cg.y); gm.gC.push_back(cg.z);
+    gm.g_normal.push_back(nf.x); gm.g_normal.push_back(nf.y); gm.g_normal.push_back(nf.z);
+    // reflected second moments R M2 R, R = I - 2 n n^T
+    const double* m = &gm.M2[6 * gm.f_owner[f]];
+    double S[3][3] = {{m[0], m[3], m[4]}, {m[3], m[1], m[5]}, {m[4], m[5], m[2]}};
+    double n3[3] = {nf.x, nf.y, nf.z}, R[3][3], T[3][3];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) R[a][b] = (a == b) - 2.0 * n3[a] * n3[b];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        double s = 0;
+        for (int k = 0; k < 3; ++k)
+          for (int l = 0; l < 3; ++l) s += R[a][k] * S[k][l] * R[b][l];
+        T[a][b] = s;
+      }
+    gm.gM2.push_back(T[0][0]); gm.gM2.push_back(T[1][1]); gm.gM2.push_back(T[2][2]);
+    gm.gM2.push_back(T[0][1]); gm.gM2.push_back(T[0][2]); gm.gM2.push_back(T[1][2]);
+  }
+  // ---------------- CellNeighbor and h for dt ----------------
+  gm.nbr_id.assign(n_cells * 6, -1);
+  gm.nbr_shift.assign(n_cells * 18, 0.0);
+  gm.h_dt.resize(n_cells);
+  for (int64_t i = 0; i < n_cells; ++i) {
+    double smax = 0;
+    for (int p = 0; p < nfc; ++p) {
+      int64_t f = gm.cell_face[i * 6 + p];
+      smax = std::max(smax, gm.f_area[f]);
+      double sg = 1.0;
+      int64_t other;
+      if (gm.f_nb[f] < 0) {
+        other = n_cells + gm.f_ghost[f];
+        sg = 0.0;
+      } else if (gm.f_owner[f] == i) {
+        other = gm.f_nb[f];
+      } else {
+        other = gm.f_owner[f];
+        sg = -1.0;
+      }
+      gm.nbr_id[i * 6 + p] = other;
+      for (int a = 0; a < 3; ++a) gm.nbr_shift[i * 18 + p * 3 + a] = sg * gm.f_shift[3 * f + a];
+    }
+    gm.h_dt[i] = gm.V[i] / smax;
+  }
+  // ---------------- Alg. 1 stencils + sub-stencils ----------------
+  gm.big_off.assign(n_cells + 1, 0);
+  std::vector<std::vector<Member>> big(n_cells);
+  gm.sub_slot.assign(n_cells * L.M * L.NM, (int8_t)-1);
+  int max_k = 0;
+  bool bad = false;
+  int64_t bad_cell = -1;
+  int bad_code = 0;
+#pragma omp parallel for schedule(dynamic, 256) reduction(max : max_k)
+  for (int64_t i = 0; i < n_cells; ++i) {
+    std::vector<Member>& S = big[i];
+    int err = 0;
+    auto add = [&](int64_t id, P3 s) {
+      if (id == i) {
+        if (!same_shift(s, {0, 0, 0})) err = 1;
+        return;
+      }
+      for (auto& m : S)
+        if (m.id == id) {
+          if (!same_shift(m.s, s)) err = 1;
+          return;
+        }
+      S.push_back({id, s});
+    };
+    auto nb = [&](int64_t c, int p) {
+      return Member{gm.nbr_id[c * 6 + p], {gm.nbr_shift[c * 18 + 3 * p], gm.nbr_shift[c * 18 + 3 * p + 1], gm.nbr_shift[c * 18 + 3 * p + 2]}};
+    };
+    for (int p = 0; p < nfc; ++p) {
+      Member m = nb(i, p);
+      add(m.id, m.s);
+    }
+    for (int p = 0; p < nfc; ++p) {
+      Member m = nb(i, p);
+      if (m.id >= n_cells) continue;  // ghosts have no neighbours
+      for (int q = 0; q < nfc; ++q) {
+        Member m2 = nb(m.id, q);
+        add(m2.id, m.s + m2.s);
+      }
+    }
+    if ((int)S.size() > kMaxStencil) err = 2;
+    auto slot_of = [&](int64_t id) -> int {
+      for (size_t k = 0; k < S.size(); ++k)
+        if (S[k].id == id) return (int)k;
+      return -1;
+    };
+    int8_t* ss = &gm.sub_slot[i * L.M * L.NM];
+    if (ct == 4) {
+      // R16: sub m = three face neighbours {T_m} + neighbours of i_m
+      const int tri[4][3] = {{0, 1, 2}, {0, 1, 3}, {1, 2, 3}, {2, 0, 3}};
+      for (int m = 0; m < 4; ++m) {
+        int cnt = 0;
+        auto put = [&](int64_t id) {
+          if (id == i) return;
+          int s = slot_of(id);
+          for (int k = 0; k < cnt; ++k)
+            if (ss[m * L.NM + k] == s) return;
+          if (cnt < L.NM) ss[m * L.NM + cnt++] = (int8_t)s;
+          else err = 3;
+        };
+        for (int k = 0; k < 3; ++k) put(gm.nbr_id[i * 6 + tri[m][k]]);
+        int64_t im = gm.nbr_id[i * 6 + m];
+        if (im < n_cells)
+          for (int q = 0; q < 4; ++q) put(gm.nbr_id[im * 6 + q]);
+      }
+    } else {
+      const int hs[8][3] = {{0, 1, 2}, {0, 2, 3}, {0, 3, 4}, {0, 4, 1}, {5, 1, 2}, {5, 2, 3}, {5, 3, 4}, {5, 4, 1}};
+      for (int m = 0; m < 8; ++m)
+        for (int k = 0; k < 3; ++k) ss[m * 3 + k] = (int8_t)slot_of(gm.nbr_id[i * 6 + hs[m][k]]);
+    }
+    if (err) {
+#pragma omp critical
+      {
+        bad = true;
+        if (bad_cell < 0 || i < bad_cell) {
+          bad_cell = i;
+          bad_code = err;
+        }
+      }
+    }
+    max_k = std::max(max_k, (int)S.size());
+  }
+  if (bad)
+    throw Error(2, bad_code == 1 ? "periodic box too small for the two-layer stencil at cell " + std::to_string(bad_cell)
+                                 : "stencil capacity exceeded at cell " + std::to_string(bad_cell));
+  for (int64_t i = 0; i < n_cells; ++i) gm.big_off[i + 1] = gm.big_off[i] + (int64_t)big[i].size();
+  gm.big_id.resize(gm.big_off[n_cells]);
+  gm.big_shift.resize(3 * gm.big_off[n_cells]);
+  for (int64_t i = 0; i < n_cells; ++i)
+    for (size_t k = 0; k < big[i].size(); ++k) {
+      int64_t o = gm.big_off[i] + (int64_t)k;
+      gm.big_id[o] = big[i][k].id;
+      gm.big_shift[3 * o] = big[i][k].s.x; gm.big_shift[3 * o + 1] = big[i][k].s.y; gm.big_shift[3 * o + 2] = big[i][k].s.z;
+    }
+  {
+    // pad the stencil width to a capacity the reconstruction kernel is compiled for
+    const int caps[] = {14, 16, 20, 24, 32, 40};
+    L.K = 40;
+    for (int c : caps)
+      if (c >= max_k) {
+        L.K = c;
+        break;
+      }
+  }
+  // ---------------- least-squares operators (a2) ----------------
+  const int E = L.op_entries();
+  gm.op.assign((size_t)n_cells * E, 0.0);
+  int64_t lsq_bad = -1;
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int64_t i = 0; i < n_cells; ++i) {
+    const int64_t o0 = gm.big_off[i];
+    const int K = (int)(gm.big_off[i + 1] - o0);
+    const double Vi = gm.V[i];
+    const double h = std::cbrt(Vi);
+    P3 ci = centroid(i);
+    const double* mi = &gm.M2[6 * i];
+    // rows: member image centroid offset D and zero-mean quadratic moments (A.4)
+    std::vector<double> A(K * 9);
+    for (int k = 0; k < K; ++k) {
+      int64_t id = gm.big_id[o0 + k];
+      P3 ck;
+      const double* mk;
+      if (id < n_cells) {
+        ck = centroid(id);
+        mk = &gm.M2[6 * id];
+      } else {
+        int64_t g = id - n_cells;
+        ck = {gm.gC[3 * g], gm.gC[3 * g + 1], gm.gC[3 * g + 2]};
+        mk = &gm.gM2[6 * g];
+      }
+      P3 D = (ck + P3{gm.big_shift[3 * (o0 + k)], gm.big_shift[3 * (o0 + k) + 1], gm.big_shift[3 * (o0 + k) + 2]}) - ci;
+      double* r = &A[k * 9];
+      r[0] = D.x / h; r[1] = D.y / h; r[2] = D.z / h;
+      const double h2 = h * h;
+      r[3] = (mk[0] + D.x * D.x - mi[0]) / h2;
+      r[4] = (mk[1] + D.y * D.y - mi[1]) / h2;
+      r[5] = (mk[2] + D.z * D.z - mi[2]) / h2;
+      r[6] = (mk[3] + D.x * D.y - mi[3]) / h2;
+      r[7] = (mk[4] + D.x * D.z - mi[4]) / h2;
+      r[8] = (mk[5] + D.y * D.z - mi[5]) / h2;
+    }
+    double* op = &gm.op[(size_t)i * E];
+    std::vector<double> P(9 * K);
+    bool ok = K >= 9 && pinv_qr(K, 9, A.data(), P.data());
+    if (ok)
+      for (int d = 0; d < 9; ++d)
+        for (int k = 0; k < K; ++k) op[d * L.K + k] = P[d * K + k] / (d < 3 ? h : h * h);
+    const int8_t* ss = &gm.sub_slot[i * L.M * L.NM];
+    for (int m = 0; m < L.M && ok; ++m) {
+      int n = 0;
+      double As[3 * 8];
+      int slots[8];
+      for (int j = 0; j < L.NM; ++j)
+        if (ss[m * L.NM + j] >= 0) {
+          slots[n] = ss[m * L.NM + j];
+          for (int a = 0; a < 3; ++a) As[n * 3 + a] = A[slots[n] * 9 + a];
+          ++n;
+        }
+      double Ps[3 * 8];
+      if (n < 3 || !pinv_qr(n, 3, As, Ps)) {
+        ok = false;
+        break;
+      }
+      double* om = op + 9 * L.K + m * 3 * L.NM;
+      for (int d = 0; d < 3; ++d)
+        for (int j = 0; j < n; ++j) om[d * L.NM + j] = Ps[d * n + j] / h;
+    }
+    if (!ok) {
+#pragma omp critical
+      if (lsq_bad < 0 || i < lsq_bad) lsq_bad = i;
+    }
+  }
+  if (lsq_bad >= 0) throw Error(3, "rank-deficient least-squares stencil at cell " + std::to_string(lsq_bad));
+  // ---------------- partition (a3) ----------------
+  gm.n_ranks = std::max(1, n_ranks);
+  gm.part.assign(n_cells, 0);
+  if (gm.n_ranks > 1) {
+    if (cell_part) {
+      for (int64_t i = 0; i < n_cells; ++i) {
+        if (cell_part[i] < 0 || cell_part[i] >= gm.n_ranks) throw Error(1, "cell_part out of range at cell " + std::to_string(i));
+        gm.part[i] = cell_part[i];
+      }
+    } else {
+      // recursive coordinate bisection on centroids (P:730-739 objective: balance,
+      // small interfaces); splits proportional to the rank counts on each side
+      std::vector<int64_t> ids(n_cells);
+      std::iota(ids.begin(), ids.end(), 0);
+      struct Task {
+        int64_t b, e;
+        int r0, nr;
+      };
+      std::vector<Task> st{{0, n_cells, 0, gm.n_ranks}};
+      while (!st.empty()) {
+        Task t = st.back();
+        st.pop_back();
+        if (t.nr == 1) {
+          for (int64_t k = t.b; k < t.e; ++k) gm.part[ids[k]] = t.r0;
+          continue;
+        }
+        double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+        for (int64_t k = t.b; k < t.e; ++k)
+          for (int a = 0; a < 3; ++a) {
+            lo[a] = std::min(lo[a], gm.C[3 * ids[k] + a]);
+            hi[a] = std::max(hi[a], gm.C[3 * ids[k] + a]);
+          }
+        int ax = 0;
+        for (int a = 1; a < 3; ++a)
+          if (hi[a] - lo[a] > hi[ax] - lo[ax] + 1e-12) ax = a;
+        int nl = t.nr / 2;
+        int64_t cut = t.b + (t.e - t.b) * nl / t.nr;
+        std::nth_element(ids.begin() + t.b, ids.begin() + cut, ids.begin() + t.e, [&](int64_t a, int64_t b) {
+          double xa = gm.C[3 * a + ax], xb = gm.C[3 * b + ax];
+          return xa != xb ? xa < xb : a < b;
+        });
+        st.push_back({t.b, cut, t.r0, nl});
+        st.push_back({cut, t.e, t.r0 + nl, t.nr - nl});
+      }
+    }
+    for (int64_t f = 0; f < gm.nf; ++f)
+      if (gm.f_nb[f] >= 0 && gm.part[gm.f_owner[f]] != gm.part[gm.f_nb[f]]) ++gm.edge_cut;
+  }
+  return gm;
+}
+
+// ============================================================================
+// Per-rank plan: owned cells (Morton order), 3 ghost layers grouped by owner
+// rank, device arrays in entry-major layout.
+RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
+  const Layout& L = gm.lay;
+  const int64_t nc = gm.nc;
+  RankPlan rp;
+  rp.rank = rank;
+  std::vector<int64_t> owned;
+  for (int64_t i = 0; i < nc; ++i)
+    if (gm.part[i] == rank) owned.push_back(i);
+  if (owned.empty()) throw Error(1, "rank " + std::to_string(rank) + " owns no cells");
+  // Morton order over the global bounding box of centroids
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (int64_t i = 0; i < nc; ++i)
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = std::min(lo[a], gm.C[3 * i + a]);
+      hi[a] = std::max(hi[a], gm.C[3 * i + a]);
+    }
+  auto morton = [&](int64_t i) {
+    uint64_t k = 0;
+    for (int a = 0; a < 3; ++a) {
+      double s = hi[a] > lo[a] ? (gm.C[3 * i + a] - lo[a]) / (hi[a] - lo[a]) : 0.0;
+      uint64_t q = (uint64_t)std::min(2097151.0, std::max(0.0, s * 2097151.0));
+      k |= spread21(q) << a;
+    }
+    return k;
+  };
+  std::vector<uint64_t> mk(nc);
+  for (int64_t i = 0; i < nc; ++i) mk[i] = morton(i);
+  auto by_morton = [&](int64_t a, int64_t b) { return mk[a] != mk[b] ? mk[a] < mk[b] : a < b; };
+  std::sort(owned.begin(), owned.end(), by_morton);
+  rp.n_owned = (int64_t)owned.size();
+  // ghost layers by face adjacency (BC ghosts excluded)
+  std::vector<int8_t> layer(nc, -1);  // 0 owned, 1..3 ghost layers
+  for (int64_t i : owned) layer[i] = 0;
+  std::vector<int64_t> frontier = owned;
+  std::vector<std::vector<int64_t>> ghosts(3);
+  for (int l = 1; l <= 3 && gm.n_ranks > 1; ++l) {
+    std::vector<int64_t> next;
+    for (int64_t i : frontier)
+      for (int p = 0; p < L.nfaces; ++p) {
+        int64_t j = gm.nbr_id[i * 6 + p];
+        if (j < nc && layer[j] < 0) {
+          layer[j] = (int8_t)l;
+          next.push_back(j);
+        }
+      }
+    ghosts[l - 1] = next;
+    rp.ghost_layer[l - 1] = (int64_t)next.size();
+    frontier.swap(next);
+  }
+  // partition ghosts grouped by owner rank, then layer, then global id
+  std::vector<int64_t> pg;
+  for (auto& g : ghosts) pg.insert(pg.end(), g.begin(), g.end());
+  std::sort(pg.begin(), pg.end(), [&](int64_t a, int64_t b) {
+    if (gm.part[a] != gm.part[b]) return gm.part[a] < gm.part[b];
+    return a < b;  // global-id order == the owner's send order
+  });
+  rp.n_pghost = (int64_t)pg.size();
+  rp.l2g = owned;
+  rp.l2g.insert(rp.l2g.end(), pg.begin(), pg.end());
+  std::unordered_map<int64_t, int32_t> g2l;
+  g2l.reserve(rp.l2g.size() * 2);
+  for (size_t k = 0; k < rp.l2g.size(); ++k) g2l[rp.l2g[k]] = (int32_t)k;
+  // recon set = owned + layer-1 ghosts
+  rp.recon_cell.resize(rp.n_owned);
+  std::iota(rp.recon_cell.begin(), rp.recon_cell.end(), 0);
+  for (int64_t g : pg)
+    if (layer[g] == 1) rp.recon_cell.push_back(g2l[g]);
+  rp.n_recon = (int64_t)rp.recon_cell.size();
+  // BC ghosts needed: those of faces of recon cells and of their neighbours
+  std::unordered_map<int64_t, int32_t> bg2l;
+  auto local_of = [&](int64_t id) -> int32_t {
+    if (id < nc) {
+      auto it = g2l.find(id);
+      if (it == g2l.end()) throw Error(1, "ghost closure violated for cell " + std::to_string(id));
+      return it->second;
+    }
+    auto it = bg2l.find(id - nc);
+    if (it != bg2l.end()) return it->second;
+    int32_t l = (int32_t)(rp.n_owned + rp.n_pghost + (int64_t)bg2l.size());
+    bg2l[id - nc] = l;
+    int64_t g = id - nc;
+    rp.bg_cell.push_back(-1);  // resolved below
+    rp.bg_bc.push_back(gm.g_bc[g]);
+    rp.bg_normal.push_back(gm.g_normal[3 * g]);
+    rp.bg_normal.push_back(gm.g_normal[3 * g + 1]);
+    rp.bg_normal.push_back(gm.g_normal[3 * g + 2]);
+    return l;
+  };
+  const int K = L.K, M = L.M, NM = L.NM, E = L.op_entries();
+  const int64_t R = rp.n_recon;
+  rp.st_id.assign((size_t)K * R, 0);
+  rp.sub_slot.assign((size_t)M * NM * R, 0);
+  rp.op.assign((size_t)E * R, 0.0);
+  rp.geo.assign((size_t)8 * R, 0.0);
+  rp.stencil_min = 1 << 30;
+  rp.stencil_max = 0;
+  for (int64_t r = 0; r < R; ++r) {
+    int64_t gi = rp.l2g[rp.recon_cell[r]];
+    int64_t o0 = gm.big_off[gi];
+    int kk = (int)(gm.big_off[gi + 1] - o0);
+    if (r < rp.n_owned) {
+      rp.stencil_min = std::min(rp.stencil_min, kk);
+      rp.stencil_max = std::max(rp.stencil_max, kk);
+    }
+    for (int k = 0; k < K; ++k)
+      rp.st_id[(size_t)k * R + r] = k < kk ? local_of(gm.big_id[o0 + k]) : rp.recon_cell[r];
+    for (int s = 0; s < M * NM; ++s) {
+      int8_t v = gm.sub_slot[gi * M * NM + s];
+      rp.sub_slot[(size_t)s * R + r] = (uint8_t)(v < 0 ? 0 : v);
+    }
+    const double* op = &gm.op[(size_t)gi * E];
+    for (int e = 0; e < E; ++e) rp.op[(size_t)e * R + r] = op[e];
+    double V = gm.V[gi];
+    rp.geo[0 * R + r] = std::pow(V, 2.0 / 3.0);
+    rp.geo[1 * R + r] = std::pow(V, 4.0 / 3.0);
+    for (int k = 0; k < 6; ++k) rp.geo[(2 + k) * R + r] = gm.M2[6 * gi + k];
+  }
+  // faces computed by this rank: every face of an owned cell
+  std::vector<int64_t> fl;
+  {
+    std::vector<char> seen(gm.nf, 0);
+    for (int64_t i : owned)
+      for (int p = 0; p < L.nfaces; ++p) {
+        int64_t f = gm.cell_face[i * 6 + p];
+        if (!seen[f]) {
+          seen[f] = 1;
+          fl.push_back(f);
+        }
+      }
+  }
+  for (int64_t f : fl)
+    if (gm.f_nb[f] < 0) local_of(nc + gm.f_ghost[f]);
+  // order: interior faces by min local endpoint, then wall, then farfield
+  auto fkey = [&](int64_t f) -> std::pair<int, int64_t> {
+    int cls = gm.f_nb[f] >= 0 ? 0 : (gm.f_bc[f] == 1 ? 1 : 2);
+    int64_t a = g2l[gm.f_owner[f]];
+    int64_t b = gm.f_nb[f] >= 0 ? g2l[gm.f_nb[f]] : a;
+    return {cls, std::min(a, b) * 8 + 0};
+  };
+  std::stable_sort(fl.begin(), fl.end(), [&](int64_t a, int64_t b) { return fkey(a) < fkey(b); });
+  rp.n_faces = (int64_t)fl.size();
+  for (int64_t f : fl) {
+    if (gm.f_nb[f] >= 0) ++rp.n_if;
+    else if (gm.f_bc[f] == 1) ++rp.n_wf;
+    else ++rp.n_ff;
+  }
+  rp.f_geo_stride = 3 * L.nv + 3;
+  rp.f_cells.resize(2 * rp.n_faces);
+  rp.f_geo.assign((size_t)rp.f_geo_stride * rp.n_faces, 0.0);
+  std::unordered_map<int64_t, int32_t> f2l;
+  for (int64_t k = 0; k < rp.n_faces; ++k) {
+    int64_t f = fl[k];
+    f2l[f] = (int32_t)k;
+    int64_t o = gm.f_owner[f];
+    rp.f_cells[2 * k] = g2l[o];
+    rp.f_cells[2 * k + 1] = gm.f_nb[f] >= 0 ? g2l[gm.f_nb[f]] : local_of(nc + gm.f_ghost[f]);
+    double* fg = &rp.f_geo[(size_t)rp.f_geo_stride * k];
+    for (int q = 0; q < L.nv; ++q)
+      for (int a = 0; a < 3; ++a) fg[3 * q + a] = gm.f_vert[12 * f + 3 * q + a] - gm.C[3 * o + a];
+    // d = c_owner - (c_nb + shift): the neighbour evaluates at r_l + d
+    if (gm.f_nb[f] >= 0)
+      for (int a = 0; a < 3; ++a) fg[3 * L.nv + a] = gm.C[3 * o + a] - (gm.C[3 * gm.f_nb[f] + a] + gm.f_shift[3 * f + a]);
+  }
+  // update arrays
+  rp.cf.assign((size_t)L.nfaces * rp.n_owned, 0);
+  rp.inv_v.resize(rp.n_owned);
+  rp.h_dt.resize(rp.n_owned);
+  for (int64_t r = 0; r < rp.n_owned; ++r) {
+    int64_t gi = owned[r];
+    for (int p = 0; p < L.nfaces; ++p) {
+      int64_t f = gm.cell_face[gi * 6 + p];
+      int32_t lf = f2l[f];
+      rp.cf[(size_t)p * rp.n_owned + r] = gm.f_owner[f] == gi ? lf : ~lf;
+    }
+    rp.inv_v[r] = 1.0 / gm.V[gi];
+    rp.h_dt[r] = gm.h_dt[gi];
+  }
+  // resolve BC ghost interior cells (must be local)
+  for (auto& kv : bg2l) {
+    int64_t g = kv.first;
+    rp.bg_cell[kv.second - (rp.n_owned + rp.n_pghost)] = local_of(gm.g_cell[g]);
+  }
+  rp.n_bghost = (int64_t)bg2l.size();
+  // exchange plan: peers = owner ranks of my ghosts, and ranks that ghost my cells
+  if (gm.n_ranks > 1) {
+    std::vector<std::vector<int32_t>> sends(gm.n_ranks);
+    // cells I own that appear in another rank's 3-layer closure
+    std::vector<std::vector<char>> want(gm.n_ranks);
+    for (int q = 0; q < gm.n_ranks; ++q) {
+      if (q == rank) continue;
+      // BFS from q's owned cells, 3 layers
+      std::vector<int8_t> lay(nc, -1);
+      std::vector<int64_t> fr;
+      for (int64_t i = 0; i < nc; ++i)
+        if (gm.part[i] == q) {
+          lay[i] = 0;
+          fr.push_back(i);
+        }
+      for (int l = 1; l <= 3; ++l) {
+        std::vector<int64_t> nx;
+        for (int64_t i : fr)
+          for (int p = 0; p < L.nfaces; ++p) {
+            int64_t j = gm.nbr_id[i * 6 + p];
+            if (j < nc && lay[j] < 0) {
+              lay[j] = (int8_t)l;
+              nx.push_back(j);
+            }
+          }
+        fr.swap(nx);
+      }
+      std::vector<int64_t> mine;
+      for (int64_t i = 0; i < nc; ++i)
+        if (lay[i] > 0 && gm.part[i] == rank) mine.push_back(i);
+      std::sort(mine.begin(), mine.end());
+      for (int64_t i : mine) sends[q].push_back(g2l[i]);
+    }
+    for (int q = 0; q < gm.n_ranks; ++q) {
+      if (q == rank) continue;
+      int64_t off = -1, cnt = 0;
+      for (int64_t k = 0; k < rp.n_pghost; ++k)
+        if (gm.part[pg[k]] == q) {
+          if (off < 0) off = rp.n_owned + k;
+          ++cnt;
+        }
+      if (cnt == 0 && sends[q].empty()) continue;
+      rp.peers.push_back(q);
+      rp.send_off.push_back((int64_t)rp.send_list.size());
+      rp.send_cnt.push_back((int64_t)sends[q].size());
+      rp.send_list.insert(rp.send_list.end(), sends[q].begin(), sends[q].end());
+      rp.recv_off.push_back(off < 0 ? rp.n_owned : off);
+      rp.recv_cnt.push_back(cnt);
+    }
+  }
+  return rp;
+}
+
+}  // namespace hgks

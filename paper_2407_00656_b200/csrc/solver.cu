@@ -1,0 +1,732 @@
+// Device runtime and C-ABI of libhgks (include/hgks.h).
+//
+// One solver per process/GPU.  The caller owns device memory (a workspace
+// carved here) and the stream; NCCL (loaded at run time with dlopen, only when
+// n_ranks > 1) carries the per-stage halo exchange and the per-step min(dt).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/hgks.h"
+#include "internal.h"
+#include "kernels.cuh"
+
+using namespace hgks;
+
+// ============================================================================
+// errors
+// ============================================================================
+static thread_local std::string g_last_error;
+
+#define CUDA_TRY(x)                                                                                    \
+  do {                                                                                                 \
+    cudaError_t e_ = (x);                                                                              \
+    if (e_ != cudaSuccess) throw Error(HGKS_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <class F>
+static hgks_status guard(F&& f) {
+  try {
+    f();
+    return HGKS_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return HGKS_E_ARG;
+  } catch (...) {
+    g_last_error = "unknown error";
+    return HGKS_E_ARG;
+  }
+}
+
+// ============================================================================
+// NCCL, resolved at run time (no link-time dependency for single-GPU use)
+// ============================================================================
+namespace {
+typedef struct ncclComm* ncclComm_t;
+typedef struct {
+  char internal[128];
+} ncclUniqueId;
+enum { ncclUint64 = 5, ncclFloat64 = 8 };
+enum { ncclMin = 3 };
+struct Nccl {
+  void* h = nullptr;
+  int (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  int (*CommDestroy)(ncclComm_t) = nullptr;
+  int (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  int (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+};
+Nccl& nccl() {
+  static Nccl n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* nm : names) {
+      n.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+      if (n.h) break;
+    }
+    if (!n.h) return;
+    n.CommInitRank = (decltype(n.CommInitRank))dlsym(n.h, "ncclCommInitRank");
+    n.CommDestroy = (decltype(n.CommDestroy))dlsym(n.h, "ncclCommDestroy");
+    n.Send = (decltype(n.Send))dlsym(n.h, "ncclSend");
+    n.Recv = (decltype(n.Recv))dlsym(n.h, "ncclRecv");
+    n.AllReduce = (decltype(n.AllReduce))dlsym(n.h, "ncclAllReduce");
+    n.GroupStart = (decltype(n.GroupStart))dlsym(n.h, "ncclGroupStart");
+    n.GroupEnd = (decltype(n.GroupEnd))dlsym(n.h, "ncclGroupEnd");
+    n.GetErrorString = (decltype(n.GetErrorString))dlsym(n.h, "ncclGetErrorString");
+  });
+  return n;
+}
+#define NCCL_TRY(x)                                                                                              \
+  do {                                                                                                           \
+    int r_ = (x);                                                                                                \
+    if (r_ != 0)                                                                                                 \
+      throw Error(HGKS_E_NCCL, std::string(#x) + ": " + (nccl().GetErrorString ? nccl().GetErrorString(r_) : "")); \
+  } while (0)
+}  // namespace
+
+// ============================================================================
+// mesh handle
+// ============================================================================
+struct hgks_mesh {
+  GlobalMesh gm;
+  std::map<int, std::unique_ptr<RankPlan>> plans;
+  std::mutex mu;
+  const RankPlan& plan(int rank) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (rank < 0 || rank >= gm.n_ranks) throw Error(HGKS_E_ARG, "rank out of range");
+    auto it = plans.find(rank);
+    if (it == plans.end()) it = plans.emplace(rank, std::make_unique<RankPlan>(build_rank_plan(gm, rank))).first;
+    return *it->second;
+  }
+};
+
+// ============================================================================
+// workspace layout
+// ============================================================================
+namespace {
+struct Carve {
+  char* base;
+  size_t off = 0, cap;
+  template <class T>
+  T* take(size_t n) {
+    off = (off + 255) & ~size_t(255);
+    size_t bytes = n * sizeof(T);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += bytes;
+    if (base && off > cap) throw Error(HGKS_E_ARG, "workspace too small");
+    return p;
+  }
+};
+
+int round32(int64_t n) { return (int)((n + 31) / 32 * 32); }
+
+struct DevArrays {
+  double *Q, *Qtmp, *R, *ceff, *F1, *F2, *op, *geo, *f_geo, *inv_v, *h_dt, *bg_normal, *sendbuf, *stage_in, *stage_out,
+      *Lbuf;
+  int *recon_cell, *st_id, *f_cells, *cf, *bg_cell, *bg_bc, *send_list, *out_local;
+  int64_t* in_row;
+  uint8_t* sub_slot;
+  Ctrl* ctrl;
+};
+
+size_t layout(const GlobalMesh& gm, const RankPlan& rp, Carve& c, DevArrays& d) {
+  const Layout& L = gm.lay;
+  const int ldq = round32(rp.n_local());
+  const int64_t ncl = rp.n_owned + rp.n_pghost;
+  d.ctrl = c.take<Ctrl>(1);
+  d.Q = c.take<double>((size_t)5 * ldq);
+  d.Qtmp = c.take<double>((size_t)5 * ldq);
+  d.R = c.take<double>((size_t)5 * rp.n_owned);
+  d.ceff = c.take<double>((size_t)kRec * ncl);
+  d.F1 = c.take<double>((size_t)10 * rp.n_faces);
+  d.F2 = c.take<double>((size_t)5 * rp.n_faces);
+  d.recon_cell = c.take<int>(rp.n_recon);
+  d.st_id = c.take<int>((size_t)L.K * rp.n_recon);
+  d.sub_slot = c.take<uint8_t>((size_t)L.M * L.NM * rp.n_recon);
+  d.op = c.take<double>((size_t)L.op_entries() * rp.n_recon);
+  d.geo = c.take<double>((size_t)8 * rp.n_recon);
+  d.f_cells = c.take<int>((size_t)2 * rp.n_faces);
+  d.f_geo = c.take<double>((size_t)rp.f_geo_stride * rp.n_faces);
+  d.cf = c.take<int>((size_t)L.nfaces * rp.n_owned);
+  d.inv_v = c.take<double>(rp.n_owned);
+  d.h_dt = c.take<double>(rp.n_owned);
+  d.bg_cell = c.take<int>(std::max<int64_t>(1, rp.n_bghost));
+  d.bg_bc = c.take<int>(std::max<int64_t>(1, rp.n_bghost));
+  d.bg_normal = c.take<double>(std::max<int64_t>(3, 3 * rp.n_bghost));
+  d.send_list = c.take<int>(std::max<size_t>(1, rp.send_list.size()));
+  d.sendbuf = c.take<double>(std::max<size_t>(5, 5 * rp.send_list.size()));
+  d.out_local = c.take<int>(rp.n_owned);
+  d.in_row = c.take<int64_t>(rp.n_owned);
+  // staging for set/get_state: single rank copies the caller's whole array
+  const int64_t n_in = gm.n_ranks == 1 ? gm.nc : rp.n_owned;
+  d.stage_in = c.take<double>((size_t)5 * n_in);
+  d.stage_out = c.take<double>((size_t)5 * rp.n_owned);
+  d.Lbuf = c.take<double>((size_t)10 * rp.n_owned);
+  return c.off + 256;
+}
+}  // namespace
+
+// ============================================================================
+// solver
+// ============================================================================
+struct KStat {
+  int64_t launches = 0;
+  double ms = 0.0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+};
+
+struct hgks_solver {
+  hgks_mesh* mesh;
+  const RankPlan* rp;
+  Layout lay;
+  hgks_config cfg;
+  GasParams gp;
+  int rank = 0, n_ranks = 1, device = 0;
+  cudaStream_t stream = nullptr;
+  DevArrays d{};
+  int ldq = 0;
+  ncclComm_t comm = nullptr;
+  int64_t launches = 0;
+  bool profiling = false;
+  std::map<std::string, KStat> kstat;
+  std::vector<int> peers;
+  std::vector<double> host_stage;  // multi-rank set_state gather
+  double* pinned = nullptr;
+};
+
+namespace {
+
+void record_launch(hgks_solver* s, const char* name, cudaEvent_t a, cudaEvent_t b) {
+  KStat& k = s->kstat[name];
+  k.launches++;
+  if (a) k.pending.push_back({a, b});
+}
+
+template <class Launch>
+void launch(hgks_solver* s, const char* name, Launch&& fn) {
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (s->profiling) {
+    CUDA_TRY(cudaEventCreate(&a));
+    CUDA_TRY(cudaEventCreate(&b));
+    CUDA_TRY(cudaEventRecord(a, s->stream));
+  }
+  fn();
+  CUDA_TRY(cudaGetLastError());
+  if (s->profiling) CUDA_TRY(cudaEventRecord(b, s->stream));
+  s->launches++;
+  record_launch(s, name, a, b);
+}
+
+inline int blocks(int64_t n, int b) { return (int)((n + b - 1) / b); }
+
+template <int K, int M, int NM, int B>
+void run_recon_k(hgks_solver* s, const ReconArgs& a) {
+  const size_t smem = (size_t)M * 15 * B * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(k_recon<K, M, NM, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  launch(s, "k_recon", [&] { k_recon<K, M, NM, B><<<blocks(a.n_recon, B), B, smem, s->stream>>>(a); });
+}
+
+void run_recon(hgks_solver* s, const double* Q) {
+  const Layout& L = s->lay;
+  ReconArgs a;
+  a.Q = Q;
+  a.ldq = s->ldq;
+  a.n_recon = (int)s->rp->n_recon;
+  a.recon_cell = s->d.recon_cell;
+  a.st_id = s->d.st_id;
+  a.sub_slot = s->d.sub_slot;
+  a.op = s->d.op;
+  a.geo = s->d.geo;
+  a.ceff = s->d.ceff;
+  a.eps = s->cfg.eps;
+  a.omega_pow = s->cfg.omega_pow;
+  if (L.cell_type == 4) {
+    switch (L.K) {
+      case 14: run_recon_k<14, 4, 6, 128>(s, a); break;
+      case 16: run_recon_k<16, 4, 6, 128>(s, a); break;
+      case 20: run_recon_k<20, 4, 6, 128>(s, a); break;
+      case 24: run_recon_k<24, 4, 6, 128>(s, a); break;
+      case 32: run_recon_k<32, 4, 6, 128>(s, a); break;
+      default: run_recon_k<40, 4, 6, 128>(s, a); break;
+    }
+  } else {
+    switch (L.K) {
+      case 14: run_recon_k<14, 8, 3, 64>(s, a); break;
+      case 16: run_recon_k<16, 8, 3, 64>(s, a); break;
+      case 20: run_recon_k<20, 8, 3, 64>(s, a); break;
+      case 24: run_recon_k<24, 8, 3, 64>(s, a); break;
+      case 32: run_recon_k<32, 8, 3, 64>(s, a); break;
+      default: run_recon_k<40, 8, 3, 64>(s, a); break;
+    }
+  }
+}
+
+void run_flux(hgks_solver* s, const double* Q, int stage) {
+  const RankPlan& rp = *s->rp;
+  FluxArgs a;
+  a.Q = Q;
+  a.ldq = s->ldq;
+  a.ceff = s->d.ceff;
+  a.f_cells = s->d.f_cells;
+  a.f_geo = s->d.f_geo;
+  a.f_stride = rp.f_geo_stride;
+  a.n_faces = (int)rp.n_if;
+  a.face0 = 0;
+  a.F1 = s->d.F1;
+  a.F2 = s->d.F2;
+  a.ctrl = s->d.ctrl;
+  a.gamma = s->cfg.gamma;
+  a.K = (5.0 - 3.0 * s->cfg.gamma) / (s->cfg.gamma - 1.0);
+  if (s->cfg.tau_mode != 0) throw Error(HGKS_E_ARG, "tau_mode 1 (Navier-Stokes collision time) is not built yet");
+  if (rp.n_wf + rp.n_ff > 0) throw Error(HGKS_E_ARG, "wall/farfield faces are not built yet");
+  if (a.n_faces == 0) return;
+  if (s->lay.nv == 3) {
+    int nb = blocks((int64_t)a.n_faces * 3, 96);
+    if (stage == 1) launch(s, "k_flux_tau0_s1", [&] { k_flux_tau0<3, 1><<<nb, 96, 0, s->stream>>>(a); });
+    else launch(s, "k_flux_tau0_s2", [&] { k_flux_tau0<3, 2><<<nb, 96, 0, s->stream>>>(a); });
+  } else {
+    int nb = blocks((int64_t)a.n_faces * 4, 128);
+    if (stage == 1) launch(s, "k_flux_tau0_s1", [&] { k_flux_tau0<4, 1><<<nb, 128, 0, s->stream>>>(a); });
+    else launch(s, "k_flux_tau0_s2", [&] { k_flux_tau0<4, 2><<<nb, 128, 0, s->stream>>>(a); });
+  }
+}
+
+UpdateArgs update_args(hgks_solver* s) {
+  UpdateArgs u;
+  u.Q = s->d.Q;
+  u.ldq = s->ldq;
+  u.R = s->d.R;
+  u.F1 = s->d.F1;
+  u.F2 = s->d.F2;
+  u.cf = s->d.cf;
+  u.inv_v = s->d.inv_v;
+  u.h_dt = s->d.h_dt;
+  u.n_owned = (int)s->rp->n_owned;
+  u.ctrl = s->d.ctrl;
+  u.gp = s->gp;
+  return u;
+}
+
+void exchange(hgks_solver* s, double* Q) {
+  const RankPlan& rp = *s->rp;
+  if (s->n_ranks == 1 || rp.peers.empty()) return;
+  const int ns = (int)rp.send_list.size();
+  if (ns > 0)
+    launch(s, "k_pack", [&] { k_pack<<<blocks(ns, 256), 256, 0, s->stream>>>(Q, s->ldq, s->d.send_list, ns, s->d.sendbuf); });
+  Nccl& N = nccl();
+  NCCL_TRY(N.GroupStart());
+  for (size_t p = 0; p < rp.peers.size(); ++p) {
+    for (int v = 0; v < 5; ++v) {
+      if (rp.send_cnt[p] > 0)
+        NCCL_TRY(N.Send(s->d.sendbuf + (size_t)v * ns + rp.send_off[p], (size_t)rp.send_cnt[p], ncclFloat64,
+                        rp.peers[p], s->comm, s->stream));
+      if (rp.recv_cnt[p] > 0)
+        NCCL_TRY(N.Recv(Q + (size_t)v * s->ldq + rp.recv_off[p], (size_t)rp.recv_cnt[p], ncclFloat64, rp.peers[p],
+                        s->comm, s->stream));
+    }
+  }
+  NCCL_TRY(N.GroupEnd());
+}
+
+void allreduce_dt(hgks_solver* s) {
+  if (s->n_ranks == 1) return;
+  NCCL_TRY(nccl().AllReduce(&s->d.ctrl->dtmin_bits, &s->d.ctrl->dtmin_bits, 1, ncclUint64, ncclMin, s->comm,
+                            s->stream));
+}
+
+void bc_ghosts(hgks_solver* s, double* Q) {
+  const RankPlan& rp = *s->rp;
+  if (rp.n_bghost == 0) return;
+  const int first = (int)(rp.n_owned + rp.n_pghost);
+  launch(s, "k_bc_ghosts", [&] {
+    k_bc_ghosts<<<blocks(rp.n_bghost, 128), 128, 0, s->stream>>>(Q, s->ldq, first, (int)rp.n_bghost, s->d.bg_cell,
+                                                                  s->d.bg_bc, s->d.bg_normal, s->gp);
+  });
+}
+
+void stage(hgks_solver* s, int st) {
+  exchange(s, s->d.Q);
+  bc_ghosts(s, s->d.Q);
+  run_recon(s, s->d.Q);
+  run_flux(s, s->d.Q, st);
+  UpdateArgs u = update_args(s);
+  const int n = (int)s->rp->n_owned;
+  const int nf = s->lay.nfaces;
+  if (st == 1) {
+    if (nf == 4) launch(s, "k_update1", [&] { k_update1<4><<<blocks(n, 256), 256, 0, s->stream>>>(u); });
+    else launch(s, "k_update1", [&] { k_update1<6><<<blocks(n, 256), 256, 0, s->stream>>>(u); });
+  } else {
+    if (nf == 4) launch(s, "k_update2", [&] { k_update2<4><<<blocks(n, 256), 256, 0, s->stream>>>(u); });
+    else launch(s, "k_update2", [&] { k_update2<6><<<blocks(n, 256), 256, 0, s->stream>>>(u); });
+    allreduce_dt(s);
+  }
+}
+
+void init_dt(hgks_solver* s) {
+  Ctrl h;
+  CUDA_TRY(cudaMemcpyAsync(&h, s->d.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  h.dtmin_bits = 0x7fefffffffffffffull;
+  CUDA_TRY(cudaMemcpyAsync(s->d.ctrl, &h, sizeof(Ctrl), cudaMemcpyHostToDevice, s->stream));
+  const int n = (int)s->rp->n_owned;
+  launch(s, "k_dt_init", [&] {
+    k_dt_init<<<blocks(n, 256), 256, 0, s->stream>>>(s->d.Q, s->ldq, s->d.h_dt, n, s->d.ctrl, s->gp);
+  });
+  allreduce_dt(s);
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+}
+
+void upload_state(hgks_solver* s, const double* h_Q, double t, bool sync) {
+  const RankPlan& rp = *s->rp;
+  const int n = (int)rp.n_owned;
+  if (s->n_ranks == 1) {
+    CUDA_TRY(cudaMemcpyAsync(s->d.stage_in, h_Q, sizeof(double) * 5 * s->mesh->gm.nc, cudaMemcpyHostToDevice,
+                             s->stream));
+  } else {
+    double* hs = s->pinned;
+    for (int i = 0; i < n; ++i) std::memcpy(hs + 5 * (size_t)i, h_Q + 5 * rp.l2g[i], 5 * sizeof(double));
+    CUDA_TRY(cudaMemcpyAsync(s->d.stage_in, hs, sizeof(double) * 5 * n, cudaMemcpyHostToDevice, s->stream));
+  }
+  launch(s, "k_scatter_state",
+         [&] { k_scatter_state<<<blocks(n, 256), 256, 0, s->stream>>>(s->d.stage_in, s->d.in_row, n, s->d.Q, s->ldq); });
+  // time bookkeeping: t_next = t (k_step_begin starts from it), counters kept
+  Ctrl h;
+  CUDA_TRY(cudaMemcpyAsync(&h, s->d.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  h.t = t;
+  h.t_next = t;
+  h.dt = 0.0;
+  h.bad_cell = INT_MAX;
+  CUDA_TRY(cudaMemcpyAsync(s->d.ctrl, &h, sizeof(Ctrl), cudaMemcpyHostToDevice, s->stream));
+  init_dt(s);
+  (void)sync;
+}
+
+}  // namespace
+
+// ============================================================================
+// C-ABI
+// ============================================================================
+extern "C" {
+
+const char* hgks_last_error(void) { return g_last_error.c_str(); }
+const char* hgks_version(void) { return "hgks-b200 0.1 (sm_100a, fp64)"; }
+
+hgks_status hgks_mesh_create(const hgks_mesh_desc* d, hgks_mesh** out) {
+  return guard([&] {
+    if (!d || !out) throw Error(HGKS_E_ARG, "null argument");
+    auto m = std::make_unique<hgks_mesh>();
+    m->gm = build_global_mesh(d->xyz, d->n_nodes, d->cell_type, d->cell_nodes, d->n_cells, d->periodic_origin,
+                              d->periodic_length, d->bface_nodes, d->bface_tag, d->n_bfaces, d->n_ranks, d->cell_part);
+    *out = m.release();
+  });
+}
+
+hgks_status hgks_mesh_destroy(hgks_mesh* m) {
+  delete m;
+  return HGKS_OK;
+}
+
+hgks_status hgks_mesh_info(const hgks_mesh* mc, int32_t rank, hgks_mesh_stats* st) {
+  return guard([&] {
+    if (!mc || !st) throw Error(HGKS_E_ARG, "null argument");
+    hgks_mesh* m = const_cast<hgks_mesh*>(mc);
+    const RankPlan& rp = m->plan(rank);
+    std::memset(st, 0, sizeof(*st));
+    st->n_cells_global = m->gm.nc;
+    st->n_owned = rp.n_owned;
+    st->n_ghost = rp.n_pghost;
+    for (int k = 0; k < 3; ++k) st->ghost_layer[k] = rp.ghost_layer[k];
+    st->n_bghost = rp.n_bghost;
+    st->n_faces = rp.n_faces;
+    st->n_faces_bc = rp.n_wf + rp.n_ff;
+    st->stencil_min = rp.stencil_min;
+    st->stencil_max = rp.stencil_max;
+    st->n_sub = m->gm.lay.M;
+    st->n_peers = (int32_t)rp.peers.size();
+    st->send_cells = (int64_t)rp.send_list.size();
+    for (auto c : rp.recv_cnt) st->recv_cells += c;
+    st->edge_cut = m->gm.edge_cut;
+  });
+}
+
+hgks_status hgks_workspace_size(const hgks_mesh* mc, const hgks_config* cfg, int32_t rank, size_t* bytes) {
+  return guard([&] {
+    if (!mc || !bytes) throw Error(HGKS_E_ARG, "null argument");
+    (void)cfg;
+    hgks_mesh* m = const_cast<hgks_mesh*>(mc);
+    const RankPlan& rp = m->plan(rank);
+    Carve c{nullptr, 0, 0};
+    DevArrays d;
+    *bytes = layout(m->gm, rp, c, d);
+  });
+}
+
+hgks_status hgks_init(const hgks_mesh* mc, const hgks_config* cfg, const hgks_dist* dist, void* d_ws, size_t ws_bytes,
+                      void* stream, const double* h_Q0, hgks_solver** out) {
+  return guard([&] {
+    if (!mc || !cfg || !d_ws || !h_Q0 || !out) throw Error(HGKS_E_ARG, "null argument");
+    hgks_mesh* m = const_cast<hgks_mesh*>(mc);
+    auto s = std::make_unique<hgks_solver>();
+    s->mesh = m;
+    s->cfg = *cfg;
+    s->rank = dist ? dist->rank : 0;
+    s->n_ranks = dist ? dist->n_ranks : 1;
+    if (s->n_ranks != m->gm.n_ranks)
+      throw Error(HGKS_E_ARG, "dist->n_ranks differs from the mesh partition (" + std::to_string(m->gm.n_ranks) + ")");
+    if (dist) CUDA_TRY(cudaSetDevice(dist->device));
+    CUDA_TRY(cudaGetDevice(&s->device));
+    s->stream = (cudaStream_t)stream;
+    s->rp = &m->plan(s->rank);
+    s->lay = m->gm.lay;
+    const RankPlan& rp = *s->rp;
+    if (cfg->gamma <= 1.0 || cfg->gamma > 5.0 / 3.0) throw Error(HGKS_E_ARG, "gamma out of range");
+    if (!(cfg->cfl > 0) && !(cfg->fixed_dt > 0)) throw Error(HGKS_E_ARG, "need cfl > 0 or fixed_dt > 0");
+    GasParams& g = s->gp;
+    g.gamma = cfg->gamma;
+    g.K = (5.0 - 3.0 * cfg->gamma) / (cfg->gamma - 1.0);
+    g.cfl = cfg->cfl;
+    g.fixed_dt = cfg->fixed_dt;
+    g.eps = cfg->eps;
+    g.omega_pow = cfg->omega_pow;
+    g.tau_mode = cfg->tau_mode;
+    g.c1 = cfg->c1;
+    g.mu_inf = cfg->mu_inf;
+    g.t_inf = cfg->t_inf;
+    g.mu_exp = cfg->mu_exp;
+    for (int k = 0; k < 5; ++k) g.fs[k] = cfg->freestream[k];
+    s->ldq = round32(rp.n_local());
+    Carve c{(char*)d_ws, 0, ws_bytes};
+    if ((reinterpret_cast<uintptr_t>(d_ws) & 255) != 0) throw Error(HGKS_E_ARG, "workspace must be 256-byte aligned");
+    layout(m->gm, rp, c, s->d);
+    cudaStream_t st = s->stream;
+    auto up = [&](void* dst, const void* src, size_t bytes) {
+      if (bytes) CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+    };
+    up(s->d.recon_cell, rp.recon_cell.data(), rp.recon_cell.size() * sizeof(int));
+    up(s->d.st_id, rp.st_id.data(), rp.st_id.size() * sizeof(int));
+    up(s->d.sub_slot, rp.sub_slot.data(), rp.sub_slot.size());
+    up(s->d.op, rp.op.data(), rp.op.size() * sizeof(double));
+    up(s->d.geo, rp.geo.data(), rp.geo.size() * sizeof(double));
+    up(s->d.f_cells, rp.f_cells.data(), rp.f_cells.size() * sizeof(int));
+    up(s->d.f_geo, rp.f_geo.data(), rp.f_geo.size() * sizeof(double));
+    up(s->d.cf, rp.cf.data(), rp.cf.size() * sizeof(int));
+    up(s->d.inv_v, rp.inv_v.data(), rp.inv_v.size() * sizeof(double));
+    up(s->d.h_dt, rp.h_dt.data(), rp.h_dt.size() * sizeof(double));
+    up(s->d.bg_cell, rp.bg_cell.data(), rp.bg_cell.size() * sizeof(int));
+    up(s->d.bg_bc, rp.bg_bc.data(), rp.bg_bc.size() * sizeof(int));
+    up(s->d.bg_normal, rp.bg_normal.data(), rp.bg_normal.size() * sizeof(double));
+    up(s->d.send_list, rp.send_list.data(), rp.send_list.size() * sizeof(int));
+    // state maps: in_row[i] = row of owned cell i in the caller's array (single
+    // rank) or its position in the gathered staging array; out_local[k] = local
+    // id of the k-th owned cell in ascending global id
+    std::vector<int64_t> in_row(rp.n_owned);
+    for (int64_t i = 0; i < rp.n_owned; ++i) in_row[i] = s->n_ranks == 1 ? rp.l2g[i] : i;
+    std::vector<int> out_local(rp.n_owned);
+    std::iota(out_local.begin(), out_local.end(), 0);
+    std::sort(out_local.begin(), out_local.end(), [&](int a, int b) { return rp.l2g[a] < rp.l2g[b]; });
+    up(s->d.in_row, in_row.data(), in_row.size() * sizeof(int64_t));
+    up(s->d.out_local, out_local.data(), out_local.size() * sizeof(int));
+    CUDA_TRY(cudaMemsetAsync(s->d.Q, 0, sizeof(double) * 5 * s->ldq, st));
+    Ctrl h{};
+    h.bad_cell = INT_MAX;
+    h.dtmin_bits = 0x7fefffffffffffffull;
+    up(s->d.ctrl, &h, sizeof(Ctrl));
+    if (s->n_ranks > 1) {
+      Nccl& N = nccl();
+      if (!N.h || !N.CommInitRank) throw Error(HGKS_E_NCCL, "libnccl.so.2 not found");
+      ncclUniqueId id;
+      std::memcpy(id.internal, dist->nccl_id, 128);
+      NCCL_TRY(N.CommInitRank(&s->comm, s->n_ranks, id, s->rank));
+      CUDA_TRY(cudaMallocHost(&s->pinned, sizeof(double) * 5 * std::max<int64_t>(1, rp.n_owned)));
+    }
+    CUDA_TRY(cudaStreamSynchronize(st));
+    upload_state(s.get(), h_Q0, 0.0, true);
+    *out = s.release();
+  });
+}
+
+hgks_status hgks_destroy(hgks_solver* s) {
+  return guard([&] {
+    if (!s) return;
+    cudaStreamSynchronize(s->stream);
+    for (auto& kv : s->kstat)
+      for (auto& e : kv.second.pending) {
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+      }
+    if (s->comm && nccl().CommDestroy) nccl().CommDestroy(s->comm);
+    if (s->pinned) cudaFreeHost(s->pinned);
+    delete s;
+  });
+}
+
+hgks_status hgks_step(hgks_solver* s, int32_t n_steps, double t_stop, hgks_step_info* info) {
+  return guard([&] {
+    if (!s || n_steps < 0) throw Error(HGKS_E_ARG, "bad argument");
+    Ctrl before{};
+    if (info) {
+      CUDA_TRY(cudaMemcpyAsync(&before, s->d.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s->stream));
+      CUDA_TRY(cudaStreamSynchronize(s->stream));
+    }
+    for (int k = 0; k < n_steps; ++k) {
+      launch(s, "k_step_begin",
+             [&] { k_step_begin<<<1, 1, 0, s->stream>>>(s->d.ctrl, s->cfg.cfl, s->cfg.fixed_dt, t_stop); });
+      stage(s, 1);
+      stage(s, 2);
+    }
+    if (info) {
+      Ctrl h;
+      CUDA_TRY(cudaMemcpyAsync(&h, s->d.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s->stream));
+      CUDA_TRY(cudaStreamSynchronize(s->stream));
+      info->steps_done = h.steps - before.steps;
+      info->t = h.t_next;
+      info->last_dt = h.dt;
+      info->fallbacks = h.fallbacks;
+      if (h.bad_cell != INT_MAX) {
+        int64_t gid = h.bad_cell < (int)s->rp->l2g.size() ? s->rp->l2g[h.bad_cell] : -1;
+        throw Error(HGKS_E_POSITIVITY, "non-positive density or pressure at cell " + std::to_string(gid));
+      }
+      if (!(h.dt >= 0.0) || !std::isfinite(h.t_next)) throw Error(HGKS_E_STATE, "non-finite time step");
+    }
+  });
+}
+
+hgks_status hgks_set_state(hgks_solver* s, const double* h_Q, double t) {
+  return guard([&] {
+    if (!s || !h_Q) throw Error(HGKS_E_ARG, "null argument");
+    upload_state(s, h_Q, t, false);
+  });
+}
+
+hgks_status hgks_get_state(const hgks_solver* sc, double* h_Q, int64_t* h_gid, double* t) {
+  return guard([&] {
+    hgks_solver* s = const_cast<hgks_solver*>(sc);
+    if (!s || !h_Q) throw Error(HGKS_E_ARG, "null argument");
+    const int n = (int)s->rp->n_owned;
+    launch(s, "k_gather_state", [&] {
+      k_gather_state<<<blocks(n, 256), 256, 0, s->stream>>>(s->d.Q, s->ldq, s->d.out_local, n, s->d.stage_out);
+    });
+    CUDA_TRY(cudaMemcpyAsync(h_Q, s->d.stage_out, sizeof(double) * 5 * n, cudaMemcpyDeviceToHost, s->stream));
+    Ctrl h;
+    CUDA_TRY(cudaMemcpyAsync(&h, s->d.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    if (t) *t = h.t_next;
+    if (h_gid) {
+      std::vector<int64_t> g(s->rp->l2g.begin(), s->rp->l2g.begin() + n);
+      std::sort(g.begin(), g.end());
+      std::memcpy(h_gid, g.data(), sizeof(int64_t) * n);
+    }
+  });
+}
+
+hgks_status hgks_debug_residual(hgks_solver* s, const double* h_Q, double dt, double* h_L, double* h_dL) {
+  return guard([&] {
+    if (!s || !h_Q || !h_L || !h_dL) throw Error(HGKS_E_ARG, "null argument");
+    if (s->n_ranks != 1) throw Error(HGKS_E_ARG, "hgks_debug_residual is single-rank only");
+    const int n = (int)s->rp->n_owned;
+    // save state, load h_Q, run stage-1 reconstruction + flux, restore
+    CUDA_TRY(cudaMemcpyAsync(s->d.Qtmp, s->d.Q, sizeof(double) * 5 * s->ldq, cudaMemcpyDeviceToDevice, s->stream));
+    Ctrl saved;
+    CUDA_TRY(cudaMemcpyAsync(&saved, s->d.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    CUDA_TRY(cudaMemcpyAsync(s->d.stage_in, h_Q, sizeof(double) * 5 * s->mesh->gm.nc, cudaMemcpyHostToDevice,
+                             s->stream));
+    launch(s, "k_scatter_state",
+           [&] { k_scatter_state<<<blocks(n, 256), 256, 0, s->stream>>>(s->d.stage_in, s->d.in_row, n, s->d.Q, s->ldq); });
+    Ctrl h = saved;
+    h.dt = dt;
+    CUDA_TRY(cudaMemcpyAsync(s->d.ctrl, &h, sizeof(Ctrl), cudaMemcpyHostToDevice, s->stream));
+    bc_ghosts(s, s->d.Q);
+    run_recon(s, s->d.Q);
+    run_flux(s, s->d.Q, 1);
+    // L = (Q* - Q) ... computed directly on host from face fluxes for clarity
+    std::vector<double> F1((size_t)10 * s->rp->n_faces);
+    std::vector<int> cf(s->rp->cf);
+    CUDA_TRY(cudaMemcpyAsync(F1.data(), s->d.F1, F1.size() * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(s->d.Q, s->d.Qtmp, sizeof(double) * 5 * s->ldq, cudaMemcpyDeviceToDevice, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(s->d.ctrl, &saved, sizeof(Ctrl), cudaMemcpyHostToDevice, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    const int NF = s->lay.nfaces;
+    for (int i = 0; i < n; ++i) {
+      double L[5] = {0, 0, 0, 0, 0}, dL[5] = {0, 0, 0, 0, 0};
+      for (int p = 0; p < NF; ++p) {
+        int e = cf[(size_t)p * n + i];
+        int f = e >= 0 ? e : ~e;
+        double sg = e >= 0 ? -1.0 : 1.0;
+        for (int v = 0; v < 5; ++v) {
+          L[v] += sg * F1[(size_t)f * 10 + v];
+          dL[v] += sg * F1[(size_t)f * 10 + 5 + v];
+        }
+      }
+      int64_t gid = s->rp->l2g[i];
+      for (int v = 0; v < 5; ++v) {
+        h_L[gid * 5 + v] = L[v] * s->rp->inv_v[i];
+        h_dL[gid * 5 + v] = dL[v] * s->rp->inv_v[i];
+      }
+    }
+  });
+}
+
+hgks_status hgks_set_profiling(hgks_solver* s, int32_t enabled) {
+  return guard([&] {
+    if (!s) throw Error(HGKS_E_ARG, "null solver");
+    s->profiling = enabled != 0;
+  });
+}
+
+hgks_status hgks_kernel_times(hgks_solver* s, int32_t cap, char (*names)[32], int64_t* launches, double* total_ms,
+                              int32_t* n) {
+  return guard([&] {
+    if (!s || !n) throw Error(HGKS_E_ARG, "null argument");
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    int k = 0;
+    for (auto& kv : s->kstat) {
+      KStat& st = kv.second;
+      for (auto& e : st.pending) {
+        float ms = 0;
+        CUDA_TRY(cudaEventElapsedTime(&ms, e.first, e.second));
+        st.ms += ms;
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+      }
+      st.pending.clear();
+      if (k < cap) {
+        std::snprintf(names[k], 32, "%s", kv.first.c_str());
+        launches[k] = st.launches;
+        total_ms[k] = st.ms;
+      }
+      ++k;
+    }
+    *n = std::min(k, cap);
+  });
+}
+
+hgks_status hgks_launch_count(const hgks_solver* s, int64_t* launches) {
+  if (!s || !launches) return HGKS_E_ARG;
+  *launches = s->launches;
+  return HGKS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,265 @@
+"""Thin Python binding of libhgks.so (include/hgks.h): argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels of csrc/.  PyTorch provides
+device memory (the workspace tensor), the stream and torch.distributed (used
+only to broadcast the NCCL unique id).  There is no CPU fallback: if the
+library or a CUDA device is missing, these calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import build as _build
+
+_dp = C.POINTER(C.c_double)
+_i64p = C.POINTER(C.c_int64)
+_i32p = C.POINTER(C.c_int32)
+_i8p = C.POINTER(C.c_int8)
+
+HGKS_TET, HGKS_HEX = 4, 8
+ERRORS = {0: "OK", 1: "E_ARG", 2: "E_MESH", 3: "E_STENCIL", 4: "E_CUDA", 5: "E_NCCL", 6: "E_POSITIVITY",
+          7: "E_STATE"}
+
+# every symbol include/hgks.h declares (checked by tests/test_abi.py)
+EXPORTS = ["hgks_mesh_create", "hgks_mesh_destroy", "hgks_mesh_info", "hgks_workspace_size", "hgks_init",
+           "hgks_destroy", "hgks_step", "hgks_set_state", "hgks_get_state", "hgks_debug_residual",
+           "hgks_set_profiling", "hgks_kernel_times", "hgks_launch_count", "hgks_last_error", "hgks_version"]
+
+
+class MeshDesc(C.Structure):
+    _fields_ = [("xyz", _dp), ("n_nodes", C.c_int64), ("cell_type", _i8p), ("cell_nodes", _i64p),
+                ("n_cells", C.c_int64), ("periodic_origin", C.c_double * 3), ("periodic_length", C.c_double * 3),
+                ("bface_nodes", _i64p), ("bface_tag", _i32p), ("n_bfaces", C.c_int64), ("n_ranks", C.c_int32),
+                ("cell_part", _i32p)]
+
+
+class Config(C.Structure):
+    _fields_ = [("gamma", C.c_double), ("cfl", C.c_double), ("fixed_dt", C.c_double), ("tau_mode", C.c_int32),
+                ("c1", C.c_double), ("mu_inf", C.c_double), ("t_inf", C.c_double), ("mu_exp", C.c_double),
+                ("eps", C.c_double), ("omega_pow", C.c_int32), ("freestream", C.c_double * 5)]
+
+
+class Dist(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("n_ranks", C.c_int32), ("device", C.c_int32), ("nccl_id", C.c_uint8 * 128)]
+
+
+class MeshStats(C.Structure):
+    _fields_ = [("n_cells_global", C.c_int64), ("n_owned", C.c_int64), ("n_ghost", C.c_int64),
+                ("ghost_layer", C.c_int64 * 3), ("n_bghost", C.c_int64), ("n_faces", C.c_int64),
+                ("n_faces_bc", C.c_int64), ("stencil_min", C.c_int32), ("stencil_max", C.c_int32),
+                ("n_sub", C.c_int32), ("n_peers", C.c_int32), ("send_cells", C.c_int64), ("recv_cells", C.c_int64),
+                ("edge_cut", C.c_int64)]
+
+    def as_dict(self):
+        d = {}
+        for name, _ in self._fields_:
+            v = getattr(self, name)
+            d[name] = list(v) if name == "ghost_layer" else int(v)
+        return d
+
+
+class StepInfo(C.Structure):
+    _fields_ = [("steps_done", C.c_int64), ("t", C.c_double), ("last_dt", C.c_double), ("fallbacks", C.c_int64)]
+
+
+class HgksError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def lib(build_if_needed: bool = True):
+    """Load libhgks.so (building it in-tree with nvcc when sources changed)."""
+    global _lib
+    if _lib is None:
+        if build_if_needed and _build.needs_build():
+            _build.build()
+        if not os.path.exists(_build.LIB):
+            raise RuntimeError(f"libhgks.so missing at {_build.LIB}: run __graft_entry__.build()")
+        L = C.CDLL(_build.LIB)
+        L.hgks_last_error.restype = C.c_char_p
+        L.hgks_version.restype = C.c_char_p
+        L.hgks_mesh_create.argtypes = [C.POINTER(MeshDesc), C.POINTER(C.c_void_p)]
+        L.hgks_mesh_destroy.argtypes = [C.c_void_p]
+        L.hgks_mesh_info.argtypes = [C.c_void_p, C.c_int32, C.POINTER(MeshStats)]
+        L.hgks_workspace_size.argtypes = [C.c_void_p, C.POINTER(Config), C.c_int32, C.POINTER(C.c_size_t)]
+        L.hgks_init.argtypes = [C.c_void_p, C.POINTER(Config), C.POINTER(Dist), C.c_void_p, C.c_size_t, C.c_void_p,
+                                _dp, C.POINTER(C.c_void_p)]
+        L.hgks_destroy.argtypes = [C.c_void_p]
+        L.hgks_step.argtypes = [C.c_void_p, C.c_int32, C.c_double, C.POINTER(StepInfo)]
+        L.hgks_set_state.argtypes = [C.c_void_p, C.c_void_p, C.c_double]
+        L.hgks_get_state.argtypes = [C.c_void_p, C.c_void_p, _i64p, _dp]
+        L.hgks_debug_residual.argtypes = [C.c_void_p, _dp, C.c_double, _dp, _dp]
+        L.hgks_set_profiling.argtypes = [C.c_void_p, C.c_int32]
+        L.hgks_kernel_times.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, _i64p, _dp, _i32p]
+        L.hgks_launch_count.argtypes = [C.c_void_p, _i64p]
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        raise HgksError(rc, lib().hgks_last_error().decode())
+
+
+def _p(a, t=_dp):
+    return a.ctypes.data_as(t)
+
+
+@dataclass
+class SolverConfig:
+    gamma: float = 1.4
+    cfl: float = 0.3
+    fixed_dt: float = 0.0
+    tau_mode: int = 0
+    c1: float = 1.0
+    mu_inf: float = 0.0
+    t_inf: float = 1.0
+    mu_exp: float = 0.7
+    eps: float = 1e-10
+    omega_pow: int = 1
+    freestream: tuple = (1.0, 0.0, 0.0, 0.0, 1.0 / 1.4)
+
+    def c(self) -> Config:
+        return Config(self.gamma, self.cfl, self.fixed_dt, self.tau_mode, self.c1, self.mu_inf, self.t_inf,
+                      self.mu_exp, self.eps, self.omega_pow, (C.c_double * 5)(*self.freestream))
+
+
+class Mesh:
+    """hgks_mesh: host setup (geometry, faces, stencils, LSQ operators, partition)."""
+
+    def __init__(self, mi, n_ranks: int = 1, cell_part=None):
+        L = lib()
+        self._keep = [np.ascontiguousarray(mi.xyz, np.float64), np.ascontiguousarray(mi.cell_type, np.int8),
+                      np.ascontiguousarray(mi.cell_nodes, np.int64),
+                      np.ascontiguousarray(mi.bface_nodes, np.int64).reshape(-1, 4),
+                      np.ascontiguousarray(mi.bface_tag, np.int32)]
+        xyz, ct, cn, bf, bt = self._keep
+        part = None
+        if cell_part is not None:
+            part = np.ascontiguousarray(cell_part, np.int32)
+            self._keep.append(part)
+        d = MeshDesc(_p(xyz), xyz.shape[0], _p(ct, _i8p), _p(cn, _i64p), cn.shape[0],
+                     (C.c_double * 3)(*mi.periodic_origin), (C.c_double * 3)(*mi.periodic_length),
+                     _p(bf, _i64p), _p(bt, _i32p), bf.shape[0], n_ranks,
+                     _p(part, _i32p) if part is not None else None)
+        h = C.c_void_p()
+        _check(L.hgks_mesh_create(C.byref(d), C.byref(h)))
+        self.h = h
+        self.n_ranks = n_ranks
+        self.n_cells = int(cn.shape[0])
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.hgks_mesh_destroy(self.h)
+            self.h = None
+
+    def info(self, rank: int = 0) -> dict:
+        st = MeshStats()
+        _check(lib().hgks_mesh_info(self.h, rank, C.byref(st)))
+        return st.as_dict()
+
+    def workspace_size(self, cfg: SolverConfig, rank: int = 0) -> int:
+        n = C.c_size_t()
+        _check(lib().hgks_workspace_size(self.h, C.byref(cfg.c()), rank, C.byref(n)))
+        return int(n.value)
+
+
+class Solver:
+    """hgks_solver on one CUDA device.  ``Q0``: [n_cells_global, 5] float64 (caller order)."""
+
+    def __init__(self, mesh: Mesh, Q0, cfg: SolverConfig | None = None, device=None, rank: int = 0,
+                 nccl_id: bytes | None = None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("hgks needs a CUDA device (no CPU fallback)")
+        self.cfg = cfg or SolverConfig()
+        self.mesh = mesh
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        torch.cuda.set_device(self.device)
+        nbytes = mesh.workspace_size(self.cfg, rank)
+        self.ws = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+        base = self.ws.data_ptr()
+        ptr = (base + 255) // 256 * 256
+        self.stream = torch.cuda.current_stream(self.device)
+        Q0 = np.ascontiguousarray(Q0, np.float64)
+        dist = None
+        if mesh.n_ranks > 1:
+            dist = Dist(rank, mesh.n_ranks, self.device.index, (C.c_uint8 * 128)(*nccl_id))
+        h = C.c_void_p()
+        _check(lib().hgks_init(mesh.h, C.byref(self.cfg.c()), C.byref(dist) if dist else None, C.c_void_p(ptr),
+                               nbytes, C.c_void_p(self.stream.cuda_stream), _p(Q0), C.byref(h)))
+        self.h = h
+        self.rank = rank
+        self.n_owned = mesh.info(rank)["n_owned"]
+
+    def close(self):
+        if getattr(self, "h", None):
+            _check(lib().hgks_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def step(self, n_steps: int = 1, t_stop: float = 0.0, info: bool = True):
+        si = StepInfo()
+        _check(lib().hgks_step(self.h, n_steps, t_stop, C.byref(si) if info else None))
+        if info:
+            return dict(steps_done=int(si.steps_done), t=float(si.t), last_dt=float(si.last_dt),
+                        fallbacks=int(si.fallbacks))
+        return None
+
+    def set_state(self, Q, t: float = 0.0):
+        """Q: numpy [n,5] float64 or a (pinned) CPU torch tensor."""
+        ptr = Q.data_ptr() if hasattr(Q, "data_ptr") else np.ascontiguousarray(Q, np.float64).ctypes.data
+        _check(lib().hgks_set_state(self.h, C.c_void_p(ptr), t))
+
+    def get_state(self, out=None):
+        """Owned cells in ascending global id -> (Q [n_owned,5], gid, t).  ``out`` may be a pinned tensor."""
+        t = C.c_double()
+        gid = np.zeros(self.n_owned, np.int64)
+        if out is None:
+            Q = np.zeros((self.n_owned, 5))
+            _check(lib().hgks_get_state(self.h, C.c_void_p(Q.ctypes.data), _p(gid, _i64p), C.byref(t)))
+            return Q, gid, t.value
+        _check(lib().hgks_get_state(self.h, C.c_void_p(out.data_ptr()), None, C.byref(t)))
+        return out, None, t.value
+
+    def residual(self, Q, dt: float):
+        Q = np.ascontiguousarray(Q, np.float64)
+        L = np.zeros_like(Q)
+        dL = np.zeros_like(Q)
+        _check(lib().hgks_debug_residual(self.h, _p(Q), dt, _p(L), _p(dL)))
+        return L, dL
+
+    def set_profiling(self, on: bool):
+        _check(lib().hgks_set_profiling(self.h, 1 if on else 0))
+
+    def kernel_times(self) -> dict:
+        cap = 64
+        names = (C.c_char * 32 * cap)()
+        launches = np.zeros(cap, np.int64)
+        ms = np.zeros(cap)
+        n = C.c_int32()
+        _check(lib().hgks_kernel_times(self.h, cap, C.cast(names, C.c_void_p), _p(launches, _i64p), _p(ms),
+                                       C.byref(n)))
+        out = {}
+        for k in range(n.value):
+            nm = bytes(names[k]).split(b"\0", 1)[0].decode()
+            out[nm] = dict(launches=int(launches[k]), ms=float(ms[k]))
+        return out
+
+    def launch_count(self) -> int:
+        n = C.c_int64()
+        _check(lib().hgks_launch_count(self.h, C.byref(n)))
+        return int(n.value)

@@ -1,0 +1,99 @@
+"""CPU checks of the C-ABI library: it loads, exports every symbol include/hgks.h
+declares, and its host-side setup (geometry, faces, stencils, partition) agrees
+with the oracle's independently built tables.  No compute calls (no GPU here)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2407_00656_b200 import hgks, workloads as W
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "hgks.h")).read()
+    return sorted(set(re.findall(r"\b(hgks_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = hgks.lib()
+    syms = header_symbols()
+    assert len(syms) >= 14
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(hgks.EXPORTS)
+    assert b"sm_100a" in lib.hgks_version()
+
+
+def test_library_contains_sm100a_cubin():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", hgks.lib()._name], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+@pytest.mark.parametrize("mk", [lambda: W.kuhn_box(6), lambda: W.kuhn_box(5, jitter=0.1),
+                                lambda: W.cartesian_hex_box(5, jitter=0.1)])
+def test_host_setup_matches_oracle_counts(mk):
+    mi = mk()
+    m = hgks.Mesh(mi)
+    info = m.info()
+    om = O.OracleMesh(mi)
+    assert info["n_cells_global"] == om.n_cells == info["n_owned"]
+    assert info["n_faces"] == om.n_faces
+    assert info["stencil_min"] == om.min_stencil and info["stencil_max"] == om.max_stencil
+    assert info["n_sub"] == om.n_subs
+    assert info["n_ghost"] == 0 and info["n_peers"] == 0
+
+
+def test_sphere_shell_boundary_faces():
+    mi = W.sphere_shell(4)
+    m = hgks.Mesh(mi)
+    info = m.info()
+    om = O.OracleMesh(mi)
+    assert info["n_cells_global"] == 6 * 4 * 4 * 8
+    assert info["n_faces"] == om.n_faces
+    assert info["n_faces_bc"] == 2 * 6 * 16 == om.n_ghosts == info["n_bghost"]
+
+
+def test_errors_are_reported_not_thrown():
+    mi = W.kuhn_box(4)
+    bad = W.MeshInput(xyz=mi.xyz, cell_type=mi.cell_type.copy(), cell_nodes=mi.cell_nodes.copy(),
+                      periodic_length=mi.periodic_length)
+    bad.cell_nodes[3, 1] = 10 ** 9
+    with pytest.raises(hgks.HgksError) as e:
+        hgks.Mesh(bad)
+    assert e.value.code == 2 and "cell 3" in str(e.value)
+    mixed = W.MeshInput(xyz=mi.xyz, cell_type=mi.cell_type.copy(), cell_nodes=mi.cell_nodes,
+                        periodic_length=mi.periodic_length)
+    mixed.cell_type[5] = 8
+    with pytest.raises(hgks.HgksError) as e:
+        hgks.Mesh(mixed)
+    assert e.value.code == 2
+    openm = W.MeshInput(xyz=mi.xyz, cell_type=mi.cell_type, cell_nodes=mi.cell_nodes)  # not periodic
+    with pytest.raises(hgks.HgksError) as e:
+        hgks.Mesh(openm)
+    assert e.value.code == 2 and "boundary face" in str(e.value)
+    with pytest.raises(hgks.HgksError):
+        hgks.Mesh(W.kuhn_box(2))  # periodic box too small for the 2-layer stencil
+
+
+def test_workspace_size_scales_with_cells():
+    cfg = hgks.SolverConfig()
+    a = hgks.Mesh(W.kuhn_box(6)).workspace_size(cfg)
+    b = hgks.Mesh(W.kuhn_box(12)).workspace_size(cfg)
+    per_cell = (b - a) / (6 * 12 ** 3 - 6 * 6 ** 3)
+    # operators 198 doubles + record 50 + state/face/update data: ~2.5-3.5 KB per tet
+    assert 2000 < per_cell < 4000, per_cell
+
+
+def test_solver_without_cuda_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("has CUDA")
+    mi = W.kuhn_box(4)
+    with pytest.raises(RuntimeError, match="CUDA"):
+        hgks.Solver(hgks.Mesh(mi), W.advection_ic(mi))

@@ -1,0 +1,125 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bar (BASELINE.json north_star; reading R26): after 10 fp64 steps, per conserved
+variable v, max_i |Q_gpu - Q_oracle| / max_i |Q_oracle| <= 1e-10.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2407_00656_b200 import hgks, workloads as W
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+def rel_err(a, b):
+    return (np.abs(a - b).max(axis=0) / np.maximum(np.abs(b).max(axis=0), 1e-300))
+
+
+def run_pair(mi, Q0, steps, cfl=0.3, per_step=True, ocfg=None, gcfg=None):
+    ocfg = ocfg or O.OracleConfig(cfl=cfl)
+    gcfg = gcfg or hgks.SolverConfig(cfl=cfl)
+    g = hgks.Solver(hgks.Mesh(mi), Q0, gcfg)
+    o = O.OracleSolver(O.OracleMesh(mi), Q0, ocfg)
+    errs = []
+    for k in range(steps if per_step else 1):
+        n = 1 if per_step else steps
+        gi = g.step(n)
+        o.step(n)
+        Qg, gid, tg = g.get_state()
+        Qo, to, dto, fbo = o.state()
+        assert np.array_equal(gid, np.arange(mi.n_cells))
+        assert abs(tg - to) <= 1e-13 * max(1.0, to), (tg, to)
+        assert gi["fallbacks"] == fbo
+        errs.append(rel_err(Qg, Qo))
+    return np.array(errs), g, o
+
+
+def test_c1_residual_matches_oracle(cuda_ok):
+    mi = W.kuhn_box(6)
+    Q0 = W.advection_ic(mi)
+    g = hgks.Solver(hgks.Mesh(mi), Q0)
+    o = O.OracleSolver(O.OracleMesh(mi), Q0)
+    dt = o.dt()
+    Lg, dLg = g.residual(Q0, dt)
+    Lo, dLo, _ = o.residual(Q0, dt)
+    assert rel_err(Lg, Lo).max() < 1e-11, rel_err(Lg, Lo)
+    assert rel_err(dLg, dLo).max() < 1e-11, rel_err(dLg, dLo)
+
+
+def test_c1_ten_steps(cuda_ok):
+    """C1: 1296 Kuhn tets, periodic [0,2]^3, tau = 0, CFL 0.3, 10 steps, every step."""
+    mi = W.kuhn_box(6)
+    errs, _, _ = run_pair(mi, W.advection_ic(mi), 10)
+    assert errs.max() <= TOL, errs.max(axis=0)
+
+
+def test_jittered_tets_ten_steps(cuda_ok):
+    mi = W.kuhn_box(6, jitter=0.1)
+    Q0 = W.advection_ic(mi)
+    errs, _, _ = run_pair(mi, Q0, 10)
+    assert errs.max() <= TOL, errs.max(axis=0)
+
+
+def test_ragged_box_fixed_dt(cuda_ok):
+    """Non-cubic box (7x5x6 cubes, ragged against every tile size), fixed dt."""
+    mi = W.kuhn_box(7, 5, 6, h=2.0 / 6)
+    Q0 = W.random_smooth_ic(mi, seed=7)
+    errs, _, _ = run_pair(mi, Q0, 10, ocfg=O.OracleConfig(fixed_dt=2e-3), gcfg=hgks.SolverConfig(fixed_dt=2e-3))
+    assert errs.max() <= TOL, errs.max(axis=0)
+
+
+def test_hex_box_ten_steps(cuda_ok):
+    mi = W.cartesian_hex_box(6, jitter=0.1)
+    Q0 = W.random_smooth_ic(mi, seed=3)
+    errs, _, _ = run_pair(mi, Q0, 10, cfl=0.5)
+    assert errs.max() <= TOL, errs.max(axis=0)
+
+
+def test_stress_step_density(cuda_ok):
+    """C1s-like (tau = 0 variant): density step, nonlinear weights far from gamma."""
+    mi = W.kuhn_box(6)
+    Q0 = W.density_step_ic(mi)
+    errs, _, _ = run_pair(mi, Q0, 10)
+    assert errs.max() <= TOL, errs.max(axis=0)
+
+
+def test_t_stop_clipping(cuda_ok):
+    mi = W.kuhn_box(6)
+    Q0 = W.advection_ic(mi)
+    g = hgks.Solver(hgks.Mesh(mi), Q0)
+    o = O.OracleSolver(O.OracleMesh(mi), Q0)
+    info = g.step(100, t_stop=0.05)
+    o.step(100, 0.05)
+    Qo, to, _, _ = o.state()
+    Qg, _, tg = g.get_state()
+    assert tg == 0.05 and to == 0.05
+    assert rel_err(Qg, Qo).max() <= TOL
+    assert g.step(5, t_stop=0.05)["steps_done"] == 0
+
+
+def test_bench_size_one_step(cuda_ok):
+    """configs[1] at the bench size N=48 (663,552 tets): one full step, every cell vs the oracle."""
+    mi = W.kuhn_box(48)
+    Q0 = W.advection_ic(mi)
+    errs, _, _ = run_pair(mi, Q0, 1)
+    assert errs.max() <= TOL, errs.max(axis=0)
+
+
+def test_conservation_and_free_stream_gpu(cuda_ok):
+    mi = W.kuhn_box(8, jitter=0.1)
+    V = O.OracleMesh(mi).geometry()[0][: mi.n_cells]
+    Q0 = W.uniform_state(mi.n_cells, 1.0, (0.3, -0.2, 0.5), 1.0)
+    g = hgks.Solver(hgks.Mesh(mi), Q0)
+    g.step(20)
+    Q, _, _ = g.get_state()
+    assert np.abs(Q - Q0).max() <= 1e-12
+    Q0 = W.advection_ic(mi)
+    g = hgks.Solver(hgks.Mesh(mi), Q0)
+    g.step(20)
+    Q, _, _ = g.get_state()
+    tot0 = (Q0 * V[:, None]).sum(0)
+    tot = (Q * V[:, None]).sum(0)
+    assert np.abs(tot - tot0).max() <= 1e-12 * np.abs(tot0).max()
