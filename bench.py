@@ -1,0 +1,326 @@
+"""Benchmark: fp64 cell-updates/s of the HGKS hot path on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+One step = one full S2O4 step (2 stages of halo exchange + WENO reconstruction
++ face flux + update, plus the CFL min) over every cell.  Workload (N = 1):
+configs[1] of BASELINE.json at its largest member, the 48^3 Kuhn box (663,552
+tets, periodic, tau = 0, CFL 0.3, accuracy-test IC).  N > 1 (torchrun, one
+process per GPU): weak scaling, one 48^3 block per GPU (box extended along
+x/y/z, RCB partition, NCCL halo exchange + allreduce-min).
+
+--impl reference times the CPU oracle (oracle/) on the box's host cores on a
+bounded sample of the same workload family (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_BLOCK = 48            # cubes per axis per GPU block (configs[1] top size)
+GAMMA = 1.4
+CFL = 0.3
+METRIC = "fp64 cell-updates/sec at 1/2/4/8 B200; % HBM/FP64 roofline"
+UNIT = "cell-updates/s"
+
+
+def box_dims(n_gpus: int):
+    """Weak-scaling box: n_gpus blocks of N_BLOCK^3 cubes (factor 2 per axis, x first)."""
+    dims = [1, 1, 1]
+    k, ax = n_gpus, 0
+    while k > 1:
+        if k % 2:
+            dims[ax] *= k
+            break
+        dims[ax] *= 2
+        k //= 2
+        ax = (ax + 1) % 3
+    return [d * N_BLOCK for d in dims]
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    hbm = None
+    if os.path.exists(path):
+        hbm = json.load(open(path)).get("hbm_gbs")
+    src = "MEASURED_PEAKS.json" if hbm else "fallback B200_PROFILING.md"
+    fp64 = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
+    return (hbm or 6650.0), src, fp64["fp64_tflops"], "profiles/fp64_peak.json (DFMA microbenchmark on this pool)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[2 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# algorithmic bytes / flops per unit, tets
+def recon_bytes_per_cell(K=14, M=4, NM=6):
+    op = (9 * K + M * 3 * NM) * 8      # LSQ operators
+    idx = K * 4 + M * NM * 1 + 4       # stencil ids, sub-stencil slots, recon cell id
+    geo = 8 * 8                        # V^{2/3}, V^{4/3}, M2
+    q = 5 * 8                          # the cell's own state (neighbours: each state read once overall)
+    rec = 50 * 8                       # effective-polynomial record written
+    return op + idx + geo + q + rec
+
+
+def cpu_oracle_rate(N: int, steps: int, threads: int):
+    from oracle import oracle as O
+    from paper_2407_00656_b200 import workloads as W
+    mi = W.kuhn_box(N)
+    m = O.OracleMesh(mi)
+    s = O.OracleSolver(m, W.advection_ic(mi, gamma=GAMMA), O.OracleConfig(cfl=CFL), threads=threads)
+    t0 = time.perf_counter()
+    s.step(steps)
+    dt = time.perf_counter() - t0
+    return m.n_cells * steps / dt, dt, m.n_cells
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    from oracle import oracle as O
+    from paper_2407_00656_b200 import workloads as W
+    Ns = 24
+    mi = W.kuhn_box(Ns)
+    m = O.OracleMesh(mi)
+    s = O.OracleSolver(m, W.advection_ic(mi, gamma=GAMMA), O.OracleConfig(cfl=CFL), threads=threads)
+    s.step(args.warmup)
+    t0 = time.perf_counter()
+    s.step(args.steps)
+    dt = time.perf_counter() - t0
+    value = m.n_cells * args.steps / dt
+    sample = (f"each step: one full S2O4 step of the oracle on the {Ns}^3 Kuhn box ({m.n_cells} tets, same "
+              f"per-cell work as the {N_BLOCK}^3 workload)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"configs[1]: Kuhn periodic tets, accuracy-test IC, tau=0, CFL {CFL}",
+                       "cells": m.n_cells},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2407_00656_b200 import hgks, workloads as W
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    nx, ny, nz = box_dims(world)
+    mi = W.kuhn_box(nx, ny, nz, h=2.0 / N_BLOCK)
+    Q0 = W.advection_ic(mi, gamma=GAMMA)
+    mesh = hgks.Mesh(mi, n_ranks=world)
+    nid = None
+    if world > 1:
+        obj = [hgks.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    cfg = hgks.SolverConfig(gamma=GAMMA, cfl=CFL)
+    s = hgks.Solver(mesh, Q0, cfg, device=local, rank=rank, nccl_id=nid)
+    info = mesh.info(rank)
+    n_owned = info["n_owned"]
+    stream = s.stream
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    # ---------------- warm-up ----------------
+    s.step(args.warmup, info=False)
+    barrier()
+    # ---------------- reference pass without per-kernel events (reported as ms_per_step_unprofiled) ----------------
+    evA, evB = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    evA.record(stream)
+    s.step(args.steps, info=False)
+    evB.record(stream)
+    barrier()
+    ms_unprof = evA.elapsed_time(evB)
+    # ---------------- timed region (device time, CUDA events on the solver stream) ----------------
+    s.set_profiling(True)
+    launches0 = s.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        s.step(args.steps, info=False)
+        ev1.record(stream)
+        barrier()
+    launches = s.launch_count() - launches0
+    ms = ev0.elapsed_time(ev1)
+    s.set_profiling(False)
+    ktimes = s.kernel_times()
+    st = s.step(0)  # sync + positivity check
+    t_ms = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    tot_cells = torch.tensor([n_owned], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot_cells, op=dist.ReduceOp.SUM)
+    ms_max = float(t_ms.item())
+    cells = float(tot_cells.item())
+    value = cells * args.steps / (ms_max * 1e-3)
+
+    # ---------------- end to end through the public API with host buffers ----------------
+    Qh = torch.from_numpy(np.ascontiguousarray(Q0)).pin_memory()
+    out = torch.empty((n_owned, 5), dtype=torch.float64).pin_memory()
+    e2e_steps = max(1, args.e2e_steps)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    t_host0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        s.set_state(Qh, 0.0)          # H2D of this step's inputs
+        s.step(1, info=False)
+        s.get_state(out)              # D2H of the step's result (synchronises)
+    e1.record(stream)
+    e1.synchronize()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_value = cells * e2e_steps / (float(e2e_ms.item()) * 1e-3)
+    h2d = (mi.n_cells if world == 1 else n_owned) * 5 * 8
+    d2h = n_owned * 5 * 8
+
+    # ---------------- roofline of the dominant kernel ----------------
+    hbm_peak, hbm_src, fp64_peak, fp64_src = peaks()
+    top = max(ktimes.items(), key=lambda kv: kv[1]["ms"])
+    name, kt = top
+    avg_ms = kt["ms"] / max(1, kt["launches"])
+    roof = None
+    if name.startswith("k_recon"):
+        bytes_per_launch = recon_bytes_per_cell() * info["n_owned"] + 0 * info["n_ghost"]
+        # recon also runs over layer-1 ghosts for N > 1
+        n_recon = info["n_owned"] + info["ghost_layer"][0]
+        bytes_per_launch = recon_bytes_per_cell() * n_recon
+        achieved = bytes_per_launch / (avg_ms * 1e-3) / 1e9
+        roof = {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": None,
+                "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,
+                "peak_source": hbm_src + " (burst copy)"}
+    else:
+        flops = json.load(open(os.path.join(ROOT, "profiles", "flops_per_unit.json")))
+        fpl = flops.get(name, {}).get("flops_per_launch_per_face", None)
+        nf = info["n_faces"]
+        if fpl:
+            achieved = fpl * nf / (avg_ms * 1e-3) / 1e12
+            roof = {"kernel": name, "bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                    "frac": achieved / fp64_peak, "traffic": None, "avg_launch_ms": avg_ms,
+                    "peak_source": fp64_src}
+    traffic_path = os.path.join(ROOT, "profiles", "traffic.json")
+    if roof and os.path.exists(traffic_path):
+        tr = json.load(open(traffic_path)).get(roof["kernel"])
+        if tr:
+            roof["traffic"] = tr["dram_bytes_per_launch"] * (n_recon / tr["cells"] if "cells" in tr else 1.0)
+
+    # ---------------- CPU baseline (oracle, rank 0, bounded sample) ----------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = len(os.sched_getaffinity(0))
+        rate, secs, ncell = cpu_oracle_rate(N_BLOCK, 1, threads)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
+               "sample": f"1 step of the same {N_BLOCK}^3 Kuhn-box workload ({ncell} tets), {secs:.1f} s"}
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "ms_per_step_unprofiled": ms_unprof / args.steps,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator: periodic Kuhn tets, exact-average accuracy-test IC)",
+            "config": {"workload": f"configs[1] top size: {N_BLOCK}^3 Kuhn box per GPU, 6 tets/cube, periodic, "
+                                   f"tau=0, CFL {CFL}", "cells": int(cells), "box_cubes": [nx, ny, nz],
+                       "parallelism": f"domain decomposition x{world} (RCB, 3 ghost layers, NCCL)",
+                       "l2": "no flush: per-step working set %.2f GB > 126 MB L2" % (mesh.workspace_size(cfg) / 1e9)},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "steps": e2e_steps},
+            "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
+            "kernels": {k: {"launches": v["launches"], "avg_ms": v["ms"] / max(1, v["launches"]),
+                            "share": v["ms"] / max(1e-30, sum(x["ms"] for x in ktimes.values()))}
+                        for k, v in ktimes.items()},
+            "fallbacks": st["fallbacks"],
+        }
+        print(json.dumps(line), flush=True)
+    s.close()
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
