@@ -235,269 +235,7 @@ __global__ void __launch_bounds__(BLOCK) k_recon(ReconArgs a) {
   }
 }
 
-// ----------------------------------------------------------------------------
-// a8 + a9: face flux for tau = 0, one thread per Gauss point.
-// ----------------------------------------------------------------------------
-struct FluxArgs {
-  const double* __restrict__ Q;
-  int ldq;
-  const double* __restrict__ ceff;
-  const int* __restrict__ f_cells;  // [n][2]
-  const double* __restrict__ f_geo; // [n][stride]
-  int f_stride;
-  int n_faces;                      // faces in this launch
-  int face0;                        // first face index
-  double* __restrict__ F1;          // stage 1: [n_faces][10] (F*S, dF*S)
-  double* __restrict__ F2;          // stage 2: [n_faces][5]  (dF*S)
-  Ctrl* ctrl;
-  double gamma, K;
-};
-
-// evaluate the effective polynomial of a cell at X (relative to its centroid)
-__device__ __forceinline__ void eval_poly(const double* __restrict__ rec, const double X[3], double val[5],
-                                          double grad[5][3]) {
-  const double xx = X[0] * X[0], yy = X[1] * X[1], zz = X[2] * X[2];
-  const double xy = X[0] * X[1], xz = X[0] * X[2], yz = X[1] * X[2];
-#pragma unroll
-  for (int v = 0; v < 5; ++v) {
-    const double c0 = __ldg(rec + v);
-    const double lx = __ldg(rec + 5 + v), ly = __ldg(rec + 10 + v), lz = __ldg(rec + 15 + v);
-    const double qxx = __ldg(rec + 20 + v), qyy = __ldg(rec + 25 + v), qzz = __ldg(rec + 30 + v);
-    const double qxy = __ldg(rec + 35 + v), qxz = __ldg(rec + 40 + v), qyz = __ldg(rec + 45 + v);
-    val[v] = c0 + lx * X[0] + ly * X[1] + lz * X[2] + qxx * xx + qyy * yy + qzz * zz + qxy * xy + qxz * xz + qyz * yz;
-    grad[v][0] = lx + 2.0 * qxx * X[0] + qxy * X[1] + qxz * X[2];
-    grad[v][1] = ly + 2.0 * qyy * X[1] + qxy * X[0] + qyz * X[2];
-    grad[v][2] = lz + 2.0 * qzz * X[2] + qxz * X[0] + qyz * X[1];
-  }
-}
-
-// Gauss point g of a face from its vertices (relative to the owner centroid), R10
-template <int NV>
-__device__ __forceinline__ void face_gp(const double* __restrict__ fg, int g, double x[3], double n[3], double& wS) {
-  if (NV == 3) {
-    double p[3][3];
-#pragma unroll
-    for (int q = 0; q < 3; ++q)
-#pragma unroll
-      for (int a = 0; a < 3; ++a) p[q][a] = __ldg(fg + 3 * q + a);
-    const double e1[3] = {p[1][0] - p[0][0], p[1][1] - p[0][1], p[1][2] - p[0][2]};
-    const double e2[3] = {p[2][0] - p[0][0], p[2][1] - p[0][1], p[2][2] - p[0][2]};
-    double nn[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
-    const double a2 = sqrt(nn[0] * nn[0] + nn[1] * nn[1] + nn[2] * nn[2]);
-    const double l0 = g == 0 ? 2.0 / 3.0 : 1.0 / 6.0, l1 = g == 1 ? 2.0 / 3.0 : 1.0 / 6.0,
-                 l2 = g == 2 ? 2.0 / 3.0 : 1.0 / 6.0;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      x[a] = l0 * p[0][a] + l1 * p[1][a] + l2 * p[2][a];
-      n[a] = nn[a] / a2;
-    }
-    wS = a2 / 6.0;
-  } else {
-    double p[4][3];
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-#pragma unroll
-      for (int a = 0; a < 3; ++a) p[q][a] = __ldg(fg + 3 * q + a);
-    const double h = 0.28867513459481287;  // 1/(2 sqrt 3)
-    const double s = (g & 1) ? 0.5 + h : 0.5 - h, t = (g >> 1) ? 0.5 + h : 0.5 - h;
-    double ds[3], dt[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      x[a] = (1 - s) * (1 - t) * p[0][a] + s * (1 - t) * p[1][a] + s * t * p[2][a] + (1 - s) * t * p[3][a];
-      ds[a] = (1 - t) * (p[1][a] - p[0][a]) + t * (p[2][a] - p[3][a]);
-      dt[a] = (1 - s) * (p[3][a] - p[0][a]) + s * (p[2][a] - p[1][a]);
-    }
-    double nn[3] = {ds[1] * dt[2] - ds[2] * dt[1], ds[2] * dt[0] - ds[0] * dt[2], ds[0] * dt[1] - ds[1] * dt[0]};
-    const double an = sqrt(nn[0] * nn[0] + nn[1] * nn[1] + nn[2] * nn[2]);
-#pragma unroll
-    for (int a = 0; a < 3; ++a) n[a] = nn[a] / an;
-    wS = 0.25 * an;
-  }
-}
-
-// local frame (R11): t1 = normalize(n x e*), e* the axis with the smallest |n.e|
-__device__ __forceinline__ void frame(const double n[3], double t1[3], double t2[3]) {
-  int k = 0;
-  if (fabs(n[1]) < fabs(n[k])) k = 1;
-  if (fabs(n[2]) < fabs(n[k])) k = 2;
-  double e[3] = {0.0, 0.0, 0.0};
-  e[k] = 1.0;
-  double c[3] = {n[1] * e[2] - n[2] * e[1], n[2] * e[0] - n[0] * e[2], n[0] * e[1] - n[1] * e[0]};
-  double inv = 1.0 / sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
-#pragma unroll
-  for (int a = 0; a < 3; ++a) t1[a] = c[a] * inv;
-  t2[0] = n[1] * t1[2] - n[2] * t1[1];
-  t2[1] = n[2] * t1[0] - n[0] * t1[2];
-  t2[2] = n[0] * t1[1] - n[1] * t1[0];
-}
-
-// rotate value + gradient (global) into the local frame: q[5], dq[3][5] (derivative along n, t1, t2)
-__device__ __forceinline__ void to_local(const double val[5], const double grad[5][3], const double n[3],
-                                         const double t1[3], const double t2[3], double q[5], double dq[3][5]) {
-  q[0] = val[0];
-  q[4] = val[4];
-  q[1] = val[1] * n[0] + val[2] * n[1] + val[3] * n[2];
-  q[2] = val[1] * t1[0] + val[2] * t1[1] + val[3] * t1[2];
-  q[3] = val[1] * t2[0] + val[2] * t2[1] + val[3] * t2[2];
-  const double* dirs[3] = {n, t1, t2};
-#pragma unroll
-  for (int j = 0; j < 3; ++j) {
-    const double* e = dirs[j];
-    double d[5];
-#pragma unroll
-    for (int v = 0; v < 5; ++v) d[v] = grad[v][0] * e[0] + grad[v][1] * e[1] + grad[v][2] * e[2];
-    dq[j][0] = d[0];
-    dq[j][4] = d[4];
-    dq[j][1] = d[1] * n[0] + d[2] * n[1] + d[3] * n[2];
-    dq[j][2] = d[1] * t1[0] + d[2] * t1[1] + d[3] * t1[2];
-    dq[j][3] = d[1] * t2[0] + d[2] * t2[1] + d[3] * t2[2];
-  }
-}
-
-// Euler-flux Jacobian-vector product along local axis j: dF_j = (dF_j/dQ) dq
-__device__ __forceinline__ void euler_jvp(int j, const double Q[5], const double dq[5], double gm1, double out[5]) {
-  const double rho = Q[0];
-  const double inv = 1.0 / rho;
-  const double u[3] = {Q[1] * inv, Q[2] * inv, Q[3] * inv};
-  const double p = gm1 * (Q[4] - 0.5 * (Q[1] * u[0] + Q[2] * u[1] + Q[3] * u[2]));
-  const double du[3] = {(dq[1] - u[0] * dq[0]) * inv, (dq[2] - u[1] * dq[0]) * inv, (dq[3] - u[2] * dq[0]) * inv};
-  const double dp = gm1 * (dq[4] - (u[0] * dq[1] + u[1] * dq[2] + u[2] * dq[3]) +
-                           0.5 * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]) * dq[0]);
-  out[0] = dq[1 + j];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) out[1 + k] = dq[1 + j] * u[k] + Q[1 + j] * du[k] + (k == j ? dp : 0.0);
-  out[4] = du[j] * (Q[4] + p) + u[j] * (dq[4] + dp);
-}
-
-template <int NV, int STAGE>
-__global__ void __launch_bounds__(NV == 3 ? 96 : 128) k_flux_tau0(FluxArgs a) {
-  constexpr int NGP = NV == 3 ? 3 : 4;
-  constexpr int BLOCK = NV == 3 ? 96 : 128;
-  constexpr int NOUT = STAGE == 1 ? 10 : 5;
-  __shared__ double red[NOUT][BLOCK];
-  const int t = blockIdx.x * BLOCK + threadIdx.x;
-  const int lf = t / NGP, g = t - lf * NGP;
-  const bool active = lf < a.n_faces;
-  double out[NOUT];
-#pragma unroll
-  for (int k = 0; k < NOUT; ++k) out[k] = 0.0;
-  if (active) {
-    const int f = a.face0 + lf;
-    const int co = __ldg(a.f_cells + 2 * f), cn = __ldg(a.f_cells + 2 * f + 1);
-    const double* fg = a.f_geo + (size_t)f * a.f_stride;
-    double x[3], n[3], wS;
-    face_gp<NV>(fg, g, x, n, wS);
-    const double xr[3] = {x[0] + __ldg(fg + 3 * NV), x[1] + __ldg(fg + 3 * NV + 1), x[2] + __ldg(fg + 3 * NV + 2)};
-    double t1[3], t2[3];
-    frame(n, t1, t2);
-    const double gm1 = a.gamma - 1.0;
-    double ql[5], dql[3][5], qr[5], dqr[3][5];
-    {
-      double val[5], grad[5][3];
-      eval_poly(a.ceff + (size_t)co * kRec, x, val, grad);
-      double pl = gm1 * (val[4] - 0.5 * (val[1] * val[1] + val[2] * val[2] + val[3] * val[3]) / val[0]);
-      if (!(val[0] > 0.0) || !(pl > 0.0)) {  // R21 positivity fallback
-        atomicAdd((unsigned long long*)&a.ctrl->fallbacks, 1ull);
-#pragma unroll
-        for (int v = 0; v < 5; ++v) {
-          val[v] = a.Q[v * a.ldq + co];
-          grad[v][0] = grad[v][1] = grad[v][2] = 0.0;
-        }
-      }
-      to_local(val, grad, n, t1, t2, ql, dql);
-    }
-    {
-      double val[5], grad[5][3];
-      eval_poly(a.ceff + (size_t)cn * kRec, xr, val, grad);
-      double pr = gm1 * (val[4] - 0.5 * (val[1] * val[1] + val[2] * val[2] + val[3] * val[3]) / val[0]);
-      if (!(val[0] > 0.0) || !(pr > 0.0)) {
-        atomicAdd((unsigned long long*)&a.ctrl->fallbacks, 1ull);
-#pragma unroll
-        for (int v = 0; v < 5; ++v) {
-          val[v] = a.Q[v * a.ldq + cn];
-          grad[v][0] = grad[v][1] = grad[v][2] = 0.0;
-        }
-      }
-      to_local(val, grad, n, t1, t2, qr, dqr);
-    }
-    // ---- Q0 = int_{u>0} psi g_l + int_{u<0} psi g_r ----
-    double Q0[5];
-    {
-      const double K = a.K;
-      const double rpi = 0.56418958354775628;  // 1/sqrt(pi)
-      // left, u > 0
-      double rl = ql[0], Ul = ql[1] / rl, Vl = ql[2] / rl, Wl = ql[3] / rl;
-      double laml = (K + 3.0) * rl / (4.0 * (ql[4] - 0.5 * rl * (Ul * Ul + Vl * Vl + Wl * Wl)));
-      double sl = sqrt(laml);
-      double a0 = 0.5 * erfc(-sl * Ul);
-      double a1 = Ul * a0 + 0.5 * exp(-laml * Ul * Ul) * rpi / sl;
-      double a2 = Ul * a1 + a0 / (2.0 * laml);
-      // right, u < 0
-      double rr = qr[0], Ur = qr[1] / rr, Vr = qr[2] / rr, Wr = qr[3] / rr;
-      double lamr = (K + 3.0) * rr / (4.0 * (qr[4] - 0.5 * rr * (Ur * Ur + Vr * Vr + Wr * Wr)));
-      double sr = sqrt(lamr);
-      double b0 = 0.5 * erfc(sr * Ur);
-      double b1 = Ur * b0 - 0.5 * exp(-lamr * Ur * Ur) * rpi / sr;
-      double b2 = Ur * b1 + b0 / (2.0 * lamr);
-      Q0[0] = rl * a0 + rr * b0;
-      Q0[1] = rl * a1 + rr * b1;
-      Q0[2] = rl * a0 * Vl + rr * b0 * Vr;
-      Q0[3] = rl * a0 * Wl + rr * b0 * Wr;
-      Q0[4] = 0.5 * rl * (a2 + a0 * (Vl * Vl + Wl * Wl + (K + 2.0) / (2.0 * laml))) +
-              0.5 * rr * (b2 + b0 * (Vr * Vr + Wr * Wr + (K + 2.0) / (2.0 * lamr)));
-    }
-    // ---- tau = 0: f = g0 (1 + A t).  F = Euler flux of Q0 and
-    //      d_t F = A_n(Q0) d_t Q0, d_t Q0 = -sum_j A_j(Q0) d_j Q0, with
-    //      d_j Q0 = (d_j Q_l + d_j Q_r)/2 (R9) ----
-    double dtQ0[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      double d0[5], jv[5];
-#pragma unroll
-      for (int v = 0; v < 5; ++v) d0[v] = 0.5 * (dql[j][v] + dqr[j][v]);
-      euler_jvp(j, Q0, d0, gm1, jv);
-#pragma unroll
-      for (int v = 0; v < 5; ++v) dtQ0[v] -= jv[v];
-    }
-    double dF[5];
-    euler_jvp(0, Q0, dtQ0, gm1, dF);
-    // rotate back and weight by omega_G S
-    if (STAGE == 1) {
-      const double u0 = Q0[1] / Q0[0];
-      const double p0 = gm1 * (Q0[4] - 0.5 * (Q0[1] * Q0[1] + Q0[2] * Q0[2] + Q0[3] * Q0[3]) / Q0[0]);
-      const double F[5] = {Q0[1], Q0[1] * u0 + p0, Q0[2] * u0, Q0[3] * u0, u0 * (Q0[4] + p0)};
-      out[0] = wS * F[0];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) out[1 + c] = wS * (F[1] * n[c] + F[2] * t1[c] + F[3] * t2[c]);
-      out[4] = wS * F[4];
-      out[5] = wS * dF[0];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) out[6 + c] = wS * (dF[1] * n[c] + dF[2] * t1[c] + dF[3] * t2[c]);
-      out[9] = wS * dF[4];
-    } else {
-      out[0] = wS * dF[0];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) out[1 + c] = wS * (dF[1] * n[c] + dF[2] * t1[c] + dF[3] * t2[c]);
-      out[4] = wS * dF[4];
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < NOUT; ++k) red[k][threadIdx.x] = out[k];
-  __syncthreads();
-  // face quadrature sum in Gauss-point order (deterministic); NOUT-wide store
-  const int faces_in_block = BLOCK / NGP;
-  for (int e = threadIdx.x; e < faces_in_block * NOUT; e += BLOCK) {
-    const int fl = e / NOUT, k = e - fl * NOUT;
-    const int face = blockIdx.x * faces_in_block + fl;
-    if (face < a.n_faces) {
-      double s = red[k][fl * NGP];
-#pragma unroll
-      for (int q = 1; q < NGP; ++q) s += red[k][fl * NGP + q];
-      double* dst = STAGE == 1 ? a.F1 : a.F2;
-      dst[(size_t)(a.face0 + face) * NOUT + k] = s;
-    }
-  }
-}
+#include "flux.cuh"
 
 // ----------------------------------------------------------------------------
 // a10: L, d_t L and the S2O4 stages
@@ -632,6 +370,15 @@ __global__ void k_step_begin(Ctrl* ctrl, double cfl, double fixed_dt, double t_s
   ctrl->t_next = tn;
   if (dt > 0.0) ctrl->steps += 1;
   ctrl->dtmin_bits = 0x7fefffffffffffffull;  // +max finite, reset for this step's accumulation
+}
+
+// reset the time bookkeeping on the device (no host round trip)
+__global__ void k_reset_ctrl(Ctrl* ctrl, double t) {
+  ctrl->t = t;
+  ctrl->t_next = t;
+  ctrl->dt = 0.0;
+  ctrl->bad_cell = 0x7fffffff;
+  ctrl->dtmin_bits = 0x7fefffffffffffffull;
 }
 
 // state layout conversions for set/get_state: AoS [n][5] in caller order <-> SoA local

@@ -64,6 +64,7 @@ enum { ncclMin = 3 };
 struct Nccl {
   void* h = nullptr;
   int (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  int (*GetUniqueId)(ncclUniqueId*) = nullptr;
   int (*CommDestroy)(ncclComm_t) = nullptr;
   int (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   int (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
@@ -83,6 +84,7 @@ Nccl& nccl() {
     }
     if (!n.h) return;
     n.CommInitRank = (decltype(n.CommInitRank))dlsym(n.h, "ncclCommInitRank");
+    n.GetUniqueId = (decltype(n.GetUniqueId))dlsym(n.h, "ncclGetUniqueId");
     n.CommDestroy = (decltype(n.CommDestroy))dlsym(n.h, "ncclCommDestroy");
     n.Send = (decltype(n.Send))dlsym(n.h, "ncclSend");
     n.Recv = (decltype(n.Recv))dlsym(n.h, "ncclRecv");
@@ -209,6 +211,7 @@ struct hgks_solver {
   std::vector<int> peers;
   std::vector<double> host_stage;  // multi-rank set_state gather
   double* pinned = nullptr;
+  std::vector<cudaEvent_t> event_pool;  // reusable profiling events
 };
 
 namespace {
@@ -219,12 +222,25 @@ void record_launch(hgks_solver* s, const char* name, cudaEvent_t a, cudaEvent_t 
   if (a) k.pending.push_back({a, b});
 }
 
+cudaEvent_t pooled_event(hgks_solver* s) {
+  if (s->event_pool.empty()) {
+    for (int k = 0; k < 64; ++k) {
+      cudaEvent_t e;
+      CUDA_TRY(cudaEventCreate(&e));
+      s->event_pool.push_back(e);
+    }
+  }
+  cudaEvent_t e = s->event_pool.back();
+  s->event_pool.pop_back();
+  return e;
+}
+
 template <class Launch>
 void launch(hgks_solver* s, const char* name, Launch&& fn) {
   cudaEvent_t a = nullptr, b = nullptr;
   if (s->profiling) {
-    CUDA_TRY(cudaEventCreate(&a));
-    CUDA_TRY(cudaEventCreate(&b));
+    a = pooled_event(s);
+    b = pooled_event(s);
     CUDA_TRY(cudaEventRecord(a, s->stream));
   }
   fn();
@@ -282,6 +298,36 @@ void run_recon(hgks_solver* s, const double* Q) {
   }
 }
 
+template <int NV, int BC>
+void launch_flux(hgks_solver* s, const FluxArgs& a, int stage, bool tau0) {
+  constexpr int NGP = NV == 3 ? 3 : 4, B = NV == 3 ? 96 : 128;
+  const int nb = blocks((int64_t)a.n_faces * NGP, B);
+  const char* names[2][2] = {{"k_flux_s1", "k_flux_s2"}, {"k_flux_tau0_s1", "k_flux_tau0_s2"}};
+  const char* nm = BC == 0 ? names[tau0][stage - 1] : (BC == 1 ? "k_flux_wall" : "k_flux_farfield");
+  if (tau0) {
+    if (stage == 1) launch(s, nm, [&] { k_flux<NV, 1, true, BC><<<nb, B, 0, s->stream>>>(a); });
+    else launch(s, nm, [&] { k_flux<NV, 2, true, BC><<<nb, B, 0, s->stream>>>(a); });
+  } else {
+    if (stage == 1) launch(s, nm, [&] { k_flux<NV, 1, false, BC><<<nb, B, 0, s->stream>>>(a); });
+    else launch(s, nm, [&] { k_flux<NV, 2, false, BC><<<nb, B, 0, s->stream>>>(a); });
+  }
+}
+
+template <int NV>
+void run_flux_nv(hgks_solver* s, FluxArgs a, int stage) {
+  const RankPlan& rp = *s->rp;
+  const bool tau0 = s->cfg.tau_mode == 0;
+  const int64_t ranges[3][2] = {{0, rp.n_if}, {rp.n_if, rp.n_wf}, {rp.n_if + rp.n_wf, rp.n_ff}};
+  for (int bc = 0; bc < 3; ++bc) {
+    a.face0 = (int)ranges[bc][0];
+    a.n_faces = (int)ranges[bc][1];
+    if (a.n_faces == 0) continue;
+    if (bc == 0) launch_flux<NV, 0>(s, a, stage, tau0);
+    else if (bc == 1) launch_flux<NV, 1>(s, a, stage, tau0);
+    else launch_flux<NV, 2>(s, a, stage, tau0);
+  }
+}
+
 void run_flux(hgks_solver* s, const double* Q, int stage) {
   const RankPlan& rp = *s->rp;
   FluxArgs a;
@@ -291,25 +337,14 @@ void run_flux(hgks_solver* s, const double* Q, int stage) {
   a.f_cells = s->d.f_cells;
   a.f_geo = s->d.f_geo;
   a.f_stride = rp.f_geo_stride;
-  a.n_faces = (int)rp.n_if;
+  a.n_faces = 0;
   a.face0 = 0;
   a.F1 = s->d.F1;
   a.F2 = s->d.F2;
   a.ctrl = s->d.ctrl;
-  a.gamma = s->cfg.gamma;
-  a.K = (5.0 - 3.0 * s->cfg.gamma) / (s->cfg.gamma - 1.0);
-  if (s->cfg.tau_mode != 0) throw Error(HGKS_E_ARG, "tau_mode 1 (Navier-Stokes collision time) is not built yet");
-  if (rp.n_wf + rp.n_ff > 0) throw Error(HGKS_E_ARG, "wall/farfield faces are not built yet");
-  if (a.n_faces == 0) return;
-  if (s->lay.nv == 3) {
-    int nb = blocks((int64_t)a.n_faces * 3, 96);
-    if (stage == 1) launch(s, "k_flux_tau0_s1", [&] { k_flux_tau0<3, 1><<<nb, 96, 0, s->stream>>>(a); });
-    else launch(s, "k_flux_tau0_s2", [&] { k_flux_tau0<3, 2><<<nb, 96, 0, s->stream>>>(a); });
-  } else {
-    int nb = blocks((int64_t)a.n_faces * 4, 128);
-    if (stage == 1) launch(s, "k_flux_tau0_s1", [&] { k_flux_tau0<4, 1><<<nb, 128, 0, s->stream>>>(a); });
-    else launch(s, "k_flux_tau0_s2", [&] { k_flux_tau0<4, 2><<<nb, 128, 0, s->stream>>>(a); });
-  }
+  a.gp = s->gp;
+  if (s->lay.nv == 3) run_flux_nv<3>(s, a, stage);
+  else run_flux_nv<4>(s, a, stage);
 }
 
 UpdateArgs update_args(hgks_solver* s) {
@@ -384,43 +419,32 @@ void stage(hgks_solver* s, int st) {
 }
 
 void init_dt(hgks_solver* s) {
-  Ctrl h;
-  CUDA_TRY(cudaMemcpyAsync(&h, s->d.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s->stream));
-  CUDA_TRY(cudaStreamSynchronize(s->stream));
-  h.dtmin_bits = 0x7fefffffffffffffull;
-  CUDA_TRY(cudaMemcpyAsync(s->d.ctrl, &h, sizeof(Ctrl), cudaMemcpyHostToDevice, s->stream));
   const int n = (int)s->rp->n_owned;
   launch(s, "k_dt_init", [&] {
     k_dt_init<<<blocks(n, 256), 256, 0, s->stream>>>(s->d.Q, s->ldq, s->d.h_dt, n, s->d.ctrl, s->gp);
   });
   allreduce_dt(s);
-  CUDA_TRY(cudaStreamSynchronize(s->stream));
 }
 
-void upload_state(hgks_solver* s, const double* h_Q, double t, bool sync) {
+// asynchronous on the stream: H2D of the caller's rows, scatter into the local
+// SoA layout, reset time, recompute the CFL bound
+void upload_state(hgks_solver* s, const double* h_Q, double t) {
   const RankPlan& rp = *s->rp;
   const int n = (int)rp.n_owned;
   if (s->n_ranks == 1) {
     CUDA_TRY(cudaMemcpyAsync(s->d.stage_in, h_Q, sizeof(double) * 5 * s->mesh->gm.nc, cudaMemcpyHostToDevice,
                              s->stream));
   } else {
+    // gather this rank's rows into pinned staging (the copy must finish before reuse)
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
     double* hs = s->pinned;
     for (int i = 0; i < n; ++i) std::memcpy(hs + 5 * (size_t)i, h_Q + 5 * rp.l2g[i], 5 * sizeof(double));
     CUDA_TRY(cudaMemcpyAsync(s->d.stage_in, hs, sizeof(double) * 5 * n, cudaMemcpyHostToDevice, s->stream));
   }
   launch(s, "k_scatter_state",
          [&] { k_scatter_state<<<blocks(n, 256), 256, 0, s->stream>>>(s->d.stage_in, s->d.in_row, n, s->d.Q, s->ldq); });
-  // time bookkeeping: t_next = t (k_step_begin starts from it), counters kept
-  Ctrl h;
-  CUDA_TRY(cudaMemcpyAsync(&h, s->d.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s->stream));
-  CUDA_TRY(cudaStreamSynchronize(s->stream));
-  h.t = t;
-  h.t_next = t;
-  h.dt = 0.0;
-  h.bad_cell = INT_MAX;
-  CUDA_TRY(cudaMemcpyAsync(s->d.ctrl, &h, sizeof(Ctrl), cudaMemcpyHostToDevice, s->stream));
+  launch(s, "k_reset_ctrl", [&] { k_reset_ctrl<<<1, 1, 0, s->stream>>>(s->d.ctrl, t); });
   init_dt(s);
-  (void)sync;
 }
 
 }  // namespace
@@ -562,7 +586,8 @@ hgks_status hgks_init(const hgks_mesh* mc, const hgks_config* cfg, const hgks_di
       CUDA_TRY(cudaMallocHost(&s->pinned, sizeof(double) * 5 * std::max<int64_t>(1, rp.n_owned)));
     }
     CUDA_TRY(cudaStreamSynchronize(st));
-    upload_state(s.get(), h_Q0, 0.0, true);
+    upload_state(s.get(), h_Q0, 0.0);
+    CUDA_TRY(cudaStreamSynchronize(st));
     *out = s.release();
   });
 }
@@ -576,6 +601,7 @@ hgks_status hgks_destroy(hgks_solver* s) {
         cudaEventDestroy(e.first);
         cudaEventDestroy(e.second);
       }
+    for (auto e : s->event_pool) cudaEventDestroy(e);
     if (s->comm && nccl().CommDestroy) nccl().CommDestroy(s->comm);
     if (s->pinned) cudaFreeHost(s->pinned);
     delete s;
@@ -616,7 +642,7 @@ hgks_status hgks_step(hgks_solver* s, int32_t n_steps, double t_stop, hgks_step_
 hgks_status hgks_set_state(hgks_solver* s, const double* h_Q, double t) {
   return guard([&] {
     if (!s || !h_Q) throw Error(HGKS_E_ARG, "null argument");
-    upload_state(s, h_Q, t, false);
+    upload_state(s, h_Q, t);
   });
 }
 
@@ -708,8 +734,8 @@ hgks_status hgks_kernel_times(hgks_solver* s, int32_t cap, char (*names)[32], in
         float ms = 0;
         CUDA_TRY(cudaEventElapsedTime(&ms, e.first, e.second));
         st.ms += ms;
-        cudaEventDestroy(e.first);
-        cudaEventDestroy(e.second);
+        s->event_pool.push_back(e.first);
+        s->event_pool.push_back(e.second);
       }
       st.pending.clear();
       if (k < cap) {
@@ -720,6 +746,17 @@ hgks_status hgks_kernel_times(hgks_solver* s, int32_t cap, char (*names)[32], in
       ++k;
     }
     *n = std::min(k, cap);
+  });
+}
+
+hgks_status hgks_nccl_unique_id(uint8_t* out) {
+  return guard([&] {
+    if (!out) throw Error(HGKS_E_ARG, "null argument");
+    Nccl& N = nccl();
+    if (!N.h || !N.GetUniqueId) throw Error(HGKS_E_NCCL, "libnccl.so.2 not found");
+    ncclUniqueId id;
+    NCCL_TRY(N.GetUniqueId(&id));
+    std::memcpy(out, id.internal, 128);
   });
 }
 
