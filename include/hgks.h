@@ -83,11 +83,17 @@ typedef struct {
   double freestream[5];/* rho, U, V, W, p for farfield faces */
 } hgks_config;
 
-/* Distributed context: one process per GPU. */
+#define HGKS_TRANSPORT_NCCL 0      /* one process per GPU, NCCL send/recv + allreduce */
+#define HGKS_TRANSPORT_LOOPBACK 1  /* all ranks in one process on one device, advanced together by
+                                      hgks_group_step (exchange = device copies); for testing the
+                                      partitioned path on a single GPU */
+
+/* Distributed context. */
 typedef struct {
   int32_t rank, n_ranks;
   int32_t device;            /* CUDA ordinal used by this rank */
-  uint8_t nccl_id[128];      /* ncclUniqueId created by rank 0, broadcast by the caller */
+  int32_t transport;         /* HGKS_TRANSPORT_* */
+  uint8_t nccl_id[128];      /* ncclUniqueId created by rank 0, broadcast by the caller (NCCL only) */
 } hgks_dist;
 
 typedef struct {
@@ -159,6 +165,24 @@ hgks_status hgks_debug_residual(hgks_solver* solver, const double* h_Q, double d
 hgks_status hgks_set_profiling(hgks_solver* solver, int32_t enabled);
 hgks_status hgks_kernel_times(hgks_solver* solver, int32_t cap, char (*names)[32], int64_t* launches,
                               double* total_ms, int32_t* n);
+/* Loopback transport: advance the solvers of ranks 0..n-1 (created with
+ * HGKS_TRANSPORT_LOOPBACK on one device and stream, in rank order) by n_steps
+ * S2O4 steps, exchanging ghosts by device copies and reducing min(dt) exactly.
+ * Asynchronous on the shared stream. */
+hgks_status hgks_group_step(hgks_solver* const* solvers, int32_t n, int32_t n_steps, double t_stop);
+
+/* Export rank `rank`'s partition plan (host, for tests and tools): l2g
+ * [n_owned + n_ghost] global ids of the local cells (owned first), peers
+ * [n_peers], per-peer send offsets/counts into send_list [send_cells] (local
+ * owned ids, the owner's global-id order) and receive ranges [recv_off,
+ * recv_off + recv_cnt) of local ghost ids.  Any pointer may be NULL. */
+hgks_status hgks_mesh_plan(const hgks_mesh* mesh, int32_t rank, int64_t* l2g, int32_t* peers, int64_t* send_off,
+                           int64_t* send_cnt, int32_t* send_list, int64_t* recv_off, int64_t* recv_cnt);
+
+/* Create the 128-byte NCCL unique id on one rank (to be broadcast by the caller,
+ * e.g. over torch.distributed, and passed in hgks_dist.nccl_id).  Host only. */
+hgks_status hgks_nccl_unique_id(uint8_t* out);
+
 /* Number of kernels launched by this solver so far (all kinds). */
 hgks_status hgks_launch_count(const hgks_solver* solver, int64_t* launches);
 

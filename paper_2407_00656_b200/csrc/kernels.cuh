@@ -372,6 +372,19 @@ __global__ void k_step_begin(Ctrl* ctrl, double cfl, double fixed_dt, double t_s
   ctrl->dtmin_bits = 0x7fefffffffffffffull;  // +max finite, reset for this step's accumulation
 }
 
+// loopback transport: exact min of the CFL bound over the ranks of one process
+constexpr int kMaxGroup = 16;
+struct GroupCtrl {
+  int n;
+  Ctrl* c[kMaxGroup];
+};
+__global__ void k_group_min(GroupCtrl g) {
+  if (threadIdx.x != 0) return;
+  unsigned long long m = g.c[0]->dtmin_bits;
+  for (int k = 1; k < g.n; ++k) m = g.c[k]->dtmin_bits < m ? g.c[k]->dtmin_bits : m;
+  for (int k = 0; k < g.n; ++k) g.c[k]->dtmin_bits = m;
+}
+
 // reset the time bookkeeping on the device (no host round trip)
 __global__ void k_reset_ctrl(Ctrl* ctrl, double t) {
   ctrl->t = t;

@@ -200,7 +200,7 @@ struct hgks_solver {
   Layout lay;
   hgks_config cfg;
   GasParams gp;
-  int rank = 0, n_ranks = 1, device = 0;
+  int rank = 0, n_ranks = 1, device = 0, transport = HGKS_TRANSPORT_NCCL;
   cudaStream_t stream = nullptr;
   DevArrays d{};
   int ldq = 0;
@@ -363,12 +363,20 @@ UpdateArgs update_args(hgks_solver* s) {
   return u;
 }
 
-void exchange(hgks_solver* s, double* Q) {
-  const RankPlan& rp = *s->rp;
-  if (s->n_ranks == 1 || rp.peers.empty()) return;
-  const int ns = (int)rp.send_list.size();
+void pack(hgks_solver* s, const double* Q) {
+  const int ns = (int)s->rp->send_list.size();
   if (ns > 0)
     launch(s, "k_pack", [&] { k_pack<<<blocks(ns, 256), 256, 0, s->stream>>>(Q, s->ldq, s->d.send_list, ns, s->d.sendbuf); });
+}
+
+// a5: halo exchange of the 3 ghost layers.  NCCL transport: grouped
+// send/recv per peer straight into the contiguous ghost ranges (no unpack).
+// Loopback transport: done by hgks_group_step across the solvers of one process.
+void exchange(hgks_solver* s, double* Q) {
+  const RankPlan& rp = *s->rp;
+  if (s->n_ranks == 1 || rp.peers.empty() || s->transport != HGKS_TRANSPORT_NCCL) return;
+  pack(s, Q);
+  const int ns = (int)rp.send_list.size();
   Nccl& N = nccl();
   NCCL_TRY(N.GroupStart());
   for (size_t p = 0; p < rp.peers.size(); ++p) {
@@ -384,8 +392,9 @@ void exchange(hgks_solver* s, double* Q) {
   NCCL_TRY(N.GroupEnd());
 }
 
+// a4: global min of the CFL bound (exact, order independent)
 void allreduce_dt(hgks_solver* s) {
-  if (s->n_ranks == 1) return;
+  if (s->n_ranks == 1 || s->transport != HGKS_TRANSPORT_NCCL) return;
   NCCL_TRY(nccl().AllReduce(&s->d.ctrl->dtmin_bits, &s->d.ctrl->dtmin_bits, 1, ncclUint64, ncclMin, s->comm,
                             s->stream));
 }
@@ -400,8 +409,8 @@ void bc_ghosts(hgks_solver* s, double* Q) {
   });
 }
 
-void stage(hgks_solver* s, int st) {
-  exchange(s, s->d.Q);
+// everything of one stage after the ghosts are current
+void stage_compute(hgks_solver* s, int st) {
   bc_ghosts(s, s->d.Q);
   run_recon(s, s->d.Q);
   run_flux(s, s->d.Q, st);
@@ -414,8 +423,13 @@ void stage(hgks_solver* s, int st) {
   } else {
     if (nf == 4) launch(s, "k_update2", [&] { k_update2<4><<<blocks(n, 256), 256, 0, s->stream>>>(u); });
     else launch(s, "k_update2", [&] { k_update2<6><<<blocks(n, 256), 256, 0, s->stream>>>(u); });
-    allreduce_dt(s);
   }
+}
+
+void stage(hgks_solver* s, int st) {
+  exchange(s, s->d.Q);
+  stage_compute(s, st);
+  if (st == 2) allreduce_dt(s);
 }
 
 void init_dt(hgks_solver* s) {
@@ -517,6 +531,7 @@ hgks_status hgks_init(const hgks_mesh* mc, const hgks_config* cfg, const hgks_di
     s->cfg = *cfg;
     s->rank = dist ? dist->rank : 0;
     s->n_ranks = dist ? dist->n_ranks : 1;
+    s->transport = dist ? dist->transport : HGKS_TRANSPORT_NCCL;
     if (s->n_ranks != m->gm.n_ranks)
       throw Error(HGKS_E_ARG, "dist->n_ranks differs from the mesh partition (" + std::to_string(m->gm.n_ranks) + ")");
     if (dist) CUDA_TRY(cudaSetDevice(dist->device));
@@ -577,14 +592,14 @@ hgks_status hgks_init(const hgks_mesh* mc, const hgks_config* cfg, const hgks_di
     h.bad_cell = INT_MAX;
     h.dtmin_bits = 0x7fefffffffffffffull;
     up(s->d.ctrl, &h, sizeof(Ctrl));
-    if (s->n_ranks > 1) {
+    if (s->n_ranks > 1 && s->transport == HGKS_TRANSPORT_NCCL) {
       Nccl& N = nccl();
       if (!N.h || !N.CommInitRank) throw Error(HGKS_E_NCCL, "libnccl.so.2 not found");
       ncclUniqueId id;
       std::memcpy(id.internal, dist->nccl_id, 128);
       NCCL_TRY(N.CommInitRank(&s->comm, s->n_ranks, id, s->rank));
-      CUDA_TRY(cudaMallocHost(&s->pinned, sizeof(double) * 5 * std::max<int64_t>(1, rp.n_owned)));
     }
+    if (s->n_ranks > 1) CUDA_TRY(cudaMallocHost(&s->pinned, sizeof(double) * 5 * std::max<int64_t>(1, rp.n_owned)));
     CUDA_TRY(cudaStreamSynchronize(st));
     upload_state(s.get(), h_Q0, 0.0);
     CUDA_TRY(cudaStreamSynchronize(st));
@@ -757,6 +772,71 @@ hgks_status hgks_nccl_unique_id(uint8_t* out) {
     ncclUniqueId id;
     NCCL_TRY(N.GetUniqueId(&id));
     std::memcpy(out, id.internal, 128);
+  });
+}
+
+hgks_status hgks_group_step(hgks_solver* const* ss, int32_t n, int32_t n_steps, double t_stop) {
+  return guard([&] {
+    if (!ss || n < 1 || n > kMaxGroup) throw Error(HGKS_E_ARG, "bad group size");
+    for (int k = 0; k < n; ++k) {
+      if (!ss[k] || ss[k]->transport != HGKS_TRANSPORT_LOOPBACK || ss[k]->n_ranks != n || ss[k]->rank != k)
+        throw Error(HGKS_E_ARG, "hgks_group_step needs the loopback solvers of ranks 0..n-1 in order");
+      if (ss[k]->stream != ss[0]->stream || ss[k]->device != ss[0]->device)
+        throw Error(HGKS_E_ARG, "loopback solvers must share one device and stream");
+    }
+    hgks_solver* s0 = ss[0];
+    GroupCtrl gc;
+    gc.n = n;
+    for (int k = 0; k < n; ++k) gc.c[k] = ss[k]->d.ctrl;
+    auto group_min = [&] { launch(s0, "k_group_min", [&] { k_group_min<<<1, 32, 0, s0->stream>>>(gc); }); };
+    // ghost copies: receiver q, peer p (in-process transport)
+    auto loop_exchange = [&] {
+      for (int k = 0; k < n; ++k) pack(ss[k], ss[k]->d.Q);
+      for (int q = 0; q < n; ++q) {
+        const RankPlan& rq = *ss[q]->rp;
+        for (size_t iq = 0; iq < rq.peers.size(); ++iq) {
+          if (rq.recv_cnt[iq] == 0) continue;
+          const hgks_solver* sp = ss[rq.peers[iq]];
+          const RankPlan& rpp = *sp->rp;
+          size_t ip = std::find(rpp.peers.begin(), rpp.peers.end(), q) - rpp.peers.begin();
+          if (ip == rpp.peers.size() || rpp.send_cnt[ip] != rq.recv_cnt[iq])
+            throw Error(HGKS_E_STATE, "inconsistent exchange plans between ranks");
+          const size_t ns = rpp.send_list.size();
+          for (int v = 0; v < 5; ++v)
+            CUDA_TRY(cudaMemcpyAsync(ss[q]->d.Q + (size_t)v * ss[q]->ldq + rq.recv_off[iq],
+                                     sp->d.sendbuf + (size_t)v * ns + rpp.send_off[ip],
+                                     sizeof(double) * rq.recv_cnt[iq], cudaMemcpyDeviceToDevice, s0->stream));
+        }
+      }
+    };
+    group_min();
+    for (int step = 0; step < n_steps; ++step) {
+      for (int k = 0; k < n; ++k)
+        launch(ss[k], "k_step_begin", [&] {
+          k_step_begin<<<1, 1, 0, s0->stream>>>(ss[k]->d.ctrl, ss[k]->cfg.cfl, ss[k]->cfg.fixed_dt, t_stop);
+        });
+      for (int st = 1; st <= 2; ++st) {
+        loop_exchange();
+        for (int k = 0; k < n; ++k) stage_compute(ss[k], st);
+      }
+      group_min();
+    }
+  });
+}
+
+hgks_status hgks_mesh_plan(const hgks_mesh* mc, int32_t rank, int64_t* l2g, int32_t* peers, int64_t* send_off,
+                           int64_t* send_cnt, int32_t* send_list, int64_t* recv_off, int64_t* recv_cnt) {
+  return guard([&] {
+    if (!mc) throw Error(HGKS_E_ARG, "null mesh");
+    hgks_mesh* m = const_cast<hgks_mesh*>(mc);
+    const RankPlan& rp = m->plan(rank);
+    if (l2g) std::copy(rp.l2g.begin(), rp.l2g.end(), l2g);
+    if (peers) std::copy(rp.peers.begin(), rp.peers.end(), peers);
+    if (send_off) std::copy(rp.send_off.begin(), rp.send_off.end(), send_off);
+    if (send_cnt) std::copy(rp.send_cnt.begin(), rp.send_cnt.end(), send_cnt);
+    if (send_list) std::copy(rp.send_list.begin(), rp.send_list.end(), send_list);
+    if (recv_off) std::copy(rp.recv_off.begin(), rp.recv_off.end(), recv_off);
+    if (recv_cnt) std::copy(rp.recv_cnt.begin(), rp.recv_cnt.end(), recv_cnt);
   });
 }
 

@@ -27,7 +27,9 @@ ERRORS = {0: "OK", 1: "E_ARG", 2: "E_MESH", 3: "E_STENCIL", 4: "E_CUDA", 5: "E_N
 # every symbol include/hgks.h declares (checked by tests/test_abi.py)
 EXPORTS = ["hgks_mesh_create", "hgks_mesh_destroy", "hgks_mesh_info", "hgks_workspace_size", "hgks_init",
            "hgks_destroy", "hgks_step", "hgks_set_state", "hgks_get_state", "hgks_debug_residual",
-           "hgks_set_profiling", "hgks_kernel_times", "hgks_launch_count", "hgks_last_error", "hgks_version"]
+           "hgks_set_profiling", "hgks_kernel_times", "hgks_launch_count", "hgks_nccl_unique_id", "hgks_group_step", "hgks_mesh_plan",
+           "hgks_last_error", "hgks_version"]
+TRANSPORT_NCCL, TRANSPORT_LOOPBACK = 0, 1
 
 
 class MeshDesc(C.Structure):
@@ -44,7 +46,8 @@ class Config(C.Structure):
 
 
 class Dist(C.Structure):
-    _fields_ = [("rank", C.c_int32), ("n_ranks", C.c_int32), ("device", C.c_int32), ("nccl_id", C.c_uint8 * 128)]
+    _fields_ = [("rank", C.c_int32), ("n_ranks", C.c_int32), ("device", C.c_int32), ("transport", C.c_int32),
+                ("nccl_id", C.c_uint8 * 128)]
 
 
 class MeshStats(C.Structure):
@@ -100,6 +103,9 @@ def lib(build_if_needed: bool = True):
         L.hgks_set_profiling.argtypes = [C.c_void_p, C.c_int32]
         L.hgks_kernel_times.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, _i64p, _dp, _i32p]
         L.hgks_launch_count.argtypes = [C.c_void_p, _i64p]
+        L.hgks_nccl_unique_id.argtypes = [C.c_void_p]
+        L.hgks_group_step.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_double]
+        L.hgks_mesh_plan.argtypes = [C.c_void_p, C.c_int32, _i64p, _i32p, _i64p, _i64p, _i32p, _i64p, _i64p]
         _lib = L
     return _lib
 
@@ -130,6 +136,12 @@ class SolverConfig:
     def c(self) -> Config:
         return Config(self.gamma, self.cfl, self.fixed_dt, self.tau_mode, self.c1, self.mu_inf, self.t_inf,
                       self.mu_exp, self.eps, self.omega_pow, (C.c_double * 5)(*self.freestream))
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(lib().hgks_nccl_unique_id(C.cast(buf, C.c_void_p)))
+    return bytes(buf)
 
 
 class Mesh:
@@ -166,17 +178,38 @@ class Mesh:
         _check(lib().hgks_mesh_info(self.h, rank, C.byref(st)))
         return st.as_dict()
 
+    def plan(self, rank: int = 0) -> dict:
+        """Partition plan of one rank (hgks_mesh_plan): local->global ids and per-peer exchange lists."""
+        st = self.info(rank)
+        nl = st["n_owned"] + st["n_ghost"]
+        npr = st["n_peers"]
+        l2g = np.zeros(nl, np.int64)
+        peers = np.zeros(max(npr, 1), np.int32)
+        so = np.zeros(max(npr, 1), np.int64); sc = np.zeros(max(npr, 1), np.int64)
+        ro = np.zeros(max(npr, 1), np.int64); rc = np.zeros(max(npr, 1), np.int64)
+        sl = np.zeros(max(st["send_cells"], 1), np.int32)
+        _check(lib().hgks_mesh_plan(self.h, rank, _p(l2g, _i64p), _p(peers, _i32p), _p(so, _i64p), _p(sc, _i64p),
+                                    _p(sl, _i32p), _p(ro, _i64p), _p(rc, _i64p)))
+        return dict(n_owned=st["n_owned"], l2g=l2g, peers=peers[:npr], send_off=so[:npr], send_cnt=sc[:npr],
+                    send_list=sl[:st["send_cells"]], recv_off=ro[:npr], recv_cnt=rc[:npr])
+
     def workspace_size(self, cfg: SolverConfig, rank: int = 0) -> int:
         n = C.c_size_t()
         _check(lib().hgks_workspace_size(self.h, C.byref(cfg.c()), rank, C.byref(n)))
         return int(n.value)
 
 
+def group_step(solvers, n_steps: int, t_stop: float = 0.0):
+    """Advance loopback solvers of ranks 0..n-1 together (hgks_group_step)."""
+    arr = (C.c_void_p * len(solvers))(*[s.h for s in solvers])
+    _check(lib().hgks_group_step(arr, len(solvers), n_steps, t_stop))
+
+
 class Solver:
     """hgks_solver on one CUDA device.  ``Q0``: [n_cells_global, 5] float64 (caller order)."""
 
     def __init__(self, mesh: Mesh, Q0, cfg: SolverConfig | None = None, device=None, rank: int = 0,
-                 nccl_id: bytes | None = None):
+                 nccl_id: bytes | None = None, transport: int = TRANSPORT_NCCL):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("hgks needs a CUDA device (no CPU fallback)")
@@ -192,7 +225,8 @@ class Solver:
         Q0 = np.ascontiguousarray(Q0, np.float64)
         dist = None
         if mesh.n_ranks > 1:
-            dist = Dist(rank, mesh.n_ranks, self.device.index, (C.c_uint8 * 128)(*nccl_id))
+            nid = nccl_id if nccl_id is not None else bytes(128)
+            dist = Dist(rank, mesh.n_ranks, self.device.index, transport, (C.c_uint8 * 128)(*nid))
         h = C.c_void_p()
         _check(lib().hgks_init(mesh.h, C.byref(self.cfg.c()), C.byref(dist) if dist else None, C.c_void_p(ptr),
                                nbytes, C.c_void_p(self.stream.cuda_stream), _p(Q0), C.byref(h)))

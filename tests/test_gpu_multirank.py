@@ -1,0 +1,69 @@
+"""Partitioned GPU path on one B200 via the loopback transport (all ranks in one
+process, ghosts exchanged by device copies, min(dt) exact): results must be
+BITWISE equal to the single-rank run, and so within the oracle
+bar.  The NCCL transport moves the same bytes with the same plans."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2407_00656_b200 import hgks, workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+def run_ranks(mi, Q0, cfg, world, steps, t_stop=0.0):
+    mesh = hgks.Mesh(mi, n_ranks=world)
+    solvers = [hgks.Solver(mesh, Q0, cfg, rank=r, transport=hgks.TRANSPORT_LOOPBACK) for r in range(world)]
+    hgks.group_step(solvers, steps, t_stop)
+    Q = np.empty_like(Q0)
+    t = None
+    for s in solvers:
+        info = s.step(0)  # sync + positivity check
+        Qr, gid, tr = s.get_state()
+        Q[gid] = Qr
+        t = tr if t is None else t
+        assert tr == t
+    return Q, t, mesh
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_kuhn_multirank_bitwise(cuda_ok, world):
+    mi = W.kuhn_box(10, 8, 8, h=0.2)
+    Q0 = W.advection_ic(mi)
+    cfg = hgks.SolverConfig(cfl=0.3)
+    s1 = hgks.Solver(hgks.Mesh(mi), Q0, cfg)
+    s1.step(10)
+    Q1, _, t1 = s1.get_state()
+    Qn, tn, mesh = run_ranks(mi, Q0, cfg, world, 10)
+    assert tn == t1
+    assert np.array_equal(Qn, Q1), np.abs(Qn - Q1).max()
+    assert mesh.info(0)["n_peers"] >= 1
+
+
+def test_sphere_multirank_bitwise_and_oracle(cuda_ok):
+    mi = W.sphere_shell(5)
+    fs = (1.0, 1.5, 0.0, 0.0, 1 / 1.4)
+    Q0 = W.random_smooth_ic(mi, seed=118, base=fs, amp=0.01)
+    cfg = hgks.SolverConfig(cfl=0.5, tau_mode=1, mu_inf=1.5 / 300, c1=1.0, t_inf=1 / 1.4, freestream=fs)
+    s1 = hgks.Solver(hgks.Mesh(mi), Q0, cfg)
+    s1.step(10)
+    Q1, _, t1 = s1.get_state()
+    Q4, t4, _ = run_ranks(mi, Q0, cfg, 4, 10)
+    assert t4 == t1 and np.array_equal(Q4, Q1)
+    oc = O.OracleConfig(cfl=0.5, tau_mode=1, mu_inf=1.5 / 300, c1=1.0, t_inf=1 / 1.4, freestream=fs)
+    o = O.OracleSolver(O.OracleMesh(mi), Q0, oc)
+    o.step(10)
+    Qo, *_ = o.state()
+    err = np.abs(Q4 - Qo).max(0) / np.abs(Qo).max(0)
+    assert err.max() <= 1e-10, err
+
+
+def test_multirank_t_stop(cuda_ok):
+    mi = W.kuhn_box(8)
+    Q0 = W.advection_ic(mi)
+    cfg = hgks.SolverConfig(cfl=0.3)
+    Q2, t2, _ = run_ranks(mi, Q0, cfg, 2, 50, t_stop=0.04)
+    s1 = hgks.Solver(hgks.Mesh(mi), Q0, cfg)
+    s1.step(50, t_stop=0.04)
+    Q1, _, t1 = s1.get_state()
+    assert t1 == t2 == 0.04 and np.array_equal(Q1, Q2)
