@@ -160,7 +160,8 @@ hgks_status hgks_debug_residual(hgks_solver* solver, const double* h_Q, double d
 
 /* Per-kernel device time: when enabled, every kernel launch is bracketed by
  * CUDA events on the solver stream.  hgks_kernel_times fills up to `cap`
- * entries of (name, launches, total milliseconds) and returns the count in *n.
+ * entries of (name, timed launches, total milliseconds over exactly those
+ * launches) and returns the count in *n.
  * Synchronises the stream. */
 hgks_status hgks_set_profiling(hgks_solver* solver, int32_t enabled);
 hgks_status hgks_kernel_times(hgks_solver* solver, int32_t cap, char (*names)[32], int64_t* launches,

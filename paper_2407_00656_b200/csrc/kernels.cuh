@@ -112,6 +112,103 @@ struct ReconArgs {
   int omega_pow;
 };
 
+// One thread per (cell, conserved variable): the smoothness indicators and the
+// nonlinear weights are per variable (R12), so the five variables of a cell
+// are independent.  Block = CT cells x 5 variables; warp y = variable y of CT
+// consecutive cells, so every operator load is a coalesced 256-byte row read
+// by 5 warps (one HBM fetch, L1 hits for the other four) and each thread keeps
+// only 9 + 3M accumulators live (4x fewer registers -> 4x more warps in flight
+// for the stencil gathers than one thread per cell).
+template <int K, int M, int NM, int CT>
+__global__ void __launch_bounds__(CT * 5) k_recon_v(ReconArgs a) {
+  const int r = blockIdx.x * CT + threadIdx.x;
+  const int v = threadIdx.y;
+  if (r >= a.n_recon) return;
+  const int R = a.n_recon;
+  const int ci = __ldg(a.recon_cell + r);
+  const double* __restrict__ Qv = a.Q + (size_t)v * a.ldq;
+  const double qi = __ldg(Qv + ci);
+  const double* __restrict__ op = a.op + r;
+  // ---- P_0: c[d] = sum_k A0+[d][k] (Q_k - Q_i) ----
+  double c[9];
+#pragma unroll
+  for (int d = 0; d < 9; ++d) c[d] = 0.0;
+#pragma unroll 7
+  for (int k = 0; k < K; ++k) {
+    const double dq = __ldg(Qv + __ldg(a.st_id + k * R + r)) - qi;
+#pragma unroll
+    for (int d = 0; d < 9; ++d) c[d] = fma(__ldg(op + (size_t)(d * K + k) * R), dq, c[d]);
+  }
+  // ---- P_m over the sub-stencils ----
+  double b[M][3];
+  const double* __restrict__ opm = op + (size_t)(9 * K) * R;
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    b[m][0] = b[m][1] = b[m][2] = 0.0;
+#pragma unroll
+    for (int j = 0; j < NM; ++j) {
+      const int s = __ldg(a.sub_slot + (m * NM + j) * R + r);
+      const double dq = __ldg(Qv + __ldg(a.st_id + s * R + r)) - qi;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) b[m][d] = fma(__ldg(opm + (size_t)((m * 3 + d) * NM + j) * R), dq, b[m][d]);
+    }
+  }
+  const double V23 = __ldg(a.geo + r), V43 = __ldg(a.geo + R + r);
+  double m2[6];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) m2[q] = __ldg(a.geo + (2 + q) * R + r);
+  // ---- smoothness indicators (closed form SURVEY A.5) ----
+  double beta0;
+  {
+    const double gx[3] = {2.0 * c[3], c[6], c[7]}, gy[3] = {c[6], 2.0 * c[4], c[8]}, gz[3] = {c[7], c[8], 2.0 * c[5]};
+    auto quadf = [&](const double g[3]) {
+      return m2[0] * g[0] * g[0] + m2[1] * g[1] * g[1] + m2[2] * g[2] * g[2] +
+             2.0 * (m2[3] * g[0] * g[1] + m2[4] * g[0] * g[2] + m2[5] * g[1] * g[2]);
+    };
+    const double s1 = c[0] * c[0] + c[1] * c[1] + c[2] * c[2] + quadf(gx) + quadf(gy) + quadf(gz);
+    const double s2 = 4.0 * (c[3] * c[3] + c[4] * c[4] + c[5] * c[5]) + c[6] * c[6] + c[7] * c[7] + c[8] * c[8];
+    beta0 = V23 * s1 + V43 * s2;
+  }
+  double betam[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) betam[m] = V23 * (b[m][0] * b[m][0] + b[m][1] * b[m][1] + b[m][2] * b[m][2]);
+  // ---- nonlinear weights and the collapse ----
+  const double gm = 0.025, g0 = 1.0 - 0.025 * M;
+  double tz = 0.0;
+#pragma unroll
+  for (int m = 0; m < M; ++m) tz += fabs(beta0 - betam[m]);
+  tz *= (1.0 / M);
+  const double r0 = tz / (beta0 + a.eps);
+  const double w0 = g0 * (1.0 + (a.omega_pow == 2 ? r0 * r0 : r0));
+  double wm[M], sum = w0;
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const double rm = tz / (betam[m] + a.eps);
+    wm[m] = gm * (1.0 + (a.omega_pow == 2 ? rm * rm : rm));
+    sum += wm[m];
+  }
+  const double inv = 1.0 / sum;
+  const double al0 = w0 * inv / g0;  // omega-bar_0 / gamma_0
+  double lin[3] = {al0 * c[0], al0 * c[1], al0 * c[2]};
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const double alm = wm[m] * inv - al0 * gm;  // omega-bar_m - omega-bar_0 gamma_m / gamma_0
+#pragma unroll
+    for (int d = 0; d < 3; ++d) lin[d] = fma(alm, b[m][d], lin[d]);
+  }
+  double quad[6];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) quad[q] = al0 * c[3 + q];
+  const double cst = qi - (quad[0] * m2[0] + quad[1] * m2[1] + quad[2] * m2[2] + quad[3] * m2[3] + quad[4] * m2[4] +
+                           quad[5] * m2[5]);
+  double* __restrict__ out = a.ceff + (size_t)ci * kRec;
+  out[v] = cst;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) out[5 + d * 5 + v] = lin[d];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) out[20 + q * 5 + v] = quad[q];
+}
+
 template <int K, int M, int NM, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) k_recon(ReconArgs a) {
   extern __shared__ double sb[];  // [M*15][BLOCK] sub-stencil slopes
