@@ -13,8 +13,7 @@
 // (included from kernels.cuh inside namespace hgks)
 
 struct FluxArgs {
-  const double* __restrict__ Q;
-  int ldq;
+  const double* __restrict__ Q;  // [n_local][QS]
   const double* __restrict__ ceff;
   const int* __restrict__ f_cells;  // [n][2]
   const double* __restrict__ f_geo; // [n][stride]
@@ -28,16 +27,20 @@ struct FluxArgs {
 };
 
 // evaluate the effective polynomial of a cell at X (relative to its centroid)
+// evaluate the effective polynomial of a cell at X (relative to its centroid);
+// record layout rec[10 v + (const, x, y, z, xx, yy, zz, xy, xz, yz)], read as
+// 16-byte vectors (80 bytes per variable)
 __device__ __forceinline__ void eval_poly(const double* __restrict__ rec, const double X[3], double val[5],
                                           double grad[5][3]) {
   const double xx = X[0] * X[0], yy = X[1] * X[1], zz = X[2] * X[2];
   const double xy = X[0] * X[1], xz = X[0] * X[2], yz = X[1] * X[2];
+  const double2* r2 = reinterpret_cast<const double2*>(rec);
 #pragma unroll
   for (int v = 0; v < 5; ++v) {
-    const double c0 = __ldg(rec + v);
-    const double lx = __ldg(rec + 5 + v), ly = __ldg(rec + 10 + v), lz = __ldg(rec + 15 + v);
-    const double qxx = __ldg(rec + 20 + v), qyy = __ldg(rec + 25 + v), qzz = __ldg(rec + 30 + v);
-    const double qxy = __ldg(rec + 35 + v), qxz = __ldg(rec + 40 + v), qyz = __ldg(rec + 45 + v);
+    const double2 a0 = __ldg(r2 + 5 * v), a1 = __ldg(r2 + 5 * v + 1), a2 = __ldg(r2 + 5 * v + 2),
+                  a3 = __ldg(r2 + 5 * v + 3), a4 = __ldg(r2 + 5 * v + 4);
+    const double c0 = a0.x, lx = a0.y, ly = a1.x, lz = a1.y, qxx = a2.x, qyy = a2.y, qzz = a3.x, qxy = a3.y,
+                 qxz = a4.x, qyz = a4.y;
     val[v] = c0 + lx * X[0] + ly * X[1] + lz * X[2] + qxx * xx + qyy * yy + qzz * zz + qxy * xy + qxz * xz + qyz * yz;
     grad[v][0] = lx + 2.0 * qxx * X[0] + qxy * X[1] + qxz * X[2];
     grad[v][1] = ly + 2.0 * qyy * X[1] + qxy * X[0] + qyz * X[2];
@@ -60,12 +63,13 @@ __device__ __forceinline__ void face_gp(const double* __restrict__ fg, int g, do
     const double a2 = sqrt(nn[0] * nn[0] + nn[1] * nn[1] + nn[2] * nn[2]);
     const double l0 = g == 0 ? 2.0 / 3.0 : 1.0 / 6.0, l1 = g == 1 ? 2.0 / 3.0 : 1.0 / 6.0,
                  l2 = g == 2 ? 2.0 / 3.0 : 1.0 / 6.0;
+    const double ia = 1.0 / a2;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       x[a] = l0 * p[0][a] + l1 * p[1][a] + l2 * p[2][a];
-      n[a] = nn[a] / a2;
+      n[a] = nn[a] * ia;
     }
-    wS = a2 / 6.0;
+    wS = a2 * (1.0 / 6.0);
   } else {
     double p[4][3];
 #pragma unroll
@@ -83,8 +87,9 @@ __device__ __forceinline__ void face_gp(const double* __restrict__ fg, int g, do
     }
     double nn[3] = {ds[1] * dt[2] - ds[2] * dt[1], ds[2] * dt[0] - ds[0] * dt[2], ds[0] * dt[1] - ds[1] * dt[0]};
     const double an = sqrt(nn[0] * nn[0] + nn[1] * nn[1] + nn[2] * nn[2]);
+    const double ia = 1.0 / an;
 #pragma unroll
-    for (int a = 0; a < 3; ++a) n[a] = nn[a] / an;
+    for (int a = 0; a < 3; ++a) n[a] = nn[a] * ia;
     wS = 0.25 * an;
   }
 }
@@ -113,10 +118,11 @@ __device__ __forceinline__ void to_local(const double val[5], const double grad[
   q[1] = val[1] * n[0] + val[2] * n[1] + val[3] * n[2];
   q[2] = val[1] * t1[0] + val[2] * t1[1] + val[3] * t1[2];
   q[3] = val[1] * t2[0] + val[2] * t2[1] + val[3] * t2[2];
-  const double* dirs[3] = {n, t1, t2};
+  // frame matrix rows (n, t1, t2), indexed with compile-time j only (stays in registers)
+  const double Rm[3][3] = {{n[0], n[1], n[2]}, {t1[0], t1[1], t1[2]}, {t2[0], t2[1], t2[2]}};
 #pragma unroll
   for (int j = 0; j < 3; ++j) {
-    const double* e = dirs[j];
+    const double* e = Rm[j];
     double d[5];
 #pragma unroll
     for (int v = 0; v < 5; ++v) d[v] = grad[v][0] * e[0] + grad[v][1] * e[1] + grad[v][2] * e[2];
@@ -129,18 +135,32 @@ __device__ __forceinline__ void to_local(const double val[5], const double grad[
 }
 
 // Euler-flux Jacobian-vector product along local axis j: dF_j = (dF_j/dQ) dq
-__device__ __forceinline__ void euler_jvp(int j, const double Q[5], const double dq[5], double gm1, double out[5]) {
-  const double rho = Q[0];
-  const double inv = 1.0 / rho;
-  const double u[3] = {Q[1] * inv, Q[2] * inv, Q[3] * inv};
-  const double p = gm1 * (Q[4] - 0.5 * (Q[1] * u[0] + Q[2] * u[1] + Q[3] * u[2]));
-  const double du[3] = {(dq[1] - u[0] * dq[0]) * inv, (dq[2] - u[1] * dq[0]) * inv, (dq[3] - u[2] * dq[0]) * inv};
-  const double dp = gm1 * (dq[4] - (u[0] * dq[1] + u[1] * dq[2] + u[2] * dq[3]) +
-                           0.5 * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]) * dq[0]);
+// Euler state quantities shared by the Jacobian-vector products below
+struct EulerState {
+  double Q[5], inv, u[3], p, H, q2h;  // H = rhoE + p, q2h = |u|^2 / 2
+};
+__device__ __forceinline__ EulerState euler_state(const double Q[5], double gm1) {
+  EulerState e;
+#pragma unroll
+  for (int v = 0; v < 5; ++v) e.Q[v] = Q[v];
+  e.inv = 1.0 / Q[0];
+  e.u[0] = Q[1] * e.inv;
+  e.u[1] = Q[2] * e.inv;
+  e.u[2] = Q[3] * e.inv;
+  e.q2h = 0.5 * (e.u[0] * e.u[0] + e.u[1] * e.u[1] + e.u[2] * e.u[2]);
+  e.p = gm1 * (Q[4] - Q[0] * e.q2h);
+  e.H = Q[4] + e.p;
+  return e;
+}
+// Euler-flux Jacobian-vector product along local axis j: dF_j = (dF_j/dQ) dq
+__device__ __forceinline__ void euler_jvp(int j, const EulerState& e, const double dq[5], double gm1, double out[5]) {
+  const double du[3] = {(dq[1] - e.u[0] * dq[0]) * e.inv, (dq[2] - e.u[1] * dq[0]) * e.inv,
+                        (dq[3] - e.u[2] * dq[0]) * e.inv};
+  const double dp = gm1 * (dq[4] - (e.u[0] * dq[1] + e.u[1] * dq[2] + e.u[2] * dq[3]) + e.q2h * dq[0]);
   out[0] = dq[1 + j];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) out[1 + k] = dq[1 + j] * u[k] + Q[1 + j] * du[k] + (k == j ? dp : 0.0);
-  out[4] = du[j] * (Q[4] + p) + u[j] * (dq[4] + dp);
+  for (int k = 0; k < 3; ++k) out[1 + k] = dq[1 + j] * e.u[k] + e.Q[1 + j] * du[k] + (k == j ? dp : 0.0);
+  out[4] = du[j] * e.H + e.u[j] * (dq[4] + dp);
 }
 
 
@@ -321,20 +341,20 @@ __device__ __forceinline__ TimeCoef time_coef(double delta, double tau) {
 __device__ __forceinline__ void equilibrium_state(const double ql[5], const double qr[5], double K, double Q0[5]) {
   const double rpi = 0.56418958354775628;  // 1/sqrt(pi)
   const Prim l = prim_of(ql, K), r = prim_of(qr, K);
-  const double sl = sqrt(l.lam);
-  const double a0 = 0.5 * erfc(-sl * l.U);
-  const double a1 = l.U * a0 + 0.5 * exp(-l.lam * l.U * l.U) * rpi / sl;
-  const double a2 = l.U * a1 + a0 / (2.0 * l.lam);
-  const double sr = sqrt(r.lam);
-  const double b0 = 0.5 * erfc(sr * r.U);
-  const double b1 = r.U * b0 - 0.5 * exp(-r.lam * r.U * r.U) * rpi / sr;
-  const double b2 = r.U * b1 + b0 / (2.0 * r.lam);
+  const double hl = 0.5 / l.lam, hr = 0.5 / r.lam;  // 1/(2 lambda)
+  const double isl = rsqrt(l.lam), isr = rsqrt(r.lam);
+  const double a0 = 0.5 * erfc(-(l.lam * isl) * l.U);
+  const double a1 = l.U * a0 + 0.5 * exp(-l.lam * l.U * l.U) * rpi * isl;
+  const double a2 = l.U * a1 + a0 * hl;
+  const double b0 = 0.5 * erfc((r.lam * isr) * r.U);
+  const double b1 = r.U * b0 - 0.5 * exp(-r.lam * r.U * r.U) * rpi * isr;
+  const double b2 = r.U * b1 + b0 * hr;
   Q0[0] = l.rho * a0 + r.rho * b0;
   Q0[1] = l.rho * a1 + r.rho * b1;
   Q0[2] = l.rho * a0 * l.V + r.rho * b0 * r.V;
   Q0[3] = l.rho * a0 * l.W + r.rho * b0 * r.W;
-  Q0[4] = 0.5 * l.rho * (a2 + a0 * (l.V * l.V + l.W * l.W + (K + 2.0) / (2.0 * l.lam))) +
-          0.5 * r.rho * (b2 + b0 * (r.V * r.V + r.W * r.W + (K + 2.0) / (2.0 * r.lam)));
+  Q0[4] = 0.5 * l.rho * (a2 + a0 * (l.V * l.V + l.W * l.W + (K + 2.0) * hl)) +
+          0.5 * r.rho * (b2 + b0 * (r.V * r.V + r.W * r.W + (K + 2.0) * hr));
 }
 
 // one side of Eq. (flux) for a Maxwellian (with its slopes) accumulated into I_half, I_full
@@ -400,7 +420,7 @@ __device__ __forceinline__ void boundary_right(const double ql[5], const double 
 }
 
 template <int NV, int STAGE, bool TAU0, int BC>
-__global__ void __launch_bounds__(NV == 3 ? 96 : 128) k_flux(FluxArgs a) {
+__global__ void __launch_bounds__(NV == 3 ? 96 : 128, TAU0 ? (NV == 3 ? 5 : 4) : 1) k_flux(FluxArgs a) {
   constexpr int NGP = NV == 3 ? 3 : 4;
   constexpr int BLOCK = NV == 3 ? 96 : 128;
   constexpr int NOUT = STAGE == 1 ? 10 : 5;
@@ -421,17 +441,90 @@ __global__ void __launch_bounds__(NV == 3 ? 96 : 128) k_flux(FluxArgs a) {
     frame(n, t1, t2);
     const double K = a.gp.K;
     const double gm1 = a.gp.gamma - 1.0;
+    // positivity check without a division: for rho > 0, p > 0  <=>  rho*rhoE - |m|^2/2 > 0 (R21)
+    auto admissible = [](const double q[5]) {
+      return q[0] > 0.0 && (q[0] * q[4] - 0.5 * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3])) > 0.0;
+    };
+    auto rotate_value = [&](const double v5[5], double q[5]) {
+      q[0] = v5[0];
+      q[4] = v5[4];
+      q[1] = v5[1] * n[0] + v5[2] * n[1] + v5[3] * n[2];
+      q[2] = v5[1] * t1[0] + v5[2] * t1[1] + v5[3] * t1[2];
+      q[3] = v5[1] * t2[0] + v5[2] * t2[1] + v5[3] * t2[2];
+    };
+    double F[5], dF[5];
+    if (TAU0 && BC == 0) {
+      // tau = 0 interior face: only the average of the two gradients enters (R9),
+      // so it is summed in the global frame and rotated once
+      double ql[5], qr[5], gs[5][3];
+      {
+        double vl[5];
+        eval_poly(a.ceff + (size_t)co * kRec, x, vl, gs);
+        if (!admissible(vl)) {
+          atomicAdd((unsigned long long*)&a.ctrl->fallbacks, 1ull);
+#pragma unroll
+          for (int v = 0; v < 5; ++v) {
+            vl[v] = a.Q[(size_t)co * QS + v];
+            gs[v][0] = gs[v][1] = gs[v][2] = 0.0;
+          }
+        }
+        rotate_value(vl, ql);
+      }
+      {
+        const int cn = __ldg(a.f_cells + 2 * f + 1);
+        const double xr[3] = {x[0] + __ldg(fg + 3 * NV), x[1] + __ldg(fg + 3 * NV + 1),
+                              x[2] + __ldg(fg + 3 * NV + 2)};
+        double vr[5], gr[5][3];
+        eval_poly(a.ceff + (size_t)cn * kRec, xr, vr, gr);
+        if (!admissible(vr)) {
+          atomicAdd((unsigned long long*)&a.ctrl->fallbacks, 1ull);
+#pragma unroll
+          for (int v = 0; v < 5; ++v) {
+            vr[v] = a.Q[(size_t)cn * QS + v];
+            gr[v][0] = gr[v][1] = gr[v][2] = 0.0;
+          }
+        }
+        rotate_value(vr, qr);
+#pragma unroll
+        for (int v = 0; v < 5; ++v)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) gs[v][c] = 0.5 * (gs[v][c] + gr[v][c]);
+      }
+      double dq0[3][5];
+      {
+        double zero[5] = {0, 0, 0, 0, 0}, dummy[5];
+        to_local(zero, gs, n, t1, t2, dummy, dq0);
+      }
+      double Q0[5];
+      equilibrium_state(ql, qr, K, Q0);
+      // f = g0 (1 + A t): F = Euler flux of Q0, d_t F = A_n(Q0) d_t Q0,
+      // d_t Q0 = -sum_j A_j(Q0) d_j Q0
+      const EulerState es = euler_state(Q0, gm1);
+      double dtQ0[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        double jv[5];
+        euler_jvp(j, es, dq0[j], gm1, jv);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) dtQ0[v] -= jv[v];
+      }
+      euler_jvp(0, es, dtQ0, gm1, dF);
+      F[0] = Q0[1];
+      F[1] = Q0[1] * es.u[0] + es.p;
+      F[2] = Q0[2] * es.u[0];
+      F[3] = Q0[3] * es.u[0];
+      F[4] = es.u[0] * es.H;
+    } else {
     double ql[5], dql[3][5], qr[5], dqr[3][5];
     double vl[5];
     {
       double grad[5][3];
       eval_poly(a.ceff + (size_t)co * kRec, x, vl, grad);
-      const double pl = gm1 * (vl[4] - 0.5 * (vl[1] * vl[1] + vl[2] * vl[2] + vl[3] * vl[3]) / vl[0]);
-      if (!(vl[0] > 0.0) || !(pl > 0.0)) {  // R21 positivity fallback
+      if (!admissible(vl)) {  // R21 positivity fallback
         atomicAdd((unsigned long long*)&a.ctrl->fallbacks, 1ull);
 #pragma unroll
         for (int v = 0; v < 5; ++v) {
-          vl[v] = a.Q[v * a.ldq + co];
+          vl[v] = a.Q[(size_t)co * QS + v];
           grad[v][0] = grad[v][1] = grad[v][2] = 0.0;
         }
       }
@@ -442,12 +535,11 @@ __global__ void __launch_bounds__(NV == 3 ? 96 : 128) k_flux(FluxArgs a) {
       const double xr[3] = {x[0] + __ldg(fg + 3 * NV), x[1] + __ldg(fg + 3 * NV + 1), x[2] + __ldg(fg + 3 * NV + 2)};
       double val[5], grad[5][3];
       eval_poly(a.ceff + (size_t)cn * kRec, xr, val, grad);
-      const double pr = gm1 * (val[4] - 0.5 * (val[1] * val[1] + val[2] * val[2] + val[3] * val[3]) / val[0]);
-      if (!(val[0] > 0.0) || !(pr > 0.0)) {
+      if (!admissible(val)) {
         atomicAdd((unsigned long long*)&a.ctrl->fallbacks, 1ull);
 #pragma unroll
         for (int v = 0; v < 5; ++v) {
-          val[v] = a.Q[v * a.ldq + cn];
+          val[v] = a.Q[(size_t)cn * QS + v];
           grad[v][0] = grad[v][1] = grad[v][2] = 0.0;
         }
       }
@@ -457,28 +549,24 @@ __global__ void __launch_bounds__(NV == 3 ? 96 : 128) k_flux(FluxArgs a) {
     }
     double Q0[5];
     equilibrium_state(ql, qr, K, Q0);
-    double F[5], dF[5];
     if (TAU0) {
-      // f = g0 (1 + A t): F = Euler flux of Q0, d_t F = A_n(Q0) d_t Q0,
-      // d_t Q0 = -sum_j A_j(Q0) d_j Q0, d_j Q0 = (d_j Q_l + d_j Q_r)/2 (R9)
       double dtQ0[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+      const EulerState es = euler_state(Q0, gm1);
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
         double d0[5], jv[5];
 #pragma unroll
         for (int v = 0; v < 5; ++v) d0[v] = 0.5 * (dql[j][v] + dqr[j][v]);
-        euler_jvp(j, Q0, d0, gm1, jv);
+        euler_jvp(j, es, d0, gm1, jv);
 #pragma unroll
         for (int v = 0; v < 5; ++v) dtQ0[v] -= jv[v];
       }
-      euler_jvp(0, Q0, dtQ0, gm1, dF);
-      const double u0 = Q0[1] / Q0[0];
-      const double p0 = gm1 * (Q0[4] - 0.5 * (Q0[1] * Q0[1] + Q0[2] * Q0[2] + Q0[3] * Q0[3]) / Q0[0]);
+      euler_jvp(0, es, dtQ0, gm1, dF);
       F[0] = Q0[1];
-      F[1] = Q0[1] * u0 + p0;
-      F[2] = Q0[2] * u0;
-      F[3] = Q0[3] * u0;
-      F[4] = u0 * (Q0[4] + p0);
+      F[1] = Q0[1] * es.u[0] + es.p;
+      F[2] = Q0[2] * es.u[0];
+      F[3] = Q0[3] * es.u[0];
+      F[4] = es.u[0] * es.H;
     } else {
       // collision time (R7): tau = mu(T0)/p0 + c1 |pl - pr|/(pl + pr) dt
       const double dt = a.ctrl->dt;
@@ -502,6 +590,7 @@ __global__ void __launch_bounds__(NV == 3 ? 96 : 128) k_flux(FluxArgs a) {
         F[v] = (4.0 * Ih[v] - If[v]) / dt;
         dF[v] = 4.0 * (If[v] - 2.0 * Ih[v]) / (dt * dt);
       }
+    }
     }
     // rotate back to the global frame and weight by omega_G S
     if (STAGE == 1) {

@@ -78,11 +78,13 @@ struct RankPlan {
   std::vector<int64_t> l2g;             // [n_owned + n_pghost] global ids
   // reconstruction set: owned cells then layer-1 ghosts
   int64_t n_recon = 0;
+  int64_t ld = 0;                       // n_recon padded to the 128-cell tile
   std::vector<int32_t> recon_cell;      // [n_recon] local cell id
-  std::vector<int32_t> st_id;           // [K][n_recon] local ids (entry-major)
-  std::vector<uint8_t> sub_slot;        // [M*NM][n_recon]
-  std::vector<double> op;               // [op_entries][n_recon]
-  std::vector<double> geo;              // [8][n_recon]: V^{2/3}, V^{4/3}, M2 (xx,yy,zz,xy,xz,yz)
+  std::vector<int32_t> st_id;           // [K][ld] local ids (entry-major; host only)
+  std::vector<int32_t> st_id_tiled;     // same, tiled entry-major (device)
+  std::vector<uint8_t> sub_slot;        // [M*NM] per cell, tiled entry-major
+  std::vector<double> op;               // [op_entries] per cell, tiled entry-major (kernels.cuh k_recon)
+  std::vector<double> geo;              // [8] per cell, tiled: V^{2/3}, V^{4/3}, M2 (xx,yy,zz,xy,xz,yz)
   // faces: interior [0, n_if), wall [n_if, n_if + n_wf), farfield after
   int64_t n_faces = 0, n_if = 0, n_wf = 0, n_ff = 0;
   std::vector<int32_t> f_cells;         // [n_faces][2] local owner / neighbour (bc faces: ghost id)

@@ -1,7 +1,7 @@
 // sm_100a fp64 kernels of the HGKS hot path.
 //
 //   k_bc_ghosts   a6  boundary-condition ghost states (wall mirror / farfield)
-//   k_recon       a7  WENO reconstruction: LSQ apply, beta, weights, collapse
+//   k_recon       a7  WENO reconstruction (tile-staged stencils): LSQ apply, beta, weights, collapse
 //                     to ONE effective quadratic per cell (50 doubles)
 //   k_flux_tau0   a8+a9 per Gauss point: evaluate both polynomials, local
 //                     frame, Q0 by kinetic upwinding, F and d_t F of f = g0(1+A t)
@@ -71,14 +71,19 @@ __device__ inline void farfield_riemann(const double qi[5], const double n[3], c
   qb[4] = p / (g - 1.0) + 0.5 * rho * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
 }
 
-__global__ void k_bc_ghosts(double* __restrict__ Q, int ldq, int first, int n, const int* __restrict__ bg_cell,
+// Conserved state of a cell: one 48-byte row (rho, rhoU, rhoV, rhoW, rhoE, pad),
+// so a stencil gather is 3 aligned 16-byte loads and a ghost range is one
+// contiguous block (single message per peer in the halo exchange).
+constexpr int QS = 6;
+
+__global__ void k_bc_ghosts(double* __restrict__ Q, int first, int n, const int* __restrict__ bg_cell,
                             const int* __restrict__ bg_bc, const double* __restrict__ bg_normal, GasParams gp) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
-  int c = bg_cell[k];
+  const double* qc = Q + (size_t)bg_cell[k] * QS;
   double qi[5];
 #pragma unroll
-  for (int v = 0; v < 5; ++v) qi[v] = Q[v * ldq + c];
+  for (int v = 0; v < 5; ++v) qi[v] = qc[v];
   double qb[5];
   if (bg_bc[k] == 1) {
     qb[0] = qi[0]; qb[1] = -qi[1]; qb[2] = -qi[2]; qb[3] = -qi[3]; qb[4] = qi[4];
@@ -86,249 +91,208 @@ __global__ void k_bc_ghosts(double* __restrict__ Q, int ldq, int first, int n, c
     double n3[3] = {bg_normal[3 * k], bg_normal[3 * k + 1], bg_normal[3 * k + 2]};
     farfield_riemann(qi, n3, gp, qb);
   }
+  double* qg = Q + (size_t)(first + k) * QS;
 #pragma unroll
-  for (int v = 0; v < 5; ++v) Q[v * ldq + first + k] = qb[v];
+  for (int v = 0; v < 5; ++v) qg[v] = qb[v];
 }
 
 // ----------------------------------------------------------------------------
-// a7: WENO reconstruction, one thread per reconstructed cell.
-// Output record per local cell (50 doubles): [const(5) | lin x,y,z (3x5) |
-// quad xx,yy,zz,xy,xz,yz (6x5)], so that at X = x - c_i
-//   Q(x) = const + sum_a lin_a X_a + quad . (X_a X_b)       (Eq. weno collapsed)
+// a7: WENO reconstruction, one thread per reconstructed cell, 128-cell blocks.
+// Output record per local cell (50 doubles), variable-major: for v = 0..4,
+// rec[10 v + (const, x, y, z, xx, yy, zz, xy, xz, yz)] so that at X = x - c_i
+//   Q_v(x) = const + lin . X + quad . (X_a X_b)       (Eq. weno collapsed)
 // ----------------------------------------------------------------------------
 constexpr int kRec = 50;
+constexpr int kTile = 128;        // reconstructed cells per block
 
 struct ReconArgs {
-  const double* __restrict__ Q;  // [5][ldq]
-  int ldq;
+  const double* __restrict__ Q;         // [n_local][QS]
   int n_recon;
-  const int* __restrict__ recon_cell;
-  const int* __restrict__ st_id;        // [K][n_recon]
-  const uint8_t* __restrict__ sub_slot; // [M*NM][n_recon]
-  const double* __restrict__ op;        // [E][n_recon]
-  const double* __restrict__ geo;       // [8][n_recon]
-  double* __restrict__ ceff;            // [n_cells_local][50]
+  int ld;                               // n_recon padded to kTile (tiled entry-major arrays, setup.cpp)
+  const int* __restrict__ recon_cell;   // [n_recon] local cell id
+  const int* __restrict__ st_id;        // [K] per cell, tiled: stencil member local ids
+  const uint8_t* __restrict__ sub_slot; // [M*NM] per cell, tiled: sub-stencil member -> big-stencil slot
+  const double* __restrict__ op;        // [E] per cell, tiled: LSQ operators in streaming order
+  const double* __restrict__ geo;       // [8] per cell, tiled: V^{2/3}, V^{4/3}, M2 (xx,yy,zz,xy,xz,yz)
+  double* __restrict__ ceff;            // [n_local][50]
   double eps;
   int omega_pow;
 };
 
-// One thread per (cell, conserved variable): the smoothness indicators and the
-// nonlinear weights are per variable (R12), so the five variables of a cell
-// are independent.  Block = CT cells x 5 variables; warp y = variable y of CT
-// consecutive cells, so every operator load is a coalesced 256-byte row read
-// by 5 warps (one HBM fetch, L1 hits for the other four) and each thread keeps
-// only 9 + 3M accumulators live (4x fewer registers -> 4x more warps in flight
-// for the stencil gathers than one thread per cell).
-template <int K, int M, int NM, int CT>
-__global__ void __launch_bounds__(CT * 5) k_recon_v(ReconArgs a) {
-  const int r = blockIdx.x * CT + threadIdx.x;
-  const int v = threadIdx.y;
-  if (r >= a.n_recon) return;
-  const int R = a.n_recon;
-  const int ci = __ldg(a.recon_cell + r);
-  const double* __restrict__ Qv = a.Q + (size_t)v * a.ldq;
-  const double qi = __ldg(Qv + ci);
-  const double* __restrict__ op = a.op + r;
-  // ---- P_0: c[d] = sum_k A0+[d][k] (Q_k - Q_i) ----
-  double c[9];
-#pragma unroll
-  for (int d = 0; d < 9; ++d) c[d] = 0.0;
-#pragma unroll 7
-  for (int k = 0; k < K; ++k) {
-    const double dq = __ldg(Qv + __ldg(a.st_id + k * R + r)) - qi;
-#pragma unroll
-    for (int d = 0; d < 9; ++d) c[d] = fma(__ldg(op + (size_t)(d * K + k) * R), dq, c[d]);
+// One thread per reconstructed cell (block of kTile cells).  All stencil
+// indices are loaded first and all member states are gathered at once into
+// this thread's shared-memory slots (3 x 16-byte loads per member, ~40 loads in
+// flight per thread), so the gathers cost one memory latency per cell; the
+// sub-stencils re-read them from shared memory.  The LSQ operators (1584 B per
+// tet cell, most of the kernel's HBM bytes) stream entry-major: each warp load
+// is 256 contiguous bytes.
+template <int K, int M, int NM>
+#ifndef HGKS_RECON_MINB
+#define HGKS_RECON_MINB 2
+#endif
+__global__ void __launch_bounds__(kTile, HGKS_RECON_MINB) k_recon(ReconArgs a) {
+  constexpr int QP = 5 * kTile;                      // doubles per member plane: [v][thread]
+  constexpr int E = 9 * K + 3 * M * NM;
+  extern __shared__ __align__(16) double smem[];
+  double* __restrict__ dqs = smem;                   // [K][5][kTile] Q_k - Q_i
+  const int t = threadIdx.x;
+  const int r = blockIdx.x * kTile + t;
+  const bool active = r < a.n_recon;
+  // tiled entry-major per-cell arrays (setup.cpp): entry e of this cell at (tile*NE + e)*kTile + t
+  const size_t tb = (size_t)blockIdx.x * kTile;
+  const int* __restrict__ sid = a.st_id + tb * K + t;
+  const int ci = active ? __ldg(a.recon_cell + r) : 0;
+  double qi[5];
+  {
+    const double2* q2 = reinterpret_cast<const double2*>(a.Q + (size_t)ci * QS);
+    const double2 x0 = __ldg(q2), x1 = __ldg(q2 + 1), x2 = __ldg(q2 + 2);
+    qi[0] = x0.x; qi[1] = x0.y; qi[2] = x1.x; qi[3] = x1.y; qi[4] = x2.x;
   }
-  // ---- P_m over the sub-stencils ----
-  double b[M][3];
-  const double* __restrict__ opm = op + (size_t)(9 * K) * R;
+  // gather the stencil members in groups (bounded registers, 7 x 3 loads in flight)
+  constexpr int G = 7;
 #pragma unroll
-  for (int m = 0; m < M; ++m) {
-    b[m][0] = b[m][1] = b[m][2] = 0.0;
+  for (int k0 = 0; k0 < K; k0 += G) {
+    double2 x[G][3];
 #pragma unroll
-    for (int j = 0; j < NM; ++j) {
-      const int s = __ldg(a.sub_slot + (m * NM + j) * R + r);
-      const double dq = __ldg(Qv + __ldg(a.st_id + s * R + r)) - qi;
+    for (int k = k0; k < k0 + G && k < K; ++k) {
+      const double2* q2 = reinterpret_cast<const double2*>(a.Q + (size_t)__ldg(sid + k * kTile) * QS);
+      x[k - k0][0] = __ldg(q2);
+      x[k - k0][1] = __ldg(q2 + 1);
+      x[k - k0][2] = __ldg(q2 + 2);
+    }
 #pragma unroll
-      for (int d = 0; d < 3; ++d) b[m][d] = fma(__ldg(opm + (size_t)((m * 3 + d) * NM + j) * R), dq, b[m][d]);
+    for (int k = k0; k < k0 + G && k < K; ++k) {
+      double* d = dqs + k * QP + t;
+      d[0 * kTile] = x[k - k0][0].x - qi[0];
+      d[1 * kTile] = x[k - k0][0].y - qi[1];
+      d[2 * kTile] = x[k - k0][1].x - qi[2];
+      d[3 * kTile] = x[k - k0][1].y - qi[3];
+      d[4 * kTile] = x[k - k0][2].x - qi[4];
     }
   }
-  const double V23 = __ldg(a.geo + r), V43 = __ldg(a.geo + R + r);
+  const double* __restrict__ op = a.op + tb * E + t;
+  const double* __restrict__ geo = a.geo + tb * 8 + t;
+  const uint8_t* __restrict__ ssl = a.sub_slot + tb * (M * NM) + t;
+  const double V23 = __ldg(geo), V43 = __ldg(geo + kTile);
   double m2[6];
 #pragma unroll
-  for (int q = 0; q < 6; ++q) m2[q] = __ldg(a.geo + (2 + q) * R + r);
-  // ---- smoothness indicators (closed form SURVEY A.5) ----
-  double beta0;
-  {
-    const double gx[3] = {2.0 * c[3], c[6], c[7]}, gy[3] = {c[6], 2.0 * c[4], c[8]}, gz[3] = {c[7], c[8], 2.0 * c[5]};
-    auto quadf = [&](const double g[3]) {
-      return m2[0] * g[0] * g[0] + m2[1] * g[1] * g[1] + m2[2] * g[2] * g[2] +
-             2.0 * (m2[3] * g[0] * g[1] + m2[4] * g[0] * g[2] + m2[5] * g[1] * g[2]);
-    };
-    const double s1 = c[0] * c[0] + c[1] * c[1] + c[2] * c[2] + quadf(gx) + quadf(gy) + quadf(gz);
-    const double s2 = 4.0 * (c[3] * c[3] + c[4] * c[4] + c[5] * c[5]) + c[6] * c[6] + c[7] * c[7] + c[8] * c[8];
-    beta0 = V23 * s1 + V43 * s2;
-  }
-  double betam[M];
-#pragma unroll
-  for (int m = 0; m < M; ++m) betam[m] = V23 * (b[m][0] * b[m][0] + b[m][1] * b[m][1] + b[m][2] * b[m][2]);
-  // ---- nonlinear weights and the collapse ----
-  const double gm = 0.025, g0 = 1.0 - 0.025 * M;
-  double tz = 0.0;
-#pragma unroll
-  for (int m = 0; m < M; ++m) tz += fabs(beta0 - betam[m]);
-  tz *= (1.0 / M);
-  const double r0 = tz / (beta0 + a.eps);
-  const double w0 = g0 * (1.0 + (a.omega_pow == 2 ? r0 * r0 : r0));
-  double wm[M], sum = w0;
-#pragma unroll
-  for (int m = 0; m < M; ++m) {
-    const double rm = tz / (betam[m] + a.eps);
-    wm[m] = gm * (1.0 + (a.omega_pow == 2 ? rm * rm : rm));
-    sum += wm[m];
-  }
-  const double inv = 1.0 / sum;
-  const double al0 = w0 * inv / g0;  // omega-bar_0 / gamma_0
-  double lin[3] = {al0 * c[0], al0 * c[1], al0 * c[2]};
-#pragma unroll
-  for (int m = 0; m < M; ++m) {
-    const double alm = wm[m] * inv - al0 * gm;  // omega-bar_m - omega-bar_0 gamma_m / gamma_0
-#pragma unroll
-    for (int d = 0; d < 3; ++d) lin[d] = fma(alm, b[m][d], lin[d]);
-  }
-  double quad[6];
-#pragma unroll
-  for (int q = 0; q < 6; ++q) quad[q] = al0 * c[3 + q];
-  const double cst = qi - (quad[0] * m2[0] + quad[1] * m2[1] + quad[2] * m2[2] + quad[3] * m2[3] + quad[4] * m2[4] +
-                           quad[5] * m2[5]);
-  double* __restrict__ out = a.ceff + (size_t)ci * kRec;
-  out[v] = cst;
-#pragma unroll
-  for (int d = 0; d < 3; ++d) out[5 + d * 5 + v] = lin[d];
-#pragma unroll
-  for (int q = 0; q < 6; ++q) out[20 + q * 5 + v] = quad[q];
-}
-
-template <int K, int M, int NM, int BLOCK>
-__global__ void __launch_bounds__(BLOCK) k_recon(ReconArgs a) {
-  extern __shared__ double sb[];  // [M*15][BLOCK] sub-stencil slopes
-  const int r = blockIdx.x * BLOCK + threadIdx.x;
-  if (r >= a.n_recon) return;
-  const int R = a.n_recon;
-  const int ci = a.recon_cell[r];
-  const double* __restrict__ Q = a.Q;
-  const int ldq = a.ldq;
-  double qi[5];
-#pragma unroll
-  for (int v = 0; v < 5; ++v) qi[v] = Q[v * ldq + ci];
+  for (int q = 0; q < 6; ++q) m2[q] = __ldg(geo + (2 + q) * kTile);
   // ---- P_0: c[d][v] = sum_k A0+[d][k] (Q_k - Q_i)[v] ----
   double c[9][5];
 #pragma unroll
   for (int d = 0; d < 9; ++d)
 #pragma unroll
     for (int v = 0; v < 5; ++v) c[d][v] = 0.0;
-  const double* __restrict__ op = a.op + r;
 #pragma unroll 2
   for (int k = 0; k < K; ++k) {
-    const int id = a.st_id[k * R + r];
     double dq[5];
 #pragma unroll
-    for (int v = 0; v < 5; ++v) dq[v] = __ldg(Q + v * ldq + id) - qi[v];
+    for (int v = 0; v < 5; ++v) dq[v] = dqs[k * QP + v * kTile + t];
 #pragma unroll
     for (int d = 0; d < 9; ++d) {
-      const double w = __ldcs(op + (size_t)(d * K + k) * R);
+      const double w = __ldcs(op + (k * 9 + d) * kTile);
 #pragma unroll
       for (int v = 0; v < 5; ++v) c[d][v] = fma(w, dq[v], c[d][v]);
     }
   }
-  const double V23 = a.geo[0 * R + r], V43 = a.geo[1 * R + r];
-  double m2[6];
-#pragma unroll
-  for (int q = 0; q < 6; ++q) m2[q] = a.geo[(2 + q) * R + r];
-  // ---- beta_0 closed form ----
+  // smoothness indicator of P_0 (closed form SURVEY A.5)
   double beta0[5];
 #pragma unroll
   for (int v = 0; v < 5; ++v) {
-    const double cx = c[0][v], cy = c[1][v], cz = c[2][v];
-    const double cxx = c[3][v], cyy = c[4][v], czz = c[5][v], cxy = c[6][v], cxz = c[7][v], cyz = c[8][v];
-    // gradient d_a P0 = c_a + g_a . X ; g_x = (2cxx, cxy, cxz) ...
-    const double gx[3] = {2.0 * cxx, cxy, cxz}, gy[3] = {cxy, 2.0 * cyy, cyz}, gz[3] = {cxz, cyz, 2.0 * czz};
+    const double gx[3] = {2.0 * c[3][v], c[6][v], c[7][v]}, gy[3] = {c[6][v], 2.0 * c[4][v], c[8][v]},
+                 gz[3] = {c[7][v], c[8][v], 2.0 * c[5][v]};
     auto quadf = [&](const double g[3]) {
       return m2[0] * g[0] * g[0] + m2[1] * g[1] * g[1] + m2[2] * g[2] * g[2] +
              2.0 * (m2[3] * g[0] * g[1] + m2[4] * g[0] * g[2] + m2[5] * g[1] * g[2]);
     };
-    const double s1 = cx * cx + cy * cy + cz * cz + quadf(gx) + quadf(gy) + quadf(gz);
-    const double s2 = 4.0 * (cxx * cxx + cyy * cyy + czz * czz) + cxy * cxy + cxz * cxz + cyz * cyz;
+    const double s1 = c[0][v] * c[0][v] + c[1][v] * c[1][v] + c[2][v] * c[2][v] + quadf(gx) + quadf(gy) + quadf(gz);
+    const double s2 = 4.0 * (c[3][v] * c[3][v] + c[4][v] * c[4][v] + c[5][v] * c[5][v]) + c[6][v] * c[6][v] +
+                      c[7][v] * c[7][v] + c[8][v] * c[8][v];
     beta0[v] = V23 * s1 + V43 * s2;
   }
-  // ---- P_m: b[d][v] over the sub-stencils, beta_m ----
-  double betam[M][5];
-  const double* __restrict__ opm = op + (size_t)(9 * K) * R;
-#pragma unroll
-  for (int m = 0; m < M; ++m) {
-    double b[3][5];
+  const double* __restrict__ opm = op + (9 * K) * kTile;
+  auto sub_slopes = [&](int m, double b[3][5]) {  // P_m over sub-stencil m
 #pragma unroll
     for (int d = 0; d < 3; ++d)
 #pragma unroll
       for (int v = 0; v < 5; ++v) b[d][v] = 0.0;
 #pragma unroll
     for (int j = 0; j < NM; ++j) {
-      const int s = a.sub_slot[(m * NM + j) * R + r];
-      const int id = a.st_id[s * R + r];
+      const int sl = __ldg(ssl + (m * NM + j) * kTile);
       double dq[5];
 #pragma unroll
-      for (int v = 0; v < 5; ++v) dq[v] = __ldg(Q + v * ldq + id) - qi[v];
+      for (int v = 0; v < 5; ++v) dq[v] = dqs[sl * QP + v * kTile + t];
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
-        const double w = __ldcs(opm + (size_t)((m * 3 + d) * NM + j) * R);
+        const double w = __ldg(opm + ((m * NM + j) * 3 + d) * kTile);
 #pragma unroll
         for (int v = 0; v < 5; ++v) b[d][v] = fma(w, dq[v], b[d][v]);
       }
     }
+  };
+  // ---- pass 1: beta_m and the nonlinear weights ----
+  const double gm = 0.025, g0 = 1.0 - 0.025 * M;
+  double al0[5], alm[M][5];
+  {
+    double tz[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      double b[3][5];
+      sub_slopes(m, b);
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        alm[m][v] = V23 * (b[0][v] * b[0][v] + b[1][v] * b[1][v] + b[2][v] * b[2][v]);  // beta_m
+        tz[v] += fabs(beta0[v] - alm[m][v]);
+      }
+    }
 #pragma unroll
     for (int v = 0; v < 5; ++v) {
-      betam[m][v] = V23 * (b[0][v] * b[0][v] + b[1][v] * b[1][v] + b[2][v] * b[2][v]);
+      const double tzv = tz[v] * (1.0 / M);
+      const double r0 = tzv / (beta0[v] + a.eps);
+      const double w0 = g0 * (1.0 + (a.omega_pow == 2 ? r0 * r0 : r0));
+      double sum = w0;
 #pragma unroll
-      for (int d = 0; d < 3; ++d) sb[((m * 3 + d) * 5 + v) * BLOCK + threadIdx.x] = b[d][v];
+      for (int m = 0; m < M; ++m) {
+        const double rm = tzv / (alm[m][v] + a.eps);
+        alm[m][v] = gm * (1.0 + (a.omega_pow == 2 ? rm * rm : rm));  // omega_m
+        sum += alm[m][v];
+      }
+      const double inv = 1.0 / sum;
+      al0[v] = w0 * inv / g0;  // omega-bar_0 / gamma_0
+#pragma unroll
+      for (int m = 0; m < M; ++m) alm[m][v] = alm[m][v] * inv - al0[v] * gm;  // omega-bar_m - omega-bar_0 gamma_m/gamma_0
     }
   }
-  // ---- nonlinear weights and collapse ----
-  const double gm = 0.025, g0 = 1.0 - 0.025 * M;
-  double* __restrict__ out = a.ceff + (size_t)ci * kRec;
+  // ---- collapse to one quadratic ----
+  double lin[3][5];
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+#pragma unroll
+    for (int v = 0; v < 5; ++v) lin[d][v] = al0[v] * c[d][v];
+#pragma unroll
+  for (int m = 0; m < M; ++m) {  // pass 2: weighted sum of the sub-stencil slopes
+    double b[3][5];
+    sub_slopes(m, b);
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int v = 0; v < 5; ++v) lin[d][v] = fma(alm[m][v], b[d][v], lin[d][v]);
+  }
+  if (!active) return;
+  double2* dst = reinterpret_cast<double2*>(a.ceff + (size_t)ci * kRec);
 #pragma unroll
   for (int v = 0; v < 5; ++v) {
-    double tz = 0.0;
-#pragma unroll
-    for (int m = 0; m < M; ++m) tz += fabs(beta0[v] - betam[m][v]);
-    tz *= (1.0 / M);
-    double r0 = tz / (beta0[v] + a.eps);
-    double w0 = g0 * (1.0 + (a.omega_pow == 2 ? r0 * r0 : r0));
-    double wm[M], sum = w0;
-#pragma unroll
-    for (int m = 0; m < M; ++m) {
-      double rm = tz / (betam[m][v] + a.eps);
-      wm[m] = gm * (1.0 + (a.omega_pow == 2 ? rm * rm : rm));
-      sum += wm[m];
-    }
-    const double inv = 1.0 / sum;
-    const double al0 = w0 * inv / g0;  // omega-bar_0 / gamma_0
-    double lin[3] = {al0 * c[0][v], al0 * c[1][v], al0 * c[2][v]};
-#pragma unroll
-    for (int m = 0; m < M; ++m) {
-      const double alm = wm[m] * inv - al0 * gm;  // omega-bar_m - omega-bar_0 gamma_m / gamma_0
-#pragma unroll
-      for (int d = 0; d < 3; ++d) lin[d] = fma(alm, sb[((m * 3 + d) * 5 + v) * BLOCK + threadIdx.x], lin[d]);
-    }
     double quad[6];
 #pragma unroll
-    for (int q = 0; q < 6; ++q) quad[q] = al0 * c[3 + q][v];
-    double cst = qi[v] - (quad[0] * m2[0] + quad[1] * m2[1] + quad[2] * m2[2] + quad[3] * m2[3] + quad[4] * m2[4] +
-                          quad[5] * m2[5]);
-    out[v] = cst;
-#pragma unroll
-    for (int d = 0; d < 3; ++d) out[5 + d * 5 + v] = lin[d];
-#pragma unroll
-    for (int q = 0; q < 6; ++q) out[20 + q * 5 + v] = quad[q];
+    for (int q = 0; q < 6; ++q) quad[q] = al0[v] * c[3 + q][v];
+    // zero-mean basis: p_ab = X_a X_b - M2_ab
+    const double cst = qi[v] - (quad[0] * m2[0] + quad[1] * m2[1] + quad[2] * m2[2] + quad[3] * m2[3] +
+                                quad[4] * m2[4] + quad[5] * m2[5]);
+    dst[5 * v + 0] = make_double2(cst, lin[0][v]);
+    dst[5 * v + 1] = make_double2(lin[1][v], lin[2][v]);
+    dst[5 * v + 2] = make_double2(quad[0], quad[1]);
+    dst[5 * v + 3] = make_double2(quad[2], quad[3]);
+    dst[5 * v + 4] = make_double2(quad[4], quad[5]);
   }
 }
 
@@ -338,9 +302,8 @@ __global__ void __launch_bounds__(BLOCK) k_recon(ReconArgs a) {
 // a10: L, d_t L and the S2O4 stages
 // ----------------------------------------------------------------------------
 struct UpdateArgs {
-  double* __restrict__ Q;  // [5][ldq]  (stage 1: Q^n -> Q*, stage 2: -> Q^{n+1})
-  int ldq;
-  double* __restrict__ R;  // [5][n_owned]
+  double* __restrict__ Q;  // [n_local][QS]  (stage 1: Q^n -> Q*, stage 2: -> Q^{n+1})
+  double* __restrict__ R;  // [n_owned][QS]
   const double* __restrict__ F1;
   const double* __restrict__ F2;
   const int* __restrict__ cf;  // [NF][n_owned]
@@ -358,25 +321,34 @@ __global__ void __launch_bounds__(256) k_update1(UpdateArgs a) {
   double L[5] = {0, 0, 0, 0, 0}, dL[5] = {0, 0, 0, 0, 0};
 #pragma unroll
   for (int p = 0; p < NF; ++p) {  // local-face order (deterministic, partition independent)
-    const int e = a.cf[p * a.n_owned + i];
+    const int e = __ldg(a.cf + p * a.n_owned + i);
     const int f = e >= 0 ? e : ~e;
-    const double* F = a.F1 + (size_t)f * 10;
+    const double2* F = reinterpret_cast<const double2*>(a.F1 + (size_t)f * 10);
+    double v10[10];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const double2 x = __ldg(F + k);
+      v10[2 * k] = x.x;
+      v10[2 * k + 1] = x.y;
+    }
     if (e >= 0) {
 #pragma unroll
-      for (int v = 0; v < 5; ++v) { L[v] -= F[v]; dL[v] -= F[5 + v]; }
+      for (int v = 0; v < 5; ++v) { L[v] -= v10[v]; dL[v] -= v10[5 + v]; }
     } else {
 #pragma unroll
-      for (int v = 0; v < 5; ++v) { L[v] += F[v]; dL[v] += F[5 + v]; }
+      for (int v = 0; v < 5; ++v) { L[v] += v10[v]; dL[v] += v10[5 + v]; }
     }
   }
   const double iv = a.inv_v[i];
   const double dt = a.ctrl->dt;
+  double* q = a.Q + (size_t)i * QS;
+  double* r = a.R + (size_t)i * QS;
 #pragma unroll
   for (int v = 0; v < 5; ++v) {
     const double l = L[v] * iv, dl = dL[v] * iv;
-    const double q = a.Q[v * a.ldq + i];
-    a.Q[v * a.ldq + i] = q + 0.5 * dt * l + 0.125 * dt * dt * dl;
-    a.R[v * a.n_owned + i] = q + dt * l + dt * dt / 6.0 * dl;
+    const double q0 = q[v];
+    q[v] = q0 + 0.5 * dt * l + 0.125 * dt * dt * dl;
+    r[v] = q0 + dt * l + dt * dt / 6.0 * dl;
   }
 }
 
@@ -409,24 +381,26 @@ __global__ void __launch_bounds__(256) k_update2(UpdateArgs a) {
     double dL[5] = {0, 0, 0, 0, 0};
 #pragma unroll
     for (int p = 0; p < NF; ++p) {
-      const int e = a.cf[p * a.n_owned + i];
+      const int e = __ldg(a.cf + p * a.n_owned + i);
       const int f = e >= 0 ? e : ~e;
       const double* F = a.F2 + (size_t)f * 5;
       if (e >= 0) {
 #pragma unroll
-        for (int v = 0; v < 5; ++v) dL[v] -= F[v];
+        for (int v = 0; v < 5; ++v) dL[v] -= __ldg(F + v);
       } else {
 #pragma unroll
-        for (int v = 0; v < 5; ++v) dL[v] += F[v];
+        for (int v = 0; v < 5; ++v) dL[v] += __ldg(F + v);
       }
     }
     const double iv = a.inv_v[i];
     const double dt = a.ctrl->dt;
     double q[5];
+    const double* r = a.R + (size_t)i * QS;
+    double* qo = a.Q + (size_t)i * QS;
 #pragma unroll
     for (int v = 0; v < 5; ++v) {
-      q[v] = a.R[v * a.n_owned + i] + dt * dt / 6.0 * 2.0 * (dL[v] * iv);
-      a.Q[v * a.ldq + i] = q[v];
+      q[v] = r[v] + dt * dt / 6.0 * 2.0 * (dL[v] * iv);
+      qo[v] = q[v];
     }
     const double p = (a.gp.gamma - 1.0) * (q[4] - 0.5 * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3]) / q[0]);
     if (!(q[0] > 0.0) || !(p > 0.0)) atomicMin(&a.ctrl->bad_cell, i);
@@ -435,14 +409,14 @@ __global__ void __launch_bounds__(256) k_update2(UpdateArgs a) {
   block_min_dt(bound, a.ctrl);
 }
 
-__global__ void __launch_bounds__(256) k_dt_init(const double* __restrict__ Q, int ldq, const double* __restrict__ h_dt,
-                                                 int n, Ctrl* ctrl, GasParams gp) {
+__global__ void __launch_bounds__(256) k_dt_init(const double* __restrict__ Q, const double* __restrict__ h_dt, int n,
+                                                 Ctrl* ctrl, GasParams gp) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   double bound = 1e300;
   if (i < n) {
     double q[5];
 #pragma unroll
-    for (int v = 0; v < 5; ++v) q[v] = Q[v * ldq + i];
+    for (int v = 0; v < 5; ++v) q[v] = Q[(size_t)i * QS + v];
     bound = cell_dt_bound(q, h_dt[i], gp);
   }
   block_min_dt(bound, ctrl);
@@ -491,31 +465,30 @@ __global__ void k_reset_ctrl(Ctrl* ctrl, double t) {
   ctrl->dtmin_bits = 0x7fefffffffffffffull;
 }
 
-// state layout conversions for set/get_state: AoS [n][5] in caller order <-> SoA local
+// state layout conversions for set/get_state: AoS [n][5] in caller order <-> local rows
 __global__ void k_scatter_state(const double* __restrict__ in, const int64_t* __restrict__ row, int n,
-                                double* __restrict__ Q, int ldq) {
+                                double* __restrict__ Q) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int64_t r = row[i];
 #pragma unroll
-  for (int v = 0; v < 5; ++v) Q[v * ldq + i] = in[r * 5 + v];
+  for (int v = 0; v < 5; ++v) Q[(size_t)i * QS + v] = in[r * 5 + v];
+  Q[(size_t)i * QS + 5] = 0.0;
 }
-__global__ void k_gather_state(const double* __restrict__ Q, int ldq, const int* __restrict__ local_of_out, int n,
+__global__ void k_gather_state(const double* __restrict__ Q, const int* __restrict__ local_of_out, int n,
                                double* __restrict__ out) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const int i = local_of_out[k];
 #pragma unroll
-  for (int v = 0; v < 5; ++v) out[(size_t)k * 5 + v] = Q[v * ldq + i];
+  for (int v = 0; v < 5; ++v) out[(size_t)k * 5 + v] = Q[(size_t)i * QS + v];
 }
-// halo pack: SoA send buffer [5][n_send]
-__global__ void k_pack(const double* __restrict__ Q, int ldq, const int* __restrict__ list, int n,
-                       double* __restrict__ buf) {
+// halo pack: rows of the send list, [n_send][QS]
+__global__ void k_pack(const double* __restrict__ Q, const int* __restrict__ list, int n, double* __restrict__ buf) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const int i = list[k];
-#pragma unroll
-  for (int v = 0; v < 5; ++v) buf[v * n + k] = Q[v * ldq + i];
+  if (k >= n * 3) return;
+  const int j = k / 3, part = k - 3 * j;
+  reinterpret_cast<double2*>(buf)[k] = reinterpret_cast<const double2*>(Q + (size_t)list[j] * QS)[part];
 }
 
 }  // namespace hgks

@@ -744,6 +744,9 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
   std::iota(rp.recon_cell.begin(), rp.recon_cell.end(), 0);
   for (int64_t g : pg)
     if (layer[g] == 1) rp.recon_cell.push_back(g2l[g]);
+  // layer-1 ghosts in Morton order too, so their reconstruction tiles stay compact
+  std::sort(rp.recon_cell.begin() + rp.n_owned, rp.recon_cell.end(),
+            [&](int32_t a, int32_t b) { return by_morton(rp.l2g[a], rp.l2g[b]); });
   rp.n_recon = (int64_t)rp.recon_cell.size();
   // BC ghosts needed: those of faces of recon cells and of their neighbours
   std::unordered_map<int64_t, int32_t> bg2l;
@@ -766,14 +769,22 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
     return l;
   };
   const int K = L.K, M = L.M, NM = L.NM, E = L.op_entries();
-  const int64_t R = rp.n_recon;
+  const int64_t Rn = rp.n_recon;
+  // entry-major arrays use a stride padded to the 64-cell tile so every
+  // per-tile operator row is one aligned 512-byte bulk copy
+  const int64_t R = (Rn + 127) / 128 * 128;
+  rp.ld = R;
   rp.st_id.assign((size_t)K * R, 0);
   rp.sub_slot.assign((size_t)M * NM * R, 0);
   rp.op.assign((size_t)E * R, 0.0);
   rp.geo.assign((size_t)8 * R, 0.0);
+  // tiled entry-major layout: entry e of cell r at ((r/128)*NE + e)*128 + r%128, so one
+  // 128-cell block reads its operators from one contiguous range (DRAM page locality)
+  auto ti = [](int64_t r, int ne, int e) { return (size_t)(((r >> 7) * ne + e) << 7) + (size_t)(r & 127); };
+  rp.st_id_tiled.assign((size_t)K * R, 0);
   rp.stencil_min = 1 << 30;
   rp.stencil_max = 0;
-  for (int64_t r = 0; r < R; ++r) {
+  for (int64_t r = 0; r < Rn; ++r) {
     int64_t gi = rp.l2g[rp.recon_cell[r]];
     int64_t o0 = gm.big_off[gi];
     int kk = (int)(gm.big_off[gi + 1] - o0);
@@ -781,18 +792,26 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
       rp.stencil_min = std::min(rp.stencil_min, kk);
       rp.stencil_max = std::max(rp.stencil_max, kk);
     }
-    for (int k = 0; k < K; ++k)
+    for (int k = 0; k < K; ++k) {
       rp.st_id[(size_t)k * R + r] = k < kk ? local_of(gm.big_id[o0 + k]) : rp.recon_cell[r];
+      rp.st_id_tiled[ti(r, K, k)] = rp.st_id[(size_t)k * R + r];
+    }
     for (int s = 0; s < M * NM; ++s) {
       int8_t v = gm.sub_slot[gi * M * NM + s];
-      rp.sub_slot[(size_t)s * R + r] = (uint8_t)(v < 0 ? 0 : v);
+      rp.sub_slot[ti(r, M * NM, s)] = (uint8_t)(v < 0 ? 0 : v);
     }
+    // streaming order of the operator entries (kernels.cuh k_recon): A0+ member-major
+    // (row k*9 + d), then the sub-stencil operators (row 9K + (m*NM + j)*3 + d)
     const double* op = &gm.op[(size_t)gi * E];
-    for (int e = 0; e < E; ++e) rp.op[(size_t)e * R + r] = op[e];
+    for (int d = 0; d < 9; ++d)
+      for (int k = 0; k < K; ++k) rp.op[ti(r, E, k * 9 + d)] = op[d * K + k];
+    for (int m = 0; m < M; ++m)
+      for (int d = 0; d < 3; ++d)
+        for (int j = 0; j < NM; ++j) rp.op[ti(r, E, 9 * K + (m * NM + j) * 3 + d)] = op[9 * K + (m * 3 + d) * NM + j];
     double V = gm.V[gi];
-    rp.geo[0 * R + r] = std::pow(V, 2.0 / 3.0);
-    rp.geo[1 * R + r] = std::pow(V, 4.0 / 3.0);
-    for (int k = 0; k < 6; ++k) rp.geo[(2 + k) * R + r] = gm.M2[6 * gi + k];
+    rp.geo[ti(r, 8, 0)] = std::pow(V, 2.0 / 3.0);
+    rp.geo[ti(r, 8, 1)] = std::pow(V, 4.0 / 3.0);
+    for (int k = 0; k < 6; ++k) rp.geo[ti(r, 8, 2 + k)] = gm.M2[6 * gi + k];
   }
   // faces computed by this rank: every face of an owned cell
   std::vector<int64_t> fl;

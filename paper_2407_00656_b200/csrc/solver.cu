@@ -151,20 +151,20 @@ struct DevArrays {
 
 size_t layout(const GlobalMesh& gm, const RankPlan& rp, Carve& c, DevArrays& d) {
   const Layout& L = gm.lay;
-  const int ldq = round32(rp.n_local());
+  const size_t nq = (size_t)QS * round32(rp.n_local());
   const int64_t ncl = rp.n_owned + rp.n_pghost;
   d.ctrl = c.take<Ctrl>(1);
-  d.Q = c.take<double>((size_t)5 * ldq);
-  d.Qtmp = c.take<double>((size_t)5 * ldq);
-  d.R = c.take<double>((size_t)5 * rp.n_owned);
+  d.Q = c.take<double>(nq);
+  d.Qtmp = c.take<double>(nq);
+  d.R = c.take<double>((size_t)QS * rp.n_owned);
   d.ceff = c.take<double>((size_t)kRec * ncl);
   d.F1 = c.take<double>((size_t)10 * rp.n_faces);
   d.F2 = c.take<double>((size_t)5 * rp.n_faces);
   d.recon_cell = c.take<int>(rp.n_recon);
-  d.st_id = c.take<int>((size_t)L.K * rp.n_recon);
-  d.sub_slot = c.take<uint8_t>((size_t)L.M * L.NM * rp.n_recon);
-  d.op = c.take<double>((size_t)L.op_entries() * rp.n_recon);
-  d.geo = c.take<double>((size_t)8 * rp.n_recon);
+  d.st_id = c.take<int>((size_t)L.K * rp.ld);
+  d.sub_slot = c.take<uint8_t>((size_t)L.M * L.NM * rp.ld);
+  d.op = c.take<double>((size_t)L.op_entries() * rp.ld);
+  d.geo = c.take<double>((size_t)8 * rp.ld);
   d.f_cells = c.take<int>((size_t)2 * rp.n_faces);
   d.f_geo = c.take<double>((size_t)rp.f_geo_stride * rp.n_faces);
   d.cf = c.take<int>((size_t)L.nfaces * rp.n_owned);
@@ -174,7 +174,7 @@ size_t layout(const GlobalMesh& gm, const RankPlan& rp, Carve& c, DevArrays& d) 
   d.bg_bc = c.take<int>(std::max<int64_t>(1, rp.n_bghost));
   d.bg_normal = c.take<double>(std::max<int64_t>(3, 3 * rp.n_bghost));
   d.send_list = c.take<int>(std::max<size_t>(1, rp.send_list.size()));
-  d.sendbuf = c.take<double>(std::max<size_t>(5, 5 * rp.send_list.size()));
+  d.sendbuf = c.take<double>(std::max<size_t>(QS, QS * rp.send_list.size()));
   d.out_local = c.take<int>(rp.n_owned);
   d.in_row = c.take<int64_t>(rp.n_owned);
   // staging for set/get_state: single rank copies the caller's whole array
@@ -203,10 +203,10 @@ struct hgks_solver {
   hgks_config cfg;
   GasParams gp;
   int rank = 0, n_ranks = 1, device = 0, transport = HGKS_TRANSPORT_NCCL;
-  int recon_variant = 0;  // 0: thread per (cell, variable); 1: thread per cell (HGKS_RECON=cell)
+  size_t recon_smem_set = 0;
   cudaStream_t stream = nullptr;
   DevArrays d{};
-  int ldq = 0;
+  size_t nq = 0;  // doubles in Q
   ncclComm_t comm = nullptr;
   int64_t launches = 0;
   bool profiling = false;
@@ -258,31 +258,25 @@ void launch(hgks_solver* s, const char* name, Launch&& fn) {
 
 inline int blocks(int64_t n, int b) { return (int)((n + b - 1) / b); }
 
-template <int K, int M, int NM, int B>
+template <int K, int M, int NM>
 void run_recon_k(hgks_solver* s, const ReconArgs& a) {
-  const size_t smem = (size_t)M * 15 * B * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(k_recon<K, M, NM, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
+  const size_t smem = sizeof(double) * (size_t)K * 5 * kTile;
+  if (smem > s->recon_smem_set) {
+    CUDA_TRY(cudaFuncSetAttribute(k_recon<K, M, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    s->recon_smem_set = smem;
   }
-  if (s->recon_variant == 0) {
-    // one thread per (cell, variable), 64 cells x 5 variables per block
-    constexpr int CT = 64;
-    launch(s, "k_recon", [&] { k_recon_v<K, M, NM, CT><<<blocks(a.n_recon, CT), dim3(CT, 5), 0, s->stream>>>(a); });
-  } else {
-    launch(s, "k_recon", [&] { k_recon<K, M, NM, B><<<blocks(a.n_recon, B), B, smem, s->stream>>>(a); });
-  }
+  launch(s, "k_recon", [&] { k_recon<K, M, NM><<<blocks(a.n_recon, kTile), kTile, smem, s->stream>>>(a); });
 }
 
 void run_recon(hgks_solver* s, const double* Q) {
   const Layout& L = s->lay;
   ReconArgs a;
   a.Q = Q;
-  a.ldq = s->ldq;
   a.n_recon = (int)s->rp->n_recon;
+  a.ld = (int)s->rp->ld;
   a.recon_cell = s->d.recon_cell;
   a.st_id = s->d.st_id;
+
   a.sub_slot = s->d.sub_slot;
   a.op = s->d.op;
   a.geo = s->d.geo;
@@ -291,21 +285,21 @@ void run_recon(hgks_solver* s, const double* Q) {
   a.omega_pow = s->cfg.omega_pow;
   if (L.cell_type == 4) {
     switch (L.K) {
-      case 14: run_recon_k<14, 4, 6, 128>(s, a); break;
-      case 16: run_recon_k<16, 4, 6, 128>(s, a); break;
-      case 20: run_recon_k<20, 4, 6, 128>(s, a); break;
-      case 24: run_recon_k<24, 4, 6, 128>(s, a); break;
-      case 32: run_recon_k<32, 4, 6, 128>(s, a); break;
-      default: run_recon_k<40, 4, 6, 128>(s, a); break;
+      case 14: run_recon_k<14, 4, 6>(s, a); break;
+      case 16: run_recon_k<16, 4, 6>(s, a); break;
+      case 20: run_recon_k<20, 4, 6>(s, a); break;
+      case 24: run_recon_k<24, 4, 6>(s, a); break;
+      case 32: run_recon_k<32, 4, 6>(s, a); break;
+      default: run_recon_k<40, 4, 6>(s, a); break;
     }
   } else {
     switch (L.K) {
-      case 14: run_recon_k<14, 8, 3, 64>(s, a); break;
-      case 16: run_recon_k<16, 8, 3, 64>(s, a); break;
-      case 20: run_recon_k<20, 8, 3, 64>(s, a); break;
-      case 24: run_recon_k<24, 8, 3, 64>(s, a); break;
-      case 32: run_recon_k<32, 8, 3, 64>(s, a); break;
-      default: run_recon_k<40, 8, 3, 64>(s, a); break;
+      case 14: run_recon_k<14, 8, 3>(s, a); break;
+      case 16: run_recon_k<16, 8, 3>(s, a); break;
+      case 20: run_recon_k<20, 8, 3>(s, a); break;
+      case 24: run_recon_k<24, 8, 3>(s, a); break;
+      case 32: run_recon_k<32, 8, 3>(s, a); break;
+      default: run_recon_k<40, 8, 3>(s, a); break;
     }
   }
 }
@@ -344,7 +338,6 @@ void run_flux(hgks_solver* s, const double* Q, int stage) {
   const RankPlan& rp = *s->rp;
   FluxArgs a;
   a.Q = Q;
-  a.ldq = s->ldq;
   a.ceff = s->d.ceff;
   a.f_cells = s->d.f_cells;
   a.f_geo = s->d.f_geo;
@@ -362,7 +355,6 @@ void run_flux(hgks_solver* s, const double* Q, int stage) {
 UpdateArgs update_args(hgks_solver* s) {
   UpdateArgs u;
   u.Q = s->d.Q;
-  u.ldq = s->ldq;
   u.R = s->d.R;
   u.F1 = s->d.F1;
   u.F2 = s->d.F2;
@@ -378,7 +370,7 @@ UpdateArgs update_args(hgks_solver* s) {
 void pack(hgks_solver* s, const double* Q) {
   const int ns = (int)s->rp->send_list.size();
   if (ns > 0)
-    launch(s, "k_pack", [&] { k_pack<<<blocks(ns, 256), 256, 0, s->stream>>>(Q, s->ldq, s->d.send_list, ns, s->d.sendbuf); });
+    launch(s, "k_pack", [&] { k_pack<<<blocks(3 * ns, 256), 256, 0, s->stream>>>(Q, s->d.send_list, ns, s->d.sendbuf); });
 }
 
 // a5: halo exchange of the 3 ghost layers.  NCCL transport: grouped
@@ -388,18 +380,15 @@ void exchange(hgks_solver* s, double* Q) {
   const RankPlan& rp = *s->rp;
   if (s->n_ranks == 1 || rp.peers.empty() || s->transport != HGKS_TRANSPORT_NCCL) return;
   pack(s, Q);
-  const int ns = (int)rp.send_list.size();
   Nccl& N = nccl();
   NCCL_TRY(N.GroupStart());
   for (size_t p = 0; p < rp.peers.size(); ++p) {
-    for (int v = 0; v < 5; ++v) {
-      if (rp.send_cnt[p] > 0)
-        NCCL_TRY(N.Send(s->d.sendbuf + (size_t)v * ns + rp.send_off[p], (size_t)rp.send_cnt[p], ncclFloat64,
-                        rp.peers[p], s->comm, s->stream));
-      if (rp.recv_cnt[p] > 0)
-        NCCL_TRY(N.Recv(Q + (size_t)v * s->ldq + rp.recv_off[p], (size_t)rp.recv_cnt[p], ncclFloat64, rp.peers[p],
-                        s->comm, s->stream));
-    }
+    if (rp.send_cnt[p] > 0)
+      NCCL_TRY(N.Send(s->d.sendbuf + (size_t)QS * rp.send_off[p], (size_t)QS * rp.send_cnt[p], ncclFloat64,
+                      rp.peers[p], s->comm, s->stream));
+    if (rp.recv_cnt[p] > 0)
+      NCCL_TRY(N.Recv(Q + (size_t)QS * rp.recv_off[p], (size_t)QS * rp.recv_cnt[p], ncclFloat64, rp.peers[p],
+                      s->comm, s->stream));
   }
   NCCL_TRY(N.GroupEnd());
 }
@@ -416,7 +405,7 @@ void bc_ghosts(hgks_solver* s, double* Q) {
   if (rp.n_bghost == 0) return;
   const int first = (int)(rp.n_owned + rp.n_pghost);
   launch(s, "k_bc_ghosts", [&] {
-    k_bc_ghosts<<<blocks(rp.n_bghost, 128), 128, 0, s->stream>>>(Q, s->ldq, first, (int)rp.n_bghost, s->d.bg_cell,
+    k_bc_ghosts<<<blocks(rp.n_bghost, 128), 128, 0, s->stream>>>(Q, first, (int)rp.n_bghost, s->d.bg_cell,
                                                                   s->d.bg_bc, s->d.bg_normal, s->gp);
   });
 }
@@ -447,7 +436,7 @@ void stage(hgks_solver* s, int st) {
 void init_dt(hgks_solver* s) {
   const int n = (int)s->rp->n_owned;
   launch(s, "k_dt_init", [&] {
-    k_dt_init<<<blocks(n, 256), 256, 0, s->stream>>>(s->d.Q, s->ldq, s->d.h_dt, n, s->d.ctrl, s->gp);
+    k_dt_init<<<blocks(n, 256), 256, 0, s->stream>>>(s->d.Q, s->d.h_dt, n, s->d.ctrl, s->gp);
   });
   allreduce_dt(s);
 }
@@ -468,7 +457,7 @@ void upload_state(hgks_solver* s, const double* h_Q, double t) {
     CUDA_TRY(cudaMemcpyAsync(s->d.stage_in, hs, sizeof(double) * 5 * n, cudaMemcpyHostToDevice, s->stream));
   }
   launch(s, "k_scatter_state",
-         [&] { k_scatter_state<<<blocks(n, 256), 256, 0, s->stream>>>(s->d.stage_in, s->d.in_row, n, s->d.Q, s->ldq); });
+         [&] { k_scatter_state<<<blocks(n, 256), 256, 0, s->stream>>>(s->d.stage_in, s->d.in_row, n, s->d.Q); });
   launch(s, "k_reset_ctrl", [&] { k_reset_ctrl<<<1, 1, 0, s->stream>>>(s->d.ctrl, t); });
   init_dt(s);
 }
@@ -544,7 +533,6 @@ hgks_status hgks_init(const hgks_mesh* mc, const hgks_config* cfg, const hgks_di
     s->rank = dist ? dist->rank : 0;
     s->n_ranks = dist ? dist->n_ranks : 1;
     s->transport = dist ? dist->transport : HGKS_TRANSPORT_NCCL;
-    if (const char* rv = std::getenv("HGKS_RECON")) s->recon_variant = std::strcmp(rv, "cell") == 0 ? 1 : 0;
     if (s->n_ranks != m->gm.n_ranks)
       throw Error(HGKS_E_ARG, "dist->n_ranks differs from the mesh partition (" + std::to_string(m->gm.n_ranks) + ")");
     if (dist) CUDA_TRY(cudaSetDevice(dist->device));
@@ -568,7 +556,7 @@ hgks_status hgks_init(const hgks_mesh* mc, const hgks_config* cfg, const hgks_di
     g.t_inf = cfg->t_inf;
     g.mu_exp = cfg->mu_exp;
     for (int k = 0; k < 5; ++k) g.fs[k] = cfg->freestream[k];
-    s->ldq = round32(rp.n_local());
+    s->nq = (size_t)QS * round32(rp.n_local());
     Carve c{(char*)d_ws, 0, ws_bytes};
     if ((reinterpret_cast<uintptr_t>(d_ws) & 255) != 0) throw Error(HGKS_E_ARG, "workspace must be 256-byte aligned");
     layout(m->gm, rp, c, s->d);
@@ -577,7 +565,8 @@ hgks_status hgks_init(const hgks_mesh* mc, const hgks_config* cfg, const hgks_di
       if (bytes) CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
     };
     up(s->d.recon_cell, rp.recon_cell.data(), rp.recon_cell.size() * sizeof(int));
-    up(s->d.st_id, rp.st_id.data(), rp.st_id.size() * sizeof(int));
+    up(s->d.st_id, rp.st_id_tiled.data(), rp.st_id_tiled.size() * sizeof(int));
+
     up(s->d.sub_slot, rp.sub_slot.data(), rp.sub_slot.size());
     up(s->d.op, rp.op.data(), rp.op.size() * sizeof(double));
     up(s->d.geo, rp.geo.data(), rp.geo.size() * sizeof(double));
@@ -600,7 +589,7 @@ hgks_status hgks_init(const hgks_mesh* mc, const hgks_config* cfg, const hgks_di
     std::sort(out_local.begin(), out_local.end(), [&](int a, int b) { return rp.l2g[a] < rp.l2g[b]; });
     up(s->d.in_row, in_row.data(), in_row.size() * sizeof(int64_t));
     up(s->d.out_local, out_local.data(), out_local.size() * sizeof(int));
-    CUDA_TRY(cudaMemsetAsync(s->d.Q, 0, sizeof(double) * 5 * s->ldq, st));
+    CUDA_TRY(cudaMemsetAsync(s->d.Q, 0, sizeof(double) * s->nq, st));
     Ctrl h{};
     h.bad_cell = INT_MAX;
     h.dtmin_bits = 0x7fefffffffffffffull;
@@ -680,7 +669,7 @@ hgks_status hgks_get_state(const hgks_solver* sc, double* h_Q, int64_t* h_gid, d
     if (!s || !h_Q) throw Error(HGKS_E_ARG, "null argument");
     const int n = (int)s->rp->n_owned;
     launch(s, "k_gather_state", [&] {
-      k_gather_state<<<blocks(n, 256), 256, 0, s->stream>>>(s->d.Q, s->ldq, s->d.out_local, n, s->d.stage_out);
+      k_gather_state<<<blocks(n, 256), 256, 0, s->stream>>>(s->d.Q, s->d.out_local, n, s->d.stage_out);
     });
     CUDA_TRY(cudaMemcpyAsync(h_Q, s->d.stage_out, sizeof(double) * 5 * n, cudaMemcpyDeviceToHost, s->stream));
     Ctrl h;
@@ -701,14 +690,14 @@ hgks_status hgks_debug_residual(hgks_solver* s, const double* h_Q, double dt, do
     if (s->n_ranks != 1) throw Error(HGKS_E_ARG, "hgks_debug_residual is single-rank only");
     const int n = (int)s->rp->n_owned;
     // save state, load h_Q, run stage-1 reconstruction + flux, restore
-    CUDA_TRY(cudaMemcpyAsync(s->d.Qtmp, s->d.Q, sizeof(double) * 5 * s->ldq, cudaMemcpyDeviceToDevice, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(s->d.Qtmp, s->d.Q, sizeof(double) * s->nq, cudaMemcpyDeviceToDevice, s->stream));
     Ctrl saved;
     CUDA_TRY(cudaMemcpyAsync(&saved, s->d.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s->stream));
     CUDA_TRY(cudaStreamSynchronize(s->stream));
     CUDA_TRY(cudaMemcpyAsync(s->d.stage_in, h_Q, sizeof(double) * 5 * s->mesh->gm.nc, cudaMemcpyHostToDevice,
                              s->stream));
     launch(s, "k_scatter_state",
-           [&] { k_scatter_state<<<blocks(n, 256), 256, 0, s->stream>>>(s->d.stage_in, s->d.in_row, n, s->d.Q, s->ldq); });
+           [&] { k_scatter_state<<<blocks(n, 256), 256, 0, s->stream>>>(s->d.stage_in, s->d.in_row, n, s->d.Q); });
     Ctrl h = saved;
     h.dt = dt;
     CUDA_TRY(cudaMemcpyAsync(s->d.ctrl, &h, sizeof(Ctrl), cudaMemcpyHostToDevice, s->stream));
@@ -719,7 +708,7 @@ hgks_status hgks_debug_residual(hgks_solver* s, const double* h_Q, double dt, do
     std::vector<double> F1((size_t)10 * s->rp->n_faces);
     std::vector<int> cf(s->rp->cf);
     CUDA_TRY(cudaMemcpyAsync(F1.data(), s->d.F1, F1.size() * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
-    CUDA_TRY(cudaMemcpyAsync(s->d.Q, s->d.Qtmp, sizeof(double) * 5 * s->ldq, cudaMemcpyDeviceToDevice, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(s->d.Q, s->d.Qtmp, sizeof(double) * s->nq, cudaMemcpyDeviceToDevice, s->stream));
     CUDA_TRY(cudaMemcpyAsync(s->d.ctrl, &saved, sizeof(Ctrl), cudaMemcpyHostToDevice, s->stream));
     CUDA_TRY(cudaStreamSynchronize(s->stream));
     const int NF = s->lay.nfaces;
@@ -814,11 +803,8 @@ hgks_status hgks_group_step(hgks_solver* const* ss, int32_t n, int32_t n_steps, 
           size_t ip = std::find(rpp.peers.begin(), rpp.peers.end(), q) - rpp.peers.begin();
           if (ip == rpp.peers.size() || rpp.send_cnt[ip] != rq.recv_cnt[iq])
             throw Error(HGKS_E_STATE, "inconsistent exchange plans between ranks");
-          const size_t ns = rpp.send_list.size();
-          for (int v = 0; v < 5; ++v)
-            CUDA_TRY(cudaMemcpyAsync(ss[q]->d.Q + (size_t)v * ss[q]->ldq + rq.recv_off[iq],
-                                     sp->d.sendbuf + (size_t)v * ns + rpp.send_off[ip],
-                                     sizeof(double) * rq.recv_cnt[iq], cudaMemcpyDeviceToDevice, s0->stream));
+          CUDA_TRY(cudaMemcpyAsync(ss[q]->d.Q + (size_t)QS * rq.recv_off[iq], sp->d.sendbuf + (size_t)QS * rpp.send_off[ip],
+                                   sizeof(double) * QS * rq.recv_cnt[iq], cudaMemcpyDeviceToDevice, s0->stream));
         }
       }
     };

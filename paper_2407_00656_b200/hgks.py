@@ -84,9 +84,10 @@ def lib(build_if_needed: bool = True):
     if _lib is None:
         if build_if_needed and _build.needs_build():
             _build.build()
-        if not os.path.exists(_build.LIB):
-            raise RuntimeError(f"libhgks.so missing at {_build.LIB}: run __graft_entry__.build()")
-        L = C.CDLL(_build.LIB)
+        path = os.environ.get("HGKS_LIB", _build.LIB)  # experiments may point at another build
+        if not os.path.exists(path):
+            raise RuntimeError(f"libhgks.so missing at {path}: run __graft_entry__.build()")
+        L = C.CDLL(path)
         L.hgks_last_error.restype = C.c_char_p
         L.hgks_version.restype = C.c_char_p
         L.hgks_mesh_create.argtypes = [C.POINTER(MeshDesc), C.POINTER(C.c_void_p)]
