@@ -109,6 +109,8 @@ typedef struct {
   int32_t n_peers;           /* ranks this rank exchanges ghosts with */
   int64_t send_cells, recv_cells;    /* per stage */
   int64_t edge_cut;          /* faces between different ranks (global) */
+  int64_t n_early_cells;     /* owned cells reconstructed while the halo exchange is in flight */
+  int64_t n_early_faces;     /* interior faces fluxed while the halo exchange is in flight */
 } hgks_mesh_stats;
 
 typedef struct {

@@ -76,8 +76,8 @@ struct RankPlan {
   int64_t ghost_layer[3] = {0, 0, 0};
   int64_t n_local() const { return n_owned + n_pghost + n_bghost; }
   std::vector<int64_t> l2g;             // [n_owned + n_pghost] global ids
-  // reconstruction set: owned cells then layer-1 ghosts
-  int64_t n_recon = 0;
+  // reconstruction set (recon index order): [early owned | -1 pad to 128 | late owned | layer-1 ghosts]
+  int64_t n_recon = 0, n_recon_early = 0, recon_late0 = 0;
   int64_t ld = 0;                       // n_recon padded to the 128-cell tile
   std::vector<int32_t> recon_cell;      // [n_recon] local cell id
   std::vector<int32_t> st_id;           // [K][ld] local ids (entry-major; host only)
@@ -86,7 +86,7 @@ struct RankPlan {
   std::vector<double> op;               // [op_entries] per cell, tiled entry-major (kernels.cuh k_recon)
   std::vector<double> geo;              // [8] per cell, tiled: V^{2/3}, V^{4/3}, M2 (xx,yy,zz,xy,xz,yz)
   // faces: interior [0, n_if), wall [n_if, n_if + n_wf), farfield after
-  int64_t n_faces = 0, n_if = 0, n_wf = 0, n_ff = 0;
+  int64_t n_faces = 0, n_if = 0, n_if_early = 0, n_wf = 0, n_ff = 0;  // interior faces [0, n_if_early) need no ghosts
   std::vector<int32_t> f_cells;         // [n_faces][2] local owner / neighbour (bc faces: ghost id)
   std::vector<double> f_geo;            // [n_faces][FG]: nv vertices rel. owner centroid, then d (3)
   int f_geo_stride = 12;

@@ -76,10 +76,14 @@ __device__ inline void farfield_riemann(const double qi[5], const double n[3], c
 // contiguous block (single message per peer in the halo exchange).
 constexpr int QS = 6;
 
+// part 0: ghosts of owned cells (before the halo exchange completes), 1: ghosts
+// of partition-ghost cells (after it), 2: all
 __global__ void k_bc_ghosts(double* __restrict__ Q, int first, int n, const int* __restrict__ bg_cell,
-                            const int* __restrict__ bg_bc, const double* __restrict__ bg_normal, GasParams gp) {
+                            const int* __restrict__ bg_bc, const double* __restrict__ bg_normal, GasParams gp,
+                            int n_owned, int part) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
+  if (part != 2 && (bg_cell[k] < n_owned) != (part == 0)) return;
   const double* qc = Q + (size_t)bg_cell[k] * QS;
   double qi[5];
 #pragma unroll
@@ -108,6 +112,7 @@ constexpr int kTile = 128;        // reconstructed cells per block
 struct ReconArgs {
   const double* __restrict__ Q;         // [n_local][QS]
   int n_recon;
+  int tile0;                            // first 128-cell tile of this launch
   int ld;                               // n_recon padded to kTile (tiled entry-major arrays, setup.cpp)
   const int* __restrict__ recon_cell;   // [n_recon] local cell id
   const int* __restrict__ st_id;        // [K] per cell, tiled: stencil member local ids
@@ -136,12 +141,14 @@ __global__ void __launch_bounds__(kTile, HGKS_RECON_MINB) k_recon(ReconArgs a) {
   extern __shared__ __align__(16) double smem[];
   double* __restrict__ dqs = smem;                   // [K][5][kTile] Q_k - Q_i
   const int t = threadIdx.x;
-  const int r = blockIdx.x * kTile + t;
-  const bool active = r < a.n_recon;
+  const int tile = a.tile0 + blockIdx.x;
+  const int r = tile * kTile + t;
+  int ci = r < a.n_recon ? __ldg(a.recon_cell + r) : -1;  // -1: padding
+  const bool active = ci >= 0;
+  if (!active) ci = 0;
   // tiled entry-major per-cell arrays (setup.cpp): entry e of this cell at (tile*NE + e)*kTile + t
-  const size_t tb = (size_t)blockIdx.x * kTile;
+  const size_t tb = (size_t)tile * kTile;
   const int* __restrict__ sid = a.st_id + tb * K + t;
-  const int ci = active ? __ldg(a.recon_cell + r) : 0;
   double qi[5];
   {
     const double2* q2 = reinterpret_cast<const double2*>(a.Q + (size_t)ci * QS);

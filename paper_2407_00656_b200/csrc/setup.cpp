@@ -739,14 +739,36 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
   std::unordered_map<int64_t, int32_t> g2l;
   g2l.reserve(rp.l2g.size() * 2);
   for (size_t k = 0; k < rp.l2g.size(); ++k) g2l[rp.l2g[k]] = (int32_t)k;
-  // recon set = owned + layer-1 ghosts
-  rp.recon_cell.resize(rp.n_owned);
-  std::iota(rp.recon_cell.begin(), rp.recon_cell.end(), 0);
-  for (int64_t g : pg)
-    if (layer[g] == 1) rp.recon_cell.push_back(g2l[g]);
-  // layer-1 ghosts in Morton order too, so their reconstruction tiles stay compact
-  std::sort(rp.recon_cell.begin() + rp.n_owned, rp.recon_cell.end(),
-            [&](int32_t a, int32_t b) { return by_morton(rp.l2g[a], rp.l2g[b]); });
+  // Reconstruction order (P:856-866 overlap): [early | pad | late | L1 ghosts], where
+  // "early" owned cells have stencils made of owned cells and of boundary ghosts of
+  // owned cells only, so they are reconstructed while the halo exchange is in
+  // flight; the early block is padded (recon_cell = -1) to a whole 128-cell tile.
+  std::vector<char> early_cell(rp.n_owned, 0);
+  {
+    std::vector<int32_t> early, late;
+    for (int64_t i = 0; i < rp.n_owned; ++i) {
+      const int64_t gi = owned[i];
+      bool e = true;
+      for (int64_t o = gm.big_off[gi]; o < gm.big_off[gi + 1] && e; ++o) {
+        const int64_t id = gm.big_id[o];
+        const int64_t owner_cell = id < nc ? id : gm.g_cell[id - nc];
+        e = gm.part[owner_cell] == rank;
+      }
+      early_cell[i] = e;
+      (e ? early : late).push_back((int32_t)i);
+    }
+    rp.n_recon_early = (int64_t)early.size();
+    rp.recon_cell = early;
+    rp.recon_cell.resize((early.size() + 127) / 128 * 128, -1);
+    rp.recon_late0 = (int64_t)rp.recon_cell.size();
+    rp.recon_cell.insert(rp.recon_cell.end(), late.begin(), late.end());
+    const size_t g0 = rp.recon_cell.size();
+    for (int64_t g : pg)
+      if (layer[g] == 1) rp.recon_cell.push_back(g2l[g]);
+    // layer-1 ghosts in Morton order too, so their reconstruction tiles stay compact
+    std::sort(rp.recon_cell.begin() + g0, rp.recon_cell.end(),
+              [&](int32_t a, int32_t b) { return by_morton(rp.l2g[a], rp.l2g[b]); });
+  }
   rp.n_recon = (int64_t)rp.recon_cell.size();
   // BC ghosts needed: those of faces of recon cells and of their neighbours
   std::unordered_map<int64_t, int32_t> bg2l;
@@ -785,10 +807,11 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
   rp.stencil_min = 1 << 30;
   rp.stencil_max = 0;
   for (int64_t r = 0; r < Rn; ++r) {
+    if (rp.recon_cell[r] < 0) continue;  // padding of the early block
     int64_t gi = rp.l2g[rp.recon_cell[r]];
     int64_t o0 = gm.big_off[gi];
     int kk = (int)(gm.big_off[gi + 1] - o0);
-    if (r < rp.n_owned) {
+    if (rp.recon_cell[r] < rp.n_owned) {
       rp.stencil_min = std::min(rp.stencil_min, kk);
       rp.stencil_max = std::max(rp.stencil_max, kk);
     }
@@ -828,18 +851,26 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
   }
   for (int64_t f : fl)
     if (gm.f_nb[f] < 0) local_of(nc + gm.f_ghost[f]);
-  // order: interior faces by min local endpoint, then wall, then farfield
+  // order: early interior faces (both cells reconstructed before the exchange
+  // completes), late interior faces, wall, farfield; by min local endpoint within
+  auto is_early = [&](int64_t gcell) {
+    const int32_t l = g2l[gcell];
+    return l < rp.n_owned && early_cell[l];
+  };
   auto fkey = [&](int64_t f) -> std::pair<int, int64_t> {
-    int cls = gm.f_nb[f] >= 0 ? 0 : (gm.f_bc[f] == 1 ? 1 : 2);
+    int cls = gm.f_nb[f] >= 0 ? (is_early(gm.f_owner[f]) && is_early(gm.f_nb[f]) ? 0 : 1)
+                              : (gm.f_bc[f] == 1 ? 2 : 3);
     int64_t a = g2l[gm.f_owner[f]];
     int64_t b = gm.f_nb[f] >= 0 ? g2l[gm.f_nb[f]] : a;
-    return {cls, std::min(a, b) * 8 + 0};
+    return {cls, std::min(a, b)};
   };
   std::stable_sort(fl.begin(), fl.end(), [&](int64_t a, int64_t b) { return fkey(a) < fkey(b); });
   rp.n_faces = (int64_t)fl.size();
   for (int64_t f : fl) {
-    if (gm.f_nb[f] >= 0) ++rp.n_if;
-    else if (gm.f_bc[f] == 1) ++rp.n_wf;
+    const int cls = fkey(f).first;
+    if (cls == 0) ++rp.n_if_early;
+    if (cls <= 1) ++rp.n_if;
+    else if (cls == 2) ++rp.n_wf;
     else ++rp.n_ff;
   }
   rp.f_geo_stride = 3 * L.nv + 3;

@@ -204,6 +204,9 @@ struct hgks_solver {
   GasParams gp;
   int rank = 0, n_ranks = 1, device = 0, transport = HGKS_TRANSPORT_NCCL;
   size_t recon_smem_set = 0;
+  int recon_t1 = 0;  // end tile of the current reconstruction launch
+  cudaStream_t comm_stream = nullptr;  // NCCL halo exchange (overlapped with the early work)
+  cudaEvent_t ev_packed = nullptr, ev_halo = nullptr;
   cudaStream_t stream = nullptr;
   DevArrays d{};
   size_t nq = 0;  // doubles in Q
@@ -265,14 +268,21 @@ void run_recon_k(hgks_solver* s, const ReconArgs& a) {
     CUDA_TRY(cudaFuncSetAttribute(k_recon<K, M, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     s->recon_smem_set = smem;
   }
-  launch(s, "k_recon", [&] { k_recon<K, M, NM><<<blocks(a.n_recon, kTile), kTile, smem, s->stream>>>(a); });
+  const int n_tiles = s->recon_t1 - a.tile0;
+  if (n_tiles <= 0) return;
+  launch(s, "k_recon", [&] { k_recon<K, M, NM><<<n_tiles, kTile, smem, s->stream>>>(a); });
 }
 
-void run_recon(hgks_solver* s, const double* Q) {
+// part 0: tiles of the early cells, 1: the rest, 2: all
+void run_recon(hgks_solver* s, const double* Q, int part) {
   const Layout& L = s->lay;
+  const RankPlan& rp = *s->rp;
   ReconArgs a;
   a.Q = Q;
-  a.n_recon = (int)s->rp->n_recon;
+  a.n_recon = (int)rp.n_recon;
+  const int t_mid = (int)(rp.recon_late0 / kTile), t_end = (int)((rp.n_recon + kTile - 1) / kTile);
+  a.tile0 = part == 1 ? t_mid : 0;
+  s->recon_t1 = part == 0 ? t_mid : t_end;
   a.ld = (int)s->rp->ld;
   a.recon_cell = s->d.recon_cell;
   a.st_id = s->d.st_id;
@@ -320,10 +330,14 @@ void launch_flux(hgks_solver* s, const FluxArgs& a, int stage, bool tau0) {
 }
 
 template <int NV>
-void run_flux_nv(hgks_solver* s, FluxArgs a, int stage) {
+void run_flux_nv(hgks_solver* s, FluxArgs a, int stage, int part) {
   const RankPlan& rp = *s->rp;
   const bool tau0 = s->cfg.tau_mode == 0;
-  const int64_t ranges[3][2] = {{0, rp.n_if}, {rp.n_if, rp.n_wf}, {rp.n_if + rp.n_wf, rp.n_ff}};
+  // part 0: early interior faces; 1: late interior + wall + farfield; 2: all
+  const int64_t i0 = part == 1 ? rp.n_if_early : 0, i1 = part == 0 ? rp.n_if_early : rp.n_if;
+  const int64_t ranges[3][2] = {{i0, i1 - i0},
+                                {rp.n_if, part == 0 ? 0 : rp.n_wf},
+                                {rp.n_if + rp.n_wf, part == 0 ? 0 : rp.n_ff}};
   for (int bc = 0; bc < 3; ++bc) {
     a.face0 = (int)ranges[bc][0];
     a.n_faces = (int)ranges[bc][1];
@@ -334,7 +348,7 @@ void run_flux_nv(hgks_solver* s, FluxArgs a, int stage) {
   }
 }
 
-void run_flux(hgks_solver* s, const double* Q, int stage) {
+void run_flux(hgks_solver* s, const double* Q, int stage, int part) {
   const RankPlan& rp = *s->rp;
   FluxArgs a;
   a.Q = Q;
@@ -348,8 +362,8 @@ void run_flux(hgks_solver* s, const double* Q, int stage) {
   a.F2 = s->d.F2;
   a.ctrl = s->d.ctrl;
   a.gp = s->gp;
-  if (s->lay.nv == 3) run_flux_nv<3>(s, a, stage);
-  else run_flux_nv<4>(s, a, stage);
+  if (s->lay.nv == 3) run_flux_nv<3>(s, a, stage, part);
+  else run_flux_nv<4>(s, a, stage, part);
 }
 
 UpdateArgs update_args(hgks_solver* s) {
@@ -380,17 +394,26 @@ void exchange(hgks_solver* s, double* Q) {
   const RankPlan& rp = *s->rp;
   if (s->n_ranks == 1 || rp.peers.empty() || s->transport != HGKS_TRANSPORT_NCCL) return;
   pack(s, Q);
+  CUDA_TRY(cudaEventRecord(s->ev_packed, s->stream));
+  CUDA_TRY(cudaStreamWaitEvent(s->comm_stream, s->ev_packed, 0));
   Nccl& N = nccl();
   NCCL_TRY(N.GroupStart());
   for (size_t p = 0; p < rp.peers.size(); ++p) {
     if (rp.send_cnt[p] > 0)
       NCCL_TRY(N.Send(s->d.sendbuf + (size_t)QS * rp.send_off[p], (size_t)QS * rp.send_cnt[p], ncclFloat64,
-                      rp.peers[p], s->comm, s->stream));
+                      rp.peers[p], s->comm, s->comm_stream));
     if (rp.recv_cnt[p] > 0)
       NCCL_TRY(N.Recv(Q + (size_t)QS * rp.recv_off[p], (size_t)QS * rp.recv_cnt[p], ncclFloat64, rp.peers[p],
-                      s->comm, s->stream));
+                      s->comm, s->comm_stream));
   }
   NCCL_TRY(N.GroupEnd());
+  CUDA_TRY(cudaEventRecord(s->ev_halo, s->comm_stream));
+}
+
+// the compute stream waits for the ghosts (no-op without an NCCL exchange in flight)
+void wait_halo(hgks_solver* s) {
+  if (s->n_ranks == 1 || s->rp->peers.empty() || s->transport != HGKS_TRANSPORT_NCCL) return;
+  CUDA_TRY(cudaStreamWaitEvent(s->stream, s->ev_halo, 0));
 }
 
 // a4: global min of the CFL bound (exact, order independent)
@@ -400,21 +423,29 @@ void allreduce_dt(hgks_solver* s) {
                             s->stream));
 }
 
-void bc_ghosts(hgks_solver* s, double* Q) {
+void bc_ghosts(hgks_solver* s, double* Q, int part) {
   const RankPlan& rp = *s->rp;
   if (rp.n_bghost == 0) return;
   const int first = (int)(rp.n_owned + rp.n_pghost);
   launch(s, "k_bc_ghosts", [&] {
     k_bc_ghosts<<<blocks(rp.n_bghost, 128), 128, 0, s->stream>>>(Q, first, (int)rp.n_bghost, s->d.bg_cell,
-                                                                  s->d.bg_bc, s->d.bg_normal, s->gp);
+                                                                  s->d.bg_bc, s->d.bg_normal, s->gp,
+                                                                  (int)rp.n_owned, part);
   });
 }
 
-// everything of one stage after the ghosts are current
-void stage_compute(hgks_solver* s, int st) {
-  bc_ghosts(s, s->d.Q);
-  run_recon(s, s->d.Q);
-  run_flux(s, s->d.Q, st);
+// work of one stage that needs no partition-ghost data (overlaps the exchange)
+void stage_early(hgks_solver* s, int st) {
+  bc_ghosts(s, s->d.Q, 0);
+  run_recon(s, s->d.Q, 0);
+  run_flux(s, s->d.Q, st, 0);
+}
+
+// the rest of the stage, after the ghosts are current
+void stage_late(hgks_solver* s, int st) {
+  bc_ghosts(s, s->d.Q, 1);
+  run_recon(s, s->d.Q, 1);
+  run_flux(s, s->d.Q, st, 1);
   UpdateArgs u = update_args(s);
   const int n = (int)s->rp->n_owned;
   const int nf = s->lay.nfaces;
@@ -428,8 +459,10 @@ void stage_compute(hgks_solver* s, int st) {
 }
 
 void stage(hgks_solver* s, int st) {
-  exchange(s, s->d.Q);
-  stage_compute(s, st);
+  exchange(s, s->d.Q);  // NCCL on the comm stream
+  stage_early(s, st);
+  wait_halo(s);
+  stage_late(s, st);
   if (st == 2) allreduce_dt(s);
 }
 
@@ -507,6 +540,8 @@ hgks_status hgks_mesh_info(const hgks_mesh* mc, int32_t rank, hgks_mesh_stats* s
     st->send_cells = (int64_t)rp.send_list.size();
     for (auto c : rp.recv_cnt) st->recv_cells += c;
     st->edge_cut = m->gm.edge_cut;
+    st->n_early_cells = rp.n_recon_early;
+    st->n_early_faces = rp.n_if_early;
   });
 }
 
@@ -600,6 +635,9 @@ hgks_status hgks_init(const hgks_mesh* mc, const hgks_config* cfg, const hgks_di
       ncclUniqueId id;
       std::memcpy(id.internal, dist->nccl_id, 128);
       NCCL_TRY(N.CommInitRank(&s->comm, s->n_ranks, id, s->rank));
+      CUDA_TRY(cudaStreamCreateWithFlags(&s->comm_stream, cudaStreamNonBlocking));
+      CUDA_TRY(cudaEventCreateWithFlags(&s->ev_packed, cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&s->ev_halo, cudaEventDisableTiming));
     }
     if (s->n_ranks > 1) CUDA_TRY(cudaMallocHost(&s->pinned, sizeof(double) * 5 * std::max<int64_t>(1, rp.n_owned)));
     CUDA_TRY(cudaStreamSynchronize(st));
@@ -620,6 +658,9 @@ hgks_status hgks_destroy(hgks_solver* s) {
       }
     for (auto e : s->event_pool) cudaEventDestroy(e);
     if (s->comm && nccl().CommDestroy) nccl().CommDestroy(s->comm);
+    if (s->comm_stream) cudaStreamDestroy(s->comm_stream);
+    if (s->ev_packed) cudaEventDestroy(s->ev_packed);
+    if (s->ev_halo) cudaEventDestroy(s->ev_halo);
     if (s->pinned) cudaFreeHost(s->pinned);
     delete s;
   });
@@ -701,9 +742,9 @@ hgks_status hgks_debug_residual(hgks_solver* s, const double* h_Q, double dt, do
     Ctrl h = saved;
     h.dt = dt;
     CUDA_TRY(cudaMemcpyAsync(s->d.ctrl, &h, sizeof(Ctrl), cudaMemcpyHostToDevice, s->stream));
-    bc_ghosts(s, s->d.Q);
-    run_recon(s, s->d.Q);
-    run_flux(s, s->d.Q, 1);
+    bc_ghosts(s, s->d.Q, 2);
+    run_recon(s, s->d.Q, 2);
+    run_flux(s, s->d.Q, 1, 2);
     // L = (Q* - Q) ... computed directly on host from face fluxes for clarity
     std::vector<double> F1((size_t)10 * s->rp->n_faces);
     std::vector<int> cf(s->rp->cf);
@@ -793,7 +834,6 @@ hgks_status hgks_group_step(hgks_solver* const* ss, int32_t n, int32_t n_steps, 
     auto group_min = [&] { launch(s0, "k_group_min", [&] { k_group_min<<<1, 32, 0, s0->stream>>>(gc); }); };
     // ghost copies: receiver q, peer p (in-process transport)
     auto loop_exchange = [&] {
-      for (int k = 0; k < n; ++k) pack(ss[k], ss[k]->d.Q);
       for (int q = 0; q < n; ++q) {
         const RankPlan& rq = *ss[q]->rp;
         for (size_t iq = 0; iq < rq.peers.size(); ++iq) {
@@ -815,8 +855,10 @@ hgks_status hgks_group_step(hgks_solver* const* ss, int32_t n, int32_t n_steps, 
           k_step_begin<<<1, 1, 0, s0->stream>>>(ss[k]->d.ctrl, ss[k]->cfg.cfl, ss[k]->cfg.fixed_dt, t_stop);
         });
       for (int st = 1; st <= 2; ++st) {
+        for (int k = 0; k < n; ++k) pack(ss[k], ss[k]->d.Q);
+        for (int k = 0; k < n; ++k) stage_early(ss[k], st);
         loop_exchange();
-        for (int k = 0; k < n; ++k) stage_compute(ss[k], st);
+        for (int k = 0; k < n; ++k) stage_late(ss[k], st);
       }
       group_min();
     }

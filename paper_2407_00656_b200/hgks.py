@@ -55,7 +55,7 @@ class MeshStats(C.Structure):
                 ("ghost_layer", C.c_int64 * 3), ("n_bghost", C.c_int64), ("n_faces", C.c_int64),
                 ("n_faces_bc", C.c_int64), ("stencil_min", C.c_int32), ("stencil_max", C.c_int32),
                 ("n_sub", C.c_int32), ("n_peers", C.c_int32), ("send_cells", C.c_int64), ("recv_cells", C.c_int64),
-                ("edge_cut", C.c_int64)]
+                ("edge_cut", C.c_int64), ("n_early_cells", C.c_int64), ("n_early_faces", C.c_int64)]
 
     def as_dict(self):
         d = {}

@@ -47,6 +47,7 @@ def test_host_setup_matches_oracle_counts(mk):
     assert info["stencil_min"] == om.min_stencil and info["stencil_max"] == om.max_stencil
     assert info["n_sub"] == om.n_subs
     assert info["n_ghost"] == 0 and info["n_peers"] == 0
+    assert info["n_early_cells"] == info["n_owned"] and info["n_early_faces"] == info["n_faces"] - info["n_faces_bc"]
 
 
 def test_sphere_shell_boundary_faces():

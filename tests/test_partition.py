@@ -1,8 +1,8 @@
 """Multi-rank host logic (8(e)) on CPU with world-size 2/4 gloo.
 
 Each rank builds its partition plan through the C-ABI (hgks_mesh_plan) and the
-test runs the halo exchange the NCCL path performs -- SoA pack of send_list,
-one message per peer, receive straight into the contiguous ghost range --
+test runs the halo exchange the NCCL path performs -- pack of send_list in plan
+order, one message per peer, receive straight into the contiguous ghost range --
 over gloo, then checks every ghost against the global field, and checks the
 3-layer closure against the oracle's independently built stencils.
 """
@@ -49,7 +49,7 @@ def _worker(rank, world, port, kind, out_q):
         nl = l2g.size
         Q = np.full((5, nl), np.nan)
         Q[:, :n_owned] = Qg[l2g[:n_owned]].T
-        # pack exactly like k_pack: SoA [5][n_send]
+        # pack in send_list order (k_pack packs the same rows, 48-byte AoS)
         sl = plan["send_list"]
         ns = sl.size
         buf = Q[:, sl].copy()                              # [5][ns]
@@ -108,7 +108,11 @@ def test_partition_exchange_gloo(world, kind):
     # every ghost value arrived bitwise from its owner
     for r in range(world):
         assert res[r]["ghosts_ok"], r
-        assert res[r]["info"]["n_ghost"] == len(res[r]["ghosts"])
+        info = res[r]["info"]
+        assert info["n_ghost"] == len(res[r]["ghosts"])
+        # overlap split: some but not all cells/faces need no ghosts
+        assert 0 < info["n_early_cells"] < info["n_owned"]
+        assert 0 < info["n_early_faces"] < info["n_faces"]
     # send volume of all ranks == receive volume of all ranks
     assert sum(res[r]["send_total"] for r in range(world)) == sum(len(res[r]["ghosts"]) for r in range(world))
     # 3-layer closure against the oracle's independent stencils: every cell the
