@@ -166,6 +166,9 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4"],
+                    help="c2: 48^3 Kuhn box per GPU (default, BASELINE configs[1]); c3: subsonic sphere "
+                         "12x35^3 hexes (configs[2]); c4: supersonic sphere 12x70^3 hexes (configs[3])")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -184,16 +187,31 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    nx, ny, nz = box_dims(world)
-    mi = W.kuhn_box(nx, ny, nz, h=2.0 / N_BLOCK)
-    Q0 = W.advection_ic(mi, gamma=GAMMA)
+    if args.workload == "c2":
+        nx, ny, nz = box_dims(world)
+        mi = W.kuhn_box(nx, ny, nz, h=2.0 / N_BLOCK)
+        Q0 = W.advection_ic(mi, gamma=GAMMA)
+        cfg = hgks.SolverConfig(gamma=GAMMA, cfl=CFL)
+        wl = (f"configs[1] top size: {N_BLOCK}^3 Kuhn box per GPU, 6 tets/cube, periodic, tau=0, CFL {CFL}")
+        scaling, layout = "weak", (14, 4, 6)
+        extra = {"box_cubes": [nx, ny, nz]}
+    else:
+        n, ma, re = (35, 0.2535, 118.0) if args.workload == "c3" else (70, 1.5, 300.0)
+        mi = W.sphere_shell(n)
+        fs = (1.0, ma, 0.0, 0.0, 1.0 / GAMMA)
+        Q0 = W.uniform_state(mi.n_cells, 1.0, (ma, 0.0, 0.0), 1.0 / GAMMA, gamma=GAMMA)  # free-stream IC
+        cfg = hgks.SolverConfig(gamma=GAMMA, cfl=0.5, tau_mode=1, mu_inf=ma / re, c1=1.0, t_inf=1.0 / GAMMA,
+                                freestream=fs)
+        wl = (f"configs[{2 if args.workload == 'c3' else 3}]: sphere shell 12x{n}^3 hexes, Ma {ma}, Re {re}, "
+              f"NS collision time, wall + farfield, CFL 0.5, free-stream start")
+        scaling, layout = "strong", (24, 8, 3)
+        extra = {"sphere_N": n}
     mesh = hgks.Mesh(mi, n_ranks=world)
     nid = None
     if world > 1:
         obj = [hgks.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
-    cfg = hgks.SolverConfig(gamma=GAMMA, cfl=CFL)
     s = hgks.Solver(mesh, Q0, cfg, device=local, rank=rank, nccl_id=nid)
     info = mesh.info(rank)
     n_owned = info["n_owned"]
@@ -267,10 +285,9 @@ def main():
     avg_ms = kt["ms"] / max(1, kt["launches"])
     roof = None
     if name.startswith("k_recon"):
-        bytes_per_launch = recon_bytes_per_cell() * info["n_owned"] + 0 * info["n_ghost"]
-        # recon also runs over layer-1 ghosts for N > 1
+        # recon runs over owned cells and layer-1 ghosts
         n_recon = info["n_owned"] + info["ghost_layer"][0]
-        bytes_per_launch = recon_bytes_per_cell() * n_recon
+        bytes_per_launch = recon_bytes_per_cell(*layout) * n_recon
         achieved = bytes_per_launch / (avg_ms * 1e-3) / 1e9
         roof = {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": None,
@@ -278,22 +295,23 @@ def main():
                 "peak_source": hbm_src + " (burst copy)"}
     else:
         flops = json.load(open(os.path.join(ROOT, "profiles", "flops_per_unit.json")))
-        fpl = flops.get(name, {}).get("flops_per_launch_per_face", None)
-        nf = info["n_faces"]
-        if fpl:
-            achieved = fpl * nf / (avg_ms * 1e-3) / 1e12
+        fpf = flops.get(args.workload, {}).get(name, {}).get("fp64_flops_per_face")
+        nf = info["n_faces"] - info["n_faces_bc"]  # interior faces (the counts are per interior face)
+        if fpf:
+            achieved = fpf * nf / (avg_ms * 1e-3) / 1e12
             roof = {"kernel": name, "bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                     "frac": achieved / fp64_peak, "traffic": None, "avg_launch_ms": avg_ms,
-                    "peak_source": fp64_src}
+                    "flops_per_face": fpf, "flops_source": "ncu sass op counts (2 dfma + dadd + dmul), "
+                                                          "profiles/flops_per_unit.json", "peak_source": fp64_src}
     traffic_path = os.path.join(ROOT, "profiles", "traffic.json")
     if roof and os.path.exists(traffic_path):
-        tr = json.load(open(traffic_path)).get(roof["kernel"])
-        if tr:
+        tr = json.load(open(traffic_path)).get(roof["kernel"]) if args.workload == "c2" else None
+        if tr and roof["kernel"].startswith("k_recon"):
             roof["traffic"] = tr["dram_bytes_per_launch"] * (n_recon / tr["cells"] if "cells" in tr else 1.0)
 
     # ---------------- CPU baseline (oracle, rank 0, bounded sample) ----------------
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload == "c2":
         threads = len(os.sched_getaffinity(0))
         rate, secs, ncell = cpu_oracle_rate(N_BLOCK, 1, threads)
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
@@ -305,10 +323,9 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "ms_per_step_unprofiled": ms_unprof / args.steps,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded generator: periodic Kuhn tets, exact-average accuracy-test IC)",
-            "config": {"workload": f"configs[1] top size: {N_BLOCK}^3 Kuhn box per GPU, 6 tets/cube, periodic, "
-                                   f"tau=0, CFL {CFL}", "cells": int(cells), "box_cubes": [nx, ny, nz],
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded mesh generators and initial states, workloads.py)",
+            "config": {"workload": wl, "cells": int(cells), **extra,
                        "parallelism": f"domain decomposition x{world} (RCB, 3 ghost layers, NCCL)",
                        "l2": "no flush: per-step working set %.2f GB > 126 MB L2" % (mesh.workspace_size(cfg) / 1e9)},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

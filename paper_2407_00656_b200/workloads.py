@@ -206,16 +206,16 @@ def sphere_shell(n: int, r_in: float = 0.5, r_out: float = 10.0, first_cell: flo
     def nid(r, d):
         return r * ndir + d
 
-    cells = []
+    blocks = []
+    rr = np.arange(nr)[None, None, :]
     for f in range(6):
-        D = dir_id[f]
-        for i in range(n):
-            for j in range(n):
-                d00, d10, d11, d01 = D[i, j], D[i + 1, j], D[i + 1, j + 1], D[i, j + 1]
-                for r in range(nr):
-                    cells.append([nid(r, d00), nid(r, d10), nid(r, d11), nid(r, d01),
-                                  nid(r + 1, d00), nid(r + 1, d10), nid(r + 1, d11), nid(r + 1, d01)])
-    cells = np.array(cells, dtype=np.int64)
+        D = dir_id[f].astype(np.int64)
+        d00, d10 = D[:-1, :-1, None], D[1:, :-1, None]
+        d11, d01 = D[1:, 1:, None], D[:-1, 1:, None]
+        c = np.stack([nid(rr, d00), nid(rr, d10), nid(rr, d11), nid(rr, d01),
+                      nid(rr + 1, d00), nid(rr + 1, d10), nid(rr + 1, d11), nid(rr + 1, d01)], axis=-1)
+        blocks.append(c.reshape(-1, 8))   # order: i, j, r (r fastest)
+    cells = np.concatenate(blocks, 0).astype(np.int64)
     # orient every hex so that bottom face (0,1,2,3) has its right-hand normal
     # pointing into the cell (i.e. outwards radially), as for the unit cube.
     p = xyz[cells]
