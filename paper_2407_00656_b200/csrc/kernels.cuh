@@ -155,6 +155,22 @@ __global__ void __launch_bounds__(kTile, HGKS_RECON_MINB) k_recon(ReconArgs a) {
     const double2 x0 = __ldg(q2), x1 = __ldg(q2 + 1), x2 = __ldg(q2 + 2);
     qi[0] = x0.x; qi[1] = x0.y; qi[2] = x1.x; qi[3] = x1.y; qi[4] = x2.x;
   }
+#ifndef HGKS_NO_L2_PREFETCH
+  // The block's operators are one contiguous E*kTile*8-byte range (tiled layout):
+  // fire TMA bulk prefetches of it into L2 now, so the streamed operator loads
+  // below see L2 rather than DRAM latency (the warps cannot keep enough loads
+  // in flight at 255 registers).
+  if (t < 8) {
+    constexpr uint32_t bytes = (uint32_t)E * kTile * sizeof(double);
+    constexpr uint32_t chunk = ((bytes / 8) + 15) / 16 * 16;
+    const uint32_t off = t * chunk;
+    if (off < bytes) {
+      const uint32_t n = min(chunk, bytes - off);
+      const char* src = reinterpret_cast<const char*>(a.op + tb * E) + off;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(n) : "memory");
+    }
+  }
+#endif
   // gather the stencil members in groups (bounded registers, 7 x 3 loads in flight)
   constexpr int G = 7;
 #pragma unroll
