@@ -286,39 +286,6 @@ __device__ __forceinline__ Prim prim_of(const double q[5], double K) {
   return p;
 }
 
-// spatial slopes a_j (j = n, t1, t2) from derivatives and the temporal slope A
-// from <a_1 u + a_2 v + a_3 w + A> = 0
-__device__ __forceinline__ void slopes_of(const Prim& g, const Mom& full, const double dq[3][5], double K,
-                                          double a[3][5], double A[5]) {
-  const double ir = 1.0 / g.rho;
-#pragma unroll
-  for (int j = 0; j < 3; ++j) {
-    double b[5];
-#pragma unroll
-    for (int v = 0; v < 5; ++v) b[v] = dq[j][v] * ir;
-    micro_slope(b, g.U, g.V, g.W, g.lam, K, a[j]);
-  }
-  double t0[5], t1[5], t2[5], b[5];
-  slope_m<1, 0, 0>(full, a[0], t0);
-  slope_m<0, 1, 0>(full, a[1], t1);
-  slope_m<0, 0, 1>(full, a[2], t2);
-#pragma unroll
-  for (int v = 0; v < 5; ++v) b[v] = -(t0[v] + t1[v] + t2[v]);
-  micro_slope(b, g.U, g.V, g.W, g.lam, K, A);
-}
-
-// the three flux moment vectors of one Maxwellian: <u psi>, <(a.u) u psi>, <A u psi>
-__device__ __forceinline__ void flux_moments(const Mom& m, const double a[3][5], const double A[5], double m1[5],
-                                             double m2[5], double m3[5]) {
-  psi_m<1, 0, 0>(m, m1);
-  double t0[5], t1[5], t2[5];
-  slope_m<2, 0, 0>(m, a[0], t0);
-  slope_m<1, 1, 0>(m, a[1], t1);
-  slope_m<1, 0, 1>(m, a[2], t2);
-#pragma unroll
-  for (int v = 0; v < 5; ++v) m2[v] = t0[v] + t1[v] + t2[v];
-  slope_m<1, 0, 0>(m, A, m3);
-}
 
 // closed-form time integrals of the Eq. (flux) coefficients over [0, delta]
 struct TimeCoef {
@@ -357,37 +324,71 @@ __device__ __forceinline__ void equilibrium_state(const double ql[5], const doub
           0.5 * r.rho * (b2 + b0 * (r.V * r.V + r.W * r.W + (K + 2.0) * hr));
 }
 
-// one side of Eq. (flux) for a Maxwellian (with its slopes) accumulated into I_half, I_full
+// One term group of Eq. (flux) for a Maxwellian with its slopes, accumulated into
+// I_half, I_full (rho-weighted).  Full-range Maxwellian moments of the slope
+// polynomials reduce to Euler-flux Jacobian-vector products (d_j g = a_j g, so
+// rho <u_j a_j psi> = A_j(Q) d_j Q): the compatibility condition
+// for A becomes d_t Q = -sum_j A_j(Q) d_j Q, and for the equilibrium
+// part rho<u psi> = F_n(Q), rho<A u psi> = A_n(Q) d_t Q.  Only <(a.u) u psi>
+// (full range for g0) and the half-range moments of g_l, g_r need the generic
+// moment sums.
 template <int RANGE>
-__device__ __forceinline__ void add_side(const double q[5], const double dq[3][5], double K, const TimeCoef& ch,
-                                         const TimeCoef& cf, bool equilibrium, double Ih[5], double If[5]) {
+__device__ __forceinline__ void add_side(const double q[5], const double dq[3][5], double K, double gm1,
+                                         const TimeCoef& ch, const TimeCoef& cf, double Ih[5], double If[5]) {
   const Prim g = prim_of(q, K);
-  double a[3][5], A[5];
-  {
-    Mom full;
-    maxwell_moments<0>(g.U, g.V, g.W, g.lam, K, full);
-    slopes_of(g, full, dq, K, a, A);
-    if (RANGE == 0) {
-      double m1[5], m2[5], m3[5];
-      flux_moments(full, a, A, m1, m2, m3);
+  const double ir = 1.0 / g.rho;
+  double a[3][5];
 #pragma unroll
-      for (int v = 0; v < 5; ++v) {
-        Ih[v] += g.rho * (ch.c1 * m1[v] + ch.c2 * m2[v] + ch.c3 * m3[v]);
-        If[v] += g.rho * (cf.c1 * m1[v] + cf.c2 * m2[v] + cf.c3 * m3[v]);
-      }
-      return;
+  for (int j = 0; j < 3; ++j) {
+    double b[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) b[v] = dq[j][v] * ir;
+    micro_slope(b, g.U, g.V, g.W, g.lam, K, a[j]);
+  }
+  const EulerState es = euler_state(q, gm1);
+  double dtq[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // d_t Q by compatibility
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    double jv[5];
+    euler_jvp(j, es, dq[j], gm1, jv);
+#pragma unroll
+    for (int v = 0; v < 5; ++v) dtq[v] -= jv[v];
+  }
+  Mom mom;
+  maxwell_moments<RANGE>(g.U, g.V, g.W, g.lam, K, mom);
+  double m2[5];  // <(a.u) u psi> over the range
+  {
+    double t0[5], t1[5], t2[5];
+    slope_m<2, 0, 0>(mom, a[0], t0);
+    slope_m<1, 1, 0>(mom, a[1], t1);
+    slope_m<1, 0, 1>(mom, a[2], t2);
+#pragma unroll
+    for (int v = 0; v < 5; ++v) m2[v] = g.rho * (t0[v] + t1[v] + t2[v]);
+  }
+  if (RANGE == 0) {
+    // rho <u psi> = F_n(Q) and rho <A u psi> = A_n(Q) d_t Q
+    double m3[5];
+    euler_jvp(0, es, dtq, gm1, m3);
+    const double m1[5] = {q[1], q[1] * es.u[0] + es.p, q[2] * es.u[0], q[3] * es.u[0], es.u[0] * es.H};
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      Ih[v] += ch.c1 * m1[v] + ch.c2 * m2[v] + ch.c3 * m3[v];
+      If[v] += cf.c1 * m1[v] + cf.c2 * m2[v] + cf.c3 * m3[v];
+    }
+  } else {
+    double A[5], b[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) b[v] = dtq[v] * ir;
+    micro_slope(b, g.U, g.V, g.W, g.lam, K, A);
+    double m1[5], m3[5];
+    psi_m<1, 0, 0>(mom, m1);
+    slope_m<1, 0, 0>(mom, A, m3);
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      Ih[v] += g.rho * (ch.c4 * m1[v] + ch.c6 * m3[v]) + ch.c5 * m2[v];
+      If[v] += g.rho * (cf.c4 * m1[v] + cf.c6 * m3[v]) + cf.c5 * m2[v];
     }
   }
-  Mom half;
-  maxwell_moments<RANGE>(g.U, g.V, g.W, g.lam, K, half);
-  double m1[5], m2[5], m3[5];
-  flux_moments(half, a, A, m1, m2, m3);
-#pragma unroll
-  for (int v = 0; v < 5; ++v) {
-    Ih[v] += g.rho * (ch.c4 * m1[v] + ch.c5 * m2[v] + ch.c6 * m3[v]);
-    If[v] += g.rho * (cf.c4 * m1[v] + cf.c5 * m2[v] + cf.c6 * m3[v]);
-  }
-  (void)equilibrium;
 }
 
 // boundary right states in the local frame (R25)
@@ -581,9 +582,9 @@ __global__ void __launch_bounds__(NV == 3 ? 96 : 128, TAU0 ? (NV == 3 ? 5 : 4) :
       for (int j = 0; j < 3; ++j)
 #pragma unroll
         for (int v = 0; v < 5; ++v) dq0[j][v] = 0.5 * (dql[j][v] + dqr[j][v]);
-      add_side<0>(Q0, dq0, K, ch, cf, true, Ih, If);
-      add_side<1>(ql, dql, K, ch, cf, false, Ih, If);
-      add_side<2>(qr, dqr, K, ch, cf, false, Ih, If);
+      add_side<0>(Q0, dq0, K, gm1, ch, cf, Ih, If);
+      add_side<1>(ql, dql, K, gm1, ch, cf, Ih, If);
+      add_side<2>(qr, dqr, K, gm1, ch, cf, Ih, If);
       // 2x2 fit
 #pragma unroll
       for (int v = 0; v < 5; ++v) {
