@@ -109,12 +109,13 @@ class ClockSampler:
 
 
 # algorithmic bytes / flops per unit, tets
-def recon_bytes_per_cell(K=14, M=4, NM=6):
-    op = (9 * K + M * 3 * NM) * 8      # LSQ operators
+def recon_bytes_per_cell(K=14, M=4, NM=6, rs=8):
+    """rs: bytes of the working precision (8 fp64, 4 for the FP32 variant)."""
+    op = (9 * K + M * 3 * NM) * rs     # LSQ operators
     idx = K * 4 + M * NM * 1 + 4       # stencil ids, sub-stencil slots, recon cell id
-    geo = 8 * 8                        # V^{2/3}, V^{4/3}, M2
-    q = 5 * 8                          # the cell's own state (neighbours: each state read once overall)
-    rec = 50 * 8                       # effective-polynomial record written
+    geo = 8 * rs                       # V^{2/3}, V^{4/3}, M2
+    q = 5 * rs                         # the cell's own state (neighbours: each state read once overall)
+    rec = 50 * rs                      # effective-polynomial record written
     return op + idx + geo + q + rec
 
 
@@ -169,6 +170,8 @@ def main():
     ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4"],
                     help="c2: 48^3 Kuhn box per GPU (default, BASELINE configs[1]); c3: subsonic sphere "
                          "12x35^3 hexes (configs[2]); c4: supersonic sphere 12x70^3 hexes (configs[3])")
+    ap.add_argument("--precision", type=int, default=64, choices=[64, 32],
+                    help="64: the fp64 path BASELINE's metric names (default); 32: the FP32 variant (P:1098-1183)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -191,7 +194,7 @@ def main():
         nx, ny, nz = box_dims(world)
         mi = W.kuhn_box(nx, ny, nz, h=2.0 / N_BLOCK)
         Q0 = W.advection_ic(mi, gamma=GAMMA)
-        cfg = hgks.SolverConfig(gamma=GAMMA, cfl=CFL)
+        cfg = hgks.SolverConfig(gamma=GAMMA, cfl=CFL, precision=args.precision)
         wl = (f"configs[1] top size: {N_BLOCK}^3 Kuhn box per GPU, 6 tets/cube, periodic, tau=0, CFL {CFL}")
         scaling, layout = "weak", (14, 4, 6)
         extra = {"box_cubes": [nx, ny, nz]}
@@ -201,7 +204,7 @@ def main():
         fs = (1.0, ma, 0.0, 0.0, 1.0 / GAMMA)
         Q0 = W.uniform_state(mi.n_cells, 1.0, (ma, 0.0, 0.0), 1.0 / GAMMA, gamma=GAMMA)  # free-stream IC
         cfg = hgks.SolverConfig(gamma=GAMMA, cfl=0.5, tau_mode=1, mu_inf=ma / re, c1=1.0, t_inf=1.0 / GAMMA,
-                                freestream=fs)
+                                freestream=fs, precision=args.precision)
         wl = (f"configs[{2 if args.workload == 'c3' else 3}]: sphere shell 12x{n}^3 hexes, Ma {ma}, Re {re}, "
               f"NS collision time, wall + farfield, CFL 0.5, free-stream start")
         scaling, layout = "strong", (24, 8, 3)
@@ -287,7 +290,7 @@ def main():
     if name.startswith("k_recon"):
         # recon runs over owned cells and layer-1 ghosts
         n_recon = info["n_owned"] + info["ghost_layer"][0]
-        bytes_per_launch = recon_bytes_per_cell(*layout) * n_recon
+        bytes_per_launch = recon_bytes_per_cell(*layout, rs=args.precision // 8) * n_recon
         achieved = bytes_per_launch / (avg_ms * 1e-3) / 1e9
         roof = {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": None,
@@ -295,7 +298,7 @@ def main():
                 "peak_source": hbm_src + " (burst copy)"}
     else:
         flops = json.load(open(os.path.join(ROOT, "profiles", "flops_per_unit.json")))
-        fpf = flops.get(args.workload, {}).get(name, {}).get("fp64_flops_per_face")
+        fpf = flops.get(args.workload, {}).get(name, {}).get("fp64_flops_per_face") if args.precision == 64 else None
         nf = info["n_faces"] - info["n_faces_bc"]  # interior faces (the counts are per interior face)
         if fpf:
             achieved = fpf * nf / (avg_ms * 1e-3) / 1e12
@@ -305,13 +308,14 @@ def main():
                                                           "profiles/flops_per_unit.json", "peak_source": fp64_src}
     traffic_path = os.path.join(ROOT, "profiles", "traffic.json")
     if roof and os.path.exists(traffic_path):
-        tr = json.load(open(traffic_path)).get(roof["kernel"]) if args.workload == "c2" else None
+        tr = (json.load(open(traffic_path)).get(roof["kernel"])
+              if args.workload == "c2" and args.precision == 64 else None)
         if tr and roof["kernel"].startswith("k_recon"):
             roof["traffic"] = tr["dram_bytes_per_launch"] * (n_recon / tr["cells"] if "cells" in tr else 1.0)
 
     # ---------------- CPU baseline (oracle, rank 0, bounded sample) ----------------
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload == "c2":
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload == "c2" and args.precision == 64:
         threads = len(os.sched_getaffinity(0))
         rate, secs, ncell = cpu_oracle_rate(N_BLOCK, 1, threads)
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
@@ -323,7 +327,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "ms_per_step_unprofiled": ms_unprof / args.steps,
-            "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64" if args.precision == 64 else "f32",
             "data": "synthetic (seeded mesh generators and initial states, workloads.py)",
             "config": {"workload": wl, "cells": int(cells), **extra,
                        "parallelism": f"domain decomposition x{world} (RCB, 3 ghost layers, NCCL)",

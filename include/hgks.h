@@ -81,6 +81,9 @@ typedef struct {
   double eps;          /* WENO epsilon */
   int32_t omega_pow;   /* 1 (as printed) or 2 */
   double freestream[5];/* rho, U, V, W, p for farfield faces */
+  int32_t precision;   /* working precision of the hot path: 64 (fp64, the parity path) or 32
+                          (the FP32 variant; the CFL bound, time and the caller's
+                          state arrays stay fp64).  Anything else: HGKS_E_ARG from hgks_init. */
 } hgks_config;
 
 #define HGKS_TRANSPORT_NCCL 0      /* one process per GPU, NCCL send/recv + allreduce */

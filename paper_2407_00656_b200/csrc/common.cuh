@@ -1,0 +1,98 @@
+// Precision-independent device code of libhgks: the step control block, the
+// CFL bound and its exact min (fp64 in both precisions), the time bookkeeping.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hgks {
+
+constexpr int QS = 6;      // values per cell row of Q (5 conserved + 1 pad for 16-byte pairs)
+constexpr int kRec = 50;   // values per effective-polynomial record (10 coefficients x 5 variables)
+constexpr int kTile = 128; // reconstructed cells per k_recon block (tiled arrays, setup.cpp)
+
+struct Ctrl {
+  double t;          // time at the start of the current step
+  double dt;         // step size of the current step
+  double t_next;     // time after the current step
+  unsigned long long dtmin_bits;  // min over cells of h/(|U|+c+2nu/h), as ordered bits
+  long long steps;   // steps with dt > 0
+  long long fallbacks;
+  int bad_cell;      // first cell with non-positive rho/p (INT_MAX if none)
+  int pad;
+};
+
+struct GasParams {
+  double gamma, K, cfl, fixed_dt, eps, omega_pow;
+  int tau_mode;
+  double c1, mu_inf, t_inf, mu_exp;
+  double fs[5];
+};
+
+
+__device__ __forceinline__ double cell_dt_bound(const double q[5], double h, const GasParams& gp) {
+  const double rho = q[0];
+  const double u = q[1] / rho, v = q[2] / rho, w = q[3] / rho;
+  const double p = (gp.gamma - 1.0) * (q[4] - 0.5 * rho * (u * u + v * v + w * w));
+  const double c = sqrt(gp.gamma * p / rho);
+  double nu = 0.0;
+  if (gp.tau_mode == 1) nu = gp.mu_inf * pow((p / rho) / gp.t_inf, gp.mu_exp) / rho;
+  return h / (sqrt(u * u + v * v + w * w) + c + 2.0 * nu / h);
+}
+
+__device__ __forceinline__ void block_min_dt(double local, Ctrl* ctrl) {
+  // warp shuffle min, then one atomic per warp on the ordered bits of a positive double
+  unsigned long long bits = __double_as_longlong(local);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long ob = __shfl_xor_sync(0xffffffffu, bits, o);
+    bits = ob < bits ? ob : bits;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMin(&ctrl->dtmin_bits, bits);
+}
+
+
+// one thread: advance the time bookkeeping and choose this step's dt
+__global__ void k_step_begin(Ctrl* ctrl, double cfl, double fixed_dt, double t_stop) {
+  double t = ctrl->t_next;
+  double raw = fixed_dt > 0.0 ? fixed_dt : cfl * __longlong_as_double((long long)ctrl->dtmin_bits);
+  double dt = raw, tn = t + raw;
+  if (t_stop > 0.0) {
+    if (t >= t_stop) {
+      dt = 0.0;
+      tn = t;
+    } else if (t + raw > t_stop) {
+      dt = t_stop - t;
+      tn = t_stop;
+    }
+  }
+  ctrl->t = t;
+  ctrl->dt = dt;
+  ctrl->t_next = tn;
+  if (dt > 0.0) ctrl->steps += 1;
+  ctrl->dtmin_bits = 0x7fefffffffffffffull;  // +max finite, reset for this step's accumulation
+}
+
+// loopback transport: exact min of the CFL bound over the ranks of one process
+constexpr int kMaxGroup = 16;
+struct GroupCtrl {
+  int n;
+  Ctrl* c[kMaxGroup];
+};
+__global__ void k_group_min(GroupCtrl g) {
+  if (threadIdx.x != 0) return;
+  unsigned long long m = g.c[0]->dtmin_bits;
+  for (int k = 1; k < g.n; ++k) m = g.c[k]->dtmin_bits < m ? g.c[k]->dtmin_bits : m;
+  for (int k = 0; k < g.n; ++k) g.c[k]->dtmin_bits = m;
+}
+
+// reset the time bookkeeping on the device (no host round trip)
+__global__ void k_reset_ctrl(Ctrl* ctrl, double t) {
+  ctrl->t = t;
+  ctrl->t_next = t;
+  ctrl->dt = 0.0;
+  ctrl->bad_cell = 0x7fffffff;
+  ctrl->dtmin_bits = 0x7fefffffffffffffull;
+}
+
+
+}  // namespace hgks

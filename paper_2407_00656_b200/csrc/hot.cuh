@@ -1,0 +1,1134 @@
+// Hot path of libhgks, written once for a working
+// precision `Real` (double, or float for the FP32 variant of P:1098-1183).
+// kernels.cuh includes this file twice, in namespaces hgks::p64 (Real = double,
+// R2 = double2) and hgks::p32 (Real = float, R2 = float2); the time-step
+// bookkeeping (Ctrl, the CFL bound and its min) stays fp64 in common.cuh.
+//
+//   k_bc_ghosts   a6  boundary-condition ghost states (wall mirror / farfield)
+//   k_recon       a7  WENO reconstruction: LSQ apply, beta, weights, collapse
+//                     to ONE effective quadratic per cell (50 values)
+//   k_flux        a8+a9 per Gauss point: both polynomials, local frame, BGK flux
+//                     of Eq. (flux) (tau = 0 Euler-chain form or moment form),
+//                     time fit, face quadrature sum
+//   k_update1/2   a10 L, d_t L assembly in local-face order + S2O4 stages;
+//                     stage 2 fuses the per-cell CFL bound and its min (a4)
+// (no include guard: included once per precision)
+
+__device__ __forceinline__ R2 make_R2(Real x, Real y) {
+  R2 r;
+  r.x = x;
+  r.y = y;
+  return r;
+}
+
+// gas constants in the working precision
+struct GasR {
+  Real gamma, K, c1, mu_inf, t_inf, mu_exp, fs[5];
+};
+inline GasR make_gas(const GasParams& g) {
+  GasR r;
+  r.gamma = (Real)g.gamma;
+  r.K = (Real)g.K;
+  r.c1 = (Real)g.c1;
+  r.mu_inf = (Real)g.mu_inf;
+  r.t_inf = (Real)g.t_inf;
+  r.mu_exp = (Real)g.mu_exp;
+  for (int k = 0; k < 5; ++k) r.fs[k] = (Real)g.fs[k];
+  return r;
+}
+
+// ----------------------------------------------------------------------------
+// a6: boundary ghost states (R25).  Wall: velocity reversed.  Farfield: 1-D
+// Riemann invariants along the face normal.
+// ----------------------------------------------------------------------------
+__device__ inline void farfield_riemann(const Real qi[5], const Real n[3], const GasR& gp, Real qb[5]) {
+  const Real g = gp.gamma;
+  Real rho_i = qi[0];
+  Real ui[3] = {qi[1] / rho_i, qi[2] / rho_i, qi[3] / rho_i};
+  Real p_i = (g - Real(1.0)) * (qi[4] - Real(0.5) * (qi[1] * ui[0] + qi[2] * ui[1] + qi[3] * ui[2]));
+  Real c_i = sqrt(g * p_i / rho_i);
+  Real rho_f = gp.fs[0], p_f = gp.fs[4];
+  Real uf[3] = {gp.fs[1], gp.fs[2], gp.fs[3]};
+  Real c_f = sqrt(g * p_f / rho_f);
+  Real un_i = ui[0] * n[0] + ui[1] * n[1] + ui[2] * n[2];
+  Real un_f = uf[0] * n[0] + uf[1] * n[1] + uf[2] * n[2];
+  Real Rp = un_i + Real(2.0) * c_i / (g - Real(1.0)), Rm = un_f - Real(2.0) * c_f / (g - Real(1.0));
+  if (un_f + c_f < Real(0.0)) Rp = un_f + Real(2.0) * c_f / (g - Real(1.0));
+  if (un_i - c_i > Real(0.0)) Rm = un_i - Real(2.0) * c_i / (g - Real(1.0));
+  Real un = Real(0.5) * (Rp + Rm), c = Real(0.25) * (g - Real(1.0)) * (Rp - Rm);
+  Real ut[3], s;
+  if (un > Real(0.0)) {
+    for (int a = 0; a < 3; ++a) ut[a] = ui[a] - un_i * n[a];
+    s = p_i / pow(rho_i, g);
+  } else {
+    for (int a = 0; a < 3; ++a) ut[a] = uf[a] - un_f * n[a];
+    s = p_f / pow(rho_f, g);
+  }
+  Real rho = pow(c * c / (g * s), Real(1.0) / (g - Real(1.0)));
+  Real p = rho * c * c / g;
+  Real u[3] = {ut[0] + un * n[0], ut[1] + un * n[1], ut[2] + un * n[2]};
+  qb[0] = rho;
+  qb[1] = rho * u[0];
+  qb[2] = rho * u[1];
+  qb[3] = rho * u[2];
+  qb[4] = p / (g - Real(1.0)) + Real(0.5) * rho * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+}
+
+// Conserved state of a cell: one 48-byte row (rho, rhoU, rhoV, rhoW, rhoE, pad),
+// so a stencil gather is 3 aligned 16-byte loads and a ghost range is one
+// contiguous block (single message per peer in the halo exchange).
+
+// part 0: ghosts of owned cells (before the halo exchange completes), 1: ghosts
+// of partition-ghost cells (after it), 2: all
+__global__ void k_bc_ghosts(Real* __restrict__ Q, int first, int n, const int* __restrict__ bg_cell,
+                            const int* __restrict__ bg_bc, const Real* __restrict__ bg_normal, GasR gp,
+                            int n_owned, int part) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  if (part != 2 && (bg_cell[k] < n_owned) != (part == 0)) return;
+  const Real* qc = Q + (size_t)bg_cell[k] * QS;
+  Real qi[5];
+#pragma unroll
+  for (int v = 0; v < 5; ++v) qi[v] = qc[v];
+  Real qb[5];
+  if (bg_bc[k] == 1) {
+    qb[0] = qi[0]; qb[1] = -qi[1]; qb[2] = -qi[2]; qb[3] = -qi[3]; qb[4] = qi[4];
+  } else {
+    Real n3[3] = {bg_normal[3 * k], bg_normal[3 * k + 1], bg_normal[3 * k + 2]};
+    farfield_riemann(qi, n3, gp, qb);
+  }
+  Real* qg = Q + (size_t)(first + k) * QS;
+#pragma unroll
+  for (int v = 0; v < 5; ++v) qg[v] = qb[v];
+}
+
+// ----------------------------------------------------------------------------
+// a7: WENO reconstruction, one thread per reconstructed cell, 128-cell blocks.
+// Output record per local cell (50 doubles), variable-major: for v = 0..4,
+// rec[10 v + (const, x, y, z, xx, yy, zz, xy, xz, yz)] so that at X = x - c_i
+//   Q_v(x) = const + lin . X + quad . (X_a X_b)       (Eq. weno collapsed)
+// ----------------------------------------------------------------------------
+
+struct ReconArgs {
+  const Real* __restrict__ Q;         // [n_local][QS]
+  int n_recon;
+  int tile0;                            // first 128-cell tile of this launch
+  int ld;                               // n_recon padded to kTile (tiled entry-major arrays, setup.cpp)
+  const int* __restrict__ recon_cell;   // [n_recon] local cell id
+  const int* __restrict__ st_id;        // [K] per cell, tiled: stencil member local ids
+  const uint8_t* __restrict__ sub_slot; // [M*NM] per cell, tiled: sub-stencil member -> big-stencil slot
+  const Real* __restrict__ op;        // [E] per cell, tiled: LSQ operators in streaming order
+  const Real* __restrict__ geo;       // [8] per cell, tiled: V^{2/3}, V^{4/3}, M2 (xx,yy,zz,xy,xz,yz)
+  Real* __restrict__ ceff;            // [n_local][50]
+  Real eps;
+  int omega_pow;
+};
+
+// One thread per reconstructed cell (block of kTile cells).  All stencil
+// indices are loaded first and all member states are gathered at once into
+// this thread's shared-memory slots (3 x 16-byte loads per member, ~40 loads in
+// flight per thread), so the gathers cost one memory latency per cell; the
+// sub-stencils re-read them from shared memory.  The LSQ operators (1584 B per
+// tet cell, most of the kernel's HBM bytes) stream entry-major: each warp load
+// is 256 contiguous bytes.
+template <int K, int M, int NM>
+#ifndef HGKS_RECON_MINB
+#define HGKS_RECON_MINB 2
+#endif
+__global__ void __launch_bounds__(kTile, HGKS_RECON_MINB) k_recon(ReconArgs a) {
+  constexpr int QP = 5 * kTile;                      // doubles per member plane: [v][thread]
+  constexpr int E = 9 * K + 3 * M * NM;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Real* smem = reinterpret_cast<Real*>(smem_raw);
+  Real* __restrict__ dqs = smem;                   // [K][5][kTile] Q_k - Q_i
+  const int t = threadIdx.x;
+  const int tile = a.tile0 + blockIdx.x;
+  const int r = tile * kTile + t;
+  int ci = r < a.n_recon ? __ldg(a.recon_cell + r) : -1;  // -1: padding
+  const bool active = ci >= 0;
+  if (!active) ci = 0;
+  // tiled entry-major per-cell arrays (setup.cpp): entry e of this cell at (tile*NE + e)*kTile + t
+  const size_t tb = (size_t)tile * kTile;
+  const int* __restrict__ sid = a.st_id + tb * K + t;
+  Real qi[5];
+  {
+    const R2* q2 = reinterpret_cast<const R2*>(a.Q + (size_t)ci * QS);
+    const R2 x0 = __ldg(q2), x1 = __ldg(q2 + 1), x2 = __ldg(q2 + 2);
+    qi[0] = x0.x; qi[1] = x0.y; qi[2] = x1.x; qi[3] = x1.y; qi[4] = x2.x;
+  }
+#ifndef HGKS_NO_L2_PREFETCH
+  // The block's operators are one contiguous E*kTile*8-byte range (tiled layout):
+  // fire TMA bulk prefetches of it into L2 now, so the streamed operator loads
+  // below see L2 rather than DRAM latency (the warps cannot keep enough loads
+  // in flight at 255 registers).
+  if (t < 8) {
+    constexpr uint32_t bytes = (uint32_t)E * kTile * sizeof(Real);
+    constexpr uint32_t chunk = ((bytes / 8) + 15) / 16 * 16;
+    const uint32_t off = t * chunk;
+    if (off < bytes) {
+      const uint32_t n = min(chunk, bytes - off);
+      const char* src = reinterpret_cast<const char*>(a.op + tb * E) + off;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(n) : "memory");
+    }
+  }
+#endif
+  // gather the stencil members in groups (bounded registers, 7 x 3 loads in flight)
+  constexpr int G = 7;
+#pragma unroll
+  for (int k0 = 0; k0 < K; k0 += G) {
+    R2 x[G][3];
+#pragma unroll
+    for (int k = k0; k < k0 + G && k < K; ++k) {
+      const R2* q2 = reinterpret_cast<const R2*>(a.Q + (size_t)__ldg(sid + k * kTile) * QS);
+      x[k - k0][0] = __ldg(q2);
+      x[k - k0][1] = __ldg(q2 + 1);
+      x[k - k0][2] = __ldg(q2 + 2);
+    }
+#pragma unroll
+    for (int k = k0; k < k0 + G && k < K; ++k) {
+      Real* d = dqs + k * QP + t;
+      d[0 * kTile] = x[k - k0][0].x - qi[0];
+      d[1 * kTile] = x[k - k0][0].y - qi[1];
+      d[2 * kTile] = x[k - k0][1].x - qi[2];
+      d[3 * kTile] = x[k - k0][1].y - qi[3];
+      d[4 * kTile] = x[k - k0][2].x - qi[4];
+    }
+  }
+  const Real* __restrict__ op = a.op + tb * E + t;
+  const Real* __restrict__ geo = a.geo + tb * 8 + t;
+  const uint8_t* __restrict__ ssl = a.sub_slot + tb * (M * NM) + t;
+  const Real V23 = __ldg(geo), V43 = __ldg(geo + kTile);
+  Real m2[6];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) m2[q] = __ldg(geo + (2 + q) * kTile);
+  // ---- P_0: c[d][v] = sum_k A0+[d][k] (Q_k - Q_i)[v] ----
+  Real c[9][5];
+#pragma unroll
+  for (int d = 0; d < 9; ++d)
+#pragma unroll
+    for (int v = 0; v < 5; ++v) c[d][v] = Real(0.0);
+#pragma unroll 2
+  for (int k = 0; k < K; ++k) {
+    Real dq[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) dq[v] = dqs[k * QP + v * kTile + t];
+#pragma unroll
+    for (int d = 0; d < 9; ++d) {
+      const Real w = __ldcs(op + (k * 9 + d) * kTile);
+#pragma unroll
+      for (int v = 0; v < 5; ++v) c[d][v] = fma(w, dq[v], c[d][v]);
+    }
+  }
+  // smoothness indicator of P_0 (closed form SURVEY A.5)
+  Real beta0[5];
+#pragma unroll
+  for (int v = 0; v < 5; ++v) {
+    const Real gx[3] = {Real(2.0) * c[3][v], c[6][v], c[7][v]}, gy[3] = {c[6][v], Real(2.0) * c[4][v], c[8][v]},
+                 gz[3] = {c[7][v], c[8][v], Real(2.0) * c[5][v]};
+    auto quadf = [&](const Real g[3]) {
+      return m2[0] * g[0] * g[0] + m2[1] * g[1] * g[1] + m2[2] * g[2] * g[2] +
+             Real(2.0) * (m2[3] * g[0] * g[1] + m2[4] * g[0] * g[2] + m2[5] * g[1] * g[2]);
+    };
+    const Real s1 = c[0][v] * c[0][v] + c[1][v] * c[1][v] + c[2][v] * c[2][v] + quadf(gx) + quadf(gy) + quadf(gz);
+    const Real s2 = Real(4.0) * (c[3][v] * c[3][v] + c[4][v] * c[4][v] + c[5][v] * c[5][v]) + c[6][v] * c[6][v] +
+                      c[7][v] * c[7][v] + c[8][v] * c[8][v];
+    beta0[v] = V23 * s1 + V43 * s2;
+  }
+  const Real* __restrict__ opm = op + (9 * K) * kTile;
+  auto sub_slopes = [&](int m, Real b[3][5]) {  // P_m over sub-stencil m
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int v = 0; v < 5; ++v) b[d][v] = Real(0.0);
+#pragma unroll
+    for (int j = 0; j < NM; ++j) {
+      const int sl = __ldg(ssl + (m * NM + j) * kTile);
+      Real dq[5];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) dq[v] = dqs[sl * QP + v * kTile + t];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const Real w = __ldg(opm + ((m * NM + j) * 3 + d) * kTile);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) b[d][v] = fma(w, dq[v], b[d][v]);
+      }
+    }
+  };
+  // ---- pass 1: beta_m and the nonlinear weights ----
+  const Real gm = Real(0.025), g0 = Real(1.0) - Real(0.025) * M;
+  Real al0[5], alm[M][5];
+  {
+    Real tz[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      Real b[3][5];
+      sub_slopes(m, b);
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        alm[m][v] = V23 * (b[0][v] * b[0][v] + b[1][v] * b[1][v] + b[2][v] * b[2][v]);  // beta_m
+        tz[v] += fabs(beta0[v] - alm[m][v]);
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      const Real tzv = tz[v] * (Real(1.0) / M);
+      const Real r0 = tzv / (beta0[v] + a.eps);
+      const Real w0 = g0 * (Real(1.0) + (a.omega_pow == 2 ? r0 * r0 : r0));
+      Real sum = w0;
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        const Real rm = tzv / (alm[m][v] + a.eps);
+        alm[m][v] = gm * (Real(1.0) + (a.omega_pow == 2 ? rm * rm : rm));  // omega_m
+        sum += alm[m][v];
+      }
+      const Real inv = Real(1.0) / sum;
+      al0[v] = w0 * inv / g0;  // omega-bar_0 / gamma_0
+#pragma unroll
+      for (int m = 0; m < M; ++m) alm[m][v] = alm[m][v] * inv - al0[v] * gm;  // omega-bar_m - omega-bar_0 gamma_m/gamma_0
+    }
+  }
+  // ---- collapse to one quadratic ----
+  Real lin[3][5];
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+#pragma unroll
+    for (int v = 0; v < 5; ++v) lin[d][v] = al0[v] * c[d][v];
+#pragma unroll
+  for (int m = 0; m < M; ++m) {  // pass 2: weighted sum of the sub-stencil slopes
+    Real b[3][5];
+    sub_slopes(m, b);
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int v = 0; v < 5; ++v) lin[d][v] = fma(alm[m][v], b[d][v], lin[d][v]);
+  }
+  if (!active) return;
+  R2* dst = reinterpret_cast<R2*>(a.ceff + (size_t)ci * kRec);
+#pragma unroll
+  for (int v = 0; v < 5; ++v) {
+    Real quad[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) quad[q] = al0[v] * c[3 + q][v];
+    // zero-mean basis: p_ab = X_a X_b - M2_ab
+    const Real cst = qi[v] - (quad[0] * m2[0] + quad[1] * m2[1] + quad[2] * m2[2] + quad[3] * m2[3] +
+                                quad[4] * m2[4] + quad[5] * m2[5]);
+    dst[5 * v + 0] = make_R2(cst, lin[0][v]);
+    dst[5 * v + 1] = make_R2(lin[1][v], lin[2][v]);
+    dst[5 * v + 2] = make_R2(quad[0], quad[1]);
+    dst[5 * v + 3] = make_R2(quad[2], quad[3]);
+    dst[5 * v + 4] = make_R2(quad[4], quad[5]);
+  }
+}
+
+
+// a8 + a9: per Gauss point, evaluate both effective polynomials, rotate into
+// the local frame, compute the BGK interface flux of Eq. (flux)
+// and its time fit, rotate back and sum the face
+// quadrature in Gauss-point order.  One thread per Gauss point;
+// the per-face reduction goes through shared memory (deterministic, no atomics).
+//
+//   TAU0 = true : tau = 0, f = g0 (1 + A t) evaluated through the
+//                 Euler-chain identity -- exact, ~1/3 the flops
+//   TAU0 = false: full moment form with closed-form time integrals
+//   BC = 0 interior, 1 no-slip wall (mirror), 2 farfield (Riemann) (R25)
+struct FluxArgs {
+  const Real* __restrict__ Q;  // [n_local][QS]
+  const Real* __restrict__ ceff;
+  const int* __restrict__ f_cells;  // [n][2]
+  const Real* __restrict__ f_geo; // [n][stride]
+  int f_stride;
+  int n_faces;                      // faces in this launch
+  int face0;                        // first face index
+  Real* __restrict__ F1;          // stage 1: [n_faces][10] (F*S, dF*S)
+  Real* __restrict__ F2;          // stage 2: [n_faces][5]  (dF*S)
+  Ctrl* ctrl;
+  GasR gp;
+};
+
+// evaluate the effective polynomial of a cell at X (relative to its centroid)
+// evaluate the effective polynomial of a cell at X (relative to its centroid);
+// record layout rec[10 v + (const, x, y, z, xx, yy, zz, xy, xz, yz)], read as
+// 16-byte vectors (80 bytes per variable)
+__device__ __forceinline__ void eval_poly(const Real* __restrict__ rec, const Real X[3], Real val[5],
+                                          Real grad[5][3]) {
+  const Real xx = X[0] * X[0], yy = X[1] * X[1], zz = X[2] * X[2];
+  const Real xy = X[0] * X[1], xz = X[0] * X[2], yz = X[1] * X[2];
+  const R2* r2 = reinterpret_cast<const R2*>(rec);
+#pragma unroll
+  for (int v = 0; v < 5; ++v) {
+    const R2 a0 = __ldg(r2 + 5 * v), a1 = __ldg(r2 + 5 * v + 1), a2 = __ldg(r2 + 5 * v + 2),
+                  a3 = __ldg(r2 + 5 * v + 3), a4 = __ldg(r2 + 5 * v + 4);
+    const Real c0 = a0.x, lx = a0.y, ly = a1.x, lz = a1.y, qxx = a2.x, qyy = a2.y, qzz = a3.x, qxy = a3.y,
+                 qxz = a4.x, qyz = a4.y;
+    val[v] = c0 + lx * X[0] + ly * X[1] + lz * X[2] + qxx * xx + qyy * yy + qzz * zz + qxy * xy + qxz * xz + qyz * yz;
+    grad[v][0] = lx + Real(2.0) * qxx * X[0] + qxy * X[1] + qxz * X[2];
+    grad[v][1] = ly + Real(2.0) * qyy * X[1] + qxy * X[0] + qyz * X[2];
+    grad[v][2] = lz + Real(2.0) * qzz * X[2] + qxz * X[0] + qyz * X[1];
+  }
+}
+
+// Gauss point g of a face from its vertices (relative to the owner centroid), R10
+template <int NV>
+__device__ __forceinline__ void face_gp(const Real* __restrict__ fg, int g, Real x[3], Real n[3], Real& wS) {
+  if (NV == 3) {
+    Real p[3][3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) p[q][a] = __ldg(fg + 3 * q + a);
+    const Real e1[3] = {p[1][0] - p[0][0], p[1][1] - p[0][1], p[1][2] - p[0][2]};
+    const Real e2[3] = {p[2][0] - p[0][0], p[2][1] - p[0][1], p[2][2] - p[0][2]};
+    Real nn[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
+    const Real a2 = sqrt(nn[0] * nn[0] + nn[1] * nn[1] + nn[2] * nn[2]);
+    const Real l0 = g == 0 ? Real(2.0) / Real(3.0) : Real(1.0) / Real(6.0), l1 = g == 1 ? Real(2.0) / Real(3.0) : Real(1.0) / Real(6.0),
+                 l2 = g == 2 ? Real(2.0) / Real(3.0) : Real(1.0) / Real(6.0);
+    const Real ia = Real(1.0) / a2;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      x[a] = l0 * p[0][a] + l1 * p[1][a] + l2 * p[2][a];
+      n[a] = nn[a] * ia;
+    }
+    wS = a2 * (Real(1.0) / Real(6.0));
+  } else {
+    Real p[4][3];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) p[q][a] = __ldg(fg + 3 * q + a);
+    const Real h = Real(0.28867513459481287);  // 1/(2 sqrt 3)
+    const Real s = (g & 1) ? Real(0.5) + h : Real(0.5) - h, t = (g >> 1) ? Real(0.5) + h : Real(0.5) - h;
+    Real ds[3], dt[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      x[a] = (1 - s) * (1 - t) * p[0][a] + s * (1 - t) * p[1][a] + s * t * p[2][a] + (1 - s) * t * p[3][a];
+      ds[a] = (1 - t) * (p[1][a] - p[0][a]) + t * (p[2][a] - p[3][a]);
+      dt[a] = (1 - s) * (p[3][a] - p[0][a]) + s * (p[2][a] - p[1][a]);
+    }
+    Real nn[3] = {ds[1] * dt[2] - ds[2] * dt[1], ds[2] * dt[0] - ds[0] * dt[2], ds[0] * dt[1] - ds[1] * dt[0]};
+    const Real an = sqrt(nn[0] * nn[0] + nn[1] * nn[1] + nn[2] * nn[2]);
+    const Real ia = Real(1.0) / an;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) n[a] = nn[a] * ia;
+    wS = Real(0.25) * an;
+  }
+}
+
+// local frame (R11): t1 = normalize(n x e*), e* the axis with the smallest |n.e|
+__device__ __forceinline__ void frame(const Real n[3], Real t1[3], Real t2[3]) {
+  int k = 0;
+  if (fabs(n[1]) < fabs(n[k])) k = 1;
+  if (fabs(n[2]) < fabs(n[k])) k = 2;
+  Real e[3] = {Real(0.0), Real(0.0), Real(0.0)};
+  e[k] = Real(1.0);
+  Real c[3] = {n[1] * e[2] - n[2] * e[1], n[2] * e[0] - n[0] * e[2], n[0] * e[1] - n[1] * e[0]};
+  Real inv = Real(1.0) / sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) t1[a] = c[a] * inv;
+  t2[0] = n[1] * t1[2] - n[2] * t1[1];
+  t2[1] = n[2] * t1[0] - n[0] * t1[2];
+  t2[2] = n[0] * t1[1] - n[1] * t1[0];
+}
+
+// rotate value + gradient (global) into the local frame: q[5], dq[3][5] (derivative along n, t1, t2)
+__device__ __forceinline__ void to_local(const Real val[5], const Real grad[5][3], const Real n[3],
+                                         const Real t1[3], const Real t2[3], Real q[5], Real dq[3][5]) {
+  q[0] = val[0];
+  q[4] = val[4];
+  q[1] = val[1] * n[0] + val[2] * n[1] + val[3] * n[2];
+  q[2] = val[1] * t1[0] + val[2] * t1[1] + val[3] * t1[2];
+  q[3] = val[1] * t2[0] + val[2] * t2[1] + val[3] * t2[2];
+  // frame matrix rows (n, t1, t2), indexed with compile-time j only (stays in registers)
+  const Real Rm[3][3] = {{n[0], n[1], n[2]}, {t1[0], t1[1], t1[2]}, {t2[0], t2[1], t2[2]}};
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const Real* e = Rm[j];
+    Real d[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) d[v] = grad[v][0] * e[0] + grad[v][1] * e[1] + grad[v][2] * e[2];
+    dq[j][0] = d[0];
+    dq[j][4] = d[4];
+    dq[j][1] = d[1] * n[0] + d[2] * n[1] + d[3] * n[2];
+    dq[j][2] = d[1] * t1[0] + d[2] * t1[1] + d[3] * t1[2];
+    dq[j][3] = d[1] * t2[0] + d[2] * t2[1] + d[3] * t2[2];
+  }
+}
+
+// Euler-flux Jacobian-vector product along local axis j: dF_j = (dF_j/dQ) dq
+// Euler state quantities shared by the Jacobian-vector products below
+struct EulerState {
+  Real Q[5], inv, u[3], p, H, q2h;  // H = rhoE + p, q2h = |u|^2 / 2
+};
+__device__ __forceinline__ EulerState euler_state(const Real Q[5], Real gm1) {
+  EulerState e;
+#pragma unroll
+  for (int v = 0; v < 5; ++v) e.Q[v] = Q[v];
+  e.inv = Real(1.0) / Q[0];
+  e.u[0] = Q[1] * e.inv;
+  e.u[1] = Q[2] * e.inv;
+  e.u[2] = Q[3] * e.inv;
+  e.q2h = Real(0.5) * (e.u[0] * e.u[0] + e.u[1] * e.u[1] + e.u[2] * e.u[2]);
+  e.p = gm1 * (Q[4] - Q[0] * e.q2h);
+  e.H = Q[4] + e.p;
+  return e;
+}
+// Euler-flux Jacobian-vector product along local axis j: dF_j = (dF_j/dQ) dq
+__device__ __forceinline__ void euler_jvp(int j, const EulerState& e, const Real dq[5], Real gm1, Real out[5]) {
+  const Real du[3] = {(dq[1] - e.u[0] * dq[0]) * e.inv, (dq[2] - e.u[1] * dq[0]) * e.inv,
+                        (dq[3] - e.u[2] * dq[0]) * e.inv};
+  const Real dp = gm1 * (dq[4] - (e.u[0] * dq[1] + e.u[1] * dq[2] + e.u[2] * dq[3]) + e.q2h * dq[0]);
+  out[0] = dq[1 + j];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) out[1 + k] = dq[1 + j] * e.u[k] + e.Q[1 + j] * du[k] + (k == j ? dp : Real(0.0));
+  out[4] = du[j] * e.H + e.u[j] * (dq[4] + dp);
+}
+
+
+// ---------------------------------------------------------------------------
+// Moment form (general tau).  Moments of a Maxwellian normalised by rho:
+// <u^a> (full line, u>0 or u<0), <v^b>, <w^c> (full), <xi^2>, <xi^4>
+// (SURVEY A.1).  psi = (1, u, v, w, (u^2+v^2+w^2+xi^2)/2).
+// ---------------------------------------------------------------------------
+struct Mom {
+  Real U[7], V[6], W[6], X1, X2;
+};
+
+// full moments of v, w and xi; u moments over RANGE (0 full, 1 u>0, 2 u<0)
+template <int RANGE>
+__device__ __forceinline__ void maxwell_moments(Real U, Real V, Real W, Real lam, Real K, Mom& m) {
+  const Real h = Real(0.5) / lam;  // 1/(2 lambda)
+  if (RANGE == 0) {
+    m.U[0] = Real(1.0);
+    m.U[1] = U;
+  } else {
+    const Real sl = sqrt(lam);
+    const Real e = Real(0.5) * exp(-lam * U * U) * Real(0.56418958354775628) / sl;  // e^{-lam U^2} / (2 sqrt(pi lam))
+    if (RANGE == 1) {
+      m.U[0] = Real(0.5) * erfc(-sl * U);
+      m.U[1] = U * m.U[0] + e;
+    } else {
+      m.U[0] = Real(0.5) * erfc(sl * U);
+      m.U[1] = U * m.U[0] - e;
+    }
+  }
+#pragma unroll
+  for (int n = 0; n < 5; ++n) m.U[n + 2] = U * m.U[n + 1] + (n + 1) * h * m.U[n];
+  m.V[0] = Real(1.0);
+  m.V[1] = V;
+  m.W[0] = Real(1.0);
+  m.W[1] = W;
+#pragma unroll
+  for (int n = 0; n < 4; ++n) {
+    m.V[n + 2] = V * m.V[n + 1] + (n + 1) * h * m.V[n];
+    m.W[n + 2] = W * m.W[n + 1] + (n + 1) * h * m.W[n];
+  }
+  m.X1 = K * h;
+  m.X2 = K * (K + Real(2.0)) * h * h;
+}
+
+// <u^A v^B w^C psi>
+template <int A, int B, int C>
+__device__ __forceinline__ void psi_m(const Mom& m, Real o[5]) {
+  const Real uvw = m.U[A] * m.V[B] * m.W[C];
+  o[0] = uvw;
+  o[1] = m.U[A + 1] * m.V[B] * m.W[C];
+  o[2] = m.U[A] * m.V[B + 1] * m.W[C];
+  o[3] = m.U[A] * m.V[B] * m.W[C + 1];
+  o[4] = Real(0.5) * (m.U[A + 2] * m.V[B] * m.W[C] + m.U[A] * m.V[B + 2] * m.W[C] + m.U[A] * m.V[B] * m.W[C + 2] + uvw * m.X1);
+}
+// <u^A v^B w^C xi^2 psi>
+template <int A, int B, int C>
+__device__ __forceinline__ void psi_mx(const Mom& m, Real o[5]) {
+  const Real uvw = m.U[A] * m.V[B] * m.W[C];
+  o[0] = uvw * m.X1;
+  o[1] = m.U[A + 1] * m.V[B] * m.W[C] * m.X1;
+  o[2] = m.U[A] * m.V[B + 1] * m.W[C] * m.X1;
+  o[3] = m.U[A] * m.V[B] * m.W[C + 1] * m.X1;
+  o[4] = Real(0.5) * (m.X1 * (m.U[A + 2] * m.V[B] * m.W[C] + m.U[A] * m.V[B + 2] * m.W[C] + m.U[A] * m.V[B] * m.W[C + 2]) +
+                uvw * m.X2);
+}
+// <s u^A v^B w^C psi> for a slope s = s0 + s1 u + s2 v + s3 w + s4 psi_5
+template <int A, int B, int C>
+__device__ __forceinline__ void slope_m(const Mom& m, const Real s[5], Real o[5]) {
+  Real t[5];
+  psi_m<A, B, C>(m, t);
+#pragma unroll
+  for (int k = 0; k < 5; ++k) o[k] = s[0] * t[k];
+  psi_m<A + 1, B, C>(m, t);
+#pragma unroll
+  for (int k = 0; k < 5; ++k) o[k] = fma(s[1], t[k], o[k]);
+  psi_m<A, B + 1, C>(m, t);
+#pragma unroll
+  for (int k = 0; k < 5; ++k) o[k] = fma(s[2], t[k], o[k]);
+  psi_m<A, B, C + 1>(m, t);
+#pragma unroll
+  for (int k = 0; k < 5; ++k) o[k] = fma(s[3], t[k], o[k]);
+  const Real h4 = Real(0.5) * s[4];
+  psi_m<A + 2, B, C>(m, t);
+#pragma unroll
+  for (int k = 0; k < 5; ++k) o[k] = fma(h4, t[k], o[k]);
+  psi_m<A, B + 2, C>(m, t);
+#pragma unroll
+  for (int k = 0; k < 5; ++k) o[k] = fma(h4, t[k], o[k]);
+  psi_m<A, B, C + 2>(m, t);
+#pragma unroll
+  for (int k = 0; k < 5; ++k) o[k] = fma(h4, t[k], o[k]);
+  psi_mx<A, B, C>(m, t);
+#pragma unroll
+  for (int k = 0; k < 5; ++k) o[k] = fma(h4, t[k], o[k]);
+}
+
+// micro-slope a with sum_j a_j <psi_i psi_j> = b_i (b already divided by rho),
+// closed form of the 5x5 Maxwellian moment system
+__device__ __forceinline__ void micro_slope(const Real b[5], Real U, Real V, Real W, Real lam, Real K,
+                                            Real a[5]) {
+  const Real B = U * U + V * V + W * W + (K + Real(3.0)) / (Real(2.0) * lam);
+  const Real R1 = b[1] - U * b[0], R2 = b[2] - V * b[0], R3 = b[3] - W * b[0];
+  const Real R4 = Real(2.0) * b[4] - B * b[0];
+  a[4] = Real(4.0) * lam * lam / (K + Real(3.0)) * (R4 - Real(2.0) * U * R1 - Real(2.0) * V * R2 - Real(2.0) * W * R3);
+  a[1] = Real(2.0) * lam * R1 - U * a[4];
+  a[2] = Real(2.0) * lam * R2 - V * a[4];
+  a[3] = Real(2.0) * lam * R3 - W * a[4];
+  a[0] = b[0] - U * a[1] - V * a[2] - W * a[3] - Real(0.5) * a[4] * B;
+}
+
+struct Prim {
+  Real rho, U, V, W, lam;
+};
+__device__ __forceinline__ Prim prim_of(const Real q[5], Real K) {
+  Prim p;
+  p.rho = q[0];
+  const Real inv = Real(1.0) / q[0];
+  p.U = q[1] * inv;
+  p.V = q[2] * inv;
+  p.W = q[3] * inv;
+  p.lam = (K + Real(3.0)) * p.rho / (Real(4.0) * (q[4] - Real(0.5) * p.rho * (p.U * p.U + p.V * p.V + p.W * p.W)));
+  return p;
+}
+
+
+// closed-form time integrals of the Eq. (flux) coefficients over [0, delta]
+struct TimeCoef {
+  Real c1, c2, c3, c4, c5, c6;
+};
+__device__ __forceinline__ TimeCoef time_coef(Real delta, Real tau) {
+  TimeCoef c;
+  const Real e = exp(-delta / tau);
+  const Real om = Real(1.0) - e;
+  c.c1 = delta - tau * om;
+  c.c2 = Real(2.0) * tau * tau * om - tau * delta * (Real(1.0) + e);
+  c.c3 = Real(0.5) * delta * delta - tau * delta + tau * tau * om;
+  c.c4 = tau * om;
+  c.c5 = -Real(2.0) * tau * tau * om + tau * delta * e;
+  c.c6 = -tau * tau * om;
+  return c;
+}
+
+// Q0 = int_{u>0} psi g_l + int_{u<0} psi g_r
+__device__ __forceinline__ void equilibrium_state(const Real ql[5], const Real qr[5], Real K, Real Q0[5]) {
+  const Real rpi = Real(0.56418958354775628);  // 1/sqrt(pi)
+  const Prim l = prim_of(ql, K), r = prim_of(qr, K);
+  const Real hl = Real(0.5) / l.lam, hr = Real(0.5) / r.lam;  // 1/(2 lambda)
+  const Real isl = rsqrt(l.lam), isr = rsqrt(r.lam);
+  const Real a0 = Real(0.5) * erfc(-(l.lam * isl) * l.U);
+  const Real a1 = l.U * a0 + Real(0.5) * exp(-l.lam * l.U * l.U) * rpi * isl;
+  const Real a2 = l.U * a1 + a0 * hl;
+  const Real b0 = Real(0.5) * erfc((r.lam * isr) * r.U);
+  const Real b1 = r.U * b0 - Real(0.5) * exp(-r.lam * r.U * r.U) * rpi * isr;
+  const Real b2 = r.U * b1 + b0 * hr;
+  Q0[0] = l.rho * a0 + r.rho * b0;
+  Q0[1] = l.rho * a1 + r.rho * b1;
+  Q0[2] = l.rho * a0 * l.V + r.rho * b0 * r.V;
+  Q0[3] = l.rho * a0 * l.W + r.rho * b0 * r.W;
+  Q0[4] = Real(0.5) * l.rho * (a2 + a0 * (l.V * l.V + l.W * l.W + (K + Real(2.0)) * hl)) +
+          Real(0.5) * r.rho * (b2 + b0 * (r.V * r.V + r.W * r.W + (K + Real(2.0)) * hr));
+}
+
+// One term group of Eq. (flux) for a Maxwellian with its slopes, accumulated into
+// I_half, I_full (rho-weighted).  Full-range Maxwellian moments of the slope
+// polynomials reduce to Euler-flux Jacobian-vector products (d_j g = a_j g, so
+// rho <u_j a_j psi> = A_j(Q) d_j Q): the compatibility condition
+// for A becomes d_t Q = -sum_j A_j(Q) d_j Q, and for the equilibrium
+// part rho<u psi> = F_n(Q), rho<A u psi> = A_n(Q) d_t Q.  Only <(a.u) u psi>
+// (full range for g0) and the half-range moments of g_l, g_r need the generic
+// moment sums.
+template <int RANGE>
+__device__ __forceinline__ void add_side(const Real q[5], const Real dq[3][5], Real K, Real gm1,
+                                         const TimeCoef& ch, const TimeCoef& cf, Real Ih[5], Real If[5]) {
+  const Prim g = prim_of(q, K);
+  const Real ir = Real(1.0) / g.rho;
+  Real a[3][5];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    Real b[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) b[v] = dq[j][v] * ir;
+    micro_slope(b, g.U, g.V, g.W, g.lam, K, a[j]);
+  }
+  const EulerState es = euler_state(q, gm1);
+  Real dtq[5] = {Real(0.0), Real(0.0), Real(0.0), Real(0.0), Real(0.0)};  // d_t Q by compatibility
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    Real jv[5];
+    euler_jvp(j, es, dq[j], gm1, jv);
+#pragma unroll
+    for (int v = 0; v < 5; ++v) dtq[v] -= jv[v];
+  }
+  Mom mom;
+  maxwell_moments<RANGE>(g.U, g.V, g.W, g.lam, K, mom);
+  Real m2[5];  // <(a.u) u psi> over the range
+  {
+    Real t0[5], t1[5], t2[5];
+    slope_m<2, 0, 0>(mom, a[0], t0);
+    slope_m<1, 1, 0>(mom, a[1], t1);
+    slope_m<1, 0, 1>(mom, a[2], t2);
+#pragma unroll
+    for (int v = 0; v < 5; ++v) m2[v] = g.rho * (t0[v] + t1[v] + t2[v]);
+  }
+  if (RANGE == 0) {
+    // rho <u psi> = F_n(Q) and rho <A u psi> = A_n(Q) d_t Q
+    Real m3[5];
+    euler_jvp(0, es, dtq, gm1, m3);
+    const Real m1[5] = {q[1], q[1] * es.u[0] + es.p, q[2] * es.u[0], q[3] * es.u[0], es.u[0] * es.H};
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      Ih[v] += ch.c1 * m1[v] + ch.c2 * m2[v] + ch.c3 * m3[v];
+      If[v] += cf.c1 * m1[v] + cf.c2 * m2[v] + cf.c3 * m3[v];
+    }
+  } else {
+    Real A[5], b[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) b[v] = dtq[v] * ir;
+    micro_slope(b, g.U, g.V, g.W, g.lam, K, A);
+    Real m1[5], m3[5];
+    psi_m<1, 0, 0>(mom, m1);
+    slope_m<1, 0, 0>(mom, A, m3);
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      Ih[v] += g.rho * (ch.c4 * m1[v] + ch.c6 * m3[v]) + ch.c5 * m2[v];
+      If[v] += g.rho * (cf.c4 * m1[v] + cf.c6 * m3[v]) + cf.c5 * m2[v];
+    }
+  }
+}
+
+// boundary right states in the local frame (R25)
+template <int BC>
+__device__ __forceinline__ void boundary_right(const Real ql[5], const Real dql[3][5], const Real vl_global[5],
+                                               const Real n[3], const Real t1[3], const Real t2[3],
+                                               const GasR& gp, Real qr[5], Real dqr[3][5]) {
+  if (BC == 1) {  // wall mirror: all velocity components reversed, normal derivatives negated
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      const Real sv = (v >= 1 && v <= 3) ? -Real(1.0) : Real(1.0);
+      qr[v] = sv * ql[v];
+      dqr[0][v] = -sv * dql[0][v];
+      dqr[1][v] = sv * dql[1][v];
+      dqr[2][v] = sv * dql[2][v];
+    }
+  } else {  // farfield: Riemann state of the left value, zero gradient
+    Real qb[5];
+    farfield_riemann(vl_global, n, gp, qb);
+    qr[0] = qb[0];
+    qr[4] = qb[4];
+    qr[1] = qb[1] * n[0] + qb[2] * n[1] + qb[3] * n[2];
+    qr[2] = qb[1] * t1[0] + qb[2] * t1[1] + qb[3] * t1[2];
+    qr[3] = qb[1] * t2[0] + qb[2] * t2[1] + qb[3] * t2[2];
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+      for (int v = 0; v < 5; ++v) dqr[j][v] = Real(0.0);
+  }
+}
+
+template <int NV, int STAGE, bool TAU0, int BC>
+__global__ void __launch_bounds__(NV == 3 ? 96 : 128, TAU0 ? (NV == 3 ? 5 : 4) : 1) k_flux(FluxArgs a) {
+  constexpr int NGP = NV == 3 ? 3 : 4;
+  constexpr int BLOCK = NV == 3 ? 96 : 128;
+  constexpr int NOUT = STAGE == 1 ? 10 : 5;
+  __shared__ Real red[NOUT][BLOCK];
+  const int t = blockIdx.x * BLOCK + threadIdx.x;
+  const int lf = t / NGP, g = t - lf * NGP;
+  const bool active = lf < a.n_faces;
+  Real out[NOUT];
+#pragma unroll
+  for (int k = 0; k < NOUT; ++k) out[k] = Real(0.0);
+  if (active) {
+    const int f = a.face0 + lf;
+    const int co = __ldg(a.f_cells + 2 * f);
+    const Real* fg = a.f_geo + (size_t)f * a.f_stride;
+    Real x[3], n[3], wS;
+    face_gp<NV>(fg, g, x, n, wS);
+    Real t1[3], t2[3];
+    frame(n, t1, t2);
+    const Real K = a.gp.K;
+    const Real gm1 = a.gp.gamma - Real(1.0);
+    // positivity check without a division: for rho > 0, p > 0  <=>  rho*rhoE - |m|^2/2 > 0 (R21)
+    auto admissible = [](const Real q[5]) {
+      return q[0] > Real(0.0) && (q[0] * q[4] - Real(0.5) * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3])) > Real(0.0);
+    };
+    auto rotate_value = [&](const Real v5[5], Real q[5]) {
+      q[0] = v5[0];
+      q[4] = v5[4];
+      q[1] = v5[1] * n[0] + v5[2] * n[1] + v5[3] * n[2];
+      q[2] = v5[1] * t1[0] + v5[2] * t1[1] + v5[3] * t1[2];
+      q[3] = v5[1] * t2[0] + v5[2] * t2[1] + v5[3] * t2[2];
+    };
+    Real F[5], dF[5];
+    if (TAU0 && BC == 0) {
+      // tau = 0 interior face: only the average of the two gradients enters (R9),
+      // so it is summed in the global frame and rotated once
+      Real ql[5], qr[5], gs[5][3];
+      {
+        Real vl[5];
+        eval_poly(a.ceff + (size_t)co * kRec, x, vl, gs);
+        if (!admissible(vl)) {
+          atomicAdd((unsigned long long*)&a.ctrl->fallbacks, 1ull);
+#pragma unroll
+          for (int v = 0; v < 5; ++v) {
+            vl[v] = a.Q[(size_t)co * QS + v];
+            gs[v][0] = gs[v][1] = gs[v][2] = Real(0.0);
+          }
+        }
+        rotate_value(vl, ql);
+      }
+      {
+        const int cn = __ldg(a.f_cells + 2 * f + 1);
+        const Real xr[3] = {x[0] + __ldg(fg + 3 * NV), x[1] + __ldg(fg + 3 * NV + 1),
+                              x[2] + __ldg(fg + 3 * NV + 2)};
+        Real vr[5], gr[5][3];
+        eval_poly(a.ceff + (size_t)cn * kRec, xr, vr, gr);
+        if (!admissible(vr)) {
+          atomicAdd((unsigned long long*)&a.ctrl->fallbacks, 1ull);
+#pragma unroll
+          for (int v = 0; v < 5; ++v) {
+            vr[v] = a.Q[(size_t)cn * QS + v];
+            gr[v][0] = gr[v][1] = gr[v][2] = Real(0.0);
+          }
+        }
+        rotate_value(vr, qr);
+#pragma unroll
+        for (int v = 0; v < 5; ++v)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) gs[v][c] = Real(0.5) * (gs[v][c] + gr[v][c]);
+      }
+      Real dq0[3][5];
+      {
+        Real zero[5] = {0, 0, 0, 0, 0}, dummy[5];
+        to_local(zero, gs, n, t1, t2, dummy, dq0);
+      }
+      Real Q0[5];
+      equilibrium_state(ql, qr, K, Q0);
+      // f = g0 (1 + A t): F = Euler flux of Q0, d_t F = A_n(Q0) d_t Q0,
+      // d_t Q0 = -sum_j A_j(Q0) d_j Q0
+      const EulerState es = euler_state(Q0, gm1);
+      Real dtQ0[5] = {Real(0.0), Real(0.0), Real(0.0), Real(0.0), Real(0.0)};
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        Real jv[5];
+        euler_jvp(j, es, dq0[j], gm1, jv);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) dtQ0[v] -= jv[v];
+      }
+      euler_jvp(0, es, dtQ0, gm1, dF);
+      F[0] = Q0[1];
+      F[1] = Q0[1] * es.u[0] + es.p;
+      F[2] = Q0[2] * es.u[0];
+      F[3] = Q0[3] * es.u[0];
+      F[4] = es.u[0] * es.H;
+    } else {
+    Real ql[5], dql[3][5], qr[5], dqr[3][5];
+    Real vl[5];
+    {
+      Real grad[5][3];
+      eval_poly(a.ceff + (size_t)co * kRec, x, vl, grad);
+      if (!admissible(vl)) {  // R21 positivity fallback
+        atomicAdd((unsigned long long*)&a.ctrl->fallbacks, 1ull);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+          vl[v] = a.Q[(size_t)co * QS + v];
+          grad[v][0] = grad[v][1] = grad[v][2] = Real(0.0);
+        }
+      }
+      to_local(vl, grad, n, t1, t2, ql, dql);
+    }
+    if (BC == 0) {
+      const int cn = __ldg(a.f_cells + 2 * f + 1);
+      const Real xr[3] = {x[0] + __ldg(fg + 3 * NV), x[1] + __ldg(fg + 3 * NV + 1), x[2] + __ldg(fg + 3 * NV + 2)};
+      Real val[5], grad[5][3];
+      eval_poly(a.ceff + (size_t)cn * kRec, xr, val, grad);
+      if (!admissible(val)) {
+        atomicAdd((unsigned long long*)&a.ctrl->fallbacks, 1ull);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+          val[v] = a.Q[(size_t)cn * QS + v];
+          grad[v][0] = grad[v][1] = grad[v][2] = Real(0.0);
+        }
+      }
+      to_local(val, grad, n, t1, t2, qr, dqr);
+    } else {
+      boundary_right<BC>(ql, dql, vl, n, t1, t2, a.gp, qr, dqr);
+    }
+    Real Q0[5];
+    equilibrium_state(ql, qr, K, Q0);
+    if (TAU0) {
+      Real dtQ0[5] = {Real(0.0), Real(0.0), Real(0.0), Real(0.0), Real(0.0)};
+      const EulerState es = euler_state(Q0, gm1);
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        Real d0[5], jv[5];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) d0[v] = Real(0.5) * (dql[j][v] + dqr[j][v]);
+        euler_jvp(j, es, d0, gm1, jv);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) dtQ0[v] -= jv[v];
+      }
+      euler_jvp(0, es, dtQ0, gm1, dF);
+      F[0] = Q0[1];
+      F[1] = Q0[1] * es.u[0] + es.p;
+      F[2] = Q0[2] * es.u[0];
+      F[3] = Q0[3] * es.u[0];
+      F[4] = es.u[0] * es.H;
+    } else {
+      // collision time (R7): tau = mu(T0)/p0 + c1 |pl - pr|/(pl + pr) dt
+      const Real dt = a.ctrl->dt;
+      const Prim g0 = prim_of(Q0, K), gl = prim_of(ql, K), gr = prim_of(qr, K);
+      const Real p0 = g0.rho / (Real(2.0) * g0.lam), pl = gl.rho / (Real(2.0) * gl.lam), pr = gr.rho / (Real(2.0) * gr.lam);
+      const Real mu = a.gp.mu_inf * pow((p0 / g0.rho) / a.gp.t_inf, a.gp.mu_exp);
+      const Real tau = mu / p0 + a.gp.c1 * fabs(pl - pr) / (pl + pr) * dt;
+      const TimeCoef ch = time_coef(Real(0.5) * dt, tau), cf = time_coef(dt, tau);
+      Real Ih[5] = {0, 0, 0, 0, 0}, If[5] = {0, 0, 0, 0, 0};
+      Real dq0[3][5];
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int v = 0; v < 5; ++v) dq0[j][v] = Real(0.5) * (dql[j][v] + dqr[j][v]);
+      add_side<0>(Q0, dq0, K, gm1, ch, cf, Ih, If);
+      add_side<1>(ql, dql, K, gm1, ch, cf, Ih, If);
+      add_side<2>(qr, dqr, K, gm1, ch, cf, Ih, If);
+      // 2x2 fit
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        F[v] = (Real(4.0) * Ih[v] - If[v]) / dt;
+        dF[v] = Real(4.0) * (If[v] - Real(2.0) * Ih[v]) / (dt * dt);
+      }
+    }
+    }
+    // rotate back to the global frame and weight by omega_G S
+    if (STAGE == 1) {
+      out[0] = wS * F[0];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) out[1 + c] = wS * (F[1] * n[c] + F[2] * t1[c] + F[3] * t2[c]);
+      out[4] = wS * F[4];
+      out[5] = wS * dF[0];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) out[6 + c] = wS * (dF[1] * n[c] + dF[2] * t1[c] + dF[3] * t2[c]);
+      out[9] = wS * dF[4];
+    } else {
+      out[0] = wS * dF[0];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) out[1 + c] = wS * (dF[1] * n[c] + dF[2] * t1[c] + dF[3] * t2[c]);
+      out[4] = wS * dF[4];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NOUT; ++k) red[k][threadIdx.x] = out[k];
+  __syncthreads();
+  // face quadrature sum in Gauss-point order (deterministic)
+  const int faces_in_block = BLOCK / NGP;
+  for (int e = threadIdx.x; e < faces_in_block * NOUT; e += BLOCK) {
+    const int fl = e / NOUT, k = e - fl * NOUT;
+    const int face = blockIdx.x * faces_in_block + fl;
+    if (face < a.n_faces) {
+      Real s = red[k][fl * NGP];
+#pragma unroll
+      for (int q = 1; q < NGP; ++q) s += red[k][fl * NGP + q];
+      Real* dst = STAGE == 1 ? a.F1 : a.F2;
+      dst[(size_t)(a.face0 + face) * NOUT + k] = s;
+    }
+  }
+}
+
+
+
+// ----------------------------------------------------------------------------
+// a10: L, d_t L and the S2O4 stages
+// ----------------------------------------------------------------------------
+struct UpdateArgs {
+  Real* __restrict__ Q;  // [n_local][QS]  (stage 1: Q^n -> Q*, stage 2: -> Q^{n+1})
+  Real* __restrict__ R;  // [n_owned][QS]
+  const Real* __restrict__ F1;
+  const Real* __restrict__ F2;
+  const int* __restrict__ cf;  // [NF][n_owned]
+  const Real* __restrict__ inv_v;
+  const Real* __restrict__ h_dt;
+  int n_owned;
+  Ctrl* ctrl;
+  GasParams gp;
+};
+
+template <int NF>
+__global__ void __launch_bounds__(256) k_update1(UpdateArgs a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n_owned) return;
+  Real L[5] = {0, 0, 0, 0, 0}, dL[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+  for (int p = 0; p < NF; ++p) {  // local-face order (deterministic, partition independent)
+    const int e = __ldg(a.cf + p * a.n_owned + i);
+    const int f = e >= 0 ? e : ~e;
+    const R2* F = reinterpret_cast<const R2*>(a.F1 + (size_t)f * 10);
+    Real v10[10];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const R2 x = __ldg(F + k);
+      v10[2 * k] = x.x;
+      v10[2 * k + 1] = x.y;
+    }
+    if (e >= 0) {
+#pragma unroll
+      for (int v = 0; v < 5; ++v) { L[v] -= v10[v]; dL[v] -= v10[5 + v]; }
+    } else {
+#pragma unroll
+      for (int v = 0; v < 5; ++v) { L[v] += v10[v]; dL[v] += v10[5 + v]; }
+    }
+  }
+  const Real iv = a.inv_v[i];
+  const Real dt = a.ctrl->dt;
+  Real* q = a.Q + (size_t)i * QS;
+  Real* r = a.R + (size_t)i * QS;
+#pragma unroll
+  for (int v = 0; v < 5; ++v) {
+    const Real l = L[v] * iv, dl = dL[v] * iv;
+    const Real q0 = q[v];
+    q[v] = q0 + Real(0.5) * dt * l + Real(0.125) * dt * dt * dl;
+    r[v] = q0 + dt * l + dt * dt / Real(6.0) * dl;
+  }
+}
+
+
+template <int NF>
+__global__ void __launch_bounds__(256) k_update2(UpdateArgs a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double bound = 1e300;
+  if (i < a.n_owned) {
+    Real dL[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+    for (int p = 0; p < NF; ++p) {
+      const int e = __ldg(a.cf + p * a.n_owned + i);
+      const int f = e >= 0 ? e : ~e;
+      const Real* F = a.F2 + (size_t)f * 5;
+      if (e >= 0) {
+#pragma unroll
+        for (int v = 0; v < 5; ++v) dL[v] -= __ldg(F + v);
+      } else {
+#pragma unroll
+        for (int v = 0; v < 5; ++v) dL[v] += __ldg(F + v);
+      }
+    }
+    const Real iv = a.inv_v[i];
+    const Real dt = a.ctrl->dt;
+    Real q[5];
+    const Real* r = a.R + (size_t)i * QS;
+    Real* qo = a.Q + (size_t)i * QS;
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      q[v] = r[v] + dt * dt / Real(6.0) * Real(2.0) * (dL[v] * iv);
+      qo[v] = q[v];
+    }
+    const Real p = (a.gp.gamma - Real(1.0)) * (q[4] - Real(0.5) * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3]) / q[0]);
+    if (!(q[0] > Real(0.0)) || !(p > Real(0.0))) atomicMin(&a.ctrl->bad_cell, i);
+    else {
+      const double qd[5] = {q[0], q[1], q[2], q[3], q[4]};
+      bound = cell_dt_bound(qd, a.h_dt[i], a.gp);
+    }
+  }
+  block_min_dt(bound, a.ctrl);
+}
+
+__global__ void __launch_bounds__(256) k_dt_init(const Real* __restrict__ Q, const Real* __restrict__ h_dt, int n,
+                                                 Ctrl* ctrl, GasParams gp) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double bound = 1e300;
+  if (i < n) {
+    Real q[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) q[v] = Q[(size_t)i * QS + v];
+    const double qd[5] = {q[0], q[1], q[2], q[3], q[4]};
+    bound = cell_dt_bound(qd, h_dt[i], gp);
+  }
+  block_min_dt(bound, ctrl);
+}
+
+
+// state layout conversions for set/get_state: AoS [n][5] in caller order <-> local rows
+__global__ void k_scatter_state(const double* __restrict__ in, const int64_t* __restrict__ row, int n,
+                                Real* __restrict__ Q) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t r = row[i];
+#pragma unroll
+  for (int v = 0; v < 5; ++v) Q[(size_t)i * QS + v] = in[r * 5 + v];
+  Q[(size_t)i * QS + 5] = Real(0.0);
+}
+__global__ void k_gather_state(const Real* __restrict__ Q, const int* __restrict__ local_of_out, int n,
+                               double* __restrict__ out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int i = local_of_out[k];
+#pragma unroll
+  for (int v = 0; v < 5; ++v) out[(size_t)k * 5 + v] = Q[(size_t)i * QS + v];
+}
+// halo pack: rows of the send list, [n_send][QS]
+__global__ void k_pack(const Real* __restrict__ Q, const int* __restrict__ list, int n, Real* __restrict__ buf) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n * 3) return;
+  const int j = k / 3, part = k - 3 * j;
+  reinterpret_cast<R2*>(buf)[k] = reinterpret_cast<const R2*>(Q + (size_t)list[j] * QS)[part];
+}
+
+
+
+// host-side launchers of this precision's kernels (solver.cu is templated on this struct)
+struct Launch {
+  using RealT = Real;
+  using ReconArgsT = ReconArgs;
+  using FluxArgsT = FluxArgs;
+  using UpdateArgsT = UpdateArgs;
+  using GasT = GasR;
+  static GasR gas(const GasParams& g) { return make_gas(g); }
+  template <int K, int M, int NM>
+  static cudaError_t recon_smem(int bytes) {
+    return cudaFuncSetAttribute(k_recon<K, M, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  }
+  template <int K, int M, int NM>
+  static void recon(int grid, size_t smem, cudaStream_t st, const ReconArgs& a) {
+    k_recon<K, M, NM><<<grid, kTile, smem, st>>>(a);
+  }
+  template <int NV, int STAGE, bool TAU0, int BC>
+  static void flux(int grid, cudaStream_t st, const FluxArgs& a) {
+    k_flux<NV, STAGE, TAU0, BC><<<grid, NV == 3 ? 96 : 128, 0, st>>>(a);
+  }
+  template <int NF>
+  static void update1(int grid, cudaStream_t st, const UpdateArgs& u) {
+    k_update1<NF><<<grid, 256, 0, st>>>(u);
+  }
+  template <int NF>
+  static void update2(int grid, cudaStream_t st, const UpdateArgs& u) {
+    k_update2<NF><<<grid, 256, 0, st>>>(u);
+  }
+  static void bc_ghosts(int grid, cudaStream_t st, Real* Q, int first, int n, const int* bg_cell, const int* bg_bc,
+                        const Real* bg_normal, const GasR& gp, int n_owned, int part) {
+    k_bc_ghosts<<<grid, 128, 0, st>>>(Q, first, n, bg_cell, bg_bc, bg_normal, gp, n_owned, part);
+  }
+  static void dt_init(int grid, cudaStream_t st, const Real* Q, const Real* h_dt, int n, Ctrl* ctrl,
+                      const GasParams& gp) {
+    k_dt_init<<<grid, 256, 0, st>>>(Q, h_dt, n, ctrl, gp);
+  }
+  static void scatter(int grid, cudaStream_t st, const double* in, const int64_t* row, int n, Real* Q) {
+    k_scatter_state<<<grid, 256, 0, st>>>(in, row, n, Q);
+  }
+  static void gather(int grid, cudaStream_t st, const Real* Q, const int* loc, int n, double* out) {
+    k_gather_state<<<grid, 256, 0, st>>>(Q, loc, n, out);
+  }
+  static void pack(int grid, cudaStream_t st, const Real* Q, const int* list, int n, Real* buf) {
+    k_pack<<<grid, 256, 0, st>>>(Q, list, n, buf);
+  }
+};

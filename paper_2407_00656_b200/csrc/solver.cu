@@ -60,7 +60,7 @@ typedef struct ncclComm* ncclComm_t;
 typedef struct {
   char internal[128];
 } ncclUniqueId;
-enum { ncclUint64 = 5, ncclFloat64 = 8 };
+enum { ncclUint64 = 5, ncclFloat32 = 7, ncclFloat64 = 8 };
 enum { ncclMin = 3 };
 struct Nccl {
   void* h = nullptr;
@@ -141,47 +141,49 @@ struct Carve {
 int round32(int64_t n) { return (int)((n + 31) / 32 * 32); }
 
 struct DevArrays {
-  double *Q, *Qtmp, *R, *ceff, *F1, *F2, *op, *geo, *f_geo, *inv_v, *h_dt, *bg_normal, *sendbuf, *stage_in, *stage_out,
-      *Lbuf;
+  // working-precision arrays (double for fp64, float for fp32)
+  void *Q, *Qtmp, *R, *ceff, *F1, *F2, *op, *geo, *f_geo, *inv_v, *h_dt, *bg_normal, *sendbuf;
+  double *stage_in, *stage_out;  // caller-order staging, always fp64
   int *recon_cell, *st_id, *f_cells, *cf, *bg_cell, *bg_bc, *send_list, *out_local;
   int64_t* in_row;
   uint8_t* sub_slot;
   Ctrl* ctrl;
 };
 
-size_t layout(const GlobalMesh& gm, const RankPlan& rp, Carve& c, DevArrays& d) {
+// rs = bytes of the working precision
+size_t layout(const GlobalMesh& gm, const RankPlan& rp, size_t rs, Carve& c, DevArrays& d) {
   const Layout& L = gm.lay;
   const size_t nq = (size_t)QS * round32(rp.n_local());
   const int64_t ncl = rp.n_owned + rp.n_pghost;
+  auto R = [&](size_t n) { return (void*)c.take<char>(n * rs); };
   d.ctrl = c.take<Ctrl>(1);
-  d.Q = c.take<double>(nq);
-  d.Qtmp = c.take<double>(nq);
-  d.R = c.take<double>((size_t)QS * rp.n_owned);
-  d.ceff = c.take<double>((size_t)kRec * ncl);
-  d.F1 = c.take<double>((size_t)10 * rp.n_faces);
-  d.F2 = c.take<double>((size_t)5 * rp.n_faces);
+  d.Q = R(nq);
+  d.Qtmp = R(nq);
+  d.R = R((size_t)QS * rp.n_owned);
+  d.ceff = R((size_t)kRec * ncl);
+  d.F1 = R((size_t)10 * rp.n_faces);
+  d.F2 = R((size_t)5 * rp.n_faces);
   d.recon_cell = c.take<int>(rp.n_recon);
   d.st_id = c.take<int>((size_t)L.K * rp.ld);
   d.sub_slot = c.take<uint8_t>((size_t)L.M * L.NM * rp.ld);
-  d.op = c.take<double>((size_t)L.op_entries() * rp.ld);
-  d.geo = c.take<double>((size_t)8 * rp.ld);
+  d.op = R((size_t)L.op_entries() * rp.ld);
+  d.geo = R((size_t)8 * rp.ld);
   d.f_cells = c.take<int>((size_t)2 * rp.n_faces);
-  d.f_geo = c.take<double>((size_t)rp.f_geo_stride * rp.n_faces);
+  d.f_geo = R((size_t)rp.f_geo_stride * rp.n_faces);
   d.cf = c.take<int>((size_t)L.nfaces * rp.n_owned);
-  d.inv_v = c.take<double>(rp.n_owned);
-  d.h_dt = c.take<double>(rp.n_owned);
+  d.inv_v = R(rp.n_owned);
+  d.h_dt = R(rp.n_owned);
   d.bg_cell = c.take<int>(std::max<int64_t>(1, rp.n_bghost));
   d.bg_bc = c.take<int>(std::max<int64_t>(1, rp.n_bghost));
-  d.bg_normal = c.take<double>(std::max<int64_t>(3, 3 * rp.n_bghost));
+  d.bg_normal = R(std::max<int64_t>(3, 3 * rp.n_bghost));
   d.send_list = c.take<int>(std::max<size_t>(1, rp.send_list.size()));
-  d.sendbuf = c.take<double>(std::max<size_t>(QS, QS * rp.send_list.size()));
+  d.sendbuf = R(std::max<size_t>(QS, QS * rp.send_list.size()));
   d.out_local = c.take<int>(rp.n_owned);
   d.in_row = c.take<int64_t>(rp.n_owned);
   // staging for set/get_state: single rank copies the caller's whole array
   const int64_t n_in = gm.n_ranks == 1 ? gm.nc : rp.n_owned;
   d.stage_in = c.take<double>((size_t)5 * n_in);
   d.stage_out = c.take<double>((size_t)5 * rp.n_owned);
-  d.Lbuf = c.take<double>((size_t)10 * rp.n_owned);
   return c.off + 256;
 }
 }  // namespace
@@ -202,6 +204,8 @@ struct hgks_solver {
   Layout lay;
   hgks_config cfg;
   GasParams gp;
+  bool fp32 = false;  // working precision of the hot path (FP32 variant)
+  size_t rs = sizeof(double);
   int rank = 0, n_ranks = 1, device = 0, transport = HGKS_TRANSPORT_NCCL;
   size_t recon_smem_set = 0;
   int recon_t1 = 0;  // end tile of the current reconstruction launch
@@ -209,7 +213,7 @@ struct hgks_solver {
   cudaEvent_t ev_packed = nullptr, ev_halo = nullptr;
   cudaStream_t stream = nullptr;
   DevArrays d{};
-  size_t nq = 0;  // doubles in Q
+  size_t nq = 0;  // values in Q
   ncclComm_t comm = nullptr;
   int64_t launches = 0;
   bool profiling = false;
@@ -261,24 +265,35 @@ void launch(hgks_solver* s, const char* name, Launch&& fn) {
 
 inline int blocks(int64_t n, int b) { return (int)((n + b - 1) / b); }
 
-template <int K, int M, int NM>
-void run_recon_k(hgks_solver* s, const ReconArgs& a) {
-  const size_t smem = sizeof(double) * (size_t)K * 5 * kTile;
+template <class L>
+typename L::GasT make_gas_for(const GasParams& g) {
+  return L::gas(g);
+}
+
+template <class L, class T>
+typename L::RealT* as(T* p) {
+  return reinterpret_cast<typename L::RealT*>(const_cast<void*>(static_cast<const void*>(p)));
+}
+
+template <class L, int K, int M, int NM>
+void run_recon_k(hgks_solver* s, const typename L::ReconArgsT& a) {
+  const size_t smem = sizeof(typename L::RealT) * (size_t)K * 5 * kTile;
   if (smem > s->recon_smem_set) {
-    CUDA_TRY(cudaFuncSetAttribute(k_recon<K, M, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_TRY((L::template recon_smem<K, M, NM>((int)smem)));
     s->recon_smem_set = smem;
   }
   const int n_tiles = s->recon_t1 - a.tile0;
   if (n_tiles <= 0) return;
-  launch(s, "k_recon", [&] { k_recon<K, M, NM><<<n_tiles, kTile, smem, s->stream>>>(a); });
+  launch(s, "k_recon", [&] { L::template recon<K, M, NM>(n_tiles, smem, s->stream, a); });
 }
 
 // part 0: tiles of the early cells, 1: the rest, 2: all
-void run_recon(hgks_solver* s, const double* Q, int part) {
-  const Layout& L = s->lay;
+template <class L>
+void run_recon(hgks_solver* s, const void* Q, int part) {
+  const Layout& LY = s->lay;
   const RankPlan& rp = *s->rp;
-  ReconArgs a;
-  a.Q = Q;
+  typename L::ReconArgsT a;
+  a.Q = as<L>(Q);
   a.n_recon = (int)rp.n_recon;
   const int t_mid = (int)(rp.recon_late0 / kTile), t_end = (int)((rp.n_recon + kTile - 1) / kTile);
   a.tile0 = part == 1 ? t_mid : 0;
@@ -286,51 +301,50 @@ void run_recon(hgks_solver* s, const double* Q, int part) {
   a.ld = (int)s->rp->ld;
   a.recon_cell = s->d.recon_cell;
   a.st_id = s->d.st_id;
-
   a.sub_slot = s->d.sub_slot;
-  a.op = s->d.op;
-  a.geo = s->d.geo;
-  a.ceff = s->d.ceff;
-  a.eps = s->cfg.eps;
+  a.op = as<L>(s->d.op);
+  a.geo = as<L>(s->d.geo);
+  a.ceff = as<L>(s->d.ceff);
+  a.eps = (typename L::RealT)s->cfg.eps;
   a.omega_pow = s->cfg.omega_pow;
-  if (L.cell_type == 4) {
-    switch (L.K) {
-      case 14: run_recon_k<14, 4, 6>(s, a); break;
-      case 16: run_recon_k<16, 4, 6>(s, a); break;
-      case 20: run_recon_k<20, 4, 6>(s, a); break;
-      case 24: run_recon_k<24, 4, 6>(s, a); break;
-      case 32: run_recon_k<32, 4, 6>(s, a); break;
-      default: run_recon_k<40, 4, 6>(s, a); break;
+  if (LY.cell_type == 4) {
+    switch (LY.K) {
+      case 14: run_recon_k<L, 14, 4, 6>(s, a); break;
+      case 16: run_recon_k<L, 16, 4, 6>(s, a); break;
+      case 20: run_recon_k<L, 20, 4, 6>(s, a); break;
+      case 24: run_recon_k<L, 24, 4, 6>(s, a); break;
+      case 32: run_recon_k<L, 32, 4, 6>(s, a); break;
+      default: run_recon_k<L, 40, 4, 6>(s, a); break;
     }
   } else {
-    switch (L.K) {
-      case 14: run_recon_k<14, 8, 3>(s, a); break;
-      case 16: run_recon_k<16, 8, 3>(s, a); break;
-      case 20: run_recon_k<20, 8, 3>(s, a); break;
-      case 24: run_recon_k<24, 8, 3>(s, a); break;
-      case 32: run_recon_k<32, 8, 3>(s, a); break;
-      default: run_recon_k<40, 8, 3>(s, a); break;
+    switch (LY.K) {
+      case 14: run_recon_k<L, 14, 8, 3>(s, a); break;
+      case 16: run_recon_k<L, 16, 8, 3>(s, a); break;
+      case 20: run_recon_k<L, 20, 8, 3>(s, a); break;
+      case 24: run_recon_k<L, 24, 8, 3>(s, a); break;
+      case 32: run_recon_k<L, 32, 8, 3>(s, a); break;
+      default: run_recon_k<L, 40, 8, 3>(s, a); break;
     }
   }
 }
 
-template <int NV, int BC>
-void launch_flux(hgks_solver* s, const FluxArgs& a, int stage, bool tau0) {
+template <class L, int NV, int BC>
+void launch_flux(hgks_solver* s, const typename L::FluxArgsT& a, int stage, bool tau0) {
   constexpr int NGP = NV == 3 ? 3 : 4, B = NV == 3 ? 96 : 128;
   const int nb = blocks((int64_t)a.n_faces * NGP, B);
   const char* names[2][2] = {{"k_flux_s1", "k_flux_s2"}, {"k_flux_tau0_s1", "k_flux_tau0_s2"}};
   const char* nm = BC == 0 ? names[tau0][stage - 1] : (BC == 1 ? "k_flux_wall" : "k_flux_farfield");
   if (tau0) {
-    if (stage == 1) launch(s, nm, [&] { k_flux<NV, 1, true, BC><<<nb, B, 0, s->stream>>>(a); });
-    else launch(s, nm, [&] { k_flux<NV, 2, true, BC><<<nb, B, 0, s->stream>>>(a); });
+    if (stage == 1) launch(s, nm, [&] { L::template flux<NV, 1, true, BC>(nb, s->stream, a); });
+    else launch(s, nm, [&] { L::template flux<NV, 2, true, BC>(nb, s->stream, a); });
   } else {
-    if (stage == 1) launch(s, nm, [&] { k_flux<NV, 1, false, BC><<<nb, B, 0, s->stream>>>(a); });
-    else launch(s, nm, [&] { k_flux<NV, 2, false, BC><<<nb, B, 0, s->stream>>>(a); });
+    if (stage == 1) launch(s, nm, [&] { L::template flux<NV, 1, false, BC>(nb, s->stream, a); });
+    else launch(s, nm, [&] { L::template flux<NV, 2, false, BC>(nb, s->stream, a); });
   }
 }
 
-template <int NV>
-void run_flux_nv(hgks_solver* s, FluxArgs a, int stage, int part) {
+template <class L, int NV>
+void run_flux_nv(hgks_solver* s, typename L::FluxArgsT a, int stage, int part) {
   const RankPlan& rp = *s->rp;
   const bool tau0 = s->cfg.tau_mode == 0;
   // part 0: early interior faces; 1: late interior + wall + farfield; 2: all
@@ -342,69 +356,77 @@ void run_flux_nv(hgks_solver* s, FluxArgs a, int stage, int part) {
     a.face0 = (int)ranges[bc][0];
     a.n_faces = (int)ranges[bc][1];
     if (a.n_faces == 0) continue;
-    if (bc == 0) launch_flux<NV, 0>(s, a, stage, tau0);
-    else if (bc == 1) launch_flux<NV, 1>(s, a, stage, tau0);
-    else launch_flux<NV, 2>(s, a, stage, tau0);
+    if (bc == 0) launch_flux<L, NV, 0>(s, a, stage, tau0);
+    else if (bc == 1) launch_flux<L, NV, 1>(s, a, stage, tau0);
+    else launch_flux<L, NV, 2>(s, a, stage, tau0);
   }
 }
 
-void run_flux(hgks_solver* s, const double* Q, int stage, int part) {
+template <class L>
+void run_flux(hgks_solver* s, const void* Q, int stage, int part) {
   const RankPlan& rp = *s->rp;
-  FluxArgs a;
-  a.Q = Q;
-  a.ceff = s->d.ceff;
+  typename L::FluxArgsT a;
+  a.Q = as<L>(Q);
+  a.ceff = as<L>(s->d.ceff);
   a.f_cells = s->d.f_cells;
-  a.f_geo = s->d.f_geo;
+  a.f_geo = as<L>(s->d.f_geo);
   a.f_stride = rp.f_geo_stride;
   a.n_faces = 0;
   a.face0 = 0;
-  a.F1 = s->d.F1;
-  a.F2 = s->d.F2;
+  a.F1 = as<L>(s->d.F1);
+  a.F2 = as<L>(s->d.F2);
   a.ctrl = s->d.ctrl;
-  a.gp = s->gp;
-  if (s->lay.nv == 3) run_flux_nv<3>(s, a, stage, part);
-  else run_flux_nv<4>(s, a, stage, part);
+  a.gp = make_gas_for<L>(s->gp);
+  if (s->lay.nv == 3) run_flux_nv<L, 3>(s, a, stage, part);
+  else run_flux_nv<L, 4>(s, a, stage, part);
 }
 
-UpdateArgs update_args(hgks_solver* s) {
-  UpdateArgs u;
-  u.Q = s->d.Q;
-  u.R = s->d.R;
-  u.F1 = s->d.F1;
-  u.F2 = s->d.F2;
+template <class L>
+typename L::UpdateArgsT update_args(hgks_solver* s) {
+  typename L::UpdateArgsT u;
+  u.Q = as<L>(s->d.Q);
+  u.R = as<L>(s->d.R);
+  u.F1 = as<L>(s->d.F1);
+  u.F2 = as<L>(s->d.F2);
   u.cf = s->d.cf;
-  u.inv_v = s->d.inv_v;
-  u.h_dt = s->d.h_dt;
+  u.inv_v = as<L>(s->d.inv_v);
+  u.h_dt = as<L>(s->d.h_dt);
   u.n_owned = (int)s->rp->n_owned;
   u.ctrl = s->d.ctrl;
   u.gp = s->gp;
   return u;
 }
 
-void pack(hgks_solver* s, const double* Q) {
+template <class L>
+void pack(hgks_solver* s, const void* Q) {
   const int ns = (int)s->rp->send_list.size();
   if (ns > 0)
-    launch(s, "k_pack", [&] { k_pack<<<blocks(3 * ns, 256), 256, 0, s->stream>>>(Q, s->d.send_list, ns, s->d.sendbuf); });
+    launch(s, "k_pack",
+           [&] { L::pack(blocks(3 * ns, 256), s->stream, as<L>(Q), s->d.send_list, ns, as<L>(s->d.sendbuf)); });
 }
 
 // a5: halo exchange of the 3 ghost layers.  NCCL transport: grouped
 // send/recv per peer straight into the contiguous ghost ranges (no unpack).
 // Loopback transport: done by hgks_group_step across the solvers of one process.
-void exchange(hgks_solver* s, double* Q) {
+template <class L>
+void exchange(hgks_solver* s, void* Q) {
   const RankPlan& rp = *s->rp;
   if (s->n_ranks == 1 || rp.peers.empty() || s->transport != HGKS_TRANSPORT_NCCL) return;
-  pack(s, Q);
+  pack<L>(s, Q);
   CUDA_TRY(cudaEventRecord(s->ev_packed, s->stream));
   CUDA_TRY(cudaStreamWaitEvent(s->comm_stream, s->ev_packed, 0));
+  const int dtype = s->fp32 ? ncclFloat32 : ncclFloat64;
+  typename L::RealT* q = as<L>(Q);
+  typename L::RealT* sb = as<L>(s->d.sendbuf);
   Nccl& N = nccl();
   NCCL_TRY(N.GroupStart());
   for (size_t p = 0; p < rp.peers.size(); ++p) {
     if (rp.send_cnt[p] > 0)
-      NCCL_TRY(N.Send(s->d.sendbuf + (size_t)QS * rp.send_off[p], (size_t)QS * rp.send_cnt[p], ncclFloat64,
-                      rp.peers[p], s->comm, s->comm_stream));
+      NCCL_TRY(N.Send(sb + (size_t)QS * rp.send_off[p], (size_t)QS * rp.send_cnt[p], dtype, rp.peers[p], s->comm,
+                      s->comm_stream));
     if (rp.recv_cnt[p] > 0)
-      NCCL_TRY(N.Recv(Q + (size_t)QS * rp.recv_off[p], (size_t)QS * rp.recv_cnt[p], ncclFloat64, rp.peers[p],
-                      s->comm, s->comm_stream));
+      NCCL_TRY(N.Recv(q + (size_t)QS * rp.recv_off[p], (size_t)QS * rp.recv_cnt[p], dtype, rp.peers[p], s->comm,
+                      s->comm_stream));
   }
   NCCL_TRY(N.GroupEnd());
   CUDA_TRY(cudaEventRecord(s->ev_halo, s->comm_stream));
@@ -423,59 +445,63 @@ void allreduce_dt(hgks_solver* s) {
                             s->stream));
 }
 
-void bc_ghosts(hgks_solver* s, double* Q, int part) {
+template <class L>
+void bc_ghosts(hgks_solver* s, void* Q, int part) {
   const RankPlan& rp = *s->rp;
   if (rp.n_bghost == 0) return;
   const int first = (int)(rp.n_owned + rp.n_pghost);
   launch(s, "k_bc_ghosts", [&] {
-    k_bc_ghosts<<<blocks(rp.n_bghost, 128), 128, 0, s->stream>>>(Q, first, (int)rp.n_bghost, s->d.bg_cell,
-                                                                  s->d.bg_bc, s->d.bg_normal, s->gp,
-                                                                  (int)rp.n_owned, part);
+    L::bc_ghosts(blocks(rp.n_bghost, 128), s->stream, as<L>(Q), first, (int)rp.n_bghost, s->d.bg_cell, s->d.bg_bc,
+                 as<L>(s->d.bg_normal), make_gas_for<L>(s->gp), (int)rp.n_owned, part);
   });
 }
 
 // work of one stage that needs no partition-ghost data (overlaps the exchange)
+template <class L>
 void stage_early(hgks_solver* s, int st) {
-  bc_ghosts(s, s->d.Q, 0);
-  run_recon(s, s->d.Q, 0);
-  run_flux(s, s->d.Q, st, 0);
+  bc_ghosts<L>(s, s->d.Q, 0);
+  run_recon<L>(s, s->d.Q, 0);
+  run_flux<L>(s, s->d.Q, st, 0);
 }
 
 // the rest of the stage, after the ghosts are current
+template <class L>
 void stage_late(hgks_solver* s, int st) {
-  bc_ghosts(s, s->d.Q, 1);
-  run_recon(s, s->d.Q, 1);
-  run_flux(s, s->d.Q, st, 1);
-  UpdateArgs u = update_args(s);
+  bc_ghosts<L>(s, s->d.Q, 1);
+  run_recon<L>(s, s->d.Q, 1);
+  run_flux<L>(s, s->d.Q, st, 1);
+  const typename L::UpdateArgsT u = update_args<L>(s);
   const int n = (int)s->rp->n_owned;
   const int nf = s->lay.nfaces;
   if (st == 1) {
-    if (nf == 4) launch(s, "k_update1", [&] { k_update1<4><<<blocks(n, 256), 256, 0, s->stream>>>(u); });
-    else launch(s, "k_update1", [&] { k_update1<6><<<blocks(n, 256), 256, 0, s->stream>>>(u); });
+    if (nf == 4) launch(s, "k_update1", [&] { L::template update1<4>(blocks(n, 256), s->stream, u); });
+    else launch(s, "k_update1", [&] { L::template update1<6>(blocks(n, 256), s->stream, u); });
   } else {
-    if (nf == 4) launch(s, "k_update2", [&] { k_update2<4><<<blocks(n, 256), 256, 0, s->stream>>>(u); });
-    else launch(s, "k_update2", [&] { k_update2<6><<<blocks(n, 256), 256, 0, s->stream>>>(u); });
+    if (nf == 4) launch(s, "k_update2", [&] { L::template update2<4>(blocks(n, 256), s->stream, u); });
+    else launch(s, "k_update2", [&] { L::template update2<6>(blocks(n, 256), s->stream, u); });
   }
 }
 
+template <class L>
 void stage(hgks_solver* s, int st) {
-  exchange(s, s->d.Q);  // NCCL on the comm stream
-  stage_early(s, st);
+  exchange<L>(s, s->d.Q);  // NCCL on the comm stream
+  stage_early<L>(s, st);
   wait_halo(s);
-  stage_late(s, st);
+  stage_late<L>(s, st);
   if (st == 2) allreduce_dt(s);
 }
 
+template <class L>
 void init_dt(hgks_solver* s) {
   const int n = (int)s->rp->n_owned;
-  launch(s, "k_dt_init", [&] {
-    k_dt_init<<<blocks(n, 256), 256, 0, s->stream>>>(s->d.Q, s->d.h_dt, n, s->d.ctrl, s->gp);
-  });
+  launch(s, "k_dt_init",
+         [&] { L::dt_init(blocks(n, 256), s->stream, as<L>(s->d.Q), as<L>(s->d.h_dt), n, s->d.ctrl, s->gp); });
   allreduce_dt(s);
 }
 
 // asynchronous on the stream: H2D of the caller's rows, scatter into the local
-// SoA layout, reset time, recompute the CFL bound
+// rows, reset time, recompute the CFL bound
+template <class L>
 void upload_state(hgks_solver* s, const double* h_Q, double t) {
   const RankPlan& rp = *s->rp;
   const int n = (int)rp.n_owned;
@@ -490,10 +516,14 @@ void upload_state(hgks_solver* s, const double* h_Q, double t) {
     CUDA_TRY(cudaMemcpyAsync(s->d.stage_in, hs, sizeof(double) * 5 * n, cudaMemcpyHostToDevice, s->stream));
   }
   launch(s, "k_scatter_state",
-         [&] { k_scatter_state<<<blocks(n, 256), 256, 0, s->stream>>>(s->d.stage_in, s->d.in_row, n, s->d.Q); });
+         [&] { L::scatter(blocks(n, 256), s->stream, s->d.stage_in, s->d.in_row, n, as<L>(s->d.Q)); });
   launch(s, "k_reset_ctrl", [&] { k_reset_ctrl<<<1, 1, 0, s->stream>>>(s->d.ctrl, t); });
-  init_dt(s);
+  init_dt<L>(s);
 }
+
+// precision dispatch of the hot path
+#define HGKS_DISPATCH(s, fn, ...) \
+  ((s)->fp32 ? fn<p32::Launch>(__VA_ARGS__) : fn<p64::Launch>(__VA_ARGS__))
 
 }  // namespace
 
@@ -553,7 +583,8 @@ hgks_status hgks_workspace_size(const hgks_mesh* mc, const hgks_config* cfg, int
     const RankPlan& rp = m->plan(rank);
     Carve c{nullptr, 0, 0};
     DevArrays d;
-    *bytes = layout(m->gm, rp, c, d);
+    const bool fp32 = cfg && cfg->precision == 32;
+    *bytes = layout(m->gm, rp, fp32 ? sizeof(float) : sizeof(double), c, d);
   });
 }
 
@@ -591,28 +622,38 @@ hgks_status hgks_init(const hgks_mesh* mc, const hgks_config* cfg, const hgks_di
     g.t_inf = cfg->t_inf;
     g.mu_exp = cfg->mu_exp;
     for (int k = 0; k < 5; ++k) g.fs[k] = cfg->freestream[k];
+    if (cfg->precision != 64 && cfg->precision != 32) throw Error(HGKS_E_ARG, "precision must be 64 or 32");
+    s->fp32 = cfg->precision == 32;
+    s->rs = s->fp32 ? sizeof(float) : sizeof(double);
     s->nq = (size_t)QS * round32(rp.n_local());
     Carve c{(char*)d_ws, 0, ws_bytes};
     if ((reinterpret_cast<uintptr_t>(d_ws) & 255) != 0) throw Error(HGKS_E_ARG, "workspace must be 256-byte aligned");
-    layout(m->gm, rp, c, s->d);
+    layout(m->gm, rp, s->rs, c, s->d);
     cudaStream_t st = s->stream;
     auto up = [&](void* dst, const void* src, size_t bytes) {
       if (bytes) CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+    };
+    // working-precision arrays: converted on the host for fp32 (kept alive until the sync below)
+    std::vector<std::vector<float>> keep;
+    auto upr = [&](void* dst, const std::vector<double>& v) {
+      if (!s->fp32) return up(dst, v.data(), v.size() * sizeof(double));
+      keep.emplace_back(v.begin(), v.end());
+      up(dst, keep.back().data(), v.size() * sizeof(float));
     };
     up(s->d.recon_cell, rp.recon_cell.data(), rp.recon_cell.size() * sizeof(int));
     up(s->d.st_id, rp.st_id_tiled.data(), rp.st_id_tiled.size() * sizeof(int));
 
     up(s->d.sub_slot, rp.sub_slot.data(), rp.sub_slot.size());
-    up(s->d.op, rp.op.data(), rp.op.size() * sizeof(double));
-    up(s->d.geo, rp.geo.data(), rp.geo.size() * sizeof(double));
+    upr(s->d.op, rp.op);
+    upr(s->d.geo, rp.geo);
     up(s->d.f_cells, rp.f_cells.data(), rp.f_cells.size() * sizeof(int));
-    up(s->d.f_geo, rp.f_geo.data(), rp.f_geo.size() * sizeof(double));
+    upr(s->d.f_geo, rp.f_geo);
     up(s->d.cf, rp.cf.data(), rp.cf.size() * sizeof(int));
-    up(s->d.inv_v, rp.inv_v.data(), rp.inv_v.size() * sizeof(double));
-    up(s->d.h_dt, rp.h_dt.data(), rp.h_dt.size() * sizeof(double));
+    upr(s->d.inv_v, rp.inv_v);
+    upr(s->d.h_dt, rp.h_dt);
     up(s->d.bg_cell, rp.bg_cell.data(), rp.bg_cell.size() * sizeof(int));
     up(s->d.bg_bc, rp.bg_bc.data(), rp.bg_bc.size() * sizeof(int));
-    up(s->d.bg_normal, rp.bg_normal.data(), rp.bg_normal.size() * sizeof(double));
+    upr(s->d.bg_normal, rp.bg_normal);
     up(s->d.send_list, rp.send_list.data(), rp.send_list.size() * sizeof(int));
     // state maps: in_row[i] = row of owned cell i in the caller's array (single
     // rank) or its position in the gathered staging array; out_local[k] = local
@@ -624,7 +665,7 @@ hgks_status hgks_init(const hgks_mesh* mc, const hgks_config* cfg, const hgks_di
     std::sort(out_local.begin(), out_local.end(), [&](int a, int b) { return rp.l2g[a] < rp.l2g[b]; });
     up(s->d.in_row, in_row.data(), in_row.size() * sizeof(int64_t));
     up(s->d.out_local, out_local.data(), out_local.size() * sizeof(int));
-    CUDA_TRY(cudaMemsetAsync(s->d.Q, 0, sizeof(double) * s->nq, st));
+    CUDA_TRY(cudaMemsetAsync(s->d.Q, 0, s->rs * s->nq, st));
     Ctrl h{};
     h.bad_cell = INT_MAX;
     h.dtmin_bits = 0x7fefffffffffffffull;
@@ -641,7 +682,7 @@ hgks_status hgks_init(const hgks_mesh* mc, const hgks_config* cfg, const hgks_di
     }
     if (s->n_ranks > 1) CUDA_TRY(cudaMallocHost(&s->pinned, sizeof(double) * 5 * std::max<int64_t>(1, rp.n_owned)));
     CUDA_TRY(cudaStreamSynchronize(st));
-    upload_state(s.get(), h_Q0, 0.0);
+    HGKS_DISPATCH(s, upload_state, s.get(), h_Q0, 0.0);
     CUDA_TRY(cudaStreamSynchronize(st));
     *out = s.release();
   });
@@ -677,8 +718,8 @@ hgks_status hgks_step(hgks_solver* s, int32_t n_steps, double t_stop, hgks_step_
     for (int k = 0; k < n_steps; ++k) {
       launch(s, "k_step_begin",
              [&] { k_step_begin<<<1, 1, 0, s->stream>>>(s->d.ctrl, s->cfg.cfl, s->cfg.fixed_dt, t_stop); });
-      stage(s, 1);
-      stage(s, 2);
+      HGKS_DISPATCH(s, stage, s, 1);
+      HGKS_DISPATCH(s, stage, s, 2);
     }
     if (info) {
       Ctrl h;
@@ -700,7 +741,7 @@ hgks_status hgks_step(hgks_solver* s, int32_t n_steps, double t_stop, hgks_step_
 hgks_status hgks_set_state(hgks_solver* s, const double* h_Q, double t) {
   return guard([&] {
     if (!s || !h_Q) throw Error(HGKS_E_ARG, "null argument");
-    upload_state(s, h_Q, t);
+    HGKS_DISPATCH(s, upload_state, s, h_Q, t);
   });
 }
 
@@ -710,7 +751,10 @@ hgks_status hgks_get_state(const hgks_solver* sc, double* h_Q, int64_t* h_gid, d
     if (!s || !h_Q) throw Error(HGKS_E_ARG, "null argument");
     const int n = (int)s->rp->n_owned;
     launch(s, "k_gather_state", [&] {
-      k_gather_state<<<blocks(n, 256), 256, 0, s->stream>>>(s->d.Q, s->d.out_local, n, s->d.stage_out);
+      if (s->fp32)
+        p32::Launch::gather(blocks(n, 256), s->stream, (const float*)s->d.Q, s->d.out_local, n, s->d.stage_out);
+      else
+        p64::Launch::gather(blocks(n, 256), s->stream, (const double*)s->d.Q, s->d.out_local, n, s->d.stage_out);
     });
     CUDA_TRY(cudaMemcpyAsync(h_Q, s->d.stage_out, sizeof(double) * 5 * n, cudaMemcpyDeviceToHost, s->stream));
     Ctrl h;
@@ -731,27 +775,34 @@ hgks_status hgks_debug_residual(hgks_solver* s, const double* h_Q, double dt, do
     if (s->n_ranks != 1) throw Error(HGKS_E_ARG, "hgks_debug_residual is single-rank only");
     const int n = (int)s->rp->n_owned;
     // save state, load h_Q, run stage-1 reconstruction + flux, restore
-    CUDA_TRY(cudaMemcpyAsync(s->d.Qtmp, s->d.Q, sizeof(double) * s->nq, cudaMemcpyDeviceToDevice, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(s->d.Qtmp, s->d.Q, s->rs * s->nq, cudaMemcpyDeviceToDevice, s->stream));
     Ctrl saved;
     CUDA_TRY(cudaMemcpyAsync(&saved, s->d.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s->stream));
     CUDA_TRY(cudaStreamSynchronize(s->stream));
     CUDA_TRY(cudaMemcpyAsync(s->d.stage_in, h_Q, sizeof(double) * 5 * s->mesh->gm.nc, cudaMemcpyHostToDevice,
                              s->stream));
-    launch(s, "k_scatter_state",
-           [&] { k_scatter_state<<<blocks(n, 256), 256, 0, s->stream>>>(s->d.stage_in, s->d.in_row, n, s->d.Q); });
+    launch(s, "k_scatter_state", [&] {
+      if (s->fp32) p32::Launch::scatter(blocks(n, 256), s->stream, s->d.stage_in, s->d.in_row, n, (float*)s->d.Q);
+      else p64::Launch::scatter(blocks(n, 256), s->stream, s->d.stage_in, s->d.in_row, n, (double*)s->d.Q);
+    });
     Ctrl h = saved;
     h.dt = dt;
     CUDA_TRY(cudaMemcpyAsync(s->d.ctrl, &h, sizeof(Ctrl), cudaMemcpyHostToDevice, s->stream));
-    bc_ghosts(s, s->d.Q, 2);
-    run_recon(s, s->d.Q, 2);
-    run_flux(s, s->d.Q, 1, 2);
+    HGKS_DISPATCH(s, bc_ghosts, s, s->d.Q, 2);
+    HGKS_DISPATCH(s, run_recon, s, s->d.Q, 2);
+    HGKS_DISPATCH(s, run_flux, s, s->d.Q, 1, 2);
     // L = (Q* - Q) ... computed directly on host from face fluxes for clarity
     std::vector<double> F1((size_t)10 * s->rp->n_faces);
     std::vector<int> cf(s->rp->cf);
-    CUDA_TRY(cudaMemcpyAsync(F1.data(), s->d.F1, F1.size() * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
-    CUDA_TRY(cudaMemcpyAsync(s->d.Q, s->d.Qtmp, sizeof(double) * s->nq, cudaMemcpyDeviceToDevice, s->stream));
+    std::vector<float> F1f(s->fp32 ? F1.size() : 0);
+    if (s->fp32)
+      CUDA_TRY(cudaMemcpyAsync(F1f.data(), s->d.F1, F1f.size() * sizeof(float), cudaMemcpyDeviceToHost, s->stream));
+    else
+      CUDA_TRY(cudaMemcpyAsync(F1.data(), s->d.F1, F1.size() * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(s->d.Q, s->d.Qtmp, s->rs * s->nq, cudaMemcpyDeviceToDevice, s->stream));
     CUDA_TRY(cudaMemcpyAsync(s->d.ctrl, &saved, sizeof(Ctrl), cudaMemcpyHostToDevice, s->stream));
     CUDA_TRY(cudaStreamSynchronize(s->stream));
+    if (s->fp32) std::copy(F1f.begin(), F1f.end(), F1.begin());
     const int NF = s->lay.nfaces;
     for (int i = 0; i < n; ++i) {
       double L[5] = {0, 0, 0, 0, 0}, dL[5] = {0, 0, 0, 0, 0};
@@ -824,7 +875,7 @@ hgks_status hgks_group_step(hgks_solver* const* ss, int32_t n, int32_t n_steps, 
     for (int k = 0; k < n; ++k) {
       if (!ss[k] || ss[k]->transport != HGKS_TRANSPORT_LOOPBACK || ss[k]->n_ranks != n || ss[k]->rank != k)
         throw Error(HGKS_E_ARG, "hgks_group_step needs the loopback solvers of ranks 0..n-1 in order");
-      if (ss[k]->stream != ss[0]->stream || ss[k]->device != ss[0]->device)
+      if (ss[k]->stream != ss[0]->stream || ss[k]->device != ss[0]->device || ss[k]->fp32 != ss[0]->fp32)
         throw Error(HGKS_E_ARG, "loopback solvers must share one device and stream");
     }
     hgks_solver* s0 = ss[0];
@@ -843,8 +894,10 @@ hgks_status hgks_group_step(hgks_solver* const* ss, int32_t n, int32_t n_steps, 
           size_t ip = std::find(rpp.peers.begin(), rpp.peers.end(), q) - rpp.peers.begin();
           if (ip == rpp.peers.size() || rpp.send_cnt[ip] != rq.recv_cnt[iq])
             throw Error(HGKS_E_STATE, "inconsistent exchange plans between ranks");
-          CUDA_TRY(cudaMemcpyAsync(ss[q]->d.Q + (size_t)QS * rq.recv_off[iq], sp->d.sendbuf + (size_t)QS * rpp.send_off[ip],
-                                   sizeof(double) * QS * rq.recv_cnt[iq], cudaMemcpyDeviceToDevice, s0->stream));
+          const size_t rs = s0->rs;
+          CUDA_TRY(cudaMemcpyAsync((char*)ss[q]->d.Q + rs * QS * rq.recv_off[iq],
+                                   (const char*)sp->d.sendbuf + rs * QS * rpp.send_off[ip], rs * QS * rq.recv_cnt[iq],
+                                   cudaMemcpyDeviceToDevice, s0->stream));
         }
       }
     };
@@ -855,10 +908,10 @@ hgks_status hgks_group_step(hgks_solver* const* ss, int32_t n, int32_t n_steps, 
           k_step_begin<<<1, 1, 0, s0->stream>>>(ss[k]->d.ctrl, ss[k]->cfg.cfl, ss[k]->cfg.fixed_dt, t_stop);
         });
       for (int st = 1; st <= 2; ++st) {
-        for (int k = 0; k < n; ++k) pack(ss[k], ss[k]->d.Q);
-        for (int k = 0; k < n; ++k) stage_early(ss[k], st);
+        for (int k = 0; k < n; ++k) HGKS_DISPATCH(ss[k], pack, ss[k], ss[k]->d.Q);
+        for (int k = 0; k < n; ++k) HGKS_DISPATCH(ss[k], stage_early, ss[k], st);
         loop_exchange();
-        for (int k = 0; k < n; ++k) stage_late(ss[k], st);
+        for (int k = 0; k < n; ++k) HGKS_DISPATCH(ss[k], stage_late, ss[k], st);
       }
       group_min();
     }

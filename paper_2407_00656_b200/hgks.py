@@ -42,7 +42,8 @@ class MeshDesc(C.Structure):
 class Config(C.Structure):
     _fields_ = [("gamma", C.c_double), ("cfl", C.c_double), ("fixed_dt", C.c_double), ("tau_mode", C.c_int32),
                 ("c1", C.c_double), ("mu_inf", C.c_double), ("t_inf", C.c_double), ("mu_exp", C.c_double),
-                ("eps", C.c_double), ("omega_pow", C.c_int32), ("freestream", C.c_double * 5)]
+                ("eps", C.c_double), ("omega_pow", C.c_int32), ("freestream", C.c_double * 5),
+                ("precision", C.c_int32)]
 
 
 class Dist(C.Structure):
@@ -130,13 +131,19 @@ class SolverConfig:
     mu_inf: float = 0.0
     t_inf: float = 1.0
     mu_exp: float = 0.7
-    eps: float = 1e-10
+    eps: float | None = None  # WENO epsilon; None: 1e-10 (fp64) / 1e-6 (fp32), reading R27
     omega_pow: int = 1
     freestream: tuple = (1.0, 0.0, 0.0, 0.0, 1.0 / 1.4)
+    precision: int = 64  # 64: fp64 parity path; 32: FP32 variant
+
+    def eps_value(self) -> float:
+        if self.eps is not None:
+            return self.eps
+        return 1e-10 if self.precision == 64 else 1e-6
 
     def c(self) -> Config:
         return Config(self.gamma, self.cfl, self.fixed_dt, self.tau_mode, self.c1, self.mu_inf, self.t_inf,
-                      self.mu_exp, self.eps, self.omega_pow, (C.c_double * 5)(*self.freestream))
+                      self.mu_exp, self.eps_value(), self.omega_pow, (C.c_double * 5)(*self.freestream), self.precision)
 
 
 def nccl_unique_id() -> bytes:

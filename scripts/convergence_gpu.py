@@ -12,13 +12,15 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--N", type=int, nargs="+", default=[10, 20, 40])
 ap.add_argument("--omega-pow", type=int, default=1)
 ap.add_argument("--cfl", type=float, default=0.3)
-ap.add_argument("--eps", type=float, default=1e-10)
+ap.add_argument("--eps", type=float, default=None)
+ap.add_argument("--precision", type=int, default=64, choices=[64, 32])
 args = ap.parse_args()
 prev = None
 for N in args.N:
     mi = W.kuhn_box(N)
     Q0 = W.advection_ic(mi)
-    s = hgks.Solver(hgks.Mesh(mi), Q0, hgks.SolverConfig(cfl=args.cfl, omega_pow=args.omega_pow, eps=args.eps))
+    s = hgks.Solver(hgks.Mesh(mi), Q0, hgks.SolverConfig(cfl=args.cfl, omega_pow=args.omega_pow, eps=args.eps,
+                                                            precision=args.precision))
     t0 = time.time()
     steps = 0
     while True:
@@ -34,6 +36,6 @@ for N in args.N:
     order = np.log2(prev / L1) if prev else None
     print(json.dumps(dict(N=N, steps=steps, t=t, L1=L1, L2=L2, order=order, paper_L1=T3.get(N),
                           ratio=L1 / T3[N] if N in T3 else None, fallbacks=info["fallbacks"],
-                          omega_pow=args.omega_pow, cfl=args.cfl, secs=time.time() - t0)), flush=True)
+                          omega_pow=args.omega_pow, cfl=args.cfl, precision=args.precision, secs=time.time() - t0)), flush=True)
     prev = L1
     s.close()
