@@ -131,18 +131,32 @@ struct ReconArgs {
 // sub-stencils re-read them from shared memory.  The LSQ operators (1584 B per
 // tet cell, most of the kernel's HBM bytes) stream entry-major: each warp load
 // is 256 contiguous bytes.
-template <int K, int M, int NM>
 #ifndef HGKS_RECON_MINB
 #define HGKS_RECON_MINB 2
 #endif
-__global__ void __launch_bounds__(kTile, HGKS_RECON_MINB) k_recon(ReconArgs a) {
-  constexpr int QP = 5 * kTile;                      // doubles per member plane: [v][thread]
+// Block shape: a 128-cell tile per block, or half a tile per 64-thread block when
+// the member planes would not leave room for two blocks per SM (fp64 hex, K >= 20:
+// 123 KB), so three blocks (6 warps) fit instead of one.
+template <int K>
+struct ReconShape {
+  static constexpr int BT = (size_t)K * 5 * kTile * sizeof(Real) > 100 * 1024 ? 64 : 128;
+  static constexpr int SPLIT = kTile / BT;
+  static constexpr int MINB = BT == 64 ? 3 : HGKS_RECON_MINB;
+  static constexpr size_t SMEM = (size_t)K * 5 * BT * sizeof(Real);
+};
+
+template <int K, int M, int NM>
+__global__ void __launch_bounds__(ReconShape<K>::BT, ReconShape<K>::MINB) k_recon(ReconArgs a) {
+  constexpr int BT = ReconShape<K>::BT, SPLIT = ReconShape<K>::SPLIT;
+  constexpr int QP = 5 * BT;                         // values per member plane: [v][thread]
   constexpr int E = 9 * K + 3 * M * NM;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Real* smem = reinterpret_cast<Real*>(smem_raw);
-  Real* __restrict__ dqs = smem;                   // [K][5][kTile] Q_k - Q_i
-  const int t = threadIdx.x;
-  const int tile = a.tile0 + blockIdx.x;
+  Real* __restrict__ dqs = smem;                   // [K][5][BT] Q_k - Q_i
+  const int tl = threadIdx.x;
+  const int half = SPLIT == 1 ? 0 : (int)(blockIdx.x % SPLIT);
+  const int t = half * BT + tl;                      // position in the 128-cell tile
+  const int tile = a.tile0 + (int)(blockIdx.x / SPLIT);
   const int r = tile * kTile + t;
   int ci = r < a.n_recon ? __ldg(a.recon_cell + r) : -1;  // -1: padding
   const bool active = ci >= 0;
@@ -161,7 +175,7 @@ __global__ void __launch_bounds__(kTile, HGKS_RECON_MINB) k_recon(ReconArgs a) {
   // fire TMA bulk prefetches of it into L2 now, so the streamed operator loads
   // below see L2 rather than DRAM latency (the warps cannot keep enough loads
   // in flight at 255 registers).
-  if (t < 8) {
+  if (t < 8) {  // first block of the tile
     constexpr uint32_t bytes = (uint32_t)E * kTile * sizeof(Real);
     constexpr uint32_t chunk = ((bytes / 8) + 15) / 16 * 16;
     const uint32_t off = t * chunk;
@@ -186,15 +200,14 @@ __global__ void __launch_bounds__(kTile, HGKS_RECON_MINB) k_recon(ReconArgs a) {
     }
 #pragma unroll
     for (int k = k0; k < k0 + G && k < K; ++k) {
-      Real* d = dqs + k * QP + t;
-      d[0 * kTile] = x[k - k0][0].x - qi[0];
-      d[1 * kTile] = x[k - k0][0].y - qi[1];
-      d[2 * kTile] = x[k - k0][1].x - qi[2];
-      d[3 * kTile] = x[k - k0][1].y - qi[3];
-      d[4 * kTile] = x[k - k0][2].x - qi[4];
+      Real* d = dqs + k * QP + tl;
+      d[0 * BT] = x[k - k0][0].x - qi[0];
+      d[1 * BT] = x[k - k0][0].y - qi[1];
+      d[2 * BT] = x[k - k0][1].x - qi[2];
+      d[3 * BT] = x[k - k0][1].y - qi[3];
+      d[4 * BT] = x[k - k0][2].x - qi[4];
     }
   }
-  const Real* __restrict__ op = a.op + tb * E + t;
   const Real* __restrict__ geo = a.geo + tb * 8 + t;
   const uint8_t* __restrict__ ssl = a.sub_slot + tb * (M * NM) + t;
   const Real V23 = __ldg(geo), V43 = __ldg(geo + kTile);
@@ -207,16 +220,25 @@ __global__ void __launch_bounds__(kTile, HGKS_RECON_MINB) k_recon(ReconArgs a) {
   for (int d = 0; d < 9; ++d)
 #pragma unroll
     for (int v = 0; v < 5; ++v) c[d][v] = Real(0.0);
-#pragma unroll 2
-  for (int k = 0; k < K; ++k) {
-    Real dq[5];
+  // operators are tiled by entry pairs: pair p of this cell at op2[p * kTile]
+  const R2* __restrict__ op2 = reinterpret_cast<const R2*>(a.op + tb * E) + t;
+  static_assert(K % 2 == 0 && (3 * M * NM) % 2 == 0, "operator pairs");
+#pragma unroll 1
+  for (int k2 = 0; k2 < K; k2 += 2) {  // two members = 18 entries = 9 pairs
+    Real dq[2][5];
 #pragma unroll
-    for (int v = 0; v < 5; ++v) dq[v] = dqs[k * QP + v * kTile + t];
+    for (int h = 0; h < 2; ++h)
 #pragma unroll
-    for (int d = 0; d < 9; ++d) {
-      const Real w = __ldcs(op + (k * 9 + d) * kTile);
+      for (int v = 0; v < 5; ++v) dq[h][v] = dqs[(k2 + h) * QP + v * BT + tl];
+    R2 w2[9];
 #pragma unroll
-      for (int v = 0; v < 5; ++v) c[d][v] = fma(w, dq[v], c[d][v]);
+    for (int p = 0; p < 9; ++p) w2[p] = __ldcs(op2 + (k2 * 9 / 2 + p) * kTile);
+#pragma unroll
+    for (int j = 0; j < 18; ++j) {
+      const Real w = (j & 1) ? w2[j >> 1].y : w2[j >> 1].x;
+      const int h = j / 9, d = j % 9;
+#pragma unroll
+      for (int v = 0; v < 5; ++v) c[d][v] = fma(w, dq[h][v], c[d][v]);
     }
   }
   // smoothness indicator of P_0 (closed form SURVEY A.5)
@@ -234,7 +256,7 @@ __global__ void __launch_bounds__(kTile, HGKS_RECON_MINB) k_recon(ReconArgs a) {
                       c[7][v] * c[7][v] + c[8][v] * c[8][v];
     beta0[v] = V23 * s1 + V43 * s2;
   }
-  const Real* __restrict__ opm = op + (9 * K) * kTile;
+  const R2* __restrict__ opm2 = op2 + (9 * K / 2) * kTile;
   auto sub_slopes = [&](int m, Real b[3][5]) {  // P_m over sub-stencil m
 #pragma unroll
     for (int d = 0; d < 3; ++d)
@@ -245,10 +267,12 @@ __global__ void __launch_bounds__(kTile, HGKS_RECON_MINB) k_recon(ReconArgs a) {
       const int sl = __ldg(ssl + (m * NM + j) * kTile);
       Real dq[5];
 #pragma unroll
-      for (int v = 0; v < 5; ++v) dq[v] = dqs[sl * QP + v * kTile + t];
+      for (int v = 0; v < 5; ++v) dq[v] = dqs[sl * QP + v * BT + tl];
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
-        const Real w = __ldg(opm + ((m * NM + j) * 3 + d) * kTile);
+        const int e = (m * NM + j) * 3 + d;
+        const R2 wp = __ldg(opm2 + (e >> 1) * kTile);
+        const Real w = (e & 1) ? wp.y : wp.x;
 #pragma unroll
         for (int v = 0; v < 5; ++v) b[d][v] = fma(w, dq[v], b[d][v]);
       }
@@ -1095,12 +1119,14 @@ struct Launch {
   using GasT = GasR;
   static GasR gas(const GasParams& g) { return make_gas(g); }
   template <int K, int M, int NM>
-  static cudaError_t recon_smem(int bytes) {
-    return cudaFuncSetAttribute(k_recon<K, M, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  static cudaError_t recon_smem() {
+    return cudaFuncSetAttribute(k_recon<K, M, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)ReconShape<K>::SMEM);
   }
   template <int K, int M, int NM>
-  static void recon(int grid, size_t smem, cudaStream_t st, const ReconArgs& a) {
-    k_recon<K, M, NM><<<grid, kTile, smem, st>>>(a);
+  static void recon(int n_tiles, cudaStream_t st, const ReconArgs& a) {
+    using S = ReconShape<K>;
+    k_recon<K, M, NM><<<n_tiles * S::SPLIT, S::BT, S::SMEM, st>>>(a);
   }
   template <int NV, int STAGE, bool TAU0, int BC>
   static void flux(int grid, cudaStream_t st, const FluxArgs& a) {

@@ -803,6 +803,11 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
   // tiled entry-major layout: entry e of cell r at ((r/128)*NE + e)*128 + r%128, so one
   // 128-cell block reads its operators from one contiguous range (DRAM page locality)
   auto ti = [](int64_t r, int ne, int e) { return (size_t)(((r >> 7) * ne + e) << 7) + (size_t)(r & 127); };
+  // operators: tiled by entry PAIRS, so one 16-byte load gives a cell two consecutive
+  // entries (a warp load = 512 contiguous bytes); E is even (K even, 3*M*NM even)
+  auto tp = [](int64_t r, int ne, int e) {
+    return (((size_t)((r >> 7) * (ne / 2) + (e >> 1)) << 7 | (size_t)(r & 127)) << 1) | (size_t)(e & 1);
+  };
   rp.st_id_tiled.assign((size_t)K * R, 0);
   rp.stencil_min = 1 << 30;
   rp.stencil_max = 0;
@@ -827,10 +832,10 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
     // (row k*9 + d), then the sub-stencil operators (row 9K + (m*NM + j)*3 + d)
     const double* op = &gm.op[(size_t)gi * E];
     for (int d = 0; d < 9; ++d)
-      for (int k = 0; k < K; ++k) rp.op[ti(r, E, k * 9 + d)] = op[d * K + k];
+      for (int k = 0; k < K; ++k) rp.op[tp(r, E, k * 9 + d)] = op[d * K + k];
     for (int m = 0; m < M; ++m)
       for (int d = 0; d < 3; ++d)
-        for (int j = 0; j < NM; ++j) rp.op[ti(r, E, 9 * K + (m * NM + j) * 3 + d)] = op[9 * K + (m * 3 + d) * NM + j];
+        for (int j = 0; j < NM; ++j) rp.op[tp(r, E, 9 * K + (m * NM + j) * 3 + d)] = op[9 * K + (m * 3 + d) * NM + j];
     double V = gm.V[gi];
     rp.geo[ti(r, 8, 0)] = std::pow(V, 2.0 / 3.0);
     rp.geo[ti(r, 8, 1)] = std::pow(V, 4.0 / 3.0);

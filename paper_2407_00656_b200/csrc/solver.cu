@@ -277,14 +277,13 @@ typename L::RealT* as(T* p) {
 
 template <class L, int K, int M, int NM>
 void run_recon_k(hgks_solver* s, const typename L::ReconArgsT& a) {
-  const size_t smem = sizeof(typename L::RealT) * (size_t)K * 5 * kTile;
-  if (smem > s->recon_smem_set) {
-    CUDA_TRY((L::template recon_smem<K, M, NM>((int)smem)));
-    s->recon_smem_set = smem;
+  if (!s->recon_smem_set) {  // one reconstruction instantiation per solver (K, M, NM, precision fixed)
+    CUDA_TRY((L::template recon_smem<K, M, NM>()));
+    s->recon_smem_set = 1;
   }
   const int n_tiles = s->recon_t1 - a.tile0;
   if (n_tiles <= 0) return;
-  launch(s, "k_recon", [&] { L::template recon<K, M, NM>(n_tiles, smem, s->stream, a); });
+  launch(s, "k_recon", [&] { L::template recon<K, M, NM>(n_tiles, s->stream, a); });
 }
 
 // part 0: tiles of the early cells, 1: the rest, 2: all
