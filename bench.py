@@ -48,14 +48,16 @@ def box_dims(n_gpus: int):
     return [d * N_BLOCK for d in dims]
 
 
-def peaks():
+def peaks(precision=64):
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     hbm = None
     if os.path.exists(path):
         hbm = json.load(open(path)).get("hbm_gbs")
     src = "MEASURED_PEAKS.json" if hbm else "fallback B200_PROFILING.md"
-    fp64 = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
-    return (hbm or 6650.0), src, fp64["fp64_tflops"], "profiles/fp64_peak.json (DFMA microbenchmark on this pool)"
+    pk = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
+    key = "fp64_tflops" if precision == 64 else "fp32_tflops"
+    kind = "DFMA" if precision == 64 else "FFMA"
+    return (hbm or 6650.0), src, pk[key], f"profiles/fp64_peak.json {key} ({kind}-chain microbenchmark on this pool)"
 
 
 class ClockSampler:
@@ -282,7 +284,7 @@ def main():
     d2h = n_owned * 5 * 8
 
     # ---------------- roofline of the dominant kernel ----------------
-    hbm_peak, hbm_src, fp64_peak, fp64_src = peaks()
+    hbm_peak, hbm_src, alu_peak, alu_src = peaks(args.precision)
     top = max(ktimes.items(), key=lambda kv: kv[1]["ms"])
     name, kt = top
     avg_ms = kt["ms"] / max(1, kt["launches"])
@@ -298,20 +300,23 @@ def main():
                 "peak_source": hbm_src + " (burst copy)"}
     else:
         flops = json.load(open(os.path.join(ROOT, "profiles", "flops_per_unit.json")))
-        fpf = flops.get(args.workload, {}).get(name, {}).get("fp64_flops_per_face") if args.precision == 64 else None
+        fpf = flops.get(args.workload, {}).get(name, {}).get(f"fp{args.precision}_flops_per_face")
         nf = info["n_faces"] - info["n_faces_bc"]  # interior faces (the counts are per interior face)
         if fpf:
             achieved = fpf * nf / (avg_ms * 1e-3) / 1e12
-            roof = {"kernel": name, "bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-                    "frac": achieved / fp64_peak, "traffic": None, "avg_launch_ms": avg_ms,
-                    "flops_per_face": fpf, "flops_source": "ncu sass op counts (2 dfma + dadd + dmul), "
-                                                          "profiles/flops_per_unit.json", "peak_source": fp64_src}
+            roof = {"kernel": name, "bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",
+                    "frac": achieved / alu_peak, "traffic": None, "avg_launch_ms": avg_ms,
+                    "flops_per_face": fpf, "flops_source": "ncu sass op counts (2 fma + add + mul), "
+                                                          "profiles/flops_per_unit.json", "peak_source": alu_src}
     traffic_path = os.path.join(ROOT, "profiles", "traffic.json")
     if roof and os.path.exists(traffic_path):
         tr = (json.load(open(traffic_path)).get(roof["kernel"])
               if args.workload == "c2" and args.precision == 64 else None)
-        if tr and roof["kernel"].startswith("k_recon"):
-            roof["traffic"] = tr["dram_bytes_per_launch"] * (n_recon / tr["cells"] if "cells" in tr else 1.0)
+        if tr:
+            # ncu DRAM bytes of one launch on the 48^3 box, scaled to this rank's cells
+            units = info["n_owned"] + (info["ghost_layer"][0] if roof["kernel"].startswith("k_recon") else 0)
+            roof["traffic"] = tr["dram_bytes_per_launch"] * (units / tr["cells"])
+            roof["traffic_source"] = "profiles/traffic.json (ncu --set full, one launch)"
 
     # ---------------- CPU baseline (oracle, rank 0, bounded sample) ----------------
     cpu = None

@@ -767,7 +767,10 @@ __device__ __forceinline__ void boundary_right(const Real ql[5], const Real dql[
 }
 
 template <int NV, int STAGE, bool TAU0, int BC>
-__global__ void __launch_bounds__(NV == 3 ? 96 : 128, TAU0 ? (NV == 3 ? 5 : 4) : 1) k_flux(FluxArgs a) {
+#ifndef HGKS_TAU0_MINB3
+#define HGKS_TAU0_MINB3 5
+#endif
+__global__ void __launch_bounds__(NV == 3 ? 96 : 128, TAU0 ? (NV == 3 ? HGKS_TAU0_MINB3 : 4) : 1) k_flux(FluxArgs a) {
   constexpr int NGP = NV == 3 ? 3 : 4;
   constexpr int BLOCK = NV == 3 ? 96 : 128;
   constexpr int NOUT = STAGE == 1 ? 10 : 5;
