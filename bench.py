@@ -28,14 +28,15 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 N_BLOCK = 48            # cubes per axis per GPU block (configs[1] top size)
+N_BLOCK_C5 = 110        # configs[4]: ~8M tets per GPU (110^3 cubes x 6)
 GAMMA = 1.4
 CFL = 0.3
 METRIC = "fp64 cell-updates/sec at 1/2/4/8 B200; % HBM/FP64 roofline"
 UNIT = "cell-updates/s"
 
 
-def box_dims(n_gpus: int):
-    """Weak-scaling box: n_gpus blocks of N_BLOCK^3 cubes (factor 2 per axis, x first)."""
+def box_dims(n_gpus: int, nb: int = N_BLOCK):
+    """Weak-scaling box: n_gpus blocks of nb^3 cubes (factor 2 per axis, x first)."""
     dims = [1, 1, 1]
     k, ax = n_gpus, 0
     while k > 1:
@@ -45,7 +46,7 @@ def box_dims(n_gpus: int):
         dims[ax] *= 2
         k //= 2
         ax = (ax + 1) % 3
-    return [d * N_BLOCK for d in dims]
+    return [d * nb for d in dims]
 
 
 def peaks(precision=64):
@@ -169,9 +170,10 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
-    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4"],
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5"],
                     help="c2: 48^3 Kuhn box per GPU (default, BASELINE configs[1]); c3: subsonic sphere "
-                         "12x35^3 hexes (configs[2]); c4: supersonic sphere 12x70^3 hexes (configs[3])")
+                         "12x35^3 hexes (configs[2]); c4: supersonic sphere 12x70^3 hexes (configs[3]); "
+                         "c5: 110^3 Kuhn box (7,986,000 tets) per GPU (configs[4], weak scaling)")
     ap.add_argument("--precision", type=int, default=64, choices=[64, 32],
                     help="64: the fp64 path BASELINE's metric names (default); 32: the FP32 variant (P:1098-1183)")
     args = ap.parse_args()
@@ -179,11 +181,14 @@ def main():
         run_reference(args)
         return
 
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 and "OMP_NUM_THREADS" not in os.environ:
+        # every rank builds the global mesh on the host (OpenMP): share the cores
+        os.environ["OMP_NUM_THREADS"] = str(max(1, len(os.sched_getaffinity(0)) // world))
     import torch
     import torch.distributed as dist
     from paper_2407_00656_b200 import hgks, workloads as W
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
@@ -192,12 +197,15 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    if args.workload == "c2":
-        nx, ny, nz = box_dims(world)
-        mi = W.kuhn_box(nx, ny, nz, h=2.0 / N_BLOCK)
+    if args.workload in ("c2", "c5"):
+        nb = N_BLOCK if args.workload == "c2" else N_BLOCK_C5
+        nx, ny, nz = box_dims(world, nb)
+        mi = W.kuhn_box(nx, ny, nz, h=2.0 / nb)
         Q0 = W.advection_ic(mi, gamma=GAMMA)
         cfg = hgks.SolverConfig(gamma=GAMMA, cfl=CFL, precision=args.precision)
-        wl = (f"configs[1] top size: {N_BLOCK}^3 Kuhn box per GPU, 6 tets/cube, periodic, tau=0, CFL {CFL}")
+        wl = (f"configs[1] top size: {nb}^3 Kuhn box per GPU, 6 tets/cube, periodic, tau=0, CFL {CFL}"
+              if args.workload == "c2" else
+              f"configs[4]: {nb}^3 Kuhn box ({6 * nb ** 3} tets) per GPU, periodic, tau=0, CFL {CFL}")
         scaling, layout = "weak", (14, 4, 6)
         extra = {"box_cubes": [nx, ny, nz]}
     else:
@@ -300,7 +308,8 @@ def main():
                 "peak_source": hbm_src + " (burst copy)"}
     else:
         flops = json.load(open(os.path.join(ROOT, "profiles", "flops_per_unit.json")))
-        fpf = flops.get(args.workload, {}).get(name, {}).get(f"fp{args.precision}_flops_per_face")
+        fkey = "c2" if args.workload == "c5" else args.workload  # same tet kernels and per-face work
+        fpf = flops.get(fkey, {}).get(name, {}).get(f"fp{args.precision}_flops_per_face")
         nf = info["n_faces"] - info["n_faces_bc"]  # interior faces (the counts are per interior face)
         if fpf:
             achieved = fpf * nf / (avg_ms * 1e-3) / 1e12
@@ -311,7 +320,7 @@ def main():
     traffic_path = os.path.join(ROOT, "profiles", "traffic.json")
     if roof and os.path.exists(traffic_path):
         tr = (json.load(open(traffic_path)).get(roof["kernel"])
-              if args.workload == "c2" and args.precision == 64 else None)
+              if args.workload in ("c2", "c5") and args.precision == 64 else None)
         if tr:
             # ncu DRAM bytes of one launch on the 48^3 box, scaled to this rank's cells
             units = info["n_owned"] + (info["ghost_layer"][0] if roof["kernel"].startswith("k_recon") else 0)

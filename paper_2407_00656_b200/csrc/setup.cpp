@@ -7,7 +7,10 @@
 // by Gram-Schmidt QR with re-orthogonalisation to an explicit pseudo-inverse.
 #include <algorithm>
 #include <array>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <unordered_map>
@@ -16,6 +19,21 @@
 
 namespace hgks {
 namespace {
+
+// HGKS_SETUP_TIMING=1: phase times of the host setup on stderr
+struct PhaseTimer {
+  bool on = std::getenv("HGKS_SETUP_TIMING") != nullptr;
+  const char* who;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  explicit PhaseTimer(const char* w) : who(w) {}
+  void lap(const char* phase) {
+    if (!on) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[hgks setup] %s: %-28s %8.3f s\n", who, phase,
+                 std::chrono::duration<double>(t - t0).count());
+    t0 = t;
+  }
+};
 
 struct P3 {
   double x, y, z;
@@ -120,7 +138,10 @@ int face_gps(int nv, const P3* p, P3* x, P3* n, double* wS) {
 // --- least squares (a2): pseudo-inverse by Gram-Schmidt QR (CGS2) ----------
 // A is m x n (row-major), returns P (n x m) with P A = I, least-squares sense.
 bool pinv_qr(int m, int n, const double* A, double* P) {
-  std::vector<double> Q(m * n), R(n * n, 0.0);
+  constexpr int kMaxM = 64, kMaxN = 9;  // stencils have <= 40 members, <= 9 unknowns
+  if (m > kMaxM || n > kMaxN) return false;
+  double Q[kMaxM * kMaxN], R[kMaxN * kMaxN];
+  for (int k = 0; k < n * n; ++k) R[k] = 0.0;
   for (int j = 0; j < n; ++j) {
     for (int i = 0; i < m; ++i) Q[i * n + j] = A[i * n + j];
     for (int pass = 0; pass < 2; ++pass)
@@ -176,6 +197,7 @@ GlobalMesh build_global_mesh(const double* xyz, int64_t n_nodes, const int8_t* t
                              const int64_t* bface_nodes, const int32_t* bface_tag, int64_t n_bf, int32_t n_ranks,
                              const int32_t* cell_part) {
   GlobalMesh gm;
+  PhaseTimer pt("global mesh");
   if (n_cells <= 0 || n_nodes <= 0 || !xyz || !type || !cn) throw Error(1, "empty mesh");
   gm.nc = n_cells;
   gm.type.assign(type, type + n_cells);
@@ -219,6 +241,7 @@ GlobalMesh build_global_mesh(const double* xyz, int64_t n_nodes, const int8_t* t
     if (!(gm.V[i] > 0)) throw Error(2, "degenerate cell " + std::to_string(i));
   auto centroid = [&](int64_t i) { return P3{gm.C[3 * i], gm.C[3 * i + 1], gm.C[3 * i + 2]}; };
 
+  pt.lap("geometry");
   // ---------------- faces: bucket half-faces by their smallest node ----------
   const int64_t nh = n_cells * nfc;
   std::vector<std::array<int64_t, 4>> hkey(nh);
@@ -386,6 +409,7 @@ GlobalMesh build_global_mesh(const double* xyz, int64_t n_nodes, const int8_t* t
   for (int64_t i = 0; i < n_cells; ++i)
     for (int p = 0; p < nfc; ++p)
       if (gm.cell_face[i * 6 + p] < 0) throw Error(2, "open face at cell " + std::to_string(i));
+  pt.lap("faces + periodic pairing");
   // ---------------- boundary ghosts (R25) ----------------
   for (int64_t f = 0; f < gm.nf; ++f) {
     if (gm.f_nb[f] >= 0) continue;
@@ -426,6 +450,7 @@ GlobalMesh build_global_mesh(const double* xyz, int64_t n_nodes, const int8_t* t
     gm.gM2.push_back(T[0][0]); gm.gM2.push_back(T[1][1]); gm.gM2.push_back(T[2][2]);
     gm.gM2.push_back(T[0][1]); gm.gM2.push_back(T[0][2]); gm.gM2.push_back(T[1][2]);
   }
+  pt.lap("boundary ghosts");
   // ---------------- CellNeighbor and h for dt ----------------
   gm.nbr_id.assign(n_cells * 6, -1);
   gm.nbr_shift.assign(n_cells * 18, 0.0);
@@ -451,6 +476,7 @@ GlobalMesh build_global_mesh(const double* xyz, int64_t n_nodes, const int8_t* t
     }
     gm.h_dt[i] = gm.V[i] / smax;
   }
+  pt.lap("neighbours, h");
   // ---------------- Alg. 1 stencils + sub-stencils ----------------
   gm.big_off.assign(n_cells + 1, 0);
   std::vector<std::vector<Member>> big(n_cells);
@@ -554,6 +580,7 @@ GlobalMesh build_global_mesh(const double* xyz, int64_t n_nodes, const int8_t* t
         break;
       }
   }
+  pt.lap("stencils");
   // ---------------- least-squares operators (a2) ----------------
   const int E = L.op_entries();
   gm.op.assign((size_t)n_cells * E, 0.0);
@@ -567,7 +594,12 @@ GlobalMesh build_global_mesh(const double* xyz, int64_t n_nodes, const int8_t* t
     P3 ci = centroid(i);
     const double* mi = &gm.M2[6 * i];
     // rows: member image centroid offset D and zero-mean quadratic moments (A.4)
-    std::vector<double> A(K * 9);
+    double A[64 * 9];
+    if (K > 64) {
+#pragma omp critical
+      if (lsq_bad < 0 || i < lsq_bad) lsq_bad = i;
+      continue;
+    }
     for (int k = 0; k < K; ++k) {
       int64_t id = gm.big_id[o0 + k];
       P3 ck;
@@ -592,8 +624,8 @@ GlobalMesh build_global_mesh(const double* xyz, int64_t n_nodes, const int8_t* t
       r[8] = (mk[5] + D.y * D.z - mi[5]) / h2;
     }
     double* op = &gm.op[(size_t)i * E];
-    std::vector<double> P(9 * K);
-    bool ok = K >= 9 && pinv_qr(K, 9, A.data(), P.data());
+    double P[9 * 64];
+    bool ok = K >= 9 && pinv_qr(K, 9, A, P);
     if (ok)
       for (int d = 0; d < 9; ++d)
         for (int k = 0; k < K; ++k) op[d * L.K + k] = P[d * K + k] / (d < 3 ? h : h * h);
@@ -623,6 +655,7 @@ GlobalMesh build_global_mesh(const double* xyz, int64_t n_nodes, const int8_t* t
     }
   }
   if (lsq_bad >= 0) throw Error(3, "rank-deficient least-squares stencil at cell " + std::to_string(lsq_bad));
+  pt.lap("least squares");
   // ---------------- partition (a3) ----------------
   gm.n_ranks = std::max(1, n_ranks);
   gm.part.assign(n_cells, 0);
@@ -671,6 +704,7 @@ GlobalMesh build_global_mesh(const double* xyz, int64_t n_nodes, const int8_t* t
     for (int64_t f = 0; f < gm.nf; ++f)
       if (gm.f_nb[f] >= 0 && gm.part[gm.f_owner[f]] != gm.part[gm.f_nb[f]]) ++gm.edge_cut;
   }
+  pt.lap("partition");
   return gm;
 }
 
@@ -681,6 +715,7 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
   const Layout& L = gm.lay;
   const int64_t nc = gm.nc;
   RankPlan rp;
+  PhaseTimer pt("rank plan");
   rp.rank = rank;
   std::vector<int64_t> owned;
   for (int64_t i = 0; i < nc; ++i)
@@ -736,9 +771,9 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
   rp.n_pghost = (int64_t)pg.size();
   rp.l2g = owned;
   rp.l2g.insert(rp.l2g.end(), pg.begin(), pg.end());
-  std::unordered_map<int64_t, int32_t> g2l;
-  g2l.reserve(rp.l2g.size() * 2);
+  std::vector<int32_t> g2l(nc, -1);  // global cell -> local id (-1: not on this rank)
   for (size_t k = 0; k < rp.l2g.size(); ++k) g2l[rp.l2g[k]] = (int32_t)k;
+  pt.lap("morton + ghost layers");
   // Reconstruction order (P:856-866 overlap): [early | pad | late | L1 ghosts], where
   // "early" owned cells have stencils made of owned cells and of boundary ghosts of
   // owned cells only, so they are reconstructed while the halo exchange is in
@@ -770,19 +805,20 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
               [&](int32_t a, int32_t b) { return by_morton(rp.l2g[a], rp.l2g[b]); });
   }
   rp.n_recon = (int64_t)rp.recon_cell.size();
+  pt.lap("recon order");
   // BC ghosts needed: those of faces of recon cells and of their neighbours
-  std::unordered_map<int64_t, int32_t> bg2l;
+  std::vector<int32_t> bg2l(gm.g_cell.size(), -1);  // boundary ghost -> local id
+  std::vector<int64_t> bg_used;                      // boundary ghosts in local order
   auto local_of = [&](int64_t id) -> int32_t {
     if (id < nc) {
-      auto it = g2l.find(id);
-      if (it == g2l.end()) throw Error(1, "ghost closure violated for cell " + std::to_string(id));
-      return it->second;
+      if (g2l[id] < 0) throw Error(1, "ghost closure violated for cell " + std::to_string(id));
+      return g2l[id];
     }
-    auto it = bg2l.find(id - nc);
-    if (it != bg2l.end()) return it->second;
-    int32_t l = (int32_t)(rp.n_owned + rp.n_pghost + (int64_t)bg2l.size());
-    bg2l[id - nc] = l;
-    int64_t g = id - nc;
+    const int64_t g = id - nc;
+    if (bg2l[g] >= 0) return bg2l[g];
+    int32_t l = (int32_t)(rp.n_owned + rp.n_pghost + (int64_t)bg_used.size());
+    bg2l[g] = l;
+    bg_used.push_back(g);
     rp.bg_cell.push_back(-1);  // resolved below
     rp.bg_bc.push_back(gm.g_bc[g]);
     rp.bg_normal.push_back(gm.g_normal[3 * g]);
@@ -809,26 +845,45 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
     return (((size_t)((r >> 7) * (ne / 2) + (e >> 1)) << 7 | (size_t)(r & 127)) << 1) | (size_t)(e & 1);
   };
   rp.st_id_tiled.assign((size_t)K * R, 0);
-  rp.stencil_min = 1 << 30;
-  rp.stencil_max = 0;
+  // boundary ghosts met in stencils get their local ids first (serial, in
+  // reconstruction order), so the per-cell fill below only reads the maps
+  for (int64_t r = 0; r < Rn; ++r) {
+    if (rp.recon_cell[r] < 0) continue;
+    const int64_t gi = rp.l2g[rp.recon_cell[r]];
+    for (int64_t o = gm.big_off[gi]; o < gm.big_off[gi + 1]; ++o)
+      if (gm.big_id[o] >= nc) local_of(gm.big_id[o]);
+  }
+  int smin = 1 << 30, smax = 0;
+  int64_t bad = -1;
+#pragma omp parallel for schedule(static) reduction(min : smin) reduction(max : smax)
   for (int64_t r = 0; r < Rn; ++r) {
     if (rp.recon_cell[r] < 0) continue;  // padding of the early block
     int64_t gi = rp.l2g[rp.recon_cell[r]];
     int64_t o0 = gm.big_off[gi];
     int kk = (int)(gm.big_off[gi + 1] - o0);
     if (rp.recon_cell[r] < rp.n_owned) {
-      rp.stencil_min = std::min(rp.stencil_min, kk);
-      rp.stencil_max = std::max(rp.stencil_max, kk);
+      smin = std::min(smin, kk);
+      smax = std::max(smax, kk);
     }
     for (int k = 0; k < K; ++k) {
-      rp.st_id[(size_t)k * R + r] = k < kk ? local_of(gm.big_id[o0 + k]) : rp.recon_cell[r];
-      rp.st_id_tiled[ti(r, K, k)] = rp.st_id[(size_t)k * R + r];
+      int32_t l = rp.recon_cell[r];
+      if (k < kk) {
+        const int64_t id = gm.big_id[o0 + k];
+        l = id < nc ? g2l[id] : bg2l[id - nc];
+        if (l < 0) {
+#pragma omp critical
+          bad = id;
+          l = 0;
+        }
+      }
+      rp.st_id[(size_t)k * R + r] = l;
+      rp.st_id_tiled[ti(r, K, k)] = l;
     }
     for (int s = 0; s < M * NM; ++s) {
       int8_t v = gm.sub_slot[gi * M * NM + s];
       rp.sub_slot[ti(r, M * NM, s)] = (uint8_t)(v < 0 ? 0 : v);
     }
-    // streaming order of the operator entries (kernels.cuh k_recon): A0+ member-major
+    // streaming order of the operator entries (hot.cuh k_recon): A0+ member-major
     // (row k*9 + d), then the sub-stencil operators (row 9K + (m*NM + j)*3 + d)
     const double* op = &gm.op[(size_t)gi * E];
     for (int d = 0; d < 9; ++d)
@@ -841,6 +896,10 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
     rp.geo[ti(r, 8, 1)] = std::pow(V, 4.0 / 3.0);
     for (int k = 0; k < 6; ++k) rp.geo[ti(r, 8, 2 + k)] = gm.M2[6 * gi + k];
   }
+  if (bad >= 0) throw Error(1, "ghost closure violated for cell " + std::to_string(bad));
+  rp.stencil_min = smin;
+  rp.stencil_max = smax;
+  pt.lap("tiled per-cell arrays");
   // faces computed by this rank: every face of an owned cell
   std::vector<int64_t> fl;
   {
@@ -869,7 +928,15 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
     int64_t b = gm.f_nb[f] >= 0 ? g2l[gm.f_nb[f]] : a;
     return {cls, std::min(a, b)};
   };
-  std::stable_sort(fl.begin(), fl.end(), [&](int64_t a, int64_t b) { return fkey(a) < fkey(b); });
+  {
+    // sort keys computed once: (class, min local endpoint, position) = a stable sort
+    std::vector<std::pair<std::pair<int, int64_t>, int64_t>> keyed(fl.size());
+    for (size_t k = 0; k < fl.size(); ++k) keyed[k] = {fkey(fl[k]), (int64_t)k};
+    std::sort(keyed.begin(), keyed.end());
+    std::vector<int64_t> sorted(fl.size());
+    for (size_t k = 0; k < fl.size(); ++k) sorted[k] = fl[keyed[k].second];
+    fl.swap(sorted);
+  }
   rp.n_faces = (int64_t)fl.size();
   for (int64_t f : fl) {
     const int cls = fkey(f).first;
@@ -878,10 +945,11 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
     else if (cls == 2) ++rp.n_wf;
     else ++rp.n_ff;
   }
+  pt.lap("face list + order");
   rp.f_geo_stride = 3 * L.nv + 3;
   rp.f_cells.resize(2 * rp.n_faces);
   rp.f_geo.assign((size_t)rp.f_geo_stride * rp.n_faces, 0.0);
-  std::unordered_map<int64_t, int32_t> f2l;
+  std::vector<int32_t> f2l(gm.nf, -1);  // global face -> local face id
   for (int64_t k = 0; k < rp.n_faces; ++k) {
     int64_t f = fl[k];
     f2l[f] = (int32_t)k;
@@ -895,6 +963,7 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
     if (gm.f_nb[f] >= 0)
       for (int a = 0; a < 3; ++a) fg[3 * L.nv + a] = gm.C[3 * o + a] - (gm.C[3 * gm.f_nb[f] + a] + gm.f_shift[3 * f + a]);
   }
+  pt.lap("face arrays");
   // update arrays
   rp.cf.assign((size_t)L.nfaces * rp.n_owned, 0);
   rp.inv_v.resize(rp.n_owned);
@@ -910,11 +979,8 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
     rp.h_dt[r] = gm.h_dt[gi];
   }
   // resolve BC ghost interior cells (must be local)
-  for (auto& kv : bg2l) {
-    int64_t g = kv.first;
-    rp.bg_cell[kv.second - (rp.n_owned + rp.n_pghost)] = local_of(gm.g_cell[g]);
-  }
-  rp.n_bghost = (int64_t)bg2l.size();
+  for (size_t k = 0; k < bg_used.size(); ++k) rp.bg_cell[k] = local_of(gm.g_cell[bg_used[k]]);
+  rp.n_bghost = (int64_t)bg_used.size();
   // exchange plan: peers = owner ranks of my ghosts, and ranks that ghost my cells
   if (gm.n_ranks > 1) {
     std::vector<std::vector<int32_t>> sends(gm.n_ranks);
@@ -965,6 +1031,7 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
       rp.recv_cnt.push_back(cnt);
     }
   }
+  pt.lap("update arrays, plans");
   return rp;
 }
 
