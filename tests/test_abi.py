@@ -98,3 +98,27 @@ def test_solver_without_cuda_fails_loudly():
     mi = W.kuhn_box(4)
     with pytest.raises(RuntimeError, match="CUDA"):
         hgks.Solver(hgks.Mesh(mi), W.advection_ic(mi))
+
+
+def test_ctypes_structs_match_header_layout(tmp_path):
+    """The binding's ctypes structures have the header's field offsets and sizes
+    (compiled with gcc against include/hgks.h): no silent drift of the ABI."""
+    import subprocess
+    pairs = [("hgks_mesh_desc", hgks.MeshDesc), ("hgks_config", hgks.Config), ("hgks_dist", hgks.Dist),
+             ("hgks_mesh_stats", hgks.MeshStats), ("hgks_step_info", hgks.StepInfo)]
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "hgks.h"', "int main(void) {"]
+    for cname, cls in pairs:
+        lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for fname, _ in cls._fields_:
+            lines.append(f'printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    got = {tuple(l.split()[:2]): int(l.split()[2]) for l in out if l.strip()}
+    for cname, cls in pairs:
+        assert got[(cname, "size")] == ctypes.sizeof(cls), cname
+        for fname, _ in cls._fields_:
+            assert got[(cname, fname)] == getattr(cls, fname).offset, (cname, fname)
