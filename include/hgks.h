@@ -159,6 +159,18 @@ hgks_status hgks_set_state(hgks_solver* solver, const double* h_Q, double t);
  * ids; t (optional) the time.  Synchronises the stream. */
 hgks_status hgks_get_state(const hgks_solver* solver, double* h_Q, int64_t* h_gid, double* t);
 
+/* Pipelined host I/O.  hgks_set_state copies on an internal H2D stream into one of
+ * two device staging slots and the solver stream waits for it; hgks_get_state_async
+ * enqueues the gather of the current state on the solver stream and the D2H into
+ * h_Q ([n_owned][5], ascending global id) on an internal D2H stream, and returns
+ * at once.  So the copies of step k+1's input and of step k's result overlap the
+ * compute of neighbouring steps (both directions at once).  h_Q is valid, and the
+ * buffers given to either call may be reused, after hgks_sync (pinned host memory
+ * is needed for the copies to be asynchronous).  At most two results may be in
+ * flight: a third hgks_get_state_async waits on the device for the first D2H. */
+hgks_status hgks_get_state_async(hgks_solver* solver, double* h_Q);
+hgks_status hgks_sync(hgks_solver* solver);
+
 /* Parity intermediates (single rank): L(Q) and d_t L(Q)
  * for state h_Q at step dt, [n_cells][5] caller order each.  Synchronous. */
 hgks_status hgks_debug_residual(hgks_solver* solver, const double* h_Q, double dt, double* h_L, double* h_dL);

@@ -143,7 +143,7 @@ int round32(int64_t n) { return (int)((n + 31) / 32 * 32); }
 struct DevArrays {
   // working-precision arrays (double for fp64, float for fp32)
   void *Q, *Qtmp, *R, *ceff, *F1, *F2, *op, *geo, *f_geo, *inv_v, *h_dt, *bg_normal, *sendbuf;
-  double *stage_in, *stage_out;  // caller-order staging, always fp64
+  double *stage_in[2], *stage_out[2];  // caller-order staging (fp64), double-buffered for pipelining
   int *recon_cell, *st_id, *f_cells, *cf, *bg_cell, *bg_bc, *send_list, *out_local;
   int64_t* in_row;
   uint8_t* sub_slot;
@@ -182,8 +182,10 @@ size_t layout(const GlobalMesh& gm, const RankPlan& rp, size_t rs, Carve& c, Dev
   d.in_row = c.take<int64_t>(rp.n_owned);
   // staging for set/get_state: single rank copies the caller's whole array
   const int64_t n_in = gm.n_ranks == 1 ? gm.nc : rp.n_owned;
-  d.stage_in = c.take<double>((size_t)5 * n_in);
-  d.stage_out = c.take<double>((size_t)5 * rp.n_owned);
+  for (int k = 0; k < 2; ++k) {
+    d.stage_in[k] = c.take<double>((size_t)5 * n_in);
+    d.stage_out[k] = c.take<double>((size_t)5 * rp.n_owned);
+  }
   return c.off + 256;
 }
 }  // namespace
@@ -220,7 +222,12 @@ struct hgks_solver {
   std::map<std::string, KStat> kstat;
   std::vector<int> peers;
   std::vector<double> host_stage;  // multi-rank set_state gather
-  double* pinned = nullptr;
+  double* pinned[2] = {nullptr, nullptr};  // multi-rank set_state gather (one per staging slot)
+  // host<->device pipelining (hgks_set_state / hgks_get_state_async): copies run on their
+  // own streams, double-buffered, ordered against the compute stream by events
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+  cudaEvent_t ev_h2d[2] = {}, ev_scattered[2] = {}, ev_gathered[2] = {}, ev_d2h[2] = {};
+  int in_slot = 0, out_slot = 0;
   std::vector<cudaEvent_t> event_pool;  // reusable profiling events
 };
 
@@ -504,20 +511,55 @@ template <class L>
 void upload_state(hgks_solver* s, const double* h_Q, double t) {
   const RankPlan& rp = *s->rp;
   const int n = (int)rp.n_owned;
+  const int k = s->in_slot;
+  s->in_slot ^= 1;
+  // the H2D into slot k waits until the scatter that last read slot k is done
+  CUDA_TRY(cudaStreamWaitEvent(s->h2d_stream, s->ev_scattered[k], 0));
   if (s->n_ranks == 1) {
-    CUDA_TRY(cudaMemcpyAsync(s->d.stage_in, h_Q, sizeof(double) * 5 * s->mesh->gm.nc, cudaMemcpyHostToDevice,
-                             s->stream));
+    CUDA_TRY(cudaMemcpyAsync(s->d.stage_in[k], h_Q, sizeof(double) * 5 * s->mesh->gm.nc, cudaMemcpyHostToDevice,
+                             s->h2d_stream));
   } else {
-    // gather this rank's rows into pinned staging (the copy must finish before reuse)
-    CUDA_TRY(cudaStreamSynchronize(s->stream));
-    double* hs = s->pinned;
+    // gather this rank's rows into pinned staging slot k (its previous copy must be done)
+    CUDA_TRY(cudaEventSynchronize(s->ev_h2d[k]));
+    double* hs = s->pinned[k];
     for (int i = 0; i < n; ++i) std::memcpy(hs + 5 * (size_t)i, h_Q + 5 * rp.l2g[i], 5 * sizeof(double));
-    CUDA_TRY(cudaMemcpyAsync(s->d.stage_in, hs, sizeof(double) * 5 * n, cudaMemcpyHostToDevice, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(s->d.stage_in[k], hs, sizeof(double) * 5 * n, cudaMemcpyHostToDevice, s->h2d_stream));
   }
+  CUDA_TRY(cudaEventRecord(s->ev_h2d[k], s->h2d_stream));
+  CUDA_TRY(cudaStreamWaitEvent(s->stream, s->ev_h2d[k], 0));
   launch(s, "k_scatter_state",
-         [&] { L::scatter(blocks(n, 256), s->stream, s->d.stage_in, s->d.in_row, n, as<L>(s->d.Q)); });
+         [&] { L::scatter(blocks(n, 256), s->stream, s->d.stage_in[k], s->d.in_row, n, as<L>(s->d.Q)); });
+  CUDA_TRY(cudaEventRecord(s->ev_scattered[k], s->stream));
   launch(s, "k_reset_ctrl", [&] { k_reset_ctrl<<<1, 1, 0, s->stream>>>(s->d.ctrl, t); });
   init_dt<L>(s);
+}
+
+// enqueue: gather the owned rows (ascending global id) into staging slot k on the
+// compute stream, then the D2H into h_Q on the copy stream
+void download_state(hgks_solver* s, double* h_Q) {
+  const int n = (int)s->rp->n_owned;
+  const int k = s->out_slot;
+  s->out_slot ^= 1;
+  CUDA_TRY(cudaStreamWaitEvent(s->stream, s->ev_d2h[k], 0));  // slot k's previous D2H is done
+  launch(s, "k_gather_state", [&] {
+    if (s->fp32)
+      p32::Launch::gather(blocks(n, 256), s->stream, (const float*)s->d.Q, s->d.out_local, n, s->d.stage_out[k]);
+    else
+      p64::Launch::gather(blocks(n, 256), s->stream, (const double*)s->d.Q, s->d.out_local, n, s->d.stage_out[k]);
+  });
+  CUDA_TRY(cudaEventRecord(s->ev_gathered[k], s->stream));
+  CUDA_TRY(cudaStreamWaitEvent(s->d2h_stream, s->ev_gathered[k], 0));
+  CUDA_TRY(cudaMemcpyAsync(h_Q, s->d.stage_out[k], sizeof(double) * 5 * n, cudaMemcpyDeviceToHost, s->d2h_stream));
+  CUDA_TRY(cudaEventRecord(s->ev_d2h[k], s->d2h_stream));
+}
+
+// the compute stream waits for every enqueued copy; then the host waits for it
+void sync_all(hgks_solver* s) {
+  for (int k = 0; k < 2; ++k) {
+    CUDA_TRY(cudaStreamWaitEvent(s->stream, s->ev_h2d[k], 0));
+    CUDA_TRY(cudaStreamWaitEvent(s->stream, s->ev_d2h[k], 0));
+  }
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
 }
 
 // precision dispatch of the hot path
@@ -679,7 +721,17 @@ hgks_status hgks_init(const hgks_mesh* mc, const hgks_config* cfg, const hgks_di
       CUDA_TRY(cudaEventCreateWithFlags(&s->ev_packed, cudaEventDisableTiming));
       CUDA_TRY(cudaEventCreateWithFlags(&s->ev_halo, cudaEventDisableTiming));
     }
-    if (s->n_ranks > 1) CUDA_TRY(cudaMallocHost(&s->pinned, sizeof(double) * 5 * std::max<int64_t>(1, rp.n_owned)));
+    if (s->n_ranks > 1)
+      for (int k = 0; k < 2; ++k)
+        CUDA_TRY(cudaMallocHost(&s->pinned[k], sizeof(double) * 5 * std::max<int64_t>(1, rp.n_owned)));
+    CUDA_TRY(cudaStreamCreateWithFlags(&s->h2d_stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&s->d2h_stream, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+      for (cudaEvent_t* e : {&s->ev_h2d[k], &s->ev_scattered[k], &s->ev_gathered[k], &s->ev_d2h[k]}) {
+        CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventRecord(*e, st));  // "already complete" for the first waits
+      }
+    }
     CUDA_TRY(cudaStreamSynchronize(st));
     HGKS_DISPATCH(s, upload_state, s.get(), h_Q0, 0.0);
     CUDA_TRY(cudaStreamSynchronize(st));
@@ -701,7 +753,15 @@ hgks_status hgks_destroy(hgks_solver* s) {
     if (s->comm_stream) cudaStreamDestroy(s->comm_stream);
     if (s->ev_packed) cudaEventDestroy(s->ev_packed);
     if (s->ev_halo) cudaEventDestroy(s->ev_halo);
-    if (s->pinned) cudaFreeHost(s->pinned);
+    cudaStreamSynchronize(s->h2d_stream);
+    cudaStreamSynchronize(s->d2h_stream);
+    for (int k = 0; k < 2; ++k) {
+      if (s->pinned[k]) cudaFreeHost(s->pinned[k]);
+      for (cudaEvent_t e : {s->ev_h2d[k], s->ev_scattered[k], s->ev_gathered[k], s->ev_d2h[k]})
+        if (e) cudaEventDestroy(e);
+    }
+    if (s->h2d_stream) cudaStreamDestroy(s->h2d_stream);
+    if (s->d2h_stream) cudaStreamDestroy(s->d2h_stream);
     delete s;
   });
 }
@@ -749,22 +809,30 @@ hgks_status hgks_get_state(const hgks_solver* sc, double* h_Q, int64_t* h_gid, d
     hgks_solver* s = const_cast<hgks_solver*>(sc);
     if (!s || !h_Q) throw Error(HGKS_E_ARG, "null argument");
     const int n = (int)s->rp->n_owned;
-    launch(s, "k_gather_state", [&] {
-      if (s->fp32)
-        p32::Launch::gather(blocks(n, 256), s->stream, (const float*)s->d.Q, s->d.out_local, n, s->d.stage_out);
-      else
-        p64::Launch::gather(blocks(n, 256), s->stream, (const double*)s->d.Q, s->d.out_local, n, s->d.stage_out);
-    });
-    CUDA_TRY(cudaMemcpyAsync(h_Q, s->d.stage_out, sizeof(double) * 5 * n, cudaMemcpyDeviceToHost, s->stream));
+    download_state(s, h_Q);
     Ctrl h;
     CUDA_TRY(cudaMemcpyAsync(&h, s->d.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s->stream));
-    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    sync_all(s);
     if (t) *t = h.t_next;
     if (h_gid) {
       std::vector<int64_t> g(s->rp->l2g.begin(), s->rp->l2g.begin() + n);
       std::sort(g.begin(), g.end());
       std::memcpy(h_gid, g.data(), sizeof(int64_t) * n);
     }
+  });
+}
+
+hgks_status hgks_get_state_async(hgks_solver* s, double* h_Q) {
+  return guard([&] {
+    if (!s || !h_Q) throw Error(HGKS_E_ARG, "null argument");
+    download_state(s, h_Q);
+  });
+}
+
+hgks_status hgks_sync(hgks_solver* s) {
+  return guard([&] {
+    if (!s) throw Error(HGKS_E_ARG, "null solver");
+    sync_all(s);
   });
 }
 
@@ -778,11 +846,12 @@ hgks_status hgks_debug_residual(hgks_solver* s, const double* h_Q, double dt, do
     Ctrl saved;
     CUDA_TRY(cudaMemcpyAsync(&saved, s->d.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s->stream));
     CUDA_TRY(cudaStreamSynchronize(s->stream));
-    CUDA_TRY(cudaMemcpyAsync(s->d.stage_in, h_Q, sizeof(double) * 5 * s->mesh->gm.nc, cudaMemcpyHostToDevice,
+    sync_all(s);  // no copy in flight may touch the staging slots
+    CUDA_TRY(cudaMemcpyAsync(s->d.stage_in[0], h_Q, sizeof(double) * 5 * s->mesh->gm.nc, cudaMemcpyHostToDevice,
                              s->stream));
     launch(s, "k_scatter_state", [&] {
-      if (s->fp32) p32::Launch::scatter(blocks(n, 256), s->stream, s->d.stage_in, s->d.in_row, n, (float*)s->d.Q);
-      else p64::Launch::scatter(blocks(n, 256), s->stream, s->d.stage_in, s->d.in_row, n, (double*)s->d.Q);
+      if (s->fp32) p32::Launch::scatter(blocks(n, 256), s->stream, s->d.stage_in[0], s->d.in_row, n, (float*)s->d.Q);
+      else p64::Launch::scatter(blocks(n, 256), s->stream, s->d.stage_in[0], s->d.in_row, n, (double*)s->d.Q);
     });
     Ctrl h = saved;
     h.dt = dt;

@@ -26,7 +26,8 @@ ERRORS = {0: "OK", 1: "E_ARG", 2: "E_MESH", 3: "E_STENCIL", 4: "E_CUDA", 5: "E_N
 
 # every symbol include/hgks.h declares (checked by tests/test_abi.py)
 EXPORTS = ["hgks_mesh_create", "hgks_mesh_destroy", "hgks_mesh_info", "hgks_workspace_size", "hgks_init",
-           "hgks_destroy", "hgks_step", "hgks_set_state", "hgks_get_state", "hgks_debug_residual",
+           "hgks_destroy", "hgks_step", "hgks_set_state", "hgks_get_state", "hgks_get_state_async",
+           "hgks_sync", "hgks_debug_residual",
            "hgks_set_profiling", "hgks_kernel_times", "hgks_launch_count", "hgks_nccl_unique_id", "hgks_group_step", "hgks_mesh_plan",
            "hgks_last_error", "hgks_version"]
 TRANSPORT_NCCL, TRANSPORT_LOOPBACK = 0, 1
@@ -223,6 +224,7 @@ class Solver:
             raise RuntimeError("hgks needs a CUDA device (no CPU fallback)")
         self.cfg = cfg or SolverConfig()
         self.mesh = mesh
+        self._inflight = []  # host buffers of enqueued copies (kept alive until sync)
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
         torch.cuda.set_device(self.device)
         nbytes = mesh.workspace_size(self.cfg, rank)
@@ -262,9 +264,24 @@ class Solver:
         return None
 
     def set_state(self, Q, t: float = 0.0):
-        """Q: numpy [n,5] float64 or a (pinned) CPU torch tensor."""
-        ptr = Q.data_ptr() if hasattr(Q, "data_ptr") else np.ascontiguousarray(Q, np.float64).ctypes.data
+        """Q: numpy [n,5] float64 or a (pinned) CPU torch tensor.  Asynchronous: the
+        buffer is kept alive here until the next sync()/get_state()."""
+        if not hasattr(Q, "data_ptr"):
+            Q = np.ascontiguousarray(Q, np.float64)
+        self._inflight.append(Q)
+        ptr = Q.data_ptr() if hasattr(Q, "data_ptr") else Q.ctypes.data
         _check(lib().hgks_set_state(self.h, C.c_void_p(ptr), t))
+
+    def get_state_async(self, out):
+        """Enqueue the download of the current state into ``out`` (pinned CPU tensor or
+        numpy [n_owned,5] float64, ascending global id); valid after sync()."""
+        self._inflight.append(out)
+        ptr = out.data_ptr() if hasattr(out, "data_ptr") else out.ctypes.data
+        _check(lib().hgks_get_state_async(self.h, C.c_void_p(ptr)))
+
+    def sync(self):
+        _check(lib().hgks_sync(self.h))
+        self._inflight.clear()
 
     def get_state(self, out=None):
         """Owned cells in ascending global id -> (Q [n_owned,5], gid, t).  ``out`` may be a pinned tensor."""
@@ -273,8 +290,10 @@ class Solver:
         if out is None:
             Q = np.zeros((self.n_owned, 5))
             _check(lib().hgks_get_state(self.h, C.c_void_p(Q.ctypes.data), _p(gid, _i64p), C.byref(t)))
+            self._inflight.clear()
             return Q, gid, t.value
         _check(lib().hgks_get_state(self.h, C.c_void_p(out.data_ptr()), None, C.byref(t)))
+        self._inflight.clear()
         return out, None, t.value
 
     def residual(self, Q, dt: float):

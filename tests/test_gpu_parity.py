@@ -184,3 +184,30 @@ def test_sphere_residual_matches_oracle(cuda_ok):
     # (SURVEY A.3), so intermediates carry ~1e-11; the 10-step state bar stays 1e-10
     assert rel_err(Lg, Lo).max() < 1e-10, rel_err(Lg, Lo)
     assert rel_err(dLg, dLo).max() < 1e-10, rel_err(dLg, dLo)
+
+
+def test_pipelined_host_io_matches_synchronous(cuda_ok):
+    """hgks_set_state / hgks_get_state_async / hgks_sync (copies on the library's own
+    streams, double-buffered) give the same bits as the synchronous calls."""
+    import torch
+    mi = W.kuhn_box(7, jitter=0.1)
+    Q0 = W.advection_ic(mi)
+    a = hgks.Solver(hgks.Mesh(mi), Q0)
+    b = hgks.Solver(hgks.Mesh(mi), Q0)
+    outs = [torch.zeros((mi.n_cells, 5), dtype=torch.float64).pin_memory() for _ in range(2)]
+    ref = []
+    Qin = torch.from_numpy(Q0.copy()).pin_memory()
+    for k in range(5):
+        a.set_state(Q0, 0.0)
+        a.step(k + 1)
+        ref.append(a.get_state()[0])
+    for k in range(5):
+        b.set_state(Qin, 0.0)
+        b.step(k + 1, info=False)
+        b.get_state_async(outs[k % 2])
+        if k % 2 == 1:
+            b.sync()
+            assert np.array_equal(outs[0].numpy(), ref[k - 1])
+            assert np.array_equal(outs[1].numpy(), ref[k])
+    b.sync()
+    assert np.array_equal(outs[0].numpy(), ref[4])
