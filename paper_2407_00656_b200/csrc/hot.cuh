@@ -1043,15 +1043,25 @@ __global__ void __launch_bounds__(256) k_update1(UpdateArgs a) {
   }
   const Real iv = a.inv_v[i];
   const Real dt = a.ctrl->dt;
-  Real* q = a.Q + (size_t)i * QS;
-  Real* r = a.R + (size_t)i * QS;
+  // rows are QS = 6 values: three 2-vectors per row (the pad slot is carried along)
+  R2* q2 = reinterpret_cast<R2*>(a.Q + (size_t)i * QS);
+  R2* r2 = reinterpret_cast<R2*>(a.R + (size_t)i * QS);
+  const R2 x0 = q2[0], x1 = q2[1], x2 = q2[2];
+  const Real q0[6] = {x0.x, x0.y, x1.x, x1.y, x2.x, x2.y};
+  Real qs[6], rs[6];
 #pragma unroll
   for (int v = 0; v < 5; ++v) {
     const Real l = L[v] * iv, dl = dL[v] * iv;
-    const Real q0 = q[v];
-    q[v] = q0 + Real(0.5) * dt * l + Real(0.125) * dt * dt * dl;
-    r[v] = q0 + dt * l + dt * dt / Real(6.0) * dl;
+    qs[v] = q0[v] + Real(0.5) * dt * l + Real(0.125) * dt * dt * dl;
+    rs[v] = q0[v] + dt * l + dt * dt / Real(6.0) * dl;
   }
+  qs[5] = rs[5] = q0[5];
+  q2[0] = make_R2(qs[0], qs[1]);
+  q2[1] = make_R2(qs[2], qs[3]);
+  q2[2] = make_R2(qs[4], qs[5]);
+  r2[0] = make_R2(rs[0], rs[1]);
+  r2[1] = make_R2(rs[2], rs[3]);
+  r2[2] = make_R2(rs[4], rs[5]);
 }
 
 
@@ -1076,14 +1086,17 @@ __global__ void __launch_bounds__(256) k_update2(UpdateArgs a) {
     }
     const Real iv = a.inv_v[i];
     const Real dt = a.ctrl->dt;
-    Real q[5];
-    const Real* r = a.R + (size_t)i * QS;
-    Real* qo = a.Q + (size_t)i * QS;
+    Real q[6];
+    const R2* r2 = reinterpret_cast<const R2*>(a.R + (size_t)i * QS);
+    R2* q2 = reinterpret_cast<R2*>(a.Q + (size_t)i * QS);
+    const R2 y0 = r2[0], y1 = r2[1], y2 = r2[2];
+    const Real r[6] = {y0.x, y0.y, y1.x, y1.y, y2.x, y2.y};
 #pragma unroll
-    for (int v = 0; v < 5; ++v) {
-      q[v] = r[v] + dt * dt / Real(6.0) * Real(2.0) * (dL[v] * iv);
-      qo[v] = q[v];
-    }
+    for (int v = 0; v < 5; ++v) q[v] = r[v] + dt * dt / Real(6.0) * Real(2.0) * (dL[v] * iv);
+    q[5] = r[5];
+    q2[0] = make_R2(q[0], q[1]);
+    q2[1] = make_R2(q[2], q[3]);
+    q2[2] = make_R2(q[4], q[5]);
     const Real p = (a.gp.gamma - Real(1.0)) * (q[4] - Real(0.5) * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3]) / q[0]);
     if (!(q[0] > Real(0.0)) || !(p > Real(0.0))) atomicMin(&a.ctrl->bad_cell, i);
     else {
