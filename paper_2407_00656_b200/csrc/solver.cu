@@ -228,6 +228,14 @@ struct hgks_solver {
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
   cudaEvent_t ev_h2d[2] = {}, ev_scattered[2] = {}, ev_gathered[2] = {}, ev_d2h[2] = {};
   int in_slot = 0, out_slot = 0;
+  // CUDA graph of one full step (single rank, profiling off): captured on an internal
+  // stream, replayed on the solver stream; re-captured when t_stop changes
+  bool use_graphs = true;  // HGKS_GRAPHS=0 disables
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t step_graph = nullptr;
+  double graph_t_stop = 0.0;
+  int64_t graph_launches = 0;  // kernel launches per replay
+  int64_t eager_steps = 0;
   std::vector<cudaEvent_t> event_pool;  // reusable profiling events
 };
 
@@ -644,6 +652,7 @@ hgks_status hgks_init(const hgks_mesh* mc, const hgks_config* cfg, const hgks_di
       throw Error(HGKS_E_ARG, "dist->n_ranks differs from the mesh partition (" + std::to_string(m->gm.n_ranks) + ")");
     if (dist) CUDA_TRY(cudaSetDevice(dist->device));
     CUDA_TRY(cudaGetDevice(&s->device));
+    if (const char* e = std::getenv("HGKS_GRAPHS")) s->use_graphs = std::atoi(e) != 0;
     s->stream = (cudaStream_t)stream;
     s->rp = &m->plan(s->rank);
     s->lay = m->gm.lay;
@@ -761,6 +770,8 @@ hgks_status hgks_destroy(hgks_solver* s) {
         if (e) cudaEventDestroy(e);
     }
     if (s->h2d_stream) cudaStreamDestroy(s->h2d_stream);
+    if (s->step_graph) cudaGraphExecDestroy(s->step_graph);
+    if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
     if (s->d2h_stream) cudaStreamDestroy(s->d2h_stream);
     delete s;
   });
@@ -774,11 +785,47 @@ hgks_status hgks_step(hgks_solver* s, int32_t n_steps, double t_stop, hgks_step_
       CUDA_TRY(cudaMemcpyAsync(&before, s->d.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s->stream));
       CUDA_TRY(cudaStreamSynchronize(s->stream));
     }
-    for (int k = 0; k < n_steps; ++k) {
+    auto one_step = [&] {
       launch(s, "k_step_begin",
              [&] { k_step_begin<<<1, 1, 0, s->stream>>>(s->d.ctrl, s->cfg.cfl, s->cfg.fixed_dt, t_stop); });
       HGKS_DISPATCH(s, stage, s, 1);
       HGKS_DISPATCH(s, stage, s, 2);
+    };
+    // graphs: single rank, not profiling, after one eager step (one-time attribute setup)
+    const bool graphs = s->use_graphs && s->n_ranks == 1 && !s->profiling && s->eager_steps > 0;
+    if (graphs && (!s->step_graph || s->graph_t_stop != t_stop)) {
+      if (s->step_graph) CUDA_TRY(cudaGraphExecDestroy(s->step_graph));
+      s->step_graph = nullptr;
+      if (!s->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking));
+      cudaStream_t user = s->stream;
+      const int64_t l0 = s->launches;
+      cudaGraph_t g = nullptr;
+      s->stream = s->cap_stream;
+      CUDA_TRY(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        one_step();
+      } catch (...) {
+        cudaStreamEndCapture(s->stream, &g);
+        if (g) cudaGraphDestroy(g);
+        s->stream = user;
+        throw;
+      }
+      CUDA_TRY(cudaStreamEndCapture(s->stream, &g));
+      s->stream = user;
+      CUDA_TRY(cudaGraphInstantiate(&s->step_graph, g, 0));
+      CUDA_TRY(cudaGraphDestroy(g));
+      s->graph_launches = s->launches - l0;
+      s->launches = l0;
+      s->graph_t_stop = t_stop;
+    }
+    for (int k = 0; k < n_steps; ++k) {
+      if (graphs) {
+        CUDA_TRY(cudaGraphLaunch(s->step_graph, s->stream));
+        s->launches += s->graph_launches;
+      } else {
+        one_step();
+        ++s->eager_steps;
+      }
     }
     if (info) {
       Ctrl h;

@@ -211,3 +211,20 @@ def test_pipelined_host_io_matches_synchronous(cuda_ok):
             assert np.array_equal(outs[1].numpy(), ref[k])
     b.sync()
     assert np.array_equal(outs[0].numpy(), ref[4])
+
+
+def test_cuda_graph_steps_match_eager(cuda_ok, monkeypatch):
+    """hgks_step replays a captured CUDA graph of one step (single rank): same bits as
+    eager launches, including t_stop clipping (the graph is re-captured per t_stop)."""
+    mi = W.kuhn_box(7, jitter=0.1)
+    Q0 = W.advection_ic(mi)
+    out = {}
+    for g in ("0", "1"):
+        monkeypatch.setenv("HGKS_GRAPHS", g)
+        s = hgks.Solver(hgks.Mesh(mi), Q0)
+        s.step(1)
+        s.step(6)
+        s.step(5, t_stop=0.08)
+        out[g] = s.get_state()
+    assert np.array_equal(out["0"][0], out["1"][0])
+    assert out["0"][2] == out["1"][2]
