@@ -223,10 +223,9 @@ __global__ void __launch_bounds__(ReconShape<K>::BT, ReconShape<K>::MINB) k_reco
   // operators are tiled by entry pairs: pair p of this cell at op2[p * kTile]
   const R2* __restrict__ op2 = reinterpret_cast<const R2*>(a.op + tb * E) + t;
   static_assert(K % 2 == 0 && (3 * M * NM) % 2 == 0, "operator pairs");
-#ifndef HGKS_RECON_UNROLL
-#define HGKS_RECON_UNROLL 2  // measured: 2 beats 1 (C2 -1 %, C3 -5 %)
-#endif
-  constexpr int kUnrollA0 = HGKS_RECON_UNROLL;
+  // measured unroll of the member-pair loop: tets (K = 14) 4, hexes (K = 24) 2
+  // (C2 0.397 -> 0.388 ms, C3 0.484 -> 0.458 ms vs no unrolling)
+  constexpr int kUnrollA0 = K <= 16 ? 4 : 2;
 #pragma unroll kUnrollA0
   for (int k2 = 0; k2 < K; k2 += 2) {  // two members = 18 entries = 9 pairs
     Real dq[2][5];
