@@ -773,9 +773,16 @@ template <int NV, int STAGE, bool TAU0, int BC>
 #ifndef HGKS_TAU0_MINB3
 #define HGKS_TAU0_MINB3 5
 #endif
-__global__ void __launch_bounds__(NV == 3 ? 96 : 128, TAU0 ? (NV == 3 ? HGKS_TAU0_MINB3 : 4) : 1) k_flux(FluxArgs a) {
+#ifndef HGKS_FLUX_FPB
+#define HGKS_FLUX_FPB 32  // faces per block
+#endif
+#ifndef HGKS_MOMENT_MINB
+#define HGKS_MOMENT_MINB 1
+#endif
+__global__ void __launch_bounds__((NV == 3 ? 3 : 4) * HGKS_FLUX_FPB,
+                                  TAU0 ? (NV == 3 ? HGKS_TAU0_MINB3 : 4) : HGKS_MOMENT_MINB) k_flux(FluxArgs a) {
   constexpr int NGP = NV == 3 ? 3 : 4;
-  constexpr int BLOCK = NV == 3 ? 96 : 128;
+  constexpr int BLOCK = NGP * HGKS_FLUX_FPB;
   constexpr int NOUT = STAGE == 1 ? 10 : 5;
   __shared__ Real red[NOUT][BLOCK];
   const int t = blockIdx.x * BLOCK + threadIdx.x;
@@ -1173,7 +1180,7 @@ struct Launch {
   }
   template <int NV, int STAGE, bool TAU0, int BC>
   static void flux(int grid, cudaStream_t st, const FluxArgs& a) {
-    k_flux<NV, STAGE, TAU0, BC><<<grid, NV == 3 ? 96 : 128, 0, st>>>(a);
+    k_flux<NV, STAGE, TAU0, BC><<<grid, (NV == 3 ? 3 : 4) * HGKS_FLUX_FPB, 0, st>>>(a);
   }
   template <int NF>
   static void update1(int grid, cudaStream_t st, const UpdateArgs& u) {

@@ -344,7 +344,7 @@ void run_recon(hgks_solver* s, const void* Q, int part) {
 
 template <class L, int NV, int BC>
 void launch_flux(hgks_solver* s, const typename L::FluxArgsT& a, int stage, bool tau0) {
-  constexpr int NGP = NV == 3 ? 3 : 4, B = NV == 3 ? 96 : 128;
+  constexpr int NGP = NV == 3 ? 3 : 4, B = NGP * HGKS_FLUX_FPB;
   const int nb = blocks((int64_t)a.n_faces * NGP, B);
   const char* names[2][2] = {{"k_flux_s1", "k_flux_s2"}, {"k_flux_tau0_s1", "k_flux_tau0_s2"}};
   const char* nm = BC == 0 ? names[tau0][stage - 1] : (BC == 1 ? "k_flux_wall" : "k_flux_farfield");
