@@ -141,7 +141,11 @@ def run_reference(args):
     threads = len(os.sched_getaffinity(0))
     from oracle import oracle as O
     from paper_2407_00656_b200 import workloads as W
-    Ns = 24
+    # bounded sample: every timed step is one full oracle step on an Ns^3 Kuhn box, Ns chosen so
+    # the whole --steps/--warmup run stays near two minutes (the oracle does ~6e4 cell-updates/s
+    # on 16 host cores; its cost per cell does not depend on the box size)
+    cells_budget = 120.0 * 6e4 / max(1, args.steps + args.warmup)
+    Ns = int(max(8, min(24, (cells_budget / 6.0) ** (1.0 / 3.0))))
     mi = W.kuhn_box(Ns)
     m = O.OracleMesh(mi)
     s = O.OracleSolver(m, W.advection_ic(mi, gamma=GAMMA), O.OracleConfig(cfl=CFL), threads=threads)
