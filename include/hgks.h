@@ -201,6 +201,12 @@ hgks_status hgks_mesh_plan(const hgks_mesh* mesh, int32_t rank, int64_t* l2g, in
  * e.g. over torch.distributed, and passed in hgks_dist.nccl_id).  Host only. */
 hgks_status hgks_nccl_unique_id(uint8_t* out);
 
+/* Diagnostic of the NCCL transport on the current device: a one-rank communicator
+ * does exactly the calls a multi-rank step makes (grouped ncclSend/ncclRecv of
+ * fp64 and fp32 halo buffers, here to itself, and the uint64 ncclAllReduce(min) of
+ * the CFL bound) and checks the results.  HGKS_E_NCCL with a message on failure. */
+hgks_status hgks_nccl_selftest(void);
+
 /* Number of kernels launched by this solver so far (all kinds). */
 hgks_status hgks_launch_count(const hgks_solver* solver, int64_t* launches);
 

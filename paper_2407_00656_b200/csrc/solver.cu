@@ -984,6 +984,75 @@ hgks_status hgks_nccl_unique_id(uint8_t* out) {
   });
 }
 
+hgks_status hgks_nccl_selftest(void) {
+  return guard([&] {
+    Nccl& N = nccl();
+    if (!N.h || !N.CommInitRank || !N.Send || !N.Recv || !N.AllReduce || !N.GroupStart || !N.GroupEnd)
+      throw Error(HGKS_E_NCCL, "libnccl.so.2 not found or incomplete");
+    ncclUniqueId id;
+    NCCL_TRY(N.GetUniqueId(&id));
+    ncclComm_t comm = nullptr;
+    NCCL_TRY(N.CommInitRank(&comm, 1, id, 0));
+    cudaStream_t st = nullptr, cs = nullptr;
+    cudaEvent_t ev = nullptr;
+    void* buf = nullptr;
+    auto cleanup = [&] {
+      if (st) cudaStreamSynchronize(st);
+      if (cs) cudaStreamSynchronize(cs);
+      if (buf) cudaFree(buf);
+      if (ev) cudaEventDestroy(ev);
+      if (st) cudaStreamDestroy(st);
+      if (cs) cudaStreamDestroy(cs);
+      if (comm && N.CommDestroy) N.CommDestroy(comm);
+    };
+    try {
+      constexpr int n = 1000;
+      CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+      CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+      CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      CUDA_TRY(cudaMalloc(&buf, 2 * n * sizeof(double) + 2 * n * sizeof(float) + 64));
+      double* d_src = (double*)buf;
+      double* d_dst = d_src + n;
+      float* f_src = (float*)(d_dst + n);
+      float* f_dst = f_src + n;
+      unsigned long long* bits = (unsigned long long*)(f_dst + n);
+      std::vector<double> hs(n);
+      std::vector<float> fs(n);
+      for (int k = 0; k < n; ++k) hs[k] = fs[k] = 0.5f * k - 7.0f;
+      const unsigned long long b0 = 0x3ff8000000000000ull;  // 1.5
+      CUDA_TRY(cudaMemcpy(d_src, hs.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(f_src, fs.data(), n * sizeof(float), cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(bits, &b0, sizeof(b0), cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemset(d_dst, 0, n * sizeof(double)));
+      CUDA_TRY(cudaMemset(f_dst, 0, n * sizeof(float)));
+      // the halo pattern of exchange(): grouped send/recv on a comm stream, event back
+      NCCL_TRY(N.GroupStart());
+      NCCL_TRY(N.Send(d_src, n, ncclFloat64, 0, comm, cs));
+      NCCL_TRY(N.Recv(d_dst, n, ncclFloat64, 0, comm, cs));
+      NCCL_TRY(N.Send(f_src, n, ncclFloat32, 0, comm, cs));
+      NCCL_TRY(N.Recv(f_dst, n, ncclFloat32, 0, comm, cs));
+      NCCL_TRY(N.GroupEnd());
+      CUDA_TRY(cudaEventRecord(ev, cs));
+      CUDA_TRY(cudaStreamWaitEvent(st, ev, 0));
+      // the dt pattern of allreduce_dt(): in-place min of the ordered bits
+      NCCL_TRY(N.AllReduce(bits, bits, 1, ncclUint64, ncclMin, comm, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+      std::vector<double> hd(n);
+      std::vector<float> fd(n);
+      unsigned long long b1 = 0;
+      CUDA_TRY(cudaMemcpy(hd.data(), d_dst, n * sizeof(double), cudaMemcpyDeviceToHost));
+      CUDA_TRY(cudaMemcpy(fd.data(), f_dst, n * sizeof(float), cudaMemcpyDeviceToHost));
+      CUDA_TRY(cudaMemcpy(&b1, bits, sizeof(b1), cudaMemcpyDeviceToHost));
+      if (hd != hs || fd != fs) throw Error(HGKS_E_NCCL, "NCCL self send/recv returned wrong data");
+      if (b1 != b0) throw Error(HGKS_E_NCCL, "NCCL allreduce(min, uint64) returned wrong data");
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
+  });
+}
+
 hgks_status hgks_group_step(hgks_solver* const* ss, int32_t n, int32_t n_steps, double t_stop) {
   return guard([&] {
     if (!ss || n < 1 || n > kMaxGroup) throw Error(HGKS_E_ARG, "bad group size");

@@ -28,7 +28,7 @@ ERRORS = {0: "OK", 1: "E_ARG", 2: "E_MESH", 3: "E_STENCIL", 4: "E_CUDA", 5: "E_N
 EXPORTS = ["hgks_mesh_create", "hgks_mesh_destroy", "hgks_mesh_info", "hgks_workspace_size", "hgks_init",
            "hgks_destroy", "hgks_step", "hgks_set_state", "hgks_get_state", "hgks_get_state_async",
            "hgks_sync", "hgks_debug_residual",
-           "hgks_set_profiling", "hgks_kernel_times", "hgks_launch_count", "hgks_nccl_unique_id", "hgks_group_step", "hgks_mesh_plan",
+           "hgks_set_profiling", "hgks_kernel_times", "hgks_launch_count", "hgks_nccl_unique_id", "hgks_nccl_selftest", "hgks_group_step", "hgks_mesh_plan",
            "hgks_last_error", "hgks_version"]
 TRANSPORT_NCCL, TRANSPORT_LOOPBACK = 0, 1
 
@@ -145,6 +145,11 @@ class SolverConfig:
     def c(self) -> Config:
         return Config(self.gamma, self.cfl, self.fixed_dt, self.tau_mode, self.c1, self.mu_inf, self.t_inf,
                       self.mu_exp, self.eps_value(), self.omega_pow, (C.c_double * 5)(*self.freestream), self.precision)
+
+
+def nccl_selftest() -> None:
+    """One-rank NCCL communicator doing the calls of a multi-rank step (diagnostic)."""
+    _check(lib().hgks_nccl_selftest())
 
 
 def nccl_unique_id() -> bytes:

@@ -67,3 +67,10 @@ def test_multirank_t_stop(cuda_ok):
     s1.step(50, t_stop=0.04)
     Q1, _, t1 = s1.get_state()
     assert t1 == t2 == 0.04 and np.array_equal(Q1, Q2)
+
+
+def test_nccl_transport_selftest(cuda_ok):
+    """The NCCL calls of a multi-rank step (grouped fp64/fp32 send/recv on a comm
+    stream, uint64 allreduce-min on the compute stream) through libhgks's runtime
+    NCCL binding, on a one-rank communicator (one GPU here)."""
+    hgks.nccl_selftest()
