@@ -100,11 +100,13 @@ def test_t_stop_clipping(cuda_ok):
     assert g.step(5, t_stop=0.05)["steps_done"] == 0
 
 
-def test_bench_size_one_step(cuda_ok):
-    """configs[1] at the bench size N=48 (663,552 tets): one full step, every cell vs the oracle."""
+def test_bench_size_steps(cuda_ok):
+    """configs[1] at the bench size N=48 (663,552 tets) in bench.py's launch configuration:
+    one eager step, then one step replayed from the captured CUDA graph; every cell vs the
+    oracle after each."""
     mi = W.kuhn_box(48)
     Q0 = W.advection_ic(mi)
-    errs, _, _ = run_pair(mi, Q0, 1)
+    errs, _, _ = run_pair(mi, Q0, 2)
     assert errs.max() <= TOL, errs.max(axis=0)
 
 
@@ -228,3 +230,11 @@ def test_cuda_graph_steps_match_eager(cuda_ok, monkeypatch):
         out[g] = s.get_state()
     assert np.array_equal(out["0"][0], out["1"][0])
     assert out["0"][2] == out["1"][2]
+
+
+def test_c3_size_steps(cuda_ok):
+    """configs[2] at the bench size (sphere shell N = 35, 514,500 hexes; NS tau, wall +
+    farfield) with the parity IC: an eager and a graph-replayed step, every cell vs the oracle."""
+    mi, Q0, oc, gc = sphere_case(35, 0.2535, 118.0)
+    errs, _, _ = run_pair(mi, Q0, 2, ocfg=oc, gcfg=gc)
+    assert errs.max() <= TOL, errs.max(axis=0)
