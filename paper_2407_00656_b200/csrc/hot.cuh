@@ -653,8 +653,9 @@ __device__ __forceinline__ TimeCoef time_coef(Real delta, Real tau) {
   return c;
 }
 
-// Q0 = int_{u>0} psi g_l + int_{u<0} psi g_r
-__device__ __forceinline__ void equilibrium_state(const Real ql[5], const Real qr[5], Real K, Real Q0[5]) {
+// Q0 = int_{u>0} psi g_l + int_{u<0} psi g_r, through the primitive
+// variables with lambda (the moment form keeps this one: measured faster there)
+__device__ __forceinline__ void equilibrium_state_lam(const Real ql[5], const Real qr[5], Real K, Real Q0[5]) {
   const Real rpi = Real(0.56418958354775628);  // 1/sqrt(pi)
   const Prim l = prim_of(ql, K), r = prim_of(qr, K);
   const Real hl = Real(0.5) / l.lam, hr = Real(0.5) / r.lam;  // 1/(2 lambda)
@@ -671,6 +672,38 @@ __device__ __forceinline__ void equilibrium_state(const Real ql[5], const Real q
   Q0[3] = l.rho * a0 * l.W + r.rho * b0 * r.W;
   Q0[4] = Real(0.5) * l.rho * (a2 + a0 * (l.V * l.V + l.W * l.W + (K + Real(2.0)) * hl)) +
           Real(0.5) * r.rho * (b2 + b0 * (r.V * r.V + r.W * r.W + (K + Real(2.0)) * hr));
+}
+
+// The same Q0 for the tau = 0 path
+// In terms of h = 1/(2 lambda) = p/rho = (gamma-1) rho e/rho and s = sqrt(lambda) U =
+// U/sqrt(2h): one division per side (1/rho) instead of three.
+__device__ __forceinline__ void equilibrium_state(const Real ql[5], const Real qr[5], Real K, Real Q0[5]) {
+  const Real rpi = Real(0.56418958354775628);  // 1/sqrt(pi)
+  const Real c2k = Real(2.0) / (K + Real(3.0));  // = gamma - 1
+  auto side = [&](const Real q[5], Real sg, Real& rho, Real& V, Real& W, Real& h, Real m[3]) {
+    rho = q[0];
+    const Real inv = Real(1.0) / q[0];
+    const Real U = q[1] * inv;
+    V = q[2] * inv;
+    W = q[3] * inv;
+    const Real rhoe = q[4] - Real(0.5) * (q[1] * U + q[2] * V + q[3] * W);
+    h = c2k * rhoe * inv;
+    const Real rs = rsqrt(h + h);   // sqrt(lambda)
+    const Real sq = (h + h) * rs;   // 1/sqrt(lambda)
+    const Real x = U * rs;
+    m[0] = Real(0.5) * erfc(-sg * x);
+    m[1] = U * m[0] + sg * (Real(0.5) * exp(-x * x) * rpi * sq);
+    m[2] = U * m[1] + m[0] * h;
+  };
+  Real rl, Vl, Wl, hl, a[3], rr, Vr, Wr, hr, b[3];
+  side(ql, Real(1.0), rl, Vl, Wl, hl, a);    // u > 0 half of g_l
+  side(qr, Real(-1.0), rr, Vr, Wr, hr, b);   // u < 0 half of g_r
+  Q0[0] = rl * a[0] + rr * b[0];
+  Q0[1] = rl * a[1] + rr * b[1];
+  Q0[2] = rl * a[0] * Vl + rr * b[0] * Vr;
+  Q0[3] = rl * a[0] * Wl + rr * b[0] * Wr;
+  Q0[4] = Real(0.5) * rl * (a[2] + a[0] * (Vl * Vl + Wl * Wl + (K + Real(2.0)) * hl)) +
+          Real(0.5) * rr * (b[2] + b[0] * (Vr * Vr + Wr * Wr + (K + Real(2.0)) * hr));
 }
 
 // One term group of Eq. (flux) for a Maxwellian with its slopes, accumulated into
@@ -927,7 +960,8 @@ __global__ void __launch_bounds__((NV == 3 ? 3 : 4) * HGKS_FLUX_FPB,
       boundary_right<BC>(ql, dql, vl, n, t1, t2, a.gp, qr, dqr);
     }
     Real Q0[5];
-    equilibrium_state(ql, qr, K, Q0);
+    if (TAU0) equilibrium_state(ql, qr, K, Q0);
+    else equilibrium_state_lam(ql, qr, K, Q0);
     if (TAU0) {
       Real dtQ0[5] = {Real(0.0), Real(0.0), Real(0.0), Real(0.0), Real(0.0)};
       const EulerState es = euler_state(Q0, gm1);
