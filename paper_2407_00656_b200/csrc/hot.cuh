@@ -348,6 +348,223 @@ __global__ void __launch_bounds__(ReconShape<K>::BT, ReconShape<K>::MINB) k_reco
 }
 
 
+// Two lanes per reconstructed cell: lane part 0 carries variables 0-2, part 1
+// variables 3-4 (its third slot repeats variable 4 and is not written), so the
+// per-thread state is three variables instead of five and three 128-thread
+// blocks (64 cells each) fit per SM; both lanes read the same operator words.
+#ifndef HGKS_RPAIR_MINB
+#define HGKS_RPAIR_MINB 3
+#endif
+template <int K, int M, int NM>
+__global__ void __launch_bounds__(128, HGKS_RPAIR_MINB) k_recon_pair(ReconArgs a) {
+  constexpr int NS = 3;  // variable slots per lane
+  constexpr int BT = 128, SPLIT = 2;                 // 64 cells per block, two blocks per tile
+  constexpr int QP = NS * BT;                        // values per member plane: [slot][thread]
+  constexpr int E = 9 * K + 3 * M * NM;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Real* smem = reinterpret_cast<Real*>(smem_raw);
+  Real* __restrict__ dqs = smem;                   // [K][NS][BT] Q_k - Q_i (this lane's slots)
+  const int tl = threadIdx.x;
+  const int part = tl & 1;                           // 0: variables 0-2, 1: variables 3-4
+  const int half = (int)(blockIdx.x % SPLIT);
+  const int t = half * 64 + (tl >> 1);               // position in the 128-cell tile
+  const int tile = a.tile0 + (int)(blockIdx.x / SPLIT);
+  const int r = tile * kTile + t;
+  int ci = r < a.n_recon ? __ldg(a.recon_cell + r) : -1;  // -1: padding
+  const bool active = ci >= 0;
+  if (!active) ci = 0;
+  // tiled entry-major per-cell arrays (setup.cpp): entry e of this cell at (tile*NE + e)*kTile + t
+  const size_t tb = (size_t)tile * kTile;
+  const int* __restrict__ sid = a.st_id + tb * K + t;
+  // this lane's slots of a state row: part 0 (v0, v1, v2), part 1 (v3, v4, v4)
+  auto slots = [&](const R2 x0, const R2 x1, Real o[NS]) {
+    o[0] = part ? x0.y : x0.x;
+    o[1] = part ? x1.x : x0.y;
+    o[2] = x1.x;
+  };
+  Real qi[NS];
+  {
+    const R2* q2 = reinterpret_cast<const R2*>(a.Q + (size_t)ci * QS) + part;
+    slots(__ldg(q2), __ldg(q2 + 1), qi);
+  }
+#ifndef HGKS_NO_L2_PREFETCH
+  // The block's operators are one contiguous E*kTile*8-byte range (tiled layout):
+  // fire TMA bulk prefetches of it into L2 now, so the streamed operator loads
+  // below see L2 rather than DRAM latency (the warps cannot keep enough loads
+  // in flight at 255 registers).
+  if (t < 8 && part == 0) {  // first block of the tile
+    constexpr uint32_t bytes = (uint32_t)E * kTile * sizeof(Real);
+    constexpr uint32_t chunk = ((bytes / 8) + 15) / 16 * 16;
+    const uint32_t off = t * chunk;
+    if (off < bytes) {
+      const uint32_t n = min(chunk, bytes - off);
+      const char* src = reinterpret_cast<const char*>(a.op + tb * E) + off;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(n) : "memory");
+    }
+  }
+#endif
+  // gather the stencil members in groups (bounded registers, 7 x 3 loads in flight)
+  constexpr int G = 7;
+#pragma unroll
+  for (int k0 = 0; k0 < K; k0 += G) {
+    R2 x[G][2];
+#pragma unroll
+    for (int k = k0; k < k0 + G && k < K; ++k) {
+      const R2* q2 = reinterpret_cast<const R2*>(a.Q + (size_t)__ldg(sid + k * kTile) * QS) + part;
+      x[k - k0][0] = __ldg(q2);
+      x[k - k0][1] = __ldg(q2 + 1);
+    }
+#pragma unroll
+    for (int k = k0; k < k0 + G && k < K; ++k) {
+      Real v3[NS];
+      slots(x[k - k0][0], x[k - k0][1], v3);
+      Real* d = dqs + k * QP + tl;
+#pragma unroll
+      for (int j = 0; j < NS; ++j) d[j * BT] = v3[j] - qi[j];
+    }
+  }
+  const Real* __restrict__ geo = a.geo + tb * 8 + t;
+  const uint8_t* __restrict__ ssl = a.sub_slot + tb * (M * NM) + t;
+  const Real V23 = __ldg(geo), V43 = __ldg(geo + kTile);
+  Real m2[6];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) m2[q] = __ldg(geo + (2 + q) * kTile);
+  // ---- P_0: c[d][v] = sum_k A0+[d][k] (Q_k - Q_i)[v] ----
+  Real c[9][NS];
+#pragma unroll
+  for (int d = 0; d < 9; ++d)
+#pragma unroll
+    for (int v = 0; v < NS; ++v) c[d][v] = Real(0.0);
+  // operators are tiled by entry pairs: pair p of this cell at op2[p * kTile]
+  const R2* __restrict__ op2 = reinterpret_cast<const R2*>(a.op + tb * E) + t;
+  static_assert(K % 2 == 0 && (3 * M * NM) % 2 == 0, "operator pairs");
+  // measured unroll of the member-pair loop: tets (K = 14) 4, hexes (K = 24) 2
+  // (C2 0.397 -> 0.388 ms, C3 0.484 -> 0.458 ms vs no unrolling)
+  constexpr int kUnrollA0 = K <= 16 ? 4 : 2;
+#pragma unroll kUnrollA0
+  for (int k2 = 0; k2 < K; k2 += 2) {  // two members = 18 entries = 9 pairs
+    Real dq[2][NS];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int v = 0; v < NS; ++v) dq[h][v] = dqs[(k2 + h) * QP + v * BT + tl];
+    R2 w2[9];
+#pragma unroll
+    for (int p = 0; p < 9; ++p) w2[p] = __ldcs(op2 + (k2 * 9 / 2 + p) * kTile);
+#pragma unroll
+    for (int j = 0; j < 18; ++j) {
+      const Real w = (j & 1) ? w2[j >> 1].y : w2[j >> 1].x;
+      const int h = j / 9, d = j % 9;
+#pragma unroll
+      for (int v = 0; v < NS; ++v) c[d][v] = fma(w, dq[h][v], c[d][v]);
+    }
+  }
+  // smoothness indicator of P_0 (closed form SURVEY A.5)
+  Real beta0[NS];
+#pragma unroll
+  for (int v = 0; v < NS; ++v) {
+    const Real gx[3] = {Real(2.0) * c[3][v], c[6][v], c[7][v]}, gy[3] = {c[6][v], Real(2.0) * c[4][v], c[8][v]},
+                 gz[3] = {c[7][v], c[8][v], Real(2.0) * c[5][v]};
+    auto quadf = [&](const Real g[3]) {
+      return m2[0] * g[0] * g[0] + m2[1] * g[1] * g[1] + m2[2] * g[2] * g[2] +
+             Real(2.0) * (m2[3] * g[0] * g[1] + m2[4] * g[0] * g[2] + m2[5] * g[1] * g[2]);
+    };
+    const Real s1 = c[0][v] * c[0][v] + c[1][v] * c[1][v] + c[2][v] * c[2][v] + quadf(gx) + quadf(gy) + quadf(gz);
+    const Real s2 = Real(4.0) * (c[3][v] * c[3][v] + c[4][v] * c[4][v] + c[5][v] * c[5][v]) + c[6][v] * c[6][v] +
+                      c[7][v] * c[7][v] + c[8][v] * c[8][v];
+    beta0[v] = V23 * s1 + V43 * s2;
+  }
+  const R2* __restrict__ opm2 = op2 + (9 * K / 2) * kTile;
+  auto sub_slopes = [&](int m, Real b[3][NS]) {  // P_m over sub-stencil m
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int v = 0; v < NS; ++v) b[d][v] = Real(0.0);
+#pragma unroll
+    for (int j = 0; j < NM; ++j) {
+      const int sl = __ldg(ssl + (m * NM + j) * kTile);
+      Real dq[NS];
+#pragma unroll
+      for (int v = 0; v < NS; ++v) dq[v] = dqs[sl * QP + v * BT + tl];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const int e = (m * NM + j) * 3 + d;
+        const R2 wp = __ldg(opm2 + (e >> 1) * kTile);
+        const Real w = (e & 1) ? wp.y : wp.x;
+#pragma unroll
+        for (int v = 0; v < NS; ++v) b[d][v] = fma(w, dq[v], b[d][v]);
+      }
+    }
+  };
+  // ---- pass 1: beta_m and the nonlinear weights ----
+  const Real gm = Real(0.025), g0 = Real(1.0) - Real(0.025) * M;
+  Real al0[NS], alm[M][NS];
+  {
+    Real tz[NS] = {0, 0, 0};
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      Real b[3][NS];
+      sub_slopes(m, b);
+#pragma unroll
+      for (int v = 0; v < NS; ++v) {
+        alm[m][v] = V23 * (b[0][v] * b[0][v] + b[1][v] * b[1][v] + b[2][v] * b[2][v]);  // beta_m
+        tz[v] += fabs(beta0[v] - alm[m][v]);
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < NS; ++v) {
+      const Real tzv = tz[v] * (Real(1.0) / M);
+      const Real r0 = tzv / (beta0[v] + a.eps);
+      const Real w0 = g0 * (Real(1.0) + (a.omega_pow == 2 ? r0 * r0 : r0));
+      Real sum = w0;
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        const Real rm = tzv / (alm[m][v] + a.eps);
+        alm[m][v] = gm * (Real(1.0) + (a.omega_pow == 2 ? rm * rm : rm));  // omega_m
+        sum += alm[m][v];
+      }
+      const Real inv = Real(1.0) / sum;
+      al0[v] = w0 * inv / g0;  // omega-bar_0 / gamma_0
+#pragma unroll
+      for (int m = 0; m < M; ++m) alm[m][v] = alm[m][v] * inv - al0[v] * gm;  // omega-bar_m - omega-bar_0 gamma_m/gamma_0
+    }
+  }
+  // ---- collapse to one quadratic ----
+  Real lin[3][NS];
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+#pragma unroll
+    for (int v = 0; v < NS; ++v) lin[d][v] = al0[v] * c[d][v];
+#pragma unroll
+  for (int m = 0; m < M; ++m) {  // pass 2: weighted sum of the sub-stencil slopes
+    Real b[3][NS];
+    sub_slopes(m, b);
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int v = 0; v < NS; ++v) lin[d][v] = fma(alm[m][v], b[d][v], lin[d][v]);
+  }
+  if (!active) return;
+  // this lane's variables: part 0 writes v = 0, 1, 2; part 1 writes v = 3, 4
+  R2* dst = reinterpret_cast<R2*>(a.ceff + (size_t)ci * kRec) + 15 * part;
+#pragma unroll
+  for (int v = 0; v < NS; ++v) {
+    if (part && v == 2) break;
+    Real quad[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) quad[q] = al0[v] * c[3 + q][v];
+    // zero-mean basis: p_ab = X_a X_b - M2_ab
+    const Real cst = qi[v] - (quad[0] * m2[0] + quad[1] * m2[1] + quad[2] * m2[2] + quad[3] * m2[3] +
+                                quad[4] * m2[4] + quad[5] * m2[5]);
+    dst[5 * v + 0] = make_R2(cst, lin[0][v]);
+    dst[5 * v + 1] = make_R2(lin[1][v], lin[2][v]);
+    dst[5 * v + 2] = make_R2(quad[0], quad[1]);
+    dst[5 * v + 3] = make_R2(quad[2], quad[3]);
+    dst[5 * v + 4] = make_R2(quad[4], quad[5]);
+  }
+}
+
+
 // a8 + a9: per Gauss point, evaluate both effective polynomials, rotate into
 // the local frame, compute the BGK interface flux of Eq. (flux)
 // and its time fit, rotate back and sum the face
@@ -1210,6 +1427,15 @@ struct Launch {
   static cudaError_t recon_smem() {
     return cudaFuncSetAttribute(k_recon<K, M, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)ReconShape<K>::SMEM);
+  }
+  template <int K, int M, int NM>
+  static cudaError_t recon_pair_smem() {
+    return cudaFuncSetAttribute(k_recon_pair<K, M, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(sizeof(Real) * (size_t)K * 3 * 128));
+  }
+  template <int K, int M, int NM>
+  static void recon_pair(int n_tiles, cudaStream_t st, const ReconArgs& a) {
+    k_recon_pair<K, M, NM><<<n_tiles * 2, 128, sizeof(Real) * (size_t)K * 3 * 128, st>>>(a);
   }
   template <int K, int M, int NM>
   static void recon(int n_tiles, cudaStream_t st, const ReconArgs& a) {

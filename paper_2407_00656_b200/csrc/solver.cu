@@ -207,6 +207,8 @@ struct hgks_solver {
   hgks_config cfg;
   GasParams gp;
   bool fp32 = false;  // working precision of the hot path (FP32 variant)
+  int recon_pair = -1;  // two lanes per reconstructed cell: -1 = measured choice (fp32 tets only:
+                        // -7 %; slower for fp64 and for fp32 hexes), HGKS_RECON_PAIR=0/1 forces
   size_t rs = sizeof(double);
   int rank = 0, n_ranks = 1, device = 0, transport = HGKS_TRANSPORT_NCCL;
   size_t recon_smem_set = 0;
@@ -294,11 +296,15 @@ template <class L, int K, int M, int NM>
 void run_recon_k(hgks_solver* s, const typename L::ReconArgsT& a) {
   if (!s->recon_smem_set) {  // one reconstruction instantiation per solver (K, M, NM, precision fixed)
     CUDA_TRY((L::template recon_smem<K, M, NM>()));
+    CUDA_TRY((L::template recon_pair_smem<K, M, NM>()));
     s->recon_smem_set = 1;
   }
   const int n_tiles = s->recon_t1 - a.tile0;
   if (n_tiles <= 0) return;
-  launch(s, "k_recon", [&] { L::template recon<K, M, NM>(n_tiles, s->stream, a); });
+  if (s->recon_pair == 1 || (s->recon_pair < 0 && s->fp32 && K <= 16))
+    launch(s, "k_recon", [&] { L::template recon_pair<K, M, NM>(n_tiles, s->stream, a); });
+  else
+    launch(s, "k_recon", [&] { L::template recon<K, M, NM>(n_tiles, s->stream, a); });
 }
 
 // part 0: tiles of the early cells, 1: the rest, 2: all
@@ -653,6 +659,7 @@ hgks_status hgks_init(const hgks_mesh* mc, const hgks_config* cfg, const hgks_di
     if (dist) CUDA_TRY(cudaSetDevice(dist->device));
     CUDA_TRY(cudaGetDevice(&s->device));
     if (const char* e = std::getenv("HGKS_GRAPHS")) s->use_graphs = std::atoi(e) != 0;
+    if (const char* e = std::getenv("HGKS_RECON_PAIR")) s->recon_pair = std::atoi(e) != 0 ? 1 : 0;
     s->stream = (cudaStream_t)stream;
     s->rp = &m->plan(s->rank);
     s->lay = m->gm.lay;

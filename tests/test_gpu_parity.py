@@ -238,3 +238,16 @@ def test_c3_size_steps(cuda_ok):
     mi, Q0, oc, gc = sphere_case(35, 0.2535, 118.0)
     errs, _, _ = run_pair(mi, Q0, 2, ocfg=oc, gcfg=gc)
     assert errs.max() <= TOL, errs.max(axis=0)
+
+
+@pytest.mark.parametrize("pair", ["0", "1"])
+def test_recon_lane_pair_variant(cuda_ok, monkeypatch, pair):
+    """Reconstruction with one or two lanes per cell (the fp32 default is two) meets the bar
+    on the jittered tet box and the sphere shell."""
+    monkeypatch.setenv("HGKS_RECON_PAIR", pair)
+    mi = W.kuhn_box(7, jitter=0.1)
+    errs, _, _ = run_pair(mi, W.advection_ic(mi), 5)
+    assert errs.max() <= TOL, errs.max(axis=0)
+    mi, Q0, oc, gc = sphere_case(4, 0.2535, 118.0)
+    errs, _, _ = run_pair(mi, Q0, 5, ocfg=oc, gcfg=gc)
+    assert errs.max() <= TOL, errs.max(axis=0)
