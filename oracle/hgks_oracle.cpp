@@ -23,8 +23,9 @@
 // numerical quadrature, slopes vs numpy solve, single-face flux vs brute-force
 // velocity/time quadrature of Eq. (flux), tau=0 Euler-chain identity,
 // S2O4 Taylor polynomial, conservation, free-stream preservation, and the
-// paper's Table 3 convergence (T3).  Parity unpinned: the farfield Riemann
-// state and wall mirror (R25) beyond free-stream/symmetry checks.
+// paper's Table 3 convergence (T3), the farfield Riemann state against the
+// characteristic conditions.  Parity unpinned: the wall mirror (R25) beyond
+// free-stream/symmetry checks.
 // ============================================================================
 #include <algorithm>
 #include <array>

@@ -12,7 +12,8 @@ Parity status per function:
                                              Euler limits, tau=0 Euler-chain identity)
   S2O4 stages ............................. pinned (Taylor polynomial of exp(z))
   full step ............................... pinned (conservation, free stream, T3 orders)
-  wall / farfield boundary states ......... parity unpinned beyond free stream + symmetry
+  farfield boundary state ................. pinned (characteristic conditions, seeded states)
+  wall boundary state ..................... parity unpinned beyond free stream + symmetry
 """
 from __future__ import annotations
 

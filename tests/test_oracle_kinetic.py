@@ -335,3 +335,50 @@ def test_farfield_state_consistency():
     qi = W.uniform_state(1, 0.8, (0.1, 0, 0), 0.9)[0]
     qf = W.uniform_state(1, 1.0, (1.5, 0, 0), 1 / 1.4)[0]
     assert np.allclose(O.farfield_state(qi, np.array([-1.0, 0, 0]), cfg), qf, rtol=1e-13)
+
+
+def test_farfield_state_characteristics():
+    """Farfield ghost state (R25) against the textbook characteristic boundary
+    condition along the face normal, on seeded random states: supersonic outflow
+    returns the interior state, supersonic inflow the free stream; subsonic faces
+    keep the outgoing invariant R+ = u_n + 2c/(g-1) of the interior and the incoming
+    R- = u_n - 2c/(g-1) of the free stream, with tangential velocity and entropy
+    p/rho^g from the upwind side."""
+    g = 1.4
+    rng = np.random.default_rng(20240700)
+
+    def prim(q):
+        rho = q[0]; u = q[1:4] / rho
+        p = (g - 1) * (q[4] - 0.5 * rho * u @ u)
+        return rho, u, p, np.sqrt(g * p / rho)
+
+    seen = set()
+    for _ in range(400):
+        n = rng.normal(size=3); n /= np.linalg.norm(n)
+        rho_i, rho_f = rng.uniform(0.3, 3.0, 2)
+        p_i, p_f = rng.uniform(0.3, 3.0, 2)
+        ui = rng.normal(size=3) * rng.uniform(0, 2.5)
+        uf = rng.normal(size=3) * rng.uniform(0, 2.5)
+        qi = np.r_[rho_i, rho_i * ui, p_i / (g - 1) + 0.5 * rho_i * ui @ ui]
+        cfg = O.OracleConfig(gamma=g, freestream=(rho_f, *uf, p_f))
+        qf = np.r_[rho_f, rho_f * uf, p_f / (g - 1) + 0.5 * rho_f * uf @ uf]
+        qb = O.farfield_state(qi, n, cfg)
+        _, _, _, c_i = prim(qi)
+        _, _, _, c_f = prim(qf)
+        un_i, un_f = ui @ n, uf @ n
+        rb, ub, pb, cb = prim(qb)
+        unb = ub @ n
+        if un_i - c_i > 0 and un_f + c_f >= 0:
+            seen.add("out")
+            assert np.allclose(qb, qi, rtol=1e-12, atol=1e-12)
+        elif un_f + c_f < 0 and un_i - c_i <= 0:
+            seen.add("in")
+            assert np.allclose(qb, qf, rtol=1e-12, atol=1e-12)
+        elif abs(un_i) < c_i and abs(un_f) < c_f:
+            seen.add("sub")
+            assert abs((unb + 2 * cb / (g - 1)) - (un_i + 2 * c_i / (g - 1))) < 1e-11
+            assert abs((unb - 2 * cb / (g - 1)) - (un_f - 2 * c_f / (g - 1))) < 1e-11
+            up_u, up_rho, up_p = (ui, rho_i, p_i) if unb > 0 else (uf, rho_f, p_f)
+            assert np.allclose(ub - unb * n, up_u - (up_u @ n) * n, atol=1e-12)
+            assert abs(pb / rb ** g - up_p / up_rho ** g) < 1e-11 * (up_p / up_rho ** g)
+    assert seen == {"out", "in", "sub"}, seen
