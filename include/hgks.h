@@ -8,7 +8,7 @@
  *   - BGK gas-kinetic flux per face Gauss point      (Eqs. flux-G/flux)
  *   - two-stage fourth-order update + CFL minimum    (Alg. 2)
  *   - halo exchange of 3 ghost layers + min(dt), NCCL
- * Readings of points where the paper is silent are DESIGN.md R1-R26.
+ * Readings of points where the paper is silent are DESIGN.md R1-R28.
  *
  * Conventions for every call:
  *   - Return value: HGKS_OK (0) or an error code below; nothing throws or
