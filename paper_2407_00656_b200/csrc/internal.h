@@ -58,9 +58,8 @@ struct GlobalMesh {
   std::vector<int64_t> big_off, big_id; // CSR
   std::vector<double> big_shift;
   std::vector<int8_t> sub_slot;         // [nc][M][NM] slot into big stencil, -1 pad
-  // least-squares operators per cell, [nc][op_entries]: A0+ (9 x K, row d,
-  // column k) then A_m+ (M x 3 x NM); physical units (R20)
-  std::vector<double> op;
+  // (least-squares operators are built per rank for its reconstructed cells:
+  //  setup.cpp cell_operators; there is no global table)
   // partition
   int32_t n_ranks = 1;
   std::vector<int32_t> part;

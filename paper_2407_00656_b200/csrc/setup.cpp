@@ -581,81 +581,8 @@ GlobalMesh build_global_mesh(const double* xyz, int64_t n_nodes, const int8_t* t
       }
   }
   pt.lap("stencils");
-  // ---------------- least-squares operators (a2) ----------------
-  const int E = L.op_entries();
-  gm.op.assign((size_t)n_cells * E, 0.0);
-  int64_t lsq_bad = -1;
-#pragma omp parallel for schedule(dynamic, 256)
-  for (int64_t i = 0; i < n_cells; ++i) {
-    const int64_t o0 = gm.big_off[i];
-    const int K = (int)(gm.big_off[i + 1] - o0);
-    const double Vi = gm.V[i];
-    const double h = std::cbrt(Vi);
-    P3 ci = centroid(i);
-    const double* mi = &gm.M2[6 * i];
-    // rows: member image centroid offset D and zero-mean quadratic moments (A.4)
-    double A[64 * 9];
-    if (K > 64) {
-#pragma omp critical
-      if (lsq_bad < 0 || i < lsq_bad) lsq_bad = i;
-      continue;
-    }
-    for (int k = 0; k < K; ++k) {
-      int64_t id = gm.big_id[o0 + k];
-      P3 ck;
-      const double* mk;
-      if (id < n_cells) {
-        ck = centroid(id);
-        mk = &gm.M2[6 * id];
-      } else {
-        int64_t g = id - n_cells;
-        ck = {gm.gC[3 * g], gm.gC[3 * g + 1], gm.gC[3 * g + 2]};
-        mk = &gm.gM2[6 * g];
-      }
-      P3 D = (ck + P3{gm.big_shift[3 * (o0 + k)], gm.big_shift[3 * (o0 + k) + 1], gm.big_shift[3 * (o0 + k) + 2]}) - ci;
-      double* r = &A[k * 9];
-      r[0] = D.x / h; r[1] = D.y / h; r[2] = D.z / h;
-      const double h2 = h * h;
-      r[3] = (mk[0] + D.x * D.x - mi[0]) / h2;
-      r[4] = (mk[1] + D.y * D.y - mi[1]) / h2;
-      r[5] = (mk[2] + D.z * D.z - mi[2]) / h2;
-      r[6] = (mk[3] + D.x * D.y - mi[3]) / h2;
-      r[7] = (mk[4] + D.x * D.z - mi[4]) / h2;
-      r[8] = (mk[5] + D.y * D.z - mi[5]) / h2;
-    }
-    double* op = &gm.op[(size_t)i * E];
-    double P[9 * 64];
-    bool ok = K >= 9 && pinv_qr(K, 9, A, P);
-    if (ok)
-      for (int d = 0; d < 9; ++d)
-        for (int k = 0; k < K; ++k) op[d * L.K + k] = P[d * K + k] / (d < 3 ? h : h * h);
-    const int8_t* ss = &gm.sub_slot[i * L.M * L.NM];
-    for (int m = 0; m < L.M && ok; ++m) {
-      int n = 0;
-      double As[3 * 8];
-      int slots[8];
-      for (int j = 0; j < L.NM; ++j)
-        if (ss[m * L.NM + j] >= 0) {
-          slots[n] = ss[m * L.NM + j];
-          for (int a = 0; a < 3; ++a) As[n * 3 + a] = A[slots[n] * 9 + a];
-          ++n;
-        }
-      double Ps[3 * 8];
-      if (n < 3 || !pinv_qr(n, 3, As, Ps)) {
-        ok = false;
-        break;
-      }
-      double* om = op + 9 * L.K + m * 3 * L.NM;
-      for (int d = 0; d < 3; ++d)
-        for (int j = 0; j < n; ++j) om[d * L.NM + j] = Ps[d * n + j] / h;
-    }
-    if (!ok) {
-#pragma omp critical
-      if (lsq_bad < 0 || i < lsq_bad) lsq_bad = i;
-    }
-  }
-  if (lsq_bad >= 0) throw Error(3, "rank-deficient least-squares stencil at cell " + std::to_string(lsq_bad));
-  pt.lap("least squares");
+  // least-squares operators (a2) are built per rank for the cells it reconstructs
+  // (cell_operators, called from build_rank_plan): no global [nc][E] table
   // ---------------- partition (a3) ----------------
   gm.n_ranks = std::max(1, n_ranks);
   gm.part.assign(n_cells, 0);
@@ -711,6 +638,70 @@ GlobalMesh build_global_mesh(const double* xyz, int64_t n_nodes, const int8_t* t
 // ============================================================================
 // Per-rank plan: owned cells (Morton order), 3 ghost layers grouped by owner
 // rank, device arrays in entry-major layout.
+// Least-squares operators of cell i (a2, P:432-442 with the scaled basis of R20),
+// written to op[E] in the global-table order: A0+ (9 x K, row d, /h^|d|) then the
+// sub-stencil pseudo-inverses (M x 3 x NM, /h).  Entries of absent members stay 0.
+// Returns false for a rank-deficient system.
+static bool cell_operators(const GlobalMesh& gm, int64_t i, double* op) {
+  const Layout& L = gm.lay;
+  const int64_t n_cells = gm.nc;
+  const int E = L.op_entries();
+  for (int e = 0; e < E; ++e) op[e] = 0.0;
+  const int64_t o0 = gm.big_off[i];
+  const int K = (int)(gm.big_off[i + 1] - o0);
+  if (K > 64 || K < 9) return false;
+  const double h = std::cbrt(gm.V[i]);
+  const P3 ci{gm.C[3 * i], gm.C[3 * i + 1], gm.C[3 * i + 2]};
+  const double* mi = &gm.M2[6 * i];
+  // rows: member image centroid offset D and zero-mean quadratic moments (A.4)
+  double A[64 * 9];
+  for (int k = 0; k < K; ++k) {
+    int64_t id = gm.big_id[o0 + k];
+    P3 ck;
+    const double* mk;
+    if (id < n_cells) {
+      ck = {gm.C[3 * id], gm.C[3 * id + 1], gm.C[3 * id + 2]};
+      mk = &gm.M2[6 * id];
+    } else {
+      int64_t g = id - n_cells;
+      ck = {gm.gC[3 * g], gm.gC[3 * g + 1], gm.gC[3 * g + 2]};
+      mk = &gm.gM2[6 * g];
+    }
+    P3 D = (ck + P3{gm.big_shift[3 * (o0 + k)], gm.big_shift[3 * (o0 + k) + 1], gm.big_shift[3 * (o0 + k) + 2]}) - ci;
+    double* r = &A[k * 9];
+    r[0] = D.x / h; r[1] = D.y / h; r[2] = D.z / h;
+    const double h2 = h * h;
+    r[3] = (mk[0] + D.x * D.x - mi[0]) / h2;
+    r[4] = (mk[1] + D.y * D.y - mi[1]) / h2;
+    r[5] = (mk[2] + D.z * D.z - mi[2]) / h2;
+    r[6] = (mk[3] + D.x * D.y - mi[3]) / h2;
+    r[7] = (mk[4] + D.x * D.z - mi[4]) / h2;
+    r[8] = (mk[5] + D.y * D.z - mi[5]) / h2;
+  }
+  double P[9 * 64];
+  if (!pinv_qr(K, 9, A, P)) return false;
+  for (int d = 0; d < 9; ++d)
+    for (int k = 0; k < K; ++k) op[d * L.K + k] = P[d * K + k] / (d < 3 ? h : h * h);
+  const int8_t* ss = &gm.sub_slot[i * L.M * L.NM];
+  for (int m = 0; m < L.M; ++m) {
+    int n = 0;
+    double As[3 * 8];
+    int slots[8];
+    for (int j = 0; j < L.NM; ++j)
+      if (ss[m * L.NM + j] >= 0) {
+        slots[n] = ss[m * L.NM + j];
+        for (int a = 0; a < 3; ++a) As[n * 3 + a] = A[slots[n] * 9 + a];
+        ++n;
+      }
+    double Ps[3 * 8];
+    if (n < 3 || !pinv_qr(n, 3, As, Ps)) return false;
+    double* om = op + 9 * L.K + m * 3 * L.NM;
+    for (int d = 0; d < 3; ++d)
+      for (int j = 0; j < n; ++j) om[d * L.NM + j] = Ps[d * n + j] / h;
+  }
+  return true;
+}
+
 RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
   const Layout& L = gm.lay;
   const int64_t nc = gm.nc;
@@ -854,7 +845,7 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
       if (gm.big_id[o] >= nc) local_of(gm.big_id[o]);
   }
   int smin = 1 << 30, smax = 0;
-  int64_t bad = -1;
+  int64_t bad = -1, lsq_bad = -1;
 #pragma omp parallel for schedule(static) reduction(min : smin) reduction(max : smax)
   for (int64_t r = 0; r < Rn; ++r) {
     if (rp.recon_cell[r] < 0) continue;  // padding of the early block
@@ -885,7 +876,11 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
     }
     // streaming order of the operator entries (hot.cuh k_recon): A0+ member-major
     // (row k*9 + d), then the sub-stencil operators (row 9K + (m*NM + j)*3 + d)
-    const double* op = &gm.op[(size_t)gi * E];
+    double op[9 * 64 + 8 * 3 * 8];
+    if (!cell_operators(gm, gi, op)) {
+#pragma omp critical
+      if (lsq_bad < 0 || gi < lsq_bad) lsq_bad = gi;
+    }
     for (int d = 0; d < 9; ++d)
       for (int k = 0; k < K; ++k) rp.op[tp(r, E, k * 9 + d)] = op[d * K + k];
     for (int m = 0; m < M; ++m)
@@ -897,6 +892,7 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
     for (int k = 0; k < 6; ++k) rp.geo[ti(r, 8, 2 + k)] = gm.M2[6 * gi + k];
   }
   if (bad >= 0) throw Error(1, "ghost closure violated for cell " + std::to_string(bad));
+  if (lsq_bad >= 0) throw Error(3, "rank-deficient least-squares stencil at cell " + std::to_string(lsq_bad));
   rp.stencil_min = smin;
   rp.stencil_max = smax;
   pt.lap("tiled per-cell arrays");
