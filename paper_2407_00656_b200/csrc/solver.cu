@@ -2,7 +2,11 @@
 //
 // One solver per process/GPU.  The caller owns device memory (a workspace
 // carved here) and the stream; NCCL (loaded at run time with dlopen, only when
-// n_ranks > 1) carries the per-stage halo exchange and the per-step min(dt).
+// n_ranks > 1) carries the per-stage halo exchange on a comm stream, overlapped
+// with the ghost-free half of every stage, and the per-step min(dt).  On one
+// rank a step is replayed from a captured CUDA graph; host state copies run on
+// two internal copy streams, double-buffered (hgks_get_state_async).  The hot
+// path is compiled for fp64 (p64) and fp32 (p32) and dispatched per solver.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
