@@ -175,9 +175,12 @@ __global__ void __launch_bounds__(ReconShape<K>::BT, ReconShape<K>::MINB) k_reco
   // fire TMA bulk prefetches of it into L2 now, so the streamed operator loads
   // below see L2 rather than DRAM latency (the warps cannot keep enough loads
   // in flight at 255 registers).
-  if (t < 8) {  // first block of the tile
+#ifndef HGKS_PF_CHUNKS
+#define HGKS_PF_CHUNKS 8
+#endif
+  if (t < HGKS_PF_CHUNKS) {  // first block of the tile
     constexpr uint32_t bytes = (uint32_t)E * kTile * sizeof(Real);
-    constexpr uint32_t chunk = ((bytes / 8) + 15) / 16 * 16;
+    constexpr uint32_t chunk = ((bytes / HGKS_PF_CHUNKS) + 15) / 16 * 16;
     const uint32_t off = t * chunk;
     if (off < bytes) {
       const uint32_t n = min(chunk, bytes - off);
