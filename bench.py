@@ -361,6 +361,11 @@ def main():
                             "share": v["ms"] / max(1e-30, sum(x["ms"] for x in ktimes.values()))}
                         for k, v in ktimes.items()},
             "fallbacks": st["fallbacks"],
+            # context only: the paper's GPU codes ran ~5x (RTX A5000) and ~9x (V100)
+            # faster than its 56-core Xeon OpenMP code; here the ratio is to the
+            # CPU oracle (a deliberately plain program) on this box's host cores
+            "context": {"paper_speedup_vs_56_core_cpu": {"A5000": 5, "V100": 9},
+                        "this_run_vs_cpu_oracle": (value / cpu["value"]) if cpu else None},
         }
         print(json.dumps(line), flush=True)
     s.close()
