@@ -747,22 +747,38 @@ struct Mom {
 };
 
 // full moments of v, w and xi; u moments over RANGE (0 full, 1 u>0, 2 u<0)
+// <u^0>, <u^1> of a Maxwellian over u > 0 (RANGE 1) or u < 0 (RANGE 2): the only
+// moments that need erfc/exp; computed once per side and shared by the
+// equilibrium state Q0 and the side's term group
+struct Half {
+  Real m0, m1;
+};
 template <int RANGE>
-__device__ __forceinline__ void maxwell_moments(Real U, Real V, Real W, Real lam, Real K, Mom& m) {
+__device__ __forceinline__ Half half_moments(Real U, Real lam) {
+  const Real sl = sqrt(lam);
+  const Real e = Real(0.5) * exp(-lam * U * U) * Real(0.56418958354775628) / sl;  // e^{-lam U^2} / (2 sqrt(pi lam))
+  Half hm;
+  if (RANGE == 1) {
+    hm.m0 = Real(0.5) * erfc(-sl * U);
+    hm.m1 = U * hm.m0 + e;
+  } else {
+    hm.m0 = Real(0.5) * erfc(sl * U);
+    hm.m1 = U * hm.m0 - e;
+  }
+  return hm;
+}
+
+template <int RANGE>
+__device__ __forceinline__ void maxwell_moments(Real U, Real V, Real W, Real lam, Real K, Mom& m,
+                                                const Half* hm = nullptr) {
   const Real h = Real(0.5) / lam;  // 1/(2 lambda)
   if (RANGE == 0) {
     m.U[0] = Real(1.0);
     m.U[1] = U;
   } else {
-    const Real sl = sqrt(lam);
-    const Real e = Real(0.5) * exp(-lam * U * U) * Real(0.56418958354775628) / sl;  // e^{-lam U^2} / (2 sqrt(pi lam))
-    if (RANGE == 1) {
-      m.U[0] = Real(0.5) * erfc(-sl * U);
-      m.U[1] = U * m.U[0] + e;
-    } else {
-      m.U[0] = Real(0.5) * erfc(sl * U);
-      m.U[1] = U * m.U[0] - e;
-    }
+    const Half x = hm ? *hm : half_moments<RANGE>(U, lam);
+    m.U[0] = x.m0;
+    m.U[1] = x.m1;
   }
 #pragma unroll
   for (int n = 0; n < 5; ++n) m.U[n + 2] = U * m.U[n + 1] + (n + 1) * h * m.U[n];
@@ -881,28 +897,7 @@ __device__ __forceinline__ TimeCoef time_coef_e(Real delta, Real tau, Real e) {
   return c;
 }
 
-// Q0 = int_{u>0} psi g_l + int_{u<0} psi g_r, through the primitive
-// variables with lambda (the moment form keeps this one: measured faster there)
-__device__ __forceinline__ void equilibrium_state_lam(const Real ql[5], const Real qr[5], Real K, Real Q0[5]) {
-  const Real rpi = Real(0.56418958354775628);  // 1/sqrt(pi)
-  const Prim l = prim_of(ql, K), r = prim_of(qr, K);
-  const Real hl = Real(0.5) / l.lam, hr = Real(0.5) / r.lam;  // 1/(2 lambda)
-  const Real isl = rsqrt(l.lam), isr = rsqrt(r.lam);
-  const Real a0 = Real(0.5) * erfc(-(l.lam * isl) * l.U);
-  const Real a1 = l.U * a0 + Real(0.5) * exp(-l.lam * l.U * l.U) * rpi * isl;
-  const Real a2 = l.U * a1 + a0 * hl;
-  const Real b0 = Real(0.5) * erfc((r.lam * isr) * r.U);
-  const Real b1 = r.U * b0 - Real(0.5) * exp(-r.lam * r.U * r.U) * rpi * isr;
-  const Real b2 = r.U * b1 + b0 * hr;
-  Q0[0] = l.rho * a0 + r.rho * b0;
-  Q0[1] = l.rho * a1 + r.rho * b1;
-  Q0[2] = l.rho * a0 * l.V + r.rho * b0 * r.V;
-  Q0[3] = l.rho * a0 * l.W + r.rho * b0 * r.W;
-  Q0[4] = Real(0.5) * l.rho * (a2 + a0 * (l.V * l.V + l.W * l.W + (K + Real(2.0)) * hl)) +
-          Real(0.5) * r.rho * (b2 + b0 * (r.V * r.V + r.W * r.W + (K + Real(2.0)) * hr));
-}
-
-// The same Q0 for the tau = 0 path
+// Q0 = int_{u>0} psi g_l + int_{u<0} psi g_r for the tau = 0 path
 // In terms of h = 1/(2 lambda) = p/rho = (gamma-1) rho e/rho and s = sqrt(lambda) U =
 // U/sqrt(2h): one division per side (1/rho) instead of three.
 __device__ __forceinline__ void equilibrium_state(const Real ql[5], const Real qr[5], Real K, Real Q0[5]) {
@@ -944,8 +939,8 @@ __device__ __forceinline__ void equilibrium_state(const Real ql[5], const Real q
 // moment sums.
 template <int RANGE>
 __device__ __forceinline__ void add_side(const Real q[5], const Real dq[3][5], Real K, Real gm1,
-                                         const TimeCoef& ch, const TimeCoef& cf, Real Ih[5], Real If[5]) {
-  const Prim g = prim_of(q, K);
+                                         const TimeCoef& ch, const TimeCoef& cf, Real Ih[5], Real If[5],
+                                         const Prim& g, const Half* hm = nullptr) {
   const Real ir = Real(1.0) / g.rho;
   Real a[3][5];
 #pragma unroll
@@ -965,7 +960,7 @@ __device__ __forceinline__ void add_side(const Real q[5], const Real dq[3][5], R
     for (int v = 0; v < 5; ++v) dtq[v] -= jv[v];
   }
   Mom mom;
-  maxwell_moments<RANGE>(g.U, g.V, g.W, g.lam, K, mom);
+  maxwell_moments<RANGE>(g.U, g.V, g.W, g.lam, K, mom, hm);
   Real m2[5];  // <(a.u) u psi> over the range
   {
     Real t0[5], t1[5], t2[5];
@@ -1188,8 +1183,31 @@ __global__ void __launch_bounds__((NV == 3 ? 3 : 4) * HGKS_FLUX_FPB,
       boundary_right<BC>(ql, dql, vl, n, t1, t2, a.gp, qr, dqr);
     }
     Real Q0[5];
-    if (TAU0) equilibrium_state(ql, qr, K, Q0);
-    else equilibrium_state_lam(ql, qr, K, Q0);
+    Prim gl, gr;
+    Half hl, hr;
+    // fp32 measured faster recomputing the halves in the term groups (register allocation)
+    constexpr bool kShareHalves = sizeof(Real) == 8;
+    if (TAU0 || !kShareHalves) {
+      equilibrium_state(ql, qr, K, Q0);
+      if (!TAU0) {
+        gl = prim_of(ql, K);
+        gr = prim_of(qr, K);
+      }
+    } else {
+      // Q0 from the half-range moments, which the g_l / g_r groups reuse
+      gl = prim_of(ql, K);
+      gr = prim_of(qr, K);
+      hl = half_moments<1>(gl.U, gl.lam);
+      hr = half_moments<2>(gr.U, gr.lam);
+      const Real hL = Real(0.5) / gl.lam, hR = Real(0.5) / gr.lam;
+      const Real a2 = gl.U * hl.m1 + hl.m0 * hL, b2 = gr.U * hr.m1 + hr.m0 * hR;
+      Q0[0] = gl.rho * hl.m0 + gr.rho * hr.m0;
+      Q0[1] = gl.rho * hl.m1 + gr.rho * hr.m1;
+      Q0[2] = gl.rho * hl.m0 * gl.V + gr.rho * hr.m0 * gr.V;
+      Q0[3] = gl.rho * hl.m0 * gl.W + gr.rho * hr.m0 * gr.W;
+      Q0[4] = Real(0.5) * gl.rho * (a2 + hl.m0 * (gl.V * gl.V + gl.W * gl.W + (K + Real(2.0)) * hL)) +
+              Real(0.5) * gr.rho * (b2 + hr.m0 * (gr.V * gr.V + gr.W * gr.W + (K + Real(2.0)) * hR));
+    }
     if (TAU0) {
       Real dtQ0[5] = {Real(0.0), Real(0.0), Real(0.0), Real(0.0), Real(0.0)};
       const EulerState es = euler_state(Q0, gm1);
@@ -1232,9 +1250,9 @@ __global__ void __launch_bounds__((NV == 3 ? 3 : 4) * HGKS_FLUX_FPB,
         for (int v = 0; v < 5; ++v) dq0[j][v] = Real(0.5) * (dql[j][v] + dqr[j][v]);
       // the two half-range groups first: each side's state dies after its group,
       // which keeps fewer values live (fewer spills) than starting with g0
-      add_side<1>(ql, dql, K, gm1, ch, cf, Ih, If);
-      add_side<2>(qr, dqr, K, gm1, ch, cf, Ih, If);
-      add_side<0>(Q0, dq0, K, gm1, ch, cf, Ih, If);
+      add_side<1>(ql, dql, K, gm1, ch, cf, Ih, If, gl, kShareHalves ? &hl : nullptr);
+      add_side<2>(qr, dqr, K, gm1, ch, cf, Ih, If, gr, kShareHalves ? &hr : nullptr);
+      add_side<0>(Q0, dq0, K, gm1, ch, cf, Ih, If, prim_of(Q0, K));
       // 2x2 fit
       const Real idt = Real(1.0) / dt;
 #pragma unroll
