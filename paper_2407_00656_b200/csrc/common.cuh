@@ -4,7 +4,37 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "erfc_fit.h"
+
 namespace hgks {
+
+// erfc(z) together with exp(-z^2), which the half-range Maxwellian moments need both
+// of.  fp64: erfcx(|z|) = P(t)/(|z| + K), t = (|z| - K)/(|z| + K), P a
+// degree-22 Chebyshev series (scripts/fit_erfc.py; absolute error of erfc <= 2e-15,
+// tests/test_erfc_fit.py), so one exp serves both and the branchy library erfc (about
+// 160 instructions per call in the flux kernels' SASS) is gone.  fp32: library calls.
+__device__ __forceinline__ void erfc_exp(double z, double& erfc_z, double& ez2) {
+  constexpr double c[HGKS_ERFC_DEG + 1] = HGKS_ERFC_COEF;
+  const double a = fabs(z);
+  const double r = 1.0 / (a + HGKS_ERFC_K);
+  const double t = (a - HGKS_ERFC_K) * r;
+  const double t2 = t + t;
+  double b1 = 0.0, b2 = 0.0;
+#pragma unroll
+  for (int k = HGKS_ERFC_DEG; k >= 1; --k) {
+    const double b0 = fma(t2, b1, c[k] - b2);
+    b2 = b1;
+    b1 = b0;
+  }
+  const double P = fma(t, b1, c[0] - b2);
+  ez2 = exp(-z * z);
+  const double v = P * r * ez2;  // erfc(|z|)
+  erfc_z = z >= 0.0 ? v : 2.0 - v;
+}
+__device__ __forceinline__ void erfc_exp(float z, float& erfc_z, float& ez2) {
+  erfc_z = erfcf(z);
+  ez2 = expf(-z * z);
+}
 
 constexpr int QS = 6;      // values per cell row of Q (5 conserved + 1 pad for 16-byte pairs)
 constexpr int kRec = 50;   // values per effective-polynomial record (10 coefficients x 5 variables)

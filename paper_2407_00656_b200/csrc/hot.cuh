@@ -756,15 +756,12 @@ struct Half {
 template <int RANGE>
 __device__ __forceinline__ Half half_moments(Real U, Real lam) {
   const Real sl = sqrt(lam);
-  const Real e = Real(0.5) * exp(-lam * U * U) * Real(0.56418958354775628) / sl;  // e^{-lam U^2} / (2 sqrt(pi lam))
+  Real ec, ex;
+  erfc_exp(RANGE == 1 ? -sl * U : sl * U, ec, ex);  // and ex = e^{-lam U^2}
+  const Real e = Real(0.5) * ex * Real(0.56418958354775628) / sl;  // e^{-lam U^2} / (2 sqrt(pi lam))
   Half hm;
-  if (RANGE == 1) {
-    hm.m0 = Real(0.5) * erfc(-sl * U);
-    hm.m1 = U * hm.m0 + e;
-  } else {
-    hm.m0 = Real(0.5) * erfc(sl * U);
-    hm.m1 = U * hm.m0 - e;
-  }
+  hm.m0 = Real(0.5) * ec;
+  hm.m1 = RANGE == 1 ? U * hm.m0 + e : U * hm.m0 - e;
   return hm;
 }
 
@@ -914,8 +911,10 @@ __device__ __forceinline__ void equilibrium_state(const Real ql[5], const Real q
     const Real rs = rsqrt(h + h);   // sqrt(lambda)
     const Real sq = (h + h) * rs;   // 1/sqrt(lambda)
     const Real x = U * rs;
-    m[0] = Real(0.5) * erfc(-sg * x);
-    m[1] = U * m[0] + sg * (Real(0.5) * exp(-x * x) * rpi * sq);
+    Real ec, ex;
+    erfc_exp(-sg * x, ec, ex);  // erfc(-sg x), exp(-x^2)
+    m[0] = Real(0.5) * ec;
+    m[1] = U * m[0] + sg * (Real(0.5) * ex * rpi * sq);
     m[2] = U * m[1] + m[0] * h;
   };
   Real rl, Vl, Wl, hl, a[3], rr, Vr, Wr, hr, b[3];
