@@ -742,6 +742,34 @@ __device__ __forceinline__ void euler_jvp(int j, const EulerState& e, const Real
 // <u^a> (full line, u>0 or u<0), <v^b>, <w^c> (full), <xi^2>, <xi^4>
 // (SURVEY A.1).  psi = (1, u, v, w, (u^2+v^2+w^2+xi^2)/2).
 // ---------------------------------------------------------------------------
+// Primitive variables of a conserved state.  lambda = rho/(2p) is carried
+// with h = 1/(2 lambda) = p/rho = (gamma - 1) rho e / rho, sl = sqrt(lambda) and
+// isl = 1/sqrt(lambda), built from one division (1/rho) and one rsqrt.
+struct Prim {
+  Real rho, U, V, W, lam, h, sl, isl;
+};
+__device__ __forceinline__ Prim prim_of(const Real q[5], Real K) {
+  Prim p;
+  p.rho = q[0];
+  const Real inv = Real(1.0) / q[0];
+  p.U = q[1] * inv;
+  p.V = q[2] * inv;
+  p.W = q[3] * inv;
+  if (sizeof(Real) == 8) {
+    const Real rhoe = q[4] - Real(0.5) * (q[1] * p.U + q[2] * p.V + q[3] * p.W);
+    p.h = (Real(2.0) / (K + Real(3.0))) * rhoe * inv;
+    p.sl = rsqrt(p.h + p.h);
+    p.lam = p.sl * p.sl;
+    p.isl = (p.h + p.h) * p.sl;
+  } else {  // fp32: measured faster with the direct lambda form
+    p.lam = (K + Real(3.0)) * p.rho / (Real(4.0) * (q[4] - Real(0.5) * p.rho * (p.U * p.U + p.V * p.V + p.W * p.W)));
+    p.h = Real(0.5) / p.lam;
+    p.sl = sqrt(p.lam);
+    p.isl = Real(1.0) / p.sl;
+  }
+  return p;
+}
+
 struct Mom {
   Real U[7], V[6], W[6], X1, X2;
 };
@@ -754,11 +782,11 @@ struct Half {
   Real m0, m1;
 };
 template <int RANGE>
-__device__ __forceinline__ Half half_moments(Real U, Real lam) {
-  const Real sl = sqrt(lam);
+__device__ __forceinline__ Half half_moments(const Prim& g) {
+  const Real U = g.U;
   Real ec, ex;
-  erfc_exp(RANGE == 1 ? -sl * U : sl * U, ec, ex);  // and ex = e^{-lam U^2}
-  const Real e = Real(0.5) * ex * Real(0.56418958354775628) / sl;  // e^{-lam U^2} / (2 sqrt(pi lam))
+  erfc_exp(RANGE == 1 ? -g.sl * U : g.sl * U, ec, ex);  // and ex = e^{-lam U^2}
+  const Real e = Real(0.5) * ex * Real(0.56418958354775628) * g.isl;  // e^{-lam U^2} / (2 sqrt(pi lam))
   Half hm;
   hm.m0 = Real(0.5) * ec;
   hm.m1 = RANGE == 1 ? U * hm.m0 + e : U * hm.m0 - e;
@@ -766,14 +794,14 @@ __device__ __forceinline__ Half half_moments(Real U, Real lam) {
 }
 
 template <int RANGE>
-__device__ __forceinline__ void maxwell_moments(Real U, Real V, Real W, Real lam, Real K, Mom& m,
-                                                const Half* hm = nullptr) {
-  const Real h = Real(0.5) / lam;  // 1/(2 lambda)
+__device__ __forceinline__ void maxwell_moments(const Prim& g, Real K, Mom& m, const Half* hm = nullptr) {
+  const Real U = g.U, V = g.V, W = g.W;
+  const Real h = g.h;  // 1/(2 lambda)
   if (RANGE == 0) {
     m.U[0] = Real(1.0);
     m.U[1] = U;
   } else {
-    const Half x = hm ? *hm : half_moments<RANGE>(U, lam);
+    const Half x = hm ? *hm : half_moments<RANGE>(g);
     m.U[0] = x.m0;
     m.U[1] = x.m1;
   }
@@ -858,19 +886,7 @@ __device__ __forceinline__ void micro_slope(const Real b[5], Real U, Real V, Rea
   a[0] = b[0] - U * a[1] - V * a[2] - W * a[3] - Real(0.5) * a[4] * B;
 }
 
-struct Prim {
-  Real rho, U, V, W, lam;
-};
-__device__ __forceinline__ Prim prim_of(const Real q[5], Real K) {
-  Prim p;
-  p.rho = q[0];
-  const Real inv = Real(1.0) / q[0];
-  p.U = q[1] * inv;
-  p.V = q[2] * inv;
-  p.W = q[3] * inv;
-  p.lam = (K + Real(3.0)) * p.rho / (Real(4.0) * (q[4] - Real(0.5) * p.rho * (p.U * p.U + p.V * p.V + p.W * p.W)));
-  return p;
-}
+
 
 
 // closed-form time integrals of the Eq. (flux) coefficients over [0, delta]
@@ -959,7 +975,7 @@ __device__ __forceinline__ void add_side(const Real q[5], const Real dq[3][5], R
     for (int v = 0; v < 5; ++v) dtq[v] -= jv[v];
   }
   Mom mom;
-  maxwell_moments<RANGE>(g.U, g.V, g.W, g.lam, K, mom, hm);
+  maxwell_moments<RANGE>(g, K, mom, hm);
   Real m2[5];  // <(a.u) u psi> over the range
   {
     Real t0[5], t1[5], t2[5];
@@ -1196,9 +1212,9 @@ __global__ void __launch_bounds__((NV == 3 ? 3 : 4) * HGKS_FLUX_FPB,
       // Q0 from the half-range moments, which the g_l / g_r groups reuse
       gl = prim_of(ql, K);
       gr = prim_of(qr, K);
-      hl = half_moments<1>(gl.U, gl.lam);
-      hr = half_moments<2>(gr.U, gr.lam);
-      const Real hL = Real(0.5) / gl.lam, hR = Real(0.5) / gr.lam;
+      hl = half_moments<1>(gl);
+      hr = half_moments<2>(gr);
+      const Real hL = gl.h, hR = gr.h;
       const Real a2 = gl.U * hl.m1 + hl.m0 * hL, b2 = gr.U * hr.m1 + hr.m0 * hR;
       Q0[0] = gl.rho * hl.m0 + gr.rho * hr.m0;
       Q0[1] = gl.rho * hl.m1 + gr.rho * hr.m1;
