@@ -13,8 +13,11 @@ namespace hgks {
 // degree-22 Chebyshev series (scripts/fit_erfc.py; absolute error of erfc <= 2e-15,
 // tests/test_erfc_fit.py), so one exp serves both and the branchy library erfc (about
 // 160 instructions per call in the flux kernels' SASS) is gone.  fp32: library calls.
+// (coefficients in constant memory: the DFMA/DADD take them as c[][] operands, no
+// per-coefficient register moves)
+__constant__ double kErfcCoef[HGKS_ERFC_DEG + 1] = HGKS_ERFC_COEF;
 __device__ __forceinline__ void erfc_exp(double z, double& erfc_z, double& ez2) {
-  constexpr double c[HGKS_ERFC_DEG + 1] = HGKS_ERFC_COEF;
+  const double* c = kErfcCoef;
   const double a = fabs(z);
   const double r = 1.0 / (a + HGKS_ERFC_K);
   const double t = (a - HGKS_ERFC_K) * r;
