@@ -13,6 +13,34 @@ namespace hgks {
 // degree-22 Chebyshev series (scripts/fit_erfc.py; absolute error of erfc <= 2e-15,
 // tests/test_erfc_fit.py), so one exp serves both and the branchy library erfc (about
 // 160 instructions per call in the flux kernels' SASS) is gone.  fp32: library calls.
+// exp(x) for x <= 0 (the Maxwellian tail exp(-z^2), exp(-dt/tau)): Cody-Waite
+// reduction x = k ln2 + r, |r| <= ln2/2 (two-part ln2), degree-12 Taylor series, 2^k
+// added to the exponent field; relative error <= 4e-16 on [-700, 0], 0 below -700
+// (tests/test_exp_neg.py).  About half the instructions of the library exp, which
+// also handles positive arguments, overflow and NaN.
+__device__ __forceinline__ double exp_neg(double x) {
+  const double xc = fmax(x, -708.0);
+  const double k = rint(xc * 1.4426950408889634);
+  const double r = fma(-k, 1.90821492927058770002e-10, fma(-k, 6.93147180369123816490e-01, xc));
+  double p = 2.08767569878680989792e-09;  // 1/12!
+  p = fma(p, r, 2.50521083854417187751e-08);
+  p = fma(p, r, 2.75573192239858906526e-07);
+  p = fma(p, r, 2.75573192239858906526e-06);
+  p = fma(p, r, 2.48015873015873015873e-05);
+  p = fma(p, r, 1.98412698412698412698e-04);
+  p = fma(p, r, 1.38888888888888888889e-03);
+  p = fma(p, r, 8.33333333333333333333e-03);
+  p = fma(p, r, 4.16666666666666666667e-02);
+  p = fma(p, r, 1.66666666666666666667e-01);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const int ki = (int)k;  // in [-1022, 0]
+  const double v = __hiloint2double(__double2hiint(p) + ki * (1 << 20), __double2loint(p));
+  return x < -700.0 ? 0.0 : v;
+}
+__device__ __forceinline__ float exp_neg(float x) { return expf(x); }
+
 // (coefficients in constant memory: the DFMA/DADD take them as c[][] operands, no
 // per-coefficient register moves)
 __constant__ double kErfcCoef[HGKS_ERFC_DEG + 1] = HGKS_ERFC_COEF;
@@ -30,7 +58,7 @@ __device__ __forceinline__ void erfc_exp(double z, double& erfc_z, double& ez2) 
     b1 = b0;
   }
   const double P = fma(t, b1, c[0] - b2);
-  ez2 = exp(-z * z);
+  ez2 = exp_neg(-z * z);
   const double v = P * r * ez2;  // erfc(|z|)
   erfc_z = z >= 0.0 ? v : 2.0 - v;
 }

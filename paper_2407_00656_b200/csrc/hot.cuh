@@ -1255,7 +1255,7 @@ __global__ void __launch_bounds__((NV == 3 ? 3 : 4) * HGKS_FLUX_FPB,
       const Real p0 = pres(Q0, i0), pl = pres(ql, il), pr = pres(qr, ir);
       const Real mu = a.gp.mu_inf * exp(a.gp.mu_exp * log((p0 * i0) / a.gp.t_inf));
       const Real tau = mu / p0 + a.gp.c1 * fabs(pl - pr) / (pl + pr) * dt;
-      const Real eh = exp(-(Real(0.5) * dt) / tau);
+      const Real eh = exp_neg(-(Real(0.5) * dt) / tau);
       const TimeCoef ch = time_coef_e(Real(0.5) * dt, tau, eh), cf = time_coef_e(dt, tau, eh * eh);
       Real Ih[5] = {0, 0, 0, 0, 0}, If[5] = {0, 0, 0, 0, 0};
       Real dq0[3][5];
