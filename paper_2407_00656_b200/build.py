@@ -12,7 +12,8 @@ ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libhgks.so")
 SOURCES = [os.path.join(PKG, "csrc", "solver.cu"), os.path.join(PKG, "csrc", "setup.cpp")]
 DEPS = SOURCES + [os.path.join(PKG, "csrc", "kernels.cuh"), os.path.join(PKG, "csrc", "hot.cuh"),
-                  os.path.join(PKG, "csrc", "common.cuh"), os.path.join(PKG, "csrc", "erfc_fit.h"), os.path.join(PKG, "csrc", "internal.h"),
+                  os.path.join(PKG, "csrc", "common.cuh"), os.path.join(PKG, "csrc", "erfc_fit.h"),
+                  os.path.join(PKG, "csrc", "moments_gen.cuh"), os.path.join(PKG, "csrc", "internal.h"),
                   os.path.join(ROOT, "include", "hgks.h")]
 
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",

@@ -872,6 +872,8 @@ __device__ __forceinline__ void slope_m(const Mom& m, const Real s[5], Real o[5]
   for (int k = 0; k < 5; ++k) o[k] = fma(h4, t[k], o[k]);
 }
 
+#include "moments_gen.cuh"
+
 // micro-slope a with sum_j a_j <psi_i psi_j> = b_i (b already divided by rho),
 // closed form of the 5x5 Maxwellian moment system
 __device__ __forceinline__ void micro_slope(const Real b[5], Real U, Real V, Real W, Real lam, Real K,
@@ -976,6 +978,36 @@ __device__ __forceinline__ void add_side(const Real q[5], const Real dq[3][5], R
   }
   Mom mom;
   maxwell_moments<RANGE>(g, K, mom, hm);
+#ifndef HGKS_GENERIC_MOMENTS
+  // straight-line moment contractions (scripts/gen_moments.py -> moments_gen.cuh):
+  // the psi_m / slope_m sums below, expanded and with common products shared
+  if (RANGE == 0) {
+    Real m2r[5];
+    moments_full(mom, a, m2r);
+    Real m3[5];
+    euler_jvp(0, es, dtq, gm1, m3);  // rho <A u psi> = A_n(Q) d_t Q
+    const Real m1[5] = {q[1], q[1] * es.u[0] + es.p, q[2] * es.u[0], q[3] * es.u[0], es.u[0] * es.H};
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      const Real m2 = g.rho * m2r[v];
+      Ih[v] += ch.c1 * m1[v] + ch.c2 * m2 + ch.c3 * m3[v];
+      If[v] += cf.c1 * m1[v] + cf.c2 * m2 + cf.c3 * m3[v];
+    }
+  } else {
+    Real A[5], b[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) b[v] = dtq[v] * ir;
+    micro_slope(b, g.U, g.V, g.W, g.lam, K, A);
+    Real m2r[5], m1[5], m3[5];
+    moments_half(mom, a, A, m2r, m1, m3);
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      const Real m2 = g.rho * m2r[v];
+      Ih[v] += g.rho * (ch.c4 * m1[v] + ch.c6 * m3[v]) + ch.c5 * m2;
+      If[v] += g.rho * (cf.c4 * m1[v] + cf.c6 * m3[v]) + cf.c5 * m2;
+    }
+  }
+#else
   Real m2[5];  // <(a.u) u psi> over the range
   {
     Real t0[5], t1[5], t2[5];
@@ -1009,6 +1041,7 @@ __device__ __forceinline__ void add_side(const Real q[5], const Real dq[3][5], R
       If[v] += g.rho * (cf.c4 * m1[v] + cf.c6 * m3[v]) + cf.c5 * m2[v];
     }
   }
+#endif
 }
 
 // boundary right states in the local frame (R25)
