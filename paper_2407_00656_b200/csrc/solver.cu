@@ -355,7 +355,9 @@ void run_recon(hgks_solver* s, const void* Q, int part) {
 template <class L, int NV, int BC>
 void launch_flux(hgks_solver* s, const typename L::FluxArgsT& a, int stage, bool tau0) {
   constexpr int NGP = NV == 3 ? 3 : 4, B = NGP * HGKS_FLUX_FPB;
-  const int nb = blocks((int64_t)a.n_faces * NGP, B);
+  // faces per block: NGP lanes per face, or 10 faces per warp with the shuffle reduction
+  constexpr int FPBk = HGKS_FLUX_WARPRED ? (B / 32) * (32 / NGP) : B / NGP;
+  const int nb = (int)((a.n_faces + FPBk - 1) / FPBk);
   const char* names[2][2] = {{"k_flux_s1", "k_flux_s2"}, {"k_flux_tau0_s1", "k_flux_tau0_s2"}};
   const char* nm = BC == 0 ? names[tau0][stage - 1] : (BC == 1 ? "k_flux_wall" : "k_flux_farfield");
   if (tau0) {
