@@ -88,7 +88,8 @@ typedef struct {
 
 #define HGKS_TRANSPORT_NCCL 0      /* one process per GPU, NCCL send/recv + allreduce */
 #define HGKS_TRANSPORT_LOOPBACK 1  /* all ranks in one process on one device, advanced together by
-                                      hgks_group_step (exchange = device copies); for testing the
+                                      hgks_group_step (exchange = fused put k_put: send rows written
+                                      straight into the receivers' ghost rows); for testing the
                                       partitioned path on a single GPU */
 
 /* Distributed context. */
@@ -185,8 +186,10 @@ hgks_status hgks_kernel_times(hgks_solver* solver, int32_t cap, char (*names)[32
                               double* total_ms, int32_t* n);
 /* Loopback transport: advance the solvers of ranks 0..n-1 (created with
  * HGKS_TRANSPORT_LOOPBACK on one device and stream, in rank order) by n_steps
- * S2O4 steps, exchanging ghosts by device copies and reducing min(dt) exactly.
- * Asynchronous on the shared stream. */
+ * S2O4 steps, exchanging ghosts by the fused put (one k_put per sending rank and stage,
+ * P:856-869) and reducing min(dt) exactly.  The first call uploads each rank's
+ * (receiver, row) put map (synchronous); later calls are asynchronous on the
+ * shared stream. */
 hgks_status hgks_group_step(hgks_solver* const* solvers, int32_t n, int32_t n_steps, double t_stop);
 
 /* Export rank `rank`'s partition plan (host, for tests and tools): l2g

@@ -1521,11 +1521,30 @@ __global__ void k_pack(const Real* __restrict__ Q, const int* __restrict__ list,
   reinterpret_cast<R2*>(buf)[k] = reinterpret_cast<const R2*>(Q + (size_t)list[j] * QS)[part];
 }
 
+// fused halo put: the send rows go straight into the
+// receivers' ghost rows (no pack buffer, no copy launch per peer).  dst[j] = (receiver
+// rank, row in the receiver's Q); peer.q[r] = rank r's Q (a device pointer on the same
+// device for the loopback transport).  Same 16-byte pairs as k_pack: the ghost rows
+// are bitwise copies.
+struct PeerQ {
+  Real* q[kMaxGroup];
+};
+__global__ void k_put(const Real* __restrict__ Q, const int* __restrict__ list, const int2* __restrict__ dst, int n,
+                      PeerQ peer) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n * 3) return;
+  const int j = k / 3, part = k - 3 * j;
+  const int2 d = __ldg(dst + j);
+  reinterpret_cast<R2*>(peer.q[d.x] + (size_t)d.y * QS)[part] =
+      reinterpret_cast<const R2*>(Q + (size_t)__ldg(list + j) * QS)[part];
+}
+
 
 
 // host-side launchers of this precision's kernels (solver.cu is templated on this struct)
 struct Launch {
   using RealT = Real;
+  using PeerQT = PeerQ;
   using ReconArgsT = ReconArgs;
   using FluxArgsT = FluxArgs;
   using UpdateArgsT = UpdateArgs;
@@ -1578,5 +1597,9 @@ struct Launch {
   }
   static void pack(int grid, cudaStream_t st, const Real* Q, const int* list, int n, Real* buf) {
     k_pack<<<grid, 256, 0, st>>>(Q, list, n, buf);
+  }
+  static void put(int grid, cudaStream_t st, const Real* Q, const int* list, const int2* dst, int n,
+                  const PeerQ& peer) {
+    k_put<<<grid, 256, 0, st>>>(Q, list, dst, n, peer);
   }
 };

@@ -149,6 +149,7 @@ struct DevArrays {
   void *Q, *Qtmp, *R, *ceff, *F1, *F2, *op, *geo, *f_geo, *inv_v, *h_dt, *bg_normal, *sendbuf;
   double *stage_in[2], *stage_out[2];  // caller-order staging (fp64), double-buffered for pipelining
   int *recon_cell, *st_id, *f_cells, *cf, *bg_cell, *bg_bc, *send_list, *out_local;
+  int2* put_dst;  // fused halo put: (receiver rank, receiver row) per send row (f3)
   int64_t* in_row;
   uint8_t* sub_slot;
   Ctrl* ctrl;
@@ -182,6 +183,7 @@ size_t layout(const GlobalMesh& gm, const RankPlan& rp, size_t rs, Carve& c, Dev
   d.bg_normal = R(std::max<int64_t>(3, 3 * rp.n_bghost));
   d.send_list = c.take<int>(std::max<size_t>(1, rp.send_list.size()));
   d.sendbuf = R(std::max<size_t>(QS, QS * rp.send_list.size()));
+  d.put_dst = c.take<int2>(std::max<size_t>(1, rp.send_list.size()));
   d.out_local = c.take<int>(rp.n_owned);
   d.in_row = c.take<int64_t>(rp.n_owned);
   // staging for set/get_state: single rank copies the caller's whole array
@@ -219,6 +221,7 @@ struct hgks_solver {
   int recon_t1 = 0;  // end tile of the current reconstruction launch
   cudaStream_t comm_stream = nullptr;  // NCCL halo exchange (overlapped with the early work)
   cudaEvent_t ev_packed = nullptr, ev_halo = nullptr;
+  bool put_ready = false;  // put_dst uploaded (loopback group, first hgks_group_step)
   cudaStream_t stream = nullptr;
   DevArrays d{};
   size_t nq = 0;  // values in Q
@@ -456,6 +459,43 @@ void exchange(hgks_solver* s, void* Q) {
   }
   NCCL_TRY(N.GroupEnd());
   CUDA_TRY(cudaEventRecord(s->ev_halo, s->comm_stream));
+}
+
+// f3: fused halo put for the loopback group -- one k_put per sending rank writes its send
+// rows straight into the receivers' ghost rows (replaces k_pack + one device copy per
+// peer pair).  The (receiver, row) map comes from the two ranks' plans (recv_off of the
+// receiver's range for this sender + position in the sender's range for that peer).
+void build_put_map(hgks_solver* const* ss, int n) {
+  for (int q = 0; q < n; ++q) {
+    hgks_solver* s = ss[q];
+    if (s->put_ready) continue;
+    const RankPlan& rq = *s->rp;
+    std::vector<int2> dst(std::max<size_t>(1, rq.send_list.size()), int2{0, 0});
+    for (size_t ip = 0; ip < rq.peers.size(); ++ip) {
+      if (rq.send_cnt[ip] == 0) continue;
+      const int p = rq.peers[ip];
+      const RankPlan& rpp = *ss[p]->rp;
+      const size_t iq = std::find(rpp.peers.begin(), rpp.peers.end(), q) - rpp.peers.begin();
+      if (iq == rpp.peers.size() || rpp.recv_cnt[iq] != rq.send_cnt[ip])
+        throw Error(HGKS_E_STATE, "inconsistent exchange plans between ranks");
+      for (int64_t k = 0; k < rq.send_cnt[ip]; ++k)
+        dst[rq.send_off[ip] + k] = int2{p, (int)(rpp.recv_off[iq] + k)};
+    }
+    CUDA_TRY(cudaMemcpy(s->d.put_dst, dst.data(), dst.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    s->put_ready = true;
+  }
+}
+
+template <class L>
+void put(hgks_solver* const* ss, int q, int n) {
+  hgks_solver* s = ss[q];
+  const int ns = (int)s->rp->send_list.size();
+  if (ns == 0) return;
+  typename L::PeerQT peer{};
+  for (int k = 0; k < n; ++k) peer.q[k] = as<L>(ss[k]->d.Q);
+  launch(s, "k_put", [&] {
+    L::put(blocks(3 * ns, 256), s->stream, as<L>(s->d.Q), s->d.send_list, s->d.put_dst, ns, peer);
+  });
 }
 
 // the compute stream waits for the ghosts (no-op without an NCCL exchange in flight)
@@ -1080,24 +1120,8 @@ hgks_status hgks_group_step(hgks_solver* const* ss, int32_t n, int32_t n_steps, 
     gc.n = n;
     for (int k = 0; k < n; ++k) gc.c[k] = ss[k]->d.ctrl;
     auto group_min = [&] { launch(s0, "k_group_min", [&] { k_group_min<<<1, 32, 0, s0->stream>>>(gc); }); };
-    // ghost copies: receiver q, peer p (in-process transport)
-    auto loop_exchange = [&] {
-      for (int q = 0; q < n; ++q) {
-        const RankPlan& rq = *ss[q]->rp;
-        for (size_t iq = 0; iq < rq.peers.size(); ++iq) {
-          if (rq.recv_cnt[iq] == 0) continue;
-          const hgks_solver* sp = ss[rq.peers[iq]];
-          const RankPlan& rpp = *sp->rp;
-          size_t ip = std::find(rpp.peers.begin(), rpp.peers.end(), q) - rpp.peers.begin();
-          if (ip == rpp.peers.size() || rpp.send_cnt[ip] != rq.recv_cnt[iq])
-            throw Error(HGKS_E_STATE, "inconsistent exchange plans between ranks");
-          const size_t rs = s0->rs;
-          CUDA_TRY(cudaMemcpyAsync((char*)ss[q]->d.Q + rs * QS * rq.recv_off[iq],
-                                   (const char*)sp->d.sendbuf + rs * QS * rpp.send_off[ip], rs * QS * rq.recv_cnt[iq],
-                                   cudaMemcpyDeviceToDevice, s0->stream));
-        }
-      }
-    };
+    // ghost rows: fused put of every rank's send rows into its receivers (f3)
+    build_put_map(ss, n);
     group_min();
     for (int step = 0; step < n_steps; ++step) {
       for (int k = 0; k < n; ++k)
@@ -1105,9 +1129,8 @@ hgks_status hgks_group_step(hgks_solver* const* ss, int32_t n, int32_t n_steps, 
           k_step_begin<<<1, 1, 0, s0->stream>>>(ss[k]->d.ctrl, ss[k]->cfg.cfl, ss[k]->cfg.fixed_dt, t_stop);
         });
       for (int st = 1; st <= 2; ++st) {
-        for (int k = 0; k < n; ++k) HGKS_DISPATCH(ss[k], pack, ss[k], ss[k]->d.Q);
+        for (int k = 0; k < n; ++k) HGKS_DISPATCH(ss[k], put, ss, k, n);
         for (int k = 0; k < n; ++k) HGKS_DISPATCH(ss[k], stage_early, ss[k], st);
-        loop_exchange();
         for (int k = 0; k < n; ++k) HGKS_DISPATCH(ss[k], stage_late, ss[k], st);
       }
       group_min();

@@ -40,6 +40,25 @@ def test_kuhn_multirank_bitwise(cuda_ok, world):
     assert mesh.info(0)["n_peers"] >= 1
 
 
+def test_loopback_fused_put(cuda_ok):
+    """f3: the loopback group moves its ghost rows with one k_put per sending rank
+    (send rows written straight into the receivers' ghost rows), 2 per step, no
+    k_pack; the result stays bitwise equal to one rank (test above)."""
+    mi = W.kuhn_box(8)
+    Q0 = W.advection_ic(mi)
+    mesh = hgks.Mesh(mi, n_ranks=2)
+    cfg = hgks.SolverConfig(cfl=0.3)
+    solvers = [hgks.Solver(mesh, Q0, cfg, rank=r, transport=hgks.TRANSPORT_LOOPBACK) for r in range(2)]
+    for s in solvers:
+        s.set_profiling(True)
+    hgks.group_step(solvers, 3)
+    for r, s in enumerate(solvers):
+        s.step(0)
+        kt = s.kernel_times()
+        assert mesh.info(r)["send_cells"] > 0
+        assert kt["k_put"]["launches"] == 6 and "k_pack" not in kt, kt
+
+
 def test_sphere_multirank_bitwise_and_oracle(cuda_ok):
     mi = W.sphere_shell(5)
     fs = (1.0, 1.5, 0.0, 0.0, 1 / 1.4)
