@@ -24,8 +24,9 @@
 // velocity/time quadrature of Eq. (flux), tau=0 Euler-chain identity,
 // S2O4 Taylor polynomial, conservation, free-stream preservation, and the
 // paper's Table 3 convergence (T3), the farfield Riemann state against the
-// characteristic conditions.  Parity unpinned: the wall mirror (R25) beyond
-// free-stream/symmetry checks.
+// characteristic conditions, and the wall mirror (R25) on a walled box: no mass
+// or energy through the wall at tau = 0 and the closed-form no-slip stagnation
+// pressure (tests/test_oracle_wall.py).
 // ============================================================================
 #include <algorithm>
 #include <array>

@@ -13,7 +13,8 @@ Parity status per function:
   S2O4 stages ............................. pinned (Taylor polynomial of exp(z))
   full step ............................... pinned (conservation, free stream, T3 orders)
   farfield boundary state ................. pinned (characteristic conditions, seeded states)
-  wall boundary state ..................... parity unpinned beyond free stream + symmetry
+  wall boundary state ..................... pinned (walled box: no mass/energy through the wall,
+                                             closed-form no-slip stagnation pressure; test_oracle_wall.py)
 """
 from __future__ import annotations
 

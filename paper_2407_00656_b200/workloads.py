@@ -135,6 +135,28 @@ def cartesian_hex_box(nx: int, ny: int | None = None, nz: int | None = None,
     )
 
 
+def walled_hex_box(n: int, h: float | None = None, jitter: float = 0.0, seed: int = 656) -> MeshInput:
+    """Closed n^3 hex box whose six sides are all WALL boundary faces (no periodicity):
+    the wall-pin workload (every wall corner case: cells with 1, 2 and 3 wall faces)."""
+    mi = cartesian_hex_box(n, h=h, jitter=jitter, seed=seed)
+    mi.periodic_length = np.zeros(3)
+
+    def nid(i, j, k):
+        return (i * (n + 1) + j) * (n + 1) + k
+
+    quads = []
+    for a in range(n):
+        for b in range(n):
+            for c0 in (0, n):
+                quads.append([nid(c0, a, b), nid(c0, a + 1, b), nid(c0, a + 1, b + 1), nid(c0, a, b + 1)])
+                quads.append([nid(a, c0, b), nid(a + 1, c0, b), nid(a + 1, c0, b + 1), nid(a, c0, b + 1)])
+                quads.append([nid(a, b, c0), nid(a + 1, b, c0), nid(a + 1, b + 1, c0), nid(a, b + 1, c0)])
+    mi.bface_nodes = np.array(quads, np.int64)
+    mi.bface_tag = np.full(len(quads), BC_WALL, np.int32)
+    mi.name = f"walled_hexbox_{n}" + ("_jit" if jitter > 0 else "")
+    return mi
+
+
 # --------------------------------------------------------------------------- #
 # Cubed-sphere hexahedral shell (C3/C4)
 # --------------------------------------------------------------------------- #

@@ -151,6 +151,21 @@ def test_hex_box_ns_tau(cuda_ok):
     assert errs.max() <= TOL, errs.max(axis=0)
 
 
+@pytest.mark.parametrize("tau", ["zero", "ns"])
+def test_walled_box(cuda_ok, tau):
+    """Closed box, six wall sides (R25 mirror ghosts; cells with 1, 2 and 3 wall
+    faces), jittered interior nodes: 10 steps, tau = 0 (Euler-chain flux with wall
+    faces) and NS tau (moment form)."""
+    mi = W.walled_hex_box(6, h=0.4, jitter=0.1)
+    Q0 = W.random_smooth_ic(mi, seed=7, base=(1.0, 0.3, 0.2, -0.25, 1 / 1.4), amp=0.05)
+    if tau == "ns":
+        oc, gc = ns_cfgs(mu=1e-2, cfl=0.5)
+    else:
+        oc, gc = O.OracleConfig(cfl=0.5), hgks.SolverConfig(cfl=0.5)
+    errs, _, _ = run_pair(mi, Q0, 10, ocfg=oc, gcfg=gc)
+    assert errs.max() <= TOL, errs.max(axis=0)
+
+
 def sphere_case(n, ma, re):
     mi = W.sphere_shell(n)
     gam = 1.4
