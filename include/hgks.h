@@ -192,6 +192,13 @@ hgks_status hgks_kernel_times(hgks_solver* solver, int32_t cap, char (*names)[32
  * shared stream. */
 hgks_status hgks_group_step(hgks_solver* const* solvers, int32_t n, int32_t n_steps, double t_stop);
 
+/* Fused halo put map of rank `rank` (host; the loopback group's k_put
+ * uses it): for send row j (the order of hgks_mesh_plan's send_list), the receiving
+ * rank recv_rank[j] and the local ghost row recv_row[j] there that takes the cell's
+ * state.  Arrays of send_cells entries, caller-allocated.  HGKS_E_STATE if two ranks'
+ * plans disagree, HGKS_E_ARG on a NULL pointer or a rank out of range. */
+hgks_status hgks_mesh_put_map(const hgks_mesh* mesh, int32_t rank, int32_t* recv_rank, int32_t* recv_row);
+
 /* Export rank `rank`'s partition plan (host, for tests and tools): l2g
  * [n_owned + n_ghost] global ids of the local cells (owned first), peers
  * [n_peers], per-peer send offsets/counts into send_list [send_cells] (local

@@ -465,23 +465,29 @@ void exchange(hgks_solver* s, void* Q) {
 // rows straight into the receivers' ghost rows (replaces k_pack + one device copy per
 // peer pair).  The (receiver, row) map comes from the two ranks' plans (recv_off of the
 // receiver's range for this sender + position in the sender's range for that peer).
+// (receiver rank, receiver row) of every send row of rank q, from the two ranks' plans
+std::vector<int2> put_map(hgks_mesh* m, int q) {
+  const RankPlan& rq = m->plan(q);
+  std::vector<int2> dst(rq.send_list.size(), int2{-1, -1});
+  for (size_t ip = 0; ip < rq.peers.size(); ++ip) {
+    if (rq.send_cnt[ip] == 0) continue;
+    const int p = rq.peers[ip];
+    const RankPlan& rpp = m->plan(p);
+    const size_t iq = std::find(rpp.peers.begin(), rpp.peers.end(), q) - rpp.peers.begin();
+    if (iq == rpp.peers.size() || rpp.recv_cnt[iq] != rq.send_cnt[ip])
+      throw Error(HGKS_E_STATE, "inconsistent exchange plans between ranks");
+    for (int64_t k = 0; k < rq.send_cnt[ip]; ++k) dst[rq.send_off[ip] + k] = int2{p, (int)(rpp.recv_off[iq] + k)};
+  }
+  return dst;
+}
+
 void build_put_map(hgks_solver* const* ss, int n) {
   for (int q = 0; q < n; ++q) {
     hgks_solver* s = ss[q];
     if (s->put_ready) continue;
-    const RankPlan& rq = *s->rp;
-    std::vector<int2> dst(std::max<size_t>(1, rq.send_list.size()), int2{0, 0});
-    for (size_t ip = 0; ip < rq.peers.size(); ++ip) {
-      if (rq.send_cnt[ip] == 0) continue;
-      const int p = rq.peers[ip];
-      const RankPlan& rpp = *ss[p]->rp;
-      const size_t iq = std::find(rpp.peers.begin(), rpp.peers.end(), q) - rpp.peers.begin();
-      if (iq == rpp.peers.size() || rpp.recv_cnt[iq] != rq.send_cnt[ip])
-        throw Error(HGKS_E_STATE, "inconsistent exchange plans between ranks");
-      for (int64_t k = 0; k < rq.send_cnt[ip]; ++k)
-        dst[rq.send_off[ip] + k] = int2{p, (int)(rpp.recv_off[iq] + k)};
-    }
-    CUDA_TRY(cudaMemcpy(s->d.put_dst, dst.data(), dst.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    std::vector<int2> dst = put_map(s->mesh, q);
+    if (!dst.empty())
+      CUDA_TRY(cudaMemcpy(s->d.put_dst, dst.data(), dst.size() * sizeof(int2), cudaMemcpyHostToDevice));
     s->put_ready = true;
   }
 }
@@ -1151,6 +1157,18 @@ hgks_status hgks_mesh_plan(const hgks_mesh* mc, int32_t rank, int64_t* l2g, int3
     if (send_list) std::copy(rp.send_list.begin(), rp.send_list.end(), send_list);
     if (recv_off) std::copy(rp.recv_off.begin(), rp.recv_off.end(), recv_off);
     if (recv_cnt) std::copy(rp.recv_cnt.begin(), rp.recv_cnt.end(), recv_cnt);
+  });
+}
+
+hgks_status hgks_mesh_put_map(const hgks_mesh* mc, int32_t rank, int32_t* recv_rank, int32_t* recv_row) {
+  return guard([&] {
+    if (!mc || !recv_rank || !recv_row) throw Error(HGKS_E_ARG, "null argument");
+    hgks_mesh* m = const_cast<hgks_mesh*>(mc);
+    const std::vector<int2> dst = put_map(m, rank);
+    for (size_t j = 0; j < dst.size(); ++j) {
+      recv_rank[j] = dst[j].x;
+      recv_row[j] = dst[j].y;
+    }
   });
 }
 

@@ -28,7 +28,7 @@ ERRORS = {0: "OK", 1: "E_ARG", 2: "E_MESH", 3: "E_STENCIL", 4: "E_CUDA", 5: "E_N
 EXPORTS = ["hgks_mesh_create", "hgks_mesh_destroy", "hgks_mesh_info", "hgks_workspace_size", "hgks_init",
            "hgks_destroy", "hgks_step", "hgks_set_state", "hgks_get_state", "hgks_get_state_async",
            "hgks_sync", "hgks_debug_residual",
-           "hgks_set_profiling", "hgks_kernel_times", "hgks_launch_count", "hgks_nccl_unique_id", "hgks_nccl_selftest", "hgks_group_step", "hgks_mesh_plan",
+           "hgks_set_profiling", "hgks_kernel_times", "hgks_launch_count", "hgks_nccl_unique_id", "hgks_nccl_selftest", "hgks_group_step", "hgks_mesh_plan", "hgks_mesh_put_map",
            "hgks_last_error", "hgks_version"]
 TRANSPORT_NCCL, TRANSPORT_LOOPBACK = 0, 1
 
@@ -109,6 +109,7 @@ def lib(build_if_needed: bool = True):
         L.hgks_nccl_unique_id.argtypes = [C.c_void_p]
         L.hgks_group_step.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_double]
         L.hgks_mesh_plan.argtypes = [C.c_void_p, C.c_int32, _i64p, _i32p, _i64p, _i64p, _i32p, _i64p, _i64p]
+        L.hgks_mesh_put_map.argtypes = [C.c_void_p, C.c_int32, _i32p, _i32p]
         _lib = L
     return _lib
 
@@ -206,6 +207,14 @@ class Mesh:
                                     _p(sl, _i32p), _p(ro, _i64p), _p(rc, _i64p)))
         return dict(n_owned=st["n_owned"], l2g=l2g, peers=peers[:npr], send_off=so[:npr], send_cnt=sc[:npr],
                     send_list=sl[:st["send_cells"]], recv_off=ro[:npr], recv_cnt=rc[:npr])
+
+    def put_map(self, rank: int = 0):
+        """Fused-put destinations of rank's send rows (hgks_mesh_put_map): (receiver rank, receiver row)."""
+        n = self.info(rank)["send_cells"]
+        rr = np.zeros(max(n, 1), np.int32)
+        row = np.zeros(max(n, 1), np.int32)
+        _check(lib().hgks_mesh_put_map(self.h, rank, _p(rr, _i32p), _p(row, _i32p)))
+        return rr[:n], row[:n]
 
     def workspace_size(self, cfg: SolverConfig, rank: int = 0) -> int:
         n = C.c_size_t()

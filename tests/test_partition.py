@@ -70,6 +70,28 @@ def _worker(rank, world, port, kind, out_q):
             ro, rc = plan["recv_off"][p], plan["recv_cnt"][p]
             Q[:, ro:ro + rc] = t.numpy().reshape(5, rc)
         ghosts_ok = bool(np.array_equal(Q.T, Qg[l2g]))
+        # fused put (f3): each send row goes to (receiver, ghost row) from hgks_mesh_put_map;
+        # emulated as one (rows, values) message per receiver, scattered by the receiver
+        rr, row = mesh.put_map(rank)
+        Qp = np.full((5, nl), np.nan)
+        Qp[:, :n_owned] = Q[:, :n_owned]
+        reqs, recv = [], []
+        for p, peer in enumerate(plan["peers"]):
+            sel = np.nonzero(rr == peer)[0]
+            if sel.size:
+                reqs.append(dist.isend(torch.from_numpy(row[sel].astype(np.float64)), int(peer)))
+                reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(Q[:, sl[sel]]).ravel()), int(peer)))
+            rc = int(plan["recv_cnt"][p])
+            if rc:
+                tr, tv = torch.empty(rc, dtype=torch.float64), torch.empty(5 * rc, dtype=torch.float64)
+                reqs.append(dist.irecv(tr, int(peer)))
+                reqs.append(dist.irecv(tv, int(peer)))
+                recv.append((tr, tv, rc))
+        for r in reqs:
+            r.wait()
+        for tr, tv, rc in recv:
+            Qp[:, tr.numpy().astype(np.int64)] = tv.numpy().reshape(5, rc)
+        ghosts_ok = ghosts_ok and bool(np.array_equal(Qp.T, Qg[l2g]))
         info = mesh.info(rank)
         out_q.put((rank, dict(owned=l2g[:n_owned].tolist(), ghosts=l2g[n_owned:].tolist(), ghosts_ok=ghosts_ok,
                               info=info, send_total=int(ns))))
@@ -137,3 +159,27 @@ def test_partition_exchange_gloo(world, kind):
                 for side in (f["owner"][fi], f["nb"][fi]):
                     if side >= 0:
                         assert stencil(int(side)) <= local, (r, c, side)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_put_map_is_a_bijection_onto_ghost_rows(world):
+    """hgks_mesh_put_map (f3): every send row of every rank lands on a ghost row of its
+    receiver holding the same global cell, and every ghost row of every rank is written
+    exactly once (host plans only; the loopback GPU tests run k_put with these maps)."""
+    mi = W.kuhn_box(8, 8, 6, h=0.25)
+    mesh = hgks.Mesh(mi, n_ranks=world)
+    plans = [mesh.plan(r) for r in range(world)]
+    hits = [np.zeros(p["l2g"].size, np.int64) for p in plans]
+    for q in range(world):
+        rr, row = mesh.put_map(q)
+        sl = plans[q]["send_list"]
+        assert rr.size == sl.size
+        for p in set(rr.tolist()):
+            sel = rr == p
+            assert p != q and p in plans[q]["peers"]
+            assert np.all(row[sel] >= plans[p]["n_owned"])
+            assert np.array_equal(plans[p]["l2g"][row[sel]], plans[q]["l2g"][sl[sel]])
+            np.add.at(hits[p], row[sel], 1)
+    for p in range(world):
+        n_owned = plans[p]["n_owned"]
+        assert np.all(hits[p][:n_owned] == 0) and np.all(hits[p][n_owned:] == 1), p
