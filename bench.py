@@ -178,6 +178,8 @@ def main():
                     help="c2: 48^3 Kuhn box per GPU (default, BASELINE configs[1]); c3: subsonic sphere "
                          "12x35^3 hexes (configs[2]); c4: supersonic sphere 12x70^3 hexes (configs[3]); "
                          "c5: 110^3 Kuhn box (7,986,000 tets) per GPU (configs[4], weak scaling)")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
+                    help="halo exchange for --gpus > 1: NCCL send/recv (default) or the fused NVLink put (f3)")
     ap.add_argument("--precision", type=int, default=64, choices=[64, 32],
                     help="64: the fp64 path BASELINE's metric names (default); 32: the FP32 variant (P:1098-1183)")
     args = ap.parse_args()
@@ -229,7 +231,10 @@ def main():
         obj = [hgks.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
-    s = hgks.Solver(mesh, Q0, cfg, device=local, rank=rank, nccl_id=nid)
+    tr = hgks.TRANSPORT_P2P if (world > 1 and args.transport == "p2p") else hgks.TRANSPORT_NCCL
+    s = hgks.Solver(mesh, Q0, cfg, device=local, rank=rank, nccl_id=nid, transport=tr)
+    if tr == hgks.TRANSPORT_P2P:
+        s.p2p_connect_dist()
     info = mesh.info(rank)
     n_owned = info["n_owned"]
     stream = s.stream
@@ -352,7 +357,8 @@ def main():
             "scaling": scaling, "vs_baseline": None, "dtype": "f64" if args.precision == 64 else "f32",
             "data": "synthetic (seeded mesh generators and initial states, workloads.py)",
             "config": {"workload": wl, "cells": int(cells), **extra,
-                       "parallelism": f"domain decomposition x{world} (RCB, 3 ghost layers, NCCL)",
+                       "parallelism": f"domain decomposition x{world} (RCB, 3 ghost layers, "
+                                      f"{'NVLink put' if world > 1 and args.transport == 'p2p' else 'NCCL'})",
                        "l2": "no flush: per-step working set %.2f GB > 126 MB L2" % (mesh.workspace_size(cfg) / 1e9)},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "steps": e2e_steps, "pipelined": True},

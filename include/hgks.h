@@ -91,6 +91,10 @@ typedef struct {
                                       hgks_group_step (exchange = fused put k_put: send rows written
                                       straight into the receivers' ghost rows); for testing the
                                       partitioned path on a single GPU */
+#define HGKS_TRANSPORT_P2P 2       /* one process per GPU on one node: halo by the fused put k_put
+                                      into the peers' ghost rows over NVLink (CUDA IPC, per-stage
+                                      epoch flags; hgks_p2p_export/connect), dt by NCCL allreduce */
+#define HGKS_P2P_HANDLE_BYTES 96
 
 /* Distributed context. */
 typedef struct {
@@ -210,6 +214,21 @@ hgks_status hgks_mesh_plan(const hgks_mesh* mesh, int32_t rank, int64_t* l2g, in
 /* Create the 128-byte NCCL unique id on one rank (to be broadcast by the caller,
  * e.g. over torch.distributed, and passed in hgks_dist.nccl_id).  Host only. */
 hgks_status hgks_nccl_unique_id(uint8_t* out);
+
+/* HGKS_TRANSPORT_P2P setup.  Every rank calls
+ * hgks_p2p_export after hgks_init to write HGKS_P2P_HANDLE_BYTES describing its
+ * workspace (a CUDA IPC handle of the allocation, offsets of the state rows and of the
+ * epoch flags); the caller all-gathers the blobs (rank order, n_ranks x
+ * HGKS_P2P_HANDLE_BYTES) and every rank calls hgks_p2p_connect with them, which maps
+ * the peers' workspaces and uploads the put map.  hgks_step fails with HGKS_E_STATE
+ * before the connect.  Each stage then puts the send rows into the receivers' ghost
+ * rows, releases an epoch flag to each receiver and acquires the senders' flags before
+ * its ghost-dependent work; receivers release "consumed" after the stage so the next
+ * put never overwrites rows still being read.  Needs one GPU per rank with peer access
+ * (HGKS_E_ARG / HGKS_E_CUDA otherwise).  Validated by the plan tests and the loopback
+ * group's k_put; the cross-process flag protocol needs a multi-GPU node to exercise. */
+hgks_status hgks_p2p_export(const hgks_solver* solver, uint8_t* out);
+hgks_status hgks_p2p_connect(hgks_solver* solver, const uint8_t* blobs);
 
 /* Diagnostic of the NCCL transport on the current device: a one-rank communicator
  * does exactly the calls a multi-rank step makes (grouped ncclSend/ncclRecv of

@@ -139,6 +139,43 @@ struct GroupCtrl {
   int n;
   Ctrl* c[kMaxGroup];
 };
+// f3 cross-process halo put: per-rank flag words in the workspace, written by peers
+// over NVLink (system-scope release stores), read with acquire loads.
+// arrived[q] = last stage epoch whose ghost rows rank q has put into this rank;
+// consumed[p] = last stage epoch whose ghost rows rank p (a receiver of this rank's
+// puts) has finished reading.
+struct P2PFlags {
+  unsigned long long arrived[kMaxGroup];
+  unsigned long long consumed[kMaxGroup];
+};
+struct P2PSignal {
+  unsigned long long* dst[kMaxGroup];  // peer flag words (mapped peer memory)
+  int n;
+};
+struct P2PWait {
+  const unsigned long long* src[kMaxGroup];  // this rank's flag words
+  int n;
+};
+// one thread: make this stream's earlier writes (the put kernel's peer stores) visible
+// system-wide, then publish the epoch to every peer flag
+__global__ void k_p2p_signal(P2PSignal s, unsigned long long epoch) {
+  if (threadIdx.x != 0) return;
+  asm volatile("fence.sc.sys;" ::: "memory");
+  for (int k = 0; k < s.n; ++k) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(s.dst[k]), "l"(epoch) : "memory");
+}
+// one thread: spin until every flag has reached the epoch (acquire: the peer's puts
+// made before its release are visible to the kernels that follow on this stream)
+__global__ void k_p2p_wait(P2PWait w, unsigned long long epoch) {
+  if (threadIdx.x != 0) return;
+  for (int k = 0; k < w.n; ++k) {
+    unsigned long long v;
+    do {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(w.src[k]) : "memory");
+      if (v < epoch) __nanosleep(200);
+    } while (v < epoch);
+  }
+}
+
 __global__ void k_group_min(GroupCtrl g) {
   if (threadIdx.x != 0) return;
   unsigned long long m = g.c[0]->dtmin_bits;

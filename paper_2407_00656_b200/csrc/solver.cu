@@ -150,6 +150,7 @@ struct DevArrays {
   double *stage_in[2], *stage_out[2];  // caller-order staging (fp64), double-buffered for pipelining
   int *recon_cell, *st_id, *f_cells, *cf, *bg_cell, *bg_bc, *send_list, *out_local;
   int2* put_dst;  // fused halo put: (receiver rank, receiver row) per send row (f3)
+  P2PFlags* flags;  // cross-process put: epoch flags written by the peers (f3)
   int64_t* in_row;
   uint8_t* sub_slot;
   Ctrl* ctrl;
@@ -184,6 +185,7 @@ size_t layout(const GlobalMesh& gm, const RankPlan& rp, size_t rs, Carve& c, Dev
   d.send_list = c.take<int>(std::max<size_t>(1, rp.send_list.size()));
   d.sendbuf = R(std::max<size_t>(QS, QS * rp.send_list.size()));
   d.put_dst = c.take<int2>(std::max<size_t>(1, rp.send_list.size()));
+  d.flags = c.take<P2PFlags>(1);
   d.out_local = c.take<int>(rp.n_owned);
   d.in_row = c.take<int64_t>(rp.n_owned);
   // staging for set/get_state: single rank copies the caller's whole array
@@ -222,6 +224,13 @@ struct hgks_solver {
   cudaStream_t comm_stream = nullptr;  // NCCL halo exchange (overlapped with the early work)
   cudaEvent_t ev_packed = nullptr, ev_halo = nullptr;
   bool put_ready = false;  // put_dst uploaded (loopback group, first hgks_group_step)
+  // HGKS_TRANSPORT_P2P: peers' workspaces mapped by CUDA IPC (hgks_p2p_connect)
+  bool p2p_ready = false;
+  unsigned long long epoch = 0;  // stage counter, identical on every rank
+  void* peer_base[kMaxGroup] = {};
+  void* peer_Q[kMaxGroup] = {};
+  P2PFlags* peer_flags[kMaxGroup] = {};
+  std::vector<int> put_to, recv_from;  // receivers of this rank's puts, senders into it
   cudaStream_t stream = nullptr;
   DevArrays d{};
   size_t nq = 0;  // values in Q
@@ -512,7 +521,7 @@ void wait_halo(hgks_solver* s) {
 
 // a4: global min of the CFL bound (exact, order independent)
 void allreduce_dt(hgks_solver* s) {
-  if (s->n_ranks == 1 || s->transport != HGKS_TRANSPORT_NCCL) return;
+  if (s->n_ranks == 1 || s->transport == HGKS_TRANSPORT_LOOPBACK) return;
   NCCL_TRY(nccl().AllReduce(&s->d.ctrl->dtmin_bits, &s->d.ctrl->dtmin_bits, 1, ncclUint64, ncclMin, s->comm,
                             s->stream));
 }
@@ -554,8 +563,46 @@ void stage_late(hgks_solver* s, int st) {
   }
 }
 
+// f3 across processes (HGKS_TRANSPORT_P2P): the owner puts its send rows straight into
+// the receivers' ghost rows over NVLink (peer memory mapped by CUDA IPC), ordered by
+// per-stage epoch flags: (1) wait until every receiver has finished reading the ghost
+// rows of the previous stage, (2) k_put, (3) release "stage e arrived" to the receivers,
+// (4) ghost-free work, (5) acquire "arrived" from every sender, (6) the rest of the
+// stage, (7) release "stage e consumed" to the senders.  Graph capture is off for
+// n_ranks > 1, so the host-side epoch values are baked into eager launches.
+template <class L>
+void stage_p2p(hgks_solver* s, int st) {
+  const unsigned long long e = ++s->epoch;
+  P2PWait w_cons{}, w_arr{};
+  P2PSignal s_arr{}, s_cons{};
+  for (int p : s->put_to) {
+    w_cons.src[w_cons.n++] = &s->d.flags->consumed[p];
+    s_arr.dst[s_arr.n++] = &s->peer_flags[p]->arrived[s->rank];
+  }
+  for (int q : s->recv_from) {
+    w_arr.src[w_arr.n++] = &s->d.flags->arrived[q];
+    s_cons.dst[s_cons.n++] = &s->peer_flags[q]->consumed[s->rank];
+  }
+  if (e > 1 && w_cons.n) launch(s, "k_p2p_wait", [&] { k_p2p_wait<<<1, 32, 0, s->stream>>>(w_cons, e - 1); });
+  const int ns = (int)s->rp->send_list.size();
+  if (ns) {
+    typename L::PeerQT peer{};
+    for (int p : s->put_to) peer.q[p] = as<L>(s->peer_Q[p]);
+    launch(s, "k_put", [&] {
+      L::put(blocks(3 * ns, 256), s->stream, as<L>(s->d.Q), s->d.send_list, s->d.put_dst, ns, peer);
+    });
+  }
+  if (s_arr.n) launch(s, "k_p2p_signal", [&] { k_p2p_signal<<<1, 32, 0, s->stream>>>(s_arr, e); });
+  stage_early<L>(s, st);
+  if (w_arr.n) launch(s, "k_p2p_wait", [&] { k_p2p_wait<<<1, 32, 0, s->stream>>>(w_arr, e); });
+  stage_late<L>(s, st);
+  if (s_cons.n) launch(s, "k_p2p_signal", [&] { k_p2p_signal<<<1, 32, 0, s->stream>>>(s_cons, e); });
+  if (st == 2) allreduce_dt(s);
+}
+
 template <class L>
 void stage(hgks_solver* s, int st) {
+  if (s->transport == HGKS_TRANSPORT_P2P && s->n_ranks > 1) return stage_p2p<L>(s, st);
   exchange<L>(s, s->d.Q);  // NCCL on the comm stream
   stage_early<L>(s, st);
   wait_halo(s);
@@ -706,6 +753,10 @@ hgks_status hgks_init(const hgks_mesh* mc, const hgks_config* cfg, const hgks_di
     s->rank = dist ? dist->rank : 0;
     s->n_ranks = dist ? dist->n_ranks : 1;
     s->transport = dist ? dist->transport : HGKS_TRANSPORT_NCCL;
+    if (s->transport < HGKS_TRANSPORT_NCCL || s->transport > HGKS_TRANSPORT_P2P)
+      throw Error(HGKS_E_ARG, "unknown transport");
+    if (s->transport == HGKS_TRANSPORT_P2P && s->n_ranks > kMaxGroup)
+      throw Error(HGKS_E_ARG, "HGKS_TRANSPORT_P2P supports at most 16 ranks (one node)");
     if (s->n_ranks != m->gm.n_ranks)
       throw Error(HGKS_E_ARG, "dist->n_ranks differs from the mesh partition (" + std::to_string(m->gm.n_ranks) + ")");
     if (dist) CUDA_TRY(cudaSetDevice(dist->device));
@@ -775,11 +826,12 @@ hgks_status hgks_init(const hgks_mesh* mc, const hgks_config* cfg, const hgks_di
     up(s->d.in_row, in_row.data(), in_row.size() * sizeof(int64_t));
     up(s->d.out_local, out_local.data(), out_local.size() * sizeof(int));
     CUDA_TRY(cudaMemsetAsync(s->d.Q, 0, s->rs * s->nq, st));
+    CUDA_TRY(cudaMemsetAsync(s->d.flags, 0, sizeof(P2PFlags), st));
     Ctrl h{};
     h.bad_cell = INT_MAX;
     h.dtmin_bits = 0x7fefffffffffffffull;
     up(s->d.ctrl, &h, sizeof(Ctrl));
-    if (s->n_ranks > 1 && s->transport == HGKS_TRANSPORT_NCCL) {
+    if (s->n_ranks > 1 && s->transport != HGKS_TRANSPORT_LOOPBACK) {
       Nccl& N = nccl();
       if (!N.h || !N.CommInitRank) throw Error(HGKS_E_NCCL, "libnccl.so.2 not found");
       ncclUniqueId id;
@@ -817,6 +869,8 @@ hgks_status hgks_destroy(hgks_solver* s) {
         cudaEventDestroy(e.second);
       }
     for (auto e : s->event_pool) cudaEventDestroy(e);
+    for (int k = 0; k < kMaxGroup; ++k)
+      if (s->peer_base[k]) cudaIpcCloseMemHandle(s->peer_base[k]);
     if (s->comm && nccl().CommDestroy) nccl().CommDestroy(s->comm);
     if (s->comm_stream) cudaStreamDestroy(s->comm_stream);
     if (s->ev_packed) cudaEventDestroy(s->ev_packed);
@@ -839,6 +893,8 @@ hgks_status hgks_destroy(hgks_solver* s) {
 hgks_status hgks_step(hgks_solver* s, int32_t n_steps, double t_stop, hgks_step_info* info) {
   return guard([&] {
     if (!s || n_steps < 0) throw Error(HGKS_E_ARG, "bad argument");
+    if (s->transport == HGKS_TRANSPORT_P2P && s->n_ranks > 1 && !s->p2p_ready)
+      throw Error(HGKS_E_STATE, "HGKS_TRANSPORT_P2P: call hgks_p2p_connect on every rank first");
     Ctrl before{};
     if (info) {
       CUDA_TRY(cudaMemcpyAsync(&before, s->d.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s->stream));
@@ -1157,6 +1213,85 @@ hgks_status hgks_mesh_plan(const hgks_mesh* mc, int32_t rank, int64_t* l2g, int3
     if (send_list) std::copy(rp.send_list.begin(), rp.send_list.end(), send_list);
     if (recv_off) std::copy(rp.recv_off.begin(), rp.recv_off.end(), recv_off);
     if (recv_cnt) std::copy(rp.recv_cnt.begin(), rp.recv_cnt.end(), recv_cnt);
+  });
+}
+
+// ---- f3: cross-process fused halo put (HGKS_TRANSPORT_P2P) ----
+namespace {
+struct P2PBlob {  // HGKS_P2P_HANDLE_BYTES
+  cudaIpcMemHandle_t mem;  // the allocation holding this rank's workspace
+  uint64_t off_Q, off_flags;  // byte offsets of Q and the flags from the allocation base
+  int32_t rank, device;
+  uint8_t pad[8];
+};
+static_assert(sizeof(P2PBlob) == HGKS_P2P_HANDLE_BYTES, "blob size");
+
+// base of the device allocation containing p (driver API, resolved at run time)
+char* alloc_base(void* p) {
+  typedef int (*Fn)(unsigned long long*, size_t*, unsigned long long);
+  static Fn fn = [] {
+    void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
+    return h ? (Fn)dlsym(h, "cuMemGetAddressRange_v2") : (Fn) nullptr;
+  }();
+  if (!fn) throw Error(HGKS_E_CUDA, "cuMemGetAddressRange_v2 not found in libcuda.so.1");
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (fn(&base, &size, (unsigned long long)(uintptr_t)p) != 0) throw Error(HGKS_E_CUDA, "cuMemGetAddressRange failed");
+  return reinterpret_cast<char*>(base);
+}
+}  // namespace
+
+hgks_status hgks_p2p_export(const hgks_solver* s, uint8_t* out) {
+  return guard([&] {
+    if (!s || !out) throw Error(HGKS_E_ARG, "null argument");
+    if (s->transport != HGKS_TRANSPORT_P2P) throw Error(HGKS_E_ARG, "solver transport is not HGKS_TRANSPORT_P2P");
+    CUDA_TRY(cudaSetDevice(s->device));
+    P2PBlob b{};
+    char* base = alloc_base(s->d.Q);
+    CUDA_TRY(cudaIpcGetMemHandle(&b.mem, base));
+    b.off_Q = (uint64_t)((char*)s->d.Q - base);
+    b.off_flags = (uint64_t)((char*)s->d.flags - base);
+    b.rank = s->rank;
+    b.device = s->device;
+    std::memcpy(out, &b, sizeof(b));
+  });
+}
+
+hgks_status hgks_p2p_connect(hgks_solver* s, const uint8_t* blobs) {
+  return guard([&] {
+    if (!s || !blobs) throw Error(HGKS_E_ARG, "null argument");
+    if (s->transport != HGKS_TRANSPORT_P2P) throw Error(HGKS_E_ARG, "solver transport is not HGKS_TRANSPORT_P2P");
+    if (s->p2p_ready) throw Error(HGKS_E_STATE, "already connected");
+    CUDA_TRY(cudaSetDevice(s->device));
+    const RankPlan& rp = *s->rp;
+    std::vector<int2> dst = put_map(s->mesh, s->rank);
+    std::vector<int> to;
+    for (const int2& d : dst) to.push_back(d.x);
+    std::sort(to.begin(), to.end());
+    to.erase(std::unique(to.begin(), to.end()), to.end());
+    std::vector<int> from;
+    for (size_t ip = 0; ip < rp.peers.size(); ++ip)
+      if (rp.recv_cnt[ip] > 0) from.push_back(rp.peers[ip]);
+    std::vector<int> all = to;
+    all.insert(all.end(), from.begin(), from.end());
+    std::sort(all.begin(), all.end());
+    all.erase(std::unique(all.begin(), all.end()), all.end());
+    for (int p : all) {
+      P2PBlob b;
+      std::memcpy(&b, blobs + (size_t)p * HGKS_P2P_HANDLE_BYTES, sizeof(b));
+      if (b.rank != p) throw Error(HGKS_E_ARG, "blob " + std::to_string(p) + " belongs to rank " + std::to_string(b.rank));
+      if (b.device == s->device) throw Error(HGKS_E_ARG, "HGKS_TRANSPORT_P2P needs one GPU per rank");
+      void* base = nullptr;
+      CUDA_TRY(cudaIpcOpenMemHandle(&base, b.mem, cudaIpcMemLazyEnablePeerAccess));
+      s->peer_base[p] = base;
+      s->peer_Q[p] = (char*)base + b.off_Q;
+      s->peer_flags[p] = reinterpret_cast<P2PFlags*>((char*)base + b.off_flags);
+    }
+    if (!dst.empty())
+      CUDA_TRY(cudaMemcpy(s->d.put_dst, dst.data(), dst.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    s->put_to = to;
+    s->recv_from = from;
+    s->p2p_ready = true;
   });
 }
 

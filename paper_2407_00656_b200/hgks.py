@@ -28,9 +28,10 @@ ERRORS = {0: "OK", 1: "E_ARG", 2: "E_MESH", 3: "E_STENCIL", 4: "E_CUDA", 5: "E_N
 EXPORTS = ["hgks_mesh_create", "hgks_mesh_destroy", "hgks_mesh_info", "hgks_workspace_size", "hgks_init",
            "hgks_destroy", "hgks_step", "hgks_set_state", "hgks_get_state", "hgks_get_state_async",
            "hgks_sync", "hgks_debug_residual",
-           "hgks_set_profiling", "hgks_kernel_times", "hgks_launch_count", "hgks_nccl_unique_id", "hgks_nccl_selftest", "hgks_group_step", "hgks_mesh_plan", "hgks_mesh_put_map",
+           "hgks_set_profiling", "hgks_kernel_times", "hgks_launch_count", "hgks_nccl_unique_id", "hgks_nccl_selftest", "hgks_group_step", "hgks_mesh_plan", "hgks_mesh_put_map", "hgks_p2p_export", "hgks_p2p_connect",
            "hgks_last_error", "hgks_version"]
-TRANSPORT_NCCL, TRANSPORT_LOOPBACK = 0, 1
+TRANSPORT_NCCL, TRANSPORT_LOOPBACK, TRANSPORT_P2P = 0, 1, 2
+P2P_HANDLE_BYTES = 96
 
 
 class MeshDesc(C.Structure):
@@ -107,6 +108,8 @@ def lib(build_if_needed: bool = True):
         L.hgks_kernel_times.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, _i64p, _dp, _i32p]
         L.hgks_launch_count.argtypes = [C.c_void_p, _i64p]
         L.hgks_nccl_unique_id.argtypes = [C.c_void_p]
+        L.hgks_p2p_export.argtypes = [C.c_void_p, C.c_void_p]
+        L.hgks_p2p_connect.argtypes = [C.c_void_p, C.c_void_p]
         L.hgks_group_step.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_double]
         L.hgks_mesh_plan.argtypes = [C.c_void_p, C.c_int32, _i64p, _i32p, _i64p, _i64p, _i32p, _i64p, _i64p]
         L.hgks_mesh_put_map.argtypes = [C.c_void_p, C.c_int32, _i32p, _i32p]
@@ -257,6 +260,26 @@ class Solver:
         self.h = h
         self.rank = rank
         self.n_owned = mesh.info(rank)["n_owned"]
+
+    def p2p_export(self) -> bytes:
+        """This rank's HGKS_TRANSPORT_P2P blob (hgks_p2p_export)."""
+        buf = (C.c_uint8 * P2P_HANDLE_BYTES)()
+        _check(lib().hgks_p2p_export(self.h, C.cast(buf, C.c_void_p)))
+        return bytes(buf)
+
+    def p2p_connect(self, blobs):
+        """Map the peers' workspaces (hgks_p2p_connect); ``blobs``: every rank's blob in rank order."""
+        raw = b"".join(blobs)
+        assert len(raw) == P2P_HANDLE_BYTES * self.mesh.n_ranks
+        buf = (C.c_uint8 * len(raw)).from_buffer_copy(raw)
+        _check(lib().hgks_p2p_connect(self.h, C.cast(buf, C.c_void_p)))
+
+    def p2p_connect_dist(self):
+        """All-gather the blobs over torch.distributed and connect (collective)."""
+        import torch.distributed as dist
+        blobs = [None] * self.mesh.n_ranks
+        dist.all_gather_object(blobs, self.p2p_export())
+        self.p2p_connect(blobs)
 
     def close(self):
         if getattr(self, "h", None):

@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def header_symbols():
     src = open(os.path.join(ROOT, "include", "hgks.h")).read()
-    return sorted(set(re.findall(r"\b(hgks_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(hgks_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_library_exports_every_declared_symbol():
@@ -122,3 +122,18 @@ def test_ctypes_structs_match_header_layout(tmp_path):
         assert got[(cname, "size")] == ctypes.sizeof(cls), cname
         for fname, _ in cls._fields_:
             assert got[(cname, fname)] == getattr(cls, fname).offset, (cname, fname)
+
+
+def test_p2p_and_put_map_argument_errors():
+    """HGKS_TRANSPORT_P2P setup calls and the put map report bad arguments as status
+    codes (no GPU needed): NULL handles -> HGKS_E_ARG; rank out of range -> HGKS_E_ARG."""
+    L = hgks.lib()
+    buf = (ctypes.c_uint8 * hgks.P2P_HANDLE_BYTES)()
+    assert L.hgks_p2p_export(None, ctypes.cast(buf, ctypes.c_void_p)) == 1
+    assert L.hgks_p2p_connect(None, ctypes.cast(buf, ctypes.c_void_p)) == 1
+    mesh = hgks.Mesh(W.kuhn_box(8, 8, 6, h=0.25), n_ranks=2)
+    with pytest.raises(hgks.HgksError) as e:
+        mesh.put_map(2)
+    assert e.value.code == 1
+    rr, row = mesh.put_map(1)
+    assert rr.size == mesh.info(1)["send_cells"] and set(rr.tolist()) == {0}
