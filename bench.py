@@ -306,30 +306,38 @@ def main():
 
     # ---------------- roofline of the dominant kernel ----------------
     hbm_peak, hbm_src, alu_peak, alu_src = peaks(args.precision)
-    top = max(ktimes.items(), key=lambda kv: kv[1]["ms"])
-    name, kt = top
-    avg_ms = kt["ms"] / max(1, kt["launches"])
-    roof = None
-    if name.startswith("k_recon"):
-        # recon runs over owned cells and layer-1 ghosts
-        n_recon = info["n_owned"] + info["ghost_layer"][0]
-        bytes_per_launch = recon_bytes_per_cell(*layout, rs=args.precision // 8) * n_recon
-        achieved = bytes_per_launch / (avg_ms * 1e-3) / 1e9
-        roof = {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": None,
-                "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,
-                "peak_source": hbm_src + " (burst copy)"}
-    else:
-        flops = json.load(open(os.path.join(ROOT, "profiles", "flops_per_unit.json")))
+    flops = json.load(open(os.path.join(ROOT, "profiles", "flops_per_unit.json")))
+
+    def roof_of(name):
+        kt = ktimes[name]
+        if kt["launches"] == 0 or kt["ms"] <= 0:
+            return None
+        avg_ms = kt["ms"] / kt["launches"]
+        if name.startswith("k_recon"):
+            # recon runs over owned cells and layer-1 ghosts
+            n_recon = info["n_owned"] + info["ghost_layer"][0]
+            bytes_per_launch = recon_bytes_per_cell(*layout, rs=args.precision // 8) * n_recon
+            achieved = bytes_per_launch / (avg_ms * 1e-3) / 1e9
+            return {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": achieved / hbm_peak, "traffic": None,
+                    "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,
+                    "peak_source": hbm_src + " (burst copy)"}
         fkey = "c2" if args.workload == "c5" else args.workload  # same tet kernels and per-face work
         fpf = flops.get(fkey, {}).get(name, {}).get(f"fp{args.precision}_flops_per_face")
         nf = info["n_faces"] - info["n_faces_bc"]  # interior faces (the counts are per interior face)
-        if fpf:
-            achieved = fpf * nf / (avg_ms * 1e-3) / 1e12
-            roof = {"kernel": name, "bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",
-                    "frac": achieved / alu_peak, "traffic": None, "avg_launch_ms": avg_ms,
-                    "flops_per_face": fpf, "flops_source": "ncu sass op counts (2 fma + add + mul), "
-                                                          "profiles/flops_per_unit.json", "peak_source": alu_src}
+        if not fpf:
+            return None
+        achieved = fpf * nf / (avg_ms * 1e-3) / 1e12
+        return {"kernel": name, "bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",
+                "frac": achieved / alu_peak, "traffic": None, "avg_launch_ms": avg_ms,
+                "flops_per_face": fpf, "flops_source": "ncu sass op counts (2 fma + add + mul), "
+                                                      "profiles/flops_per_unit.json", "peak_source": alu_src}
+
+    top = max(ktimes.items(), key=lambda kv: kv[1]["ms"])
+    roof = roof_of(top[0])
+    # the same figures for every reconstruction and flux kernel (north_star: both >= 0.5)
+    rooflines = {n: {k: r[k] for k in ("bound", "achieved", "unit", "frac", "avg_launch_ms")}
+                 for n in sorted(ktimes) if n.startswith(("k_recon", "k_flux")) for r in [roof_of(n)] if r}
     traffic_path = os.path.join(ROOT, "profiles", "traffic.json")
     if roof and os.path.exists(traffic_path):
         tr = (json.load(open(traffic_path)).get(roof["kernel"])
@@ -362,7 +370,7 @@ def main():
                        "l2": "no flush: per-step working set %.2f GB > 126 MB L2" % (mesh.workspace_size(cfg) / 1e9)},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "steps": e2e_steps, "pipelined": True},
-            "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
+            "gpu_launches": launches, "roofline": roof, "rooflines": rooflines, "cpu_baseline": cpu, "clocks": clocks,
             "kernels": {k: {"launches": v["launches"], "avg_ms": v["ms"] / max(1, v["launches"]),
                             "share": v["ms"] / max(1e-30, sum(x["ms"] for x in ktimes.values()))}
                         for k, v in ktimes.items()},
