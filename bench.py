@@ -178,6 +178,8 @@ def main():
                     help="c2: 48^3 Kuhn box per GPU (default, BASELINE configs[1]); c3: subsonic sphere "
                          "12x35^3 hexes (configs[2]); c4: supersonic sphere 12x70^3 hexes (configs[3]); "
                          "c5: 110^3 Kuhn box (7,986,000 tets) per GPU (configs[4], weak scaling)")
+    ap.add_argument("--jitter", type=float, default=0.0,
+                    help="c2/c5: interior node jitter U[-j h, j h] (seed 656), SURVEY 8(d) benchmark rule")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
                     help="halo exchange for --gpus > 1: NCCL send/recv (default) or the fused NVLink put (f3)")
     ap.add_argument("--precision", type=int, default=64, choices=[64, 32],
@@ -206,7 +208,7 @@ def main():
     if args.workload in ("c2", "c5"):
         nb = N_BLOCK if args.workload == "c2" else N_BLOCK_C5
         nx, ny, nz = box_dims(world, nb)
-        mi = W.kuhn_box(nx, ny, nz, h=2.0 / nb)
+        mi = W.kuhn_box(nx, ny, nz, h=2.0 / nb, jitter=args.jitter)
         Q0 = W.advection_ic(mi, gamma=GAMMA)
         cfg = hgks.SolverConfig(gamma=GAMMA, cfl=CFL, precision=args.precision)
         wl = (f"configs[1] top size: {nb}^3 Kuhn box per GPU, 6 tets/cube, periodic, tau=0, CFL {CFL}"
@@ -214,6 +216,9 @@ def main():
               f"configs[4]: {nb}^3 Kuhn box ({6 * nb ** 3} tets) per GPU, periodic, tau=0, CFL {CFL}")
         scaling, layout = "weak", (14, 4, 6)
         extra = {"box_cubes": [nx, ny, nz]}
+        if args.jitter > 0:
+            wl += f", nodes jittered U[-{args.jitter}h, {args.jitter}h] (seed 656)"
+            extra["jitter"] = args.jitter
     else:
         n, ma, re = (35, 0.2535, 118.0) if args.workload == "c3" else (70, 1.5, 300.0)
         mi = W.sphere_shell(n)

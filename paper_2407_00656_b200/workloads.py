@@ -319,6 +319,18 @@ def kuhn_density_mean(mesh: MeshInput, t: float = 0.0, amp: float = 0.2) -> np.n
     hk = h[kuhn]
     s0k = s0[kuhn]
     out[kuhn] = 1.0 + amp * (G(s0k + 3 * hk) - 3 * G(s0k + 2 * hk) + 3 * G(s0k + hk) - G(s0k)) / hk ** 3
+    # general tets with well-separated vertex values: the same identity with unequal
+    # spacing, mean f(s) = 3! G[s0, s1, s2, s3] (third divided difference, G^(3) = f)
+    gap = d.min(axis=1)
+    span = s_sorted[:, 3] - s_sorted[:, 0]
+    gen = ~kuhn & (gap > 0.05 * np.maximum(span, 1e-300))
+    if gen.any():
+        x = s_sorted[gen]
+        dd = G(x)
+        for k in range(1, 4):
+            dd = (dd[:, 1:] - dd[:, :-1]) / (x[:, k:] - x[:, :-k])
+        out[gen] = 1.0 + amp * 6.0 * dd[:, 0]
+        kuhn = kuhn | gen
     if (~kuhn).any():
         sub = MeshInput(xyz=mesh.xyz, cell_type=mesh.cell_type[~kuhn], cell_nodes=mesh.cell_nodes[~kuhn])
         out[~kuhn] = tet_cell_means(sub, lambda x, y, z: 1.0 + amp * np.sin(np.pi * (x + y + z - 3.0 * t)), order=8)
