@@ -178,6 +178,8 @@ def main():
                     help="c2: 48^3 Kuhn box per GPU (default, BASELINE configs[1]); c3: subsonic sphere "
                          "12x35^3 hexes (configs[2]); c4: supersonic sphere 12x70^3 hexes (configs[3]); "
                          "c5: 110^3 Kuhn box (7,986,000 tets) per GPU (configs[4], weak scaling)")
+    ap.add_argument("--box", type=int, default=0,
+                    help="c2: cubes per axis per GPU (default 48; SURVEY 8(d) also quotes N = 80)")
     ap.add_argument("--jitter", type=float, default=0.0,
                     help="c2/c5: interior node jitter U[-j h, j h] (seed 656), SURVEY 8(d) benchmark rule")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
@@ -207,11 +209,13 @@ def main():
 
     if args.workload in ("c2", "c5"):
         nb = N_BLOCK if args.workload == "c2" else N_BLOCK_C5
+        if args.box > 0 and args.workload == "c2":
+            nb = args.box
         nx, ny, nz = box_dims(world, nb)
         mi = W.kuhn_box(nx, ny, nz, h=2.0 / nb, jitter=args.jitter)
         Q0 = W.advection_ic(mi, gamma=GAMMA)
         cfg = hgks.SolverConfig(gamma=GAMMA, cfl=CFL, precision=args.precision)
-        wl = (f"configs[1] top size: {nb}^3 Kuhn box per GPU, 6 tets/cube, periodic, tau=0, CFL {CFL}"
+        wl = (f"configs[1]{' top size' if nb == N_BLOCK else ''}: {nb}^3 Kuhn box per GPU, 6 tets/cube, periodic, tau=0, CFL {CFL}"
               if args.workload == "c2" else
               f"configs[4]: {nb}^3 Kuhn box ({6 * nb ** 3} tets) per GPU, periodic, tau=0, CFL {CFL}")
         scaling, layout = "weak", (14, 4, 6)
