@@ -227,6 +227,11 @@ hgks_status hgks_nccl_unique_id(uint8_t* out);
  * put never overwrites rows still being read.  Needs one GPU per rank with peer access
  * (HGKS_E_ARG / HGKS_E_CUDA otherwise).  Validated by the plan tests and the loopback
  * group's k_put; the cross-process flag protocol needs a multi-GPU node to exercise. */
+/* Diagnostic on the current device, no peers: k_put through a pointer table into a
+ * second buffer (rows checked bitwise), k_p2p_signal on two flags (read back), then
+ * k_p2p_wait on flags that already hold the epoch.  HGKS_E_CUDA with a message on any
+ * mismatch. */
+hgks_status hgks_p2p_selftest(void);
 hgks_status hgks_p2p_export(const hgks_solver* solver, uint8_t* out);
 hgks_status hgks_p2p_connect(hgks_solver* solver, const uint8_t* blobs);
 

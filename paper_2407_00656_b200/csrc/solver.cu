@@ -1099,6 +1099,75 @@ hgks_status hgks_nccl_unique_id(uint8_t* out) {
   });
 }
 
+// Mechanics of the P2P transport's kernels on one device, with no rank waiting on
+// another: k_put through a pointer table (fp64 rows into a second buffer), k_p2p_signal
+// publishing an epoch, the flag read back, then k_p2p_wait on a flag that already holds
+// the epoch (returns at once).  The cross-process ordering needs a multi-GPU node.
+hgks_status hgks_p2p_selftest(void) {
+  return guard([&] {
+    constexpr int n = 1000;
+    double *src = nullptr, *dst = nullptr;
+    int *list = nullptr;
+    int2* map = nullptr;
+    P2PFlags* fl = nullptr;
+    auto cleanup = [&] {
+      cudaFree(src); cudaFree(dst); cudaFree(list); cudaFree(map); cudaFree(fl);
+    };
+    try {
+      CUDA_TRY(cudaMalloc(&src, sizeof(double) * QS * n));
+      CUDA_TRY(cudaMalloc(&dst, sizeof(double) * QS * (n + 7)));
+      CUDA_TRY(cudaMalloc(&list, sizeof(int) * n));
+      CUDA_TRY(cudaMalloc(&map, sizeof(int2) * n));
+      CUDA_TRY(cudaMalloc(&fl, sizeof(P2PFlags)));
+      std::vector<double> hs((size_t)QS * n), hd((size_t)QS * (n + 7), -1.0);
+      std::vector<int> hl(n);
+      std::vector<int2> hm(n);
+      for (size_t k = 0; k < hs.size(); ++k) hs[k] = 0.5 * (double)k + 1e-3;
+      for (int j = 0; j < n; ++j) {
+        hl[j] = (j * 37) % n;          // send rows in a scrambled order
+        hm[j] = int2{3, 7 + (n - 1 - j)};  // receiver "rank 3", reversed rows after 7 others
+      }
+      CUDA_TRY(cudaMemcpy(src, hs.data(), hs.size() * sizeof(double), cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(dst, hd.data(), hd.size() * sizeof(double), cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(list, hl.data(), hl.size() * sizeof(int), cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(map, hm.data(), hm.size() * sizeof(int2), cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemset(fl, 0, sizeof(P2PFlags)));
+      p64::PeerQ peer{};
+      peer.q[3] = dst;
+      p64::Launch::put(blocks(3 * n, 256), 0, src, list, map, n, peer);
+      P2PSignal sg{};
+      sg.dst[0] = &fl->arrived[5];
+      sg.dst[1] = &fl->consumed[2];
+      sg.n = 2;
+      k_p2p_signal<<<1, 32>>>(sg, 7ull);
+      CUDA_TRY(cudaGetLastError());
+      P2PFlags h{};
+      CUDA_TRY(cudaMemcpy(&h, fl, sizeof(P2PFlags), cudaMemcpyDeviceToHost));
+      if (h.arrived[5] != 7 || h.consumed[2] != 7 || h.arrived[0] != 0)
+        throw Error(HGKS_E_CUDA, "k_p2p_signal wrote wrong flags");
+      P2PWait w{};
+      w.src[0] = &fl->arrived[5];
+      w.src[1] = &fl->consumed[2];
+      w.n = 2;
+      k_p2p_wait<<<1, 32>>>(w, 7ull);
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaDeviceSynchronize());
+      CUDA_TRY(cudaMemcpy(hd.data(), dst, hd.size() * sizeof(double), cudaMemcpyDeviceToHost));
+      for (int r = 0; r < 7; ++r)
+        for (int v = 0; v < QS; ++v)
+          if (hd[(size_t)r * QS + v] != -1.0) throw Error(HGKS_E_CUDA, "k_put wrote outside its rows");
+      for (int j = 0; j < n; ++j)
+        for (int v = 0; v < QS; ++v)
+          if (hd[(size_t)(7 + n - 1 - j) * QS + v] != hs[(size_t)hl[j] * QS + v])
+            throw Error(HGKS_E_CUDA, "k_put row " + std::to_string(j) + " differs");
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
+  });
+}
+
 hgks_status hgks_nccl_selftest(void) {
   return guard([&] {
     Nccl& N = nccl();

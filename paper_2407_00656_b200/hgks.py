@@ -28,7 +28,7 @@ ERRORS = {0: "OK", 1: "E_ARG", 2: "E_MESH", 3: "E_STENCIL", 4: "E_CUDA", 5: "E_N
 EXPORTS = ["hgks_mesh_create", "hgks_mesh_destroy", "hgks_mesh_info", "hgks_workspace_size", "hgks_init",
            "hgks_destroy", "hgks_step", "hgks_set_state", "hgks_get_state", "hgks_get_state_async",
            "hgks_sync", "hgks_debug_residual",
-           "hgks_set_profiling", "hgks_kernel_times", "hgks_launch_count", "hgks_nccl_unique_id", "hgks_nccl_selftest", "hgks_group_step", "hgks_mesh_plan", "hgks_mesh_put_map", "hgks_p2p_export", "hgks_p2p_connect",
+           "hgks_set_profiling", "hgks_kernel_times", "hgks_launch_count", "hgks_nccl_unique_id", "hgks_nccl_selftest", "hgks_group_step", "hgks_mesh_plan", "hgks_mesh_put_map", "hgks_p2p_export", "hgks_p2p_connect", "hgks_p2p_selftest",
            "hgks_last_error", "hgks_version"]
 TRANSPORT_NCCL, TRANSPORT_LOOPBACK, TRANSPORT_P2P = 0, 1, 2
 P2P_HANDLE_BYTES = 96
@@ -149,6 +149,11 @@ class SolverConfig:
     def c(self) -> Config:
         return Config(self.gamma, self.cfl, self.fixed_dt, self.tau_mode, self.c1, self.mu_inf, self.t_inf,
                       self.mu_exp, self.eps_value(), self.omega_pow, (C.c_double * 5)(*self.freestream), self.precision)
+
+
+def p2p_selftest() -> None:
+    """k_put / k_p2p_signal / k_p2p_wait mechanics on one device (hgks_p2p_selftest)."""
+    _check(lib().hgks_p2p_selftest())
 
 
 def nccl_selftest() -> None:

@@ -93,3 +93,10 @@ def test_nccl_transport_selftest(cuda_ok):
     stream, uint64 allreduce-min on the compute stream) through libhgks's runtime
     NCCL binding, on a one-rank communicator (one GPU here)."""
     hgks.nccl_selftest()
+
+
+def test_p2p_kernels_selftest(cuda_ok):
+    """HGKS_TRANSPORT_P2P's kernels on one device with no cross-rank waiting: k_put via a
+    pointer table (bitwise rows, nothing outside them), flag release, acquire-wait on
+    flags already set."""
+    hgks.p2p_selftest()
