@@ -1,16 +1,18 @@
 """Benchmark: fp64 cell-updates/s of the HGKS hot path on B200 (BASELINE.json metric).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--workload c5|c2|c3|c4]
 
 One step = one full S2O4 step (2 stages of halo exchange + WENO reconstruction
-+ face flux + update, plus the CFL min) over every cell.  Workload (N = 1):
-configs[1] of BASELINE.json at its largest member, the 48^3 Kuhn box (663,552
-tets, periodic, tau = 0, CFL 0.3, accuracy-test IC).  N > 1 (torchrun, one
-process per GPU): weak scaling, one 48^3 block per GPU (box extended along
-x/y/z, RCB partition, NCCL halo exchange + allreduce-min).
++ face flux + update, plus the CFL min) over every cell.  Default workload: the
+largest single-GPU configuration of BASELINE.json, configs[4] -- the 110^3 Kuhn
+box, 7,986,000 periodic tets per GPU, tau = 0, CFL 0.3, accuracy-test IC.  N > 1
+(torchrun, one process per GPU): weak scaling, one 110^3 block per GPU (box
+extended along x/y/z, RCB partition, NCCL halo exchange + allreduce-min).
+--workload c2 (48^3, configs[1]), c3/c4 (sphere shells, configs[2]/[3]) are
+the other configurations.
 
 --impl reference times the CPU oracle (oracle/) on the box's host cores on a
-bounded sample of the same workload family (rank 0 only).
+bounded sample of the same workload (rank 0 only).
 """
 from __future__ import annotations
 
@@ -62,53 +64,88 @@ def peaks(precision=64):
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region.
+
+    NVML polled every 5 ms from a thread (so even a few-hundred-millisecond timed region
+    carries its own record; the GPU is found by its PCI bus id, robust to
+    CUDA_VISIBLE_DEVICES); nvidia-smi -lms 100 if NVML is unavailable."""
+
+    REASONS = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
+        self.rows = []  # (sm_mhz, sm_max_mhz, {reason names})
         self.proc = None
+        self.stop = threading.Event()
+        self.src = None
 
-    def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-        try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-            t0 = time.time()
-            while not self.rows and time.time() - t0 < 10:  # sampler is live before the timed region
-                time.sleep(0.02)
-            self.rows.clear()
-        except Exception:
-            self.proc = None
-        return self
+    def _nvml_handle(self):
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        p = torch.cuda.get_device_properties(self.index)
+        bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
 
-    def _read(self):
+    def _poll_nvml(self, nv, h):
+        bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self.stop.is_set():
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.rows.append((float(sm), float(mx), {k for k, b in bits.items() if r & b}))
+            time.sleep(0.005)
+
+    def _read_smi(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 6:
-                self.rows.append(parts)
+            if len(parts) == 6 and parts[0].replace(".", "").isdigit():
+                self.rows.append((float(parts[0]), float(parts[1]),
+                                  {self.REASONS[k] for k in range(4) if parts[2 + k].lower() == "active"}))
+
+    def __enter__(self):
+        try:
+            nv, h = self._nvml_handle()
+            self.t = threading.Thread(target=self._poll_nvml, args=(nv, h), daemon=True)
+            self.src = "nvml 5 ms"
+        except Exception:
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            try:
+                self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                              "--format=csv,noheader,nounits", "-lms", "100"],
+                                             stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self.t = threading.Thread(target=self._read_smi, daemon=True)
+                self.src = "nvidia-smi 100 ms"
+            except Exception:
+                return self
+        self.t.start()
+        t0 = time.time()
+        while not self.rows and time.time() - t0 < 10:  # sampler is live before the timed region
+            time.sleep(0.01)
+        self.rows.clear()
+        return self
 
     def __exit__(self, *a):
+        self.stop.set()
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+        elif self.src:
+            self.t.join(timeout=2)
 
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[2 + k].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        rows = list(self.rows)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0, "source": self.src}
+        return {"sm_mhz": float(np.median([r[0] for r in rows])), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": sorted(set().union(*[r[2] for r in rows])), "samples": len(rows), "source": self.src}
 
 
 # algorithmic bytes / flops per unit (DESIGN.md "Rooflines"), tets
@@ -122,16 +159,84 @@ def recon_bytes_per_cell(K=14, M=4, NM=6, rs=8):
     return op + idx + geo + q + rec
 
 
-def cpu_oracle_rate(N: int, steps: int, threads: int):
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def oracle_problem(workload: str, N: int):
+    """The oracle's copy of a bench workload at a bounded size: Kuhn box N^3 (c2/c5, the same
+    per-cell work at any box size) or sphere shell 12 N^3 (c3/c4)."""
     from oracle import oracle as O
     from paper_2407_00656_b200 import workloads as W
-    mi = W.kuhn_box(N)
+    if workload in ("c2", "c5"):
+        mi = W.kuhn_box(N)
+        return mi, W.advection_ic(mi, gamma=GAMMA), O.OracleConfig(cfl=CFL), f"{N}^3 Kuhn box ({6 * N ** 3} tets)"
+    ma, re, _ = SPHERE[workload]
+    mi = W.sphere_shell(N)
+    Q0 = W.uniform_state(mi.n_cells, 1.0, (ma, 0.0, 0.0), 1.0 / GAMMA, gamma=GAMMA)
+    cfg = O.OracleConfig(cfl=0.5, tau_mode=1, mu_inf=ma / re, c1=1.0, t_inf=1.0 / GAMMA,
+                         freestream=(1.0, ma, 0.0, 0.0, 1.0 / GAMMA))
+    return mi, Q0, cfg, f"sphere shell 12x{N}^3 ({12 * N ** 3} hexes, Ma {ma}, Re {re})"
+
+
+def cpu_oracle_rate(workload: str, N: int, steps: int, threads: int):
+    from oracle import oracle as O
+    mi, Q0, cfg, what = oracle_problem(workload, N)
     m = O.OracleMesh(mi)
-    s = O.OracleSolver(m, W.advection_ic(mi, gamma=GAMMA), O.OracleConfig(cfl=CFL), threads=threads)
+    s = O.OracleSolver(m, Q0, cfg, threads=threads)
     t0 = time.perf_counter()
     s.step(steps)
     dt = time.perf_counter() - t0
-    return m.n_cells * steps / dt, dt, m.n_cells
+    return m.n_cells * steps / dt, dt, what
+
+
+# bounded oracle samples per workload family: (all cores N, one core N); the oracle's cost per
+# cell does not depend on the box size, so a smaller box of the same family is the same work
+CPU_SAMPLE = {"c2": (48, 12), "c5": (48, 12), "c3": (12, 5), "c4": (12, 5)}
+
+
+def cpu_baseline(workload: str):
+    threads = len(os.sched_getaffinity(0))
+    n_all, n_one = CPU_SAMPLE[workload]
+    rate, secs, what = cpu_oracle_rate(workload, n_all, 1, threads)
+    rate1, secs1, what1 = cpu_oracle_rate(workload, n_one, 1, 1)
+    return {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"1 oracle step of the {what}, same workload family and per-cell work, {secs:.1f} s on "
+                      f"{threads} threads",
+            "one_thread": {"value": rate1, "unit": UNIT, "cores": 1,
+                           "sample": f"1 oracle step of the {what1}, {secs1:.1f} s on 1 thread"},
+            "cpu_model": cpu_model()}
+
+
+SPHERE = {"c3": (0.2535, 118.0, 35), "c4": (1.5, 300.0, 70)}
+
+
+def workload_config(workload: str, world: int, box: int = 0, jitter: float = 0.0):
+    """(config dict, scaling, recon layout) of a bench workload; no mesh is built here."""
+    if workload in ("c2", "c5"):
+        nb = N_BLOCK if workload == "c2" else N_BLOCK_C5
+        if box > 0 and workload == "c2":
+            nb = box
+        nx, ny, nz = box_dims(world, nb)
+        wl = (f"configs[1]{' top size' if nb == N_BLOCK else ''}: {nb}^3 Kuhn box per GPU, 6 tets/cube, periodic, "
+              f"tau=0, CFL {CFL}" if workload == "c2" else
+              f"configs[4]: {nb}^3 Kuhn box ({6 * nb ** 3} tets) per GPU, periodic, tau=0, CFL {CFL}")
+        cfg = {"workload": wl, "cells": 6 * nx * ny * nz, "box_cubes": [nx, ny, nz], "block_cubes": nb}
+        if jitter > 0:
+            cfg["workload"] += f", nodes jittered U[-{jitter}h, {jitter}h] (seed 656)"
+            cfg["jitter"] = jitter
+        return cfg, "weak", (14, 4, 6)
+    ma, re, n = SPHERE[workload]
+    wl = (f"configs[{2 if workload == 'c3' else 3}]: sphere shell 12x{n}^3 hexes, Ma {ma}, Re {re}, "
+          f"NS collision time, wall + farfield, CFL 0.5, free-stream start")
+    return {"workload": wl, "cells": 12 * n ** 3, "sphere_N": n}, "strong", (24, 8, 3)
 
 
 def run_reference(args):
@@ -139,29 +244,34 @@ def run_reference(args):
     if rank != 0:
         return
     threads = len(os.sched_getaffinity(0))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     from oracle import oracle as O
-    from paper_2407_00656_b200 import workloads as W
-    # bounded sample: every timed step is one full oracle step on an Ns^3 Kuhn box, Ns chosen so
-    # the whole --steps/--warmup run stays near two minutes (the oracle does ~6e4 cell-updates/s
-    # on 16 host cores; its cost per cell does not depend on the box size)
-    cells_budget = 120.0 * 6e4 / max(1, args.steps + args.warmup)
-    Ns = int(max(8, min(24, (cells_budget / 6.0) ** (1.0 / 3.0))))
-    mi = W.kuhn_box(Ns)
+    # bounded sample: every timed step is one full oracle step of the same workload family on a
+    # smaller box, sized so the whole --steps/--warmup run stays near two minutes (the oracle
+    # does ~6e4 tet cell-updates/s on 16 host cores; its cost per cell does not depend on the size)
+    if args.workload in ("c2", "c5"):
+        cells_budget = 120.0 * 6e4 / max(1, args.steps + args.warmup)
+        Ns = int(max(8, min(24, (cells_budget / 6.0) ** (1.0 / 3.0))))
+    else:
+        cells_budget = 120.0 * 1.5e4 / max(1, args.steps + args.warmup)
+        Ns = int(max(4, min(10, (cells_budget / 12.0) ** (1.0 / 3.0))))
+    mi, Q0, ocfg, what = oracle_problem(args.workload, Ns)
     m = O.OracleMesh(mi)
-    s = O.OracleSolver(m, W.advection_ic(mi, gamma=GAMMA), O.OracleConfig(cfl=CFL), threads=threads)
+    s = O.OracleSolver(m, Q0, ocfg, threads=threads)
     s.step(args.warmup)
     t0 = time.perf_counter()
     s.step(args.steps)
     dt = time.perf_counter() - t0
     value = m.n_cells * args.steps / dt
-    sample = (f"each step: one full S2O4 step of the oracle on the {Ns}^3 Kuhn box ({m.n_cells} tets, same "
-              f"per-cell work as the {N_BLOCK}^3 workload)")
+    config, scaling, _ = workload_config(args.workload, world, args.box, args.jitter)
+    sample = f"each step: one full S2O4 step of the oracle on the {what} (same per-cell work as the workload)"
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"configs[1]: Kuhn periodic tets, accuracy-test IC, tau=0, CFL {CFL}",
-                       "cells": m.n_cells},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded mesh generators and initial states, workloads.py)",
+            "config": config,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -174,10 +284,10 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=50)
-    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5"],
-                    help="c2: 48^3 Kuhn box per GPU (default, BASELINE configs[1]); c3: subsonic sphere "
-                         "12x35^3 hexes (configs[2]); c4: supersonic sphere 12x70^3 hexes (configs[3]); "
-                         "c5: 110^3 Kuhn box (7,986,000 tets) per GPU (configs[4], weak scaling)")
+    ap.add_argument("--workload", default="c5", choices=["c2", "c3", "c4", "c5"],
+                    help="c5: 110^3 Kuhn box (7,986,000 tets) per GPU (default: configs[4], the largest "
+                         "single-GPU config, weak scaling); c2: 48^3 Kuhn box per GPU (configs[1]); c3: subsonic "
+                         "sphere 12x35^3 hexes (configs[2]); c4: supersonic sphere 12x70^3 hexes (configs[3])")
     ap.add_argument("--box", type=int, default=0,
                     help="c2: cubes per axis per GPU (default 48; SURVEY 8(d) also quotes N = 80)")
     ap.add_argument("--jitter", type=float, default=0.0,
@@ -207,33 +317,19 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
+    config, scaling, layout = workload_config(args.workload, world, args.box, args.jitter)
     if args.workload in ("c2", "c5"):
-        nb = N_BLOCK if args.workload == "c2" else N_BLOCK_C5
-        if args.box > 0 and args.workload == "c2":
-            nb = args.box
-        nx, ny, nz = box_dims(world, nb)
-        mi = W.kuhn_box(nx, ny, nz, h=2.0 / nb, jitter=args.jitter)
+        nx, ny, nz = config["box_cubes"]
+        mi = W.kuhn_box(nx, ny, nz, h=2.0 / config["block_cubes"], jitter=args.jitter)
         Q0 = W.advection_ic(mi, gamma=GAMMA)
         cfg = hgks.SolverConfig(gamma=GAMMA, cfl=CFL, precision=args.precision)
-        wl = (f"configs[1]{' top size' if nb == N_BLOCK else ''}: {nb}^3 Kuhn box per GPU, 6 tets/cube, periodic, tau=0, CFL {CFL}"
-              if args.workload == "c2" else
-              f"configs[4]: {nb}^3 Kuhn box ({6 * nb ** 3} tets) per GPU, periodic, tau=0, CFL {CFL}")
-        scaling, layout = "weak", (14, 4, 6)
-        extra = {"box_cubes": [nx, ny, nz]}
-        if args.jitter > 0:
-            wl += f", nodes jittered U[-{args.jitter}h, {args.jitter}h] (seed 656)"
-            extra["jitter"] = args.jitter
     else:
-        n, ma, re = (35, 0.2535, 118.0) if args.workload == "c3" else (70, 1.5, 300.0)
+        ma, re, n = SPHERE[args.workload]
         mi = W.sphere_shell(n)
         fs = (1.0, ma, 0.0, 0.0, 1.0 / GAMMA)
         Q0 = W.uniform_state(mi.n_cells, 1.0, (ma, 0.0, 0.0), 1.0 / GAMMA, gamma=GAMMA)  # free-stream IC
         cfg = hgks.SolverConfig(gamma=GAMMA, cfl=0.5, tau_mode=1, mu_inf=ma / re, c1=1.0, t_inf=1.0 / GAMMA,
                                 freestream=fs, precision=args.precision)
-        wl = (f"configs[{2 if args.workload == 'c3' else 3}]: sphere shell 12x{n}^3 hexes, Ma {ma}, Re {re}, "
-              f"NS collision time, wall + farfield, CFL 0.5, free-stream start")
-        scaling, layout = "strong", (24, 8, 3)
-        extra = {"sphere_N": n}
     mesh = hgks.Mesh(mi, n_ranks=world)
     nid = None
     if world > 1:
@@ -359,11 +455,8 @@ def main():
 
     # ---------------- CPU baseline (oracle, rank 0, bounded sample) ----------------
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload == "c2" and args.precision == 64:
-        threads = len(os.sched_getaffinity(0))
-        rate, secs, ncell = cpu_oracle_rate(N_BLOCK, 1, threads)
-        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
-               "sample": f"1 step of the same {N_BLOCK}^3 Kuhn-box workload ({ncell} tets), {secs:.1f} s"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.precision == 64:
+        cpu = cpu_baseline(args.workload)
 
     if rank == 0:
         clocks = clk.summary()
@@ -373,7 +466,7 @@ def main():
             "ms_per_step_profiled": ms_prof / args.steps,
             "scaling": scaling, "vs_baseline": None, "dtype": "f64" if args.precision == 64 else "f32",
             "data": "synthetic (seeded mesh generators and initial states, workloads.py)",
-            "config": {"workload": wl, "cells": int(cells), **extra,
+            "config": {**config, "cells": int(cells),
                        "parallelism": f"domain decomposition x{world} (RCB, 3 ghost layers, "
                                       f"{'NVLink put' if world > 1 and args.transport == 'p2p' else 'NCCL'})",
                        "l2": "no flush: per-step working set %.2f GB > 126 MB L2" % (mesh.workspace_size(cfg) / 1e9)},

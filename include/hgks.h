@@ -150,7 +150,12 @@ hgks_status hgks_destroy(hgks_solver* solver);
  * clipped to land exactly on t_stop and no step starts at t >= t_stop.  The
  * time step is kept on the device (no host synchronisation) unless `info` is
  * non-NULL, in which case the call synchronises and fills it; positivity
- * failures are reported only then (HGKS_E_POSITIVITY, cell id in the message). */
+ * failures are reported only then (HGKS_E_POSITIVITY, cell id in the message).
+ * A step past t_stop (t >= t_stop) has dt = 0 and leaves the state unchanged.
+ * HGKS_E_STATE for n_steps > 0 on a HGKS_TRANSPORT_LOOPBACK solver of a group with
+ * n_ranks > 1 (its ghosts are filled only by hgks_group_step; n_steps = 0 with info
+ * only synchronises and reports) and for a HGKS_TRANSPORT_P2P
+ * solver before hgks_p2p_connect. */
 hgks_status hgks_step(hgks_solver* solver, int32_t n_steps, double t_stop, hgks_step_info* info);
 
 /* Replace the state (host [n_cells_global][5], caller order) and time.  Used

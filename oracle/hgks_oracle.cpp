@@ -78,6 +78,9 @@ struct Config {
   double eps = 1e-10;      // epsilon of the WENO weights (R14)
   int omega_pow = 1;       // exponent of tau_Z/(beta+eps) (R13)
   double fs[5] = {1.0, 0.0, 0.0, 0.0, 1.0 / 1.4};  // free stream rho, U, V, W, p
+  int dq0_mode = 0;        // equilibrium slopes dQ0 (P:306-308 gives only <a-bar> = dQ0/dn):
+                           // 0 average of the two reconstructed gradients (R9), 1 kinetic weighting
+                           // (R9k), 2 linear-weight (gamma) recombination averaged (R9s)
   double K() const { return (5.0 - 3.0 * gamma) / (gamma - 1.0); }
 };
 
@@ -683,8 +686,11 @@ CellPolys fit_cell(const Mesh& m, const State& st, int i, const Config& cfg) {
 }
 
 // Eq. (weno), evaluated literally at point x (cell i's coordinates):
-// value and gradient per conserved variable.
-void weno_point(const Mesh& m, const CellPolys& P, int i, const Vec3& x, double val[5], double grad[5][3]) {
+// value and gradient per conserved variable.  linear = true replaces the normalized
+// nonlinear weights omega-bar_m by the linear weights gamma_m (SPEC's central-gradient
+// recombination, reading R9s).
+void weno_point(const Mesh& m, const CellPolys& P, int i, const Vec3& x, double val[5], double grad[5][3],
+                bool linear = false) {
   const CellGeom& gi = m.geom[i];
   Vec3 X = sub(x, gi.c);
   const int M = (int)P.b.size();
@@ -700,16 +706,18 @@ void weno_point(const Mesh& m, const CellPolys& P, int i, const Vec3& x, double 
                      P.a[2][v] + 2 * P.a[5][v] * X[2] + P.a[7][v] * X[0] + P.a[8][v] * X[1]};
     double sum_gP = 0, sum_wP = 0, sum_gG[3] = {0, 0, 0}, sum_wG[3] = {0, 0, 0};
     for (int mm = 0; mm < M; ++mm) {
+      const double wb = linear ? gm : P.wbar[mm + 1][v];
       double pm = P.Q[v] + P.b[mm][0][v] * X[0] + P.b[mm][1][v] * X[1] + P.b[mm][2][v] * X[2];
       sum_gP += gm / g0 * pm;
-      sum_wP += P.wbar[mm + 1][v] * pm;
+      sum_wP += wb * pm;
       for (int a = 0; a < 3; ++a) {
         sum_gG[a] += gm / g0 * P.b[mm][a][v];
-        sum_wG[a] += P.wbar[mm + 1][v] * P.b[mm][a][v];
+        sum_wG[a] += wb * P.b[mm][a][v];
       }
     }
-    val[v] = P.wbar[0][v] * (p0 / g0 - sum_gP) + sum_wP;
-    for (int a = 0; a < 3; ++a) grad[v][a] = P.wbar[0][v] * (g0v[a] / g0 - sum_gG[a]) + sum_wG[a];
+    const double wb0 = linear ? g0 : P.wbar[0][v];
+    val[v] = wb0 * (p0 / g0 - sum_gP) + sum_wP;
+    for (int a = 0; a < 3; ++a) grad[v][a] = wb0 * (g0v[a] / g0 - sum_gG[a]) + sum_wG[a];
   }
 }
 
@@ -900,13 +908,15 @@ struct GpFluxOut {
   double I_half[5], I_full[5];  // time integrals over [0, dt/2] and [0, dt] (local frame)
   double F[5], dF[5];           // fitted F^n and d_t F^n (local frame)
   double Q0[5];
+  double dq0[3][5];             // equilibrium slopes dQ0 used (local frame), per dq0_mode
   double tau;
 };
 
 // One Gauss point, local frame (x = normal): left state (value + derivatives
-// along n, t1, t2), right state, step dt.  Eq. (flux).
+// along n, t1, t2), right state, step dt.  Eq. (flux).  dq0_ext: the
+// equilibrium slopes dQ0 when they come from outside (dq0_mode 2), else NULL.
 GpFluxOut gks_flux_local(const double ql[5], const double dql[3][5], const double qr[5], const double dqr[3][5],
-                         double dt, const Config& cfg) {
+                         double dt, const Config& cfg, const double (*dq0_ext)[5] = nullptr) {
   const double K = cfg.K();
   GpFluxOut out;
   Maxw gl = maxwellian_of(ql, K), gr = maxwellian_of(qr, K);
@@ -917,13 +927,29 @@ GpFluxOut gks_flux_local(const double ql[5], const double dql[3][5], const doubl
   for (int i = 0; i < 5; ++i) Q0[i] = gl.rho * moment(psi(i), Ml_pos) + gr.rho * moment(psi(i), Mr_neg);
   Maxw g0 = maxwellian_of(Q0, K);
   Moments M0 = moments_of(g0, kFull, K);
-  // slopes: l, r from their derivatives; equilibrium from dQ0 = (dQl + dQr)/2 (R9)
+  // slopes: l, r from their derivatives (<a^k_j> = dQ_k/dn_j)
   Slopes sl = slopes_of(gl, Ml_full, dql);
   Slopes sr = slopes_of(gr, Mr_full, dqr);
+  // equilibrium slopes from dQ0 (<a-bar_j> = dQ0/dn_j; how dQ0 is obtained is
+  // not printed):
   double dq0[3][5];
   for (int j = 0; j < 3; ++j)
-    for (int v = 0; v < 5; ++v) dq0[j][v] = 0.5 * (dql[j][v] + dqr[j][v]);
+    for (int v = 0; v < 5; ++v) {
+      if (cfg.dq0_mode == 0) {
+        dq0[j][v] = 0.5 * (dql[j][v] + dqr[j][v]);  // R9: average of the two gradients
+      } else if (cfg.dq0_mode == 1) {
+        // R9k: the j-derivative of the compatibility definition Q0 = int_{u>0} psi g_l +
+        // int_{u<0} psi g_r with d_j g_k = a^k_j g_k
+        dq0[j][v] = gl.rho * moment2(slope_poly(sl.a[j]), psi(v), Ml_pos) +
+                    gr.rho * moment2(slope_poly(sr.a[j]), psi(v), Mr_neg);
+      } else {
+        if (!dq0_ext) throw OracleError(E_ARG, "dq0_mode 2 needs the linear-weight gradients");
+        dq0[j][v] = dq0_ext[j][v];  // R9s: computed by the caller from the gamma-weighted polynomials
+      }
+    }
   Slopes s0 = slopes_of(g0, M0, dq0);
+  for (int j = 0; j < 3; ++j)
+    for (int v = 0; v < 5; ++v) out.dq0[j][v] = dq0[j][v];
   // collision time (R7)
   double tau = 0.0;
   if (cfg.tau_mode == 1) {
@@ -1063,9 +1089,11 @@ void residual(Solver& S, const double* Q, double dt, std::vector<double>& L, std
     for (const GaussPoint& gp : f.gp) {
       // values and gradients of both sides at the Gauss point (global frame)
       double vl[5], gl[5][3], vr[5], gr[5][3];
+      bool fell_l = false, fell_r = false;
       weno_point(m, polys[f.owner], f.owner, gp.x, vl, gl);
       if (vl[0] <= 0 || pressure_of(vl, cfg.gamma) <= 0) {  // R21 positivity fallback
         ++fb;
+        fell_l = true;
         for (int v = 0; v < 5; ++v) {
           vl[v] = Q[(size_t)f.owner * 5 + v];
           gl[v][0] = gl[v][1] = gl[v][2] = 0;
@@ -1095,6 +1123,7 @@ void residual(Solver& S, const double* Q, double dt, std::vector<double>& L, std
         weno_point(m, polys[f.nb], f.nb, sub(gp.x, f.shift), vr, gr);
         if (vr[0] <= 0 || pressure_of(vr, cfg.gamma) <= 0) {
           ++fb;
+          fell_r = true;
           for (int v = 0; v < 5; ++v) {
             vr[v] = Q[(size_t)f.nb * 5 + v];
             gr[v][0] = gr[v][1] = gr[v][2] = 0;
@@ -1119,7 +1148,33 @@ void residual(Solver& S, const double* Q, double dt, std::vector<double>& L, std
         for (int j = 0; j < 3; ++j)
           for (int v = 0; v < 5; ++v) dqr[j][v] = 0.0;
       }
-      GpFluxOut o = gks_flux_local(ql, dql, qr, dqr, dt, cfg);
+      // R9s (dq0_mode 2): dQ0 = average of the two cells' gradients of Eq. (weno) with the
+      // linear weights gamma in place of omega-bar (a side that fell back contributes zero;
+      // wall: the mirror of the left one; farfield: zero)
+      double dq0s[3][5] = {};
+      if (cfg.dq0_mode == 2) {
+        double v5[5], g5[5][3], q5[5], dl0[3][5] = {}, dr0[3][5] = {};
+        if (!fell_l) {
+          weno_point(m, polys[f.owner], f.owner, gp.x, v5, g5, true);
+          to_local(v5, g5, q5, dl0);
+        }
+        if (f.nb >= 0) {
+          if (!fell_r) {
+            weno_point(m, polys[f.nb], f.nb, sub(gp.x, f.shift), v5, g5, true);
+            to_local(v5, g5, q5, dr0);
+          }
+        } else if (f.bc == kWall) {
+          for (int v = 0; v < 5; ++v) {
+            double sv = (v >= 1 && v <= 3) ? -1.0 : 1.0;
+            dr0[0][v] = -sv * dl0[0][v];
+            dr0[1][v] = sv * dl0[1][v];
+            dr0[2][v] = sv * dl0[2][v];
+          }
+        }
+        for (int j = 0; j < 3; ++j)
+          for (int v = 0; v < 5; ++v) dq0s[j][v] = 0.5 * (dl0[j][v] + dr0[j][v]);
+      }
+      GpFluxOut o = gks_flux_local(ql, dql, qr, dqr, dt, cfg, cfg.dq0_mode == 2 ? dq0s : nullptr);
       // rotate back to the global frame and accumulate omega_G S F_G
       auto to_global = [&](const double a[5], double out[5]) {
         out[0] = a[0];
@@ -1231,11 +1286,13 @@ int guarded(F&& f) {
 }
 
 Config to_config(const double* c) {
-  // flat layout: gamma, cfl, fixed_dt, tau_mode, c1, mu_inf, t_inf, mu_exp, eps, omega_pow, fs[5]
+  // flat layout: gamma, cfl, fixed_dt, tau_mode, c1, mu_inf, t_inf, mu_exp, eps, omega_pow, fs[5], dq0_mode
   Config k;
   k.gamma = c[0]; k.cfl = c[1]; k.fixed_dt = c[2]; k.tau_mode = (int)c[3]; k.c1 = c[4];
   k.mu_inf = c[5]; k.t_inf = c[6]; k.mu_exp = c[7]; k.eps = c[8]; k.omega_pow = (int)c[9];
   for (int i = 0; i < 5; ++i) k.fs[i] = c[10 + i];
+  k.dq0_mode = (int)c[15];
+  if (k.dq0_mode < 0 || k.dq0_mode > 2) throw OracleError(E_ARG, "dq0_mode must be 0, 1 or 2");
   return k;
 }
 
@@ -1346,7 +1403,7 @@ int ora_fit_cell(void* hm, const double* cfgv, const double* Q, int64_t i, doubl
 
 // WENO value and gradient of cell i at points x[np][3] (cell i's coordinates)
 int ora_weno_points(void* hm, const double* cfgv, const double* Q, int64_t i, int64_t np, const double* x, double* val,
-                    double* grad) {
+                    double* grad, int linear) {
   Mesh& m = *(Mesh*)hm;
   return guarded([&] {
     Config cfg = to_config(cfgv);
@@ -1355,7 +1412,7 @@ int ora_weno_points(void* hm, const double* cfgv, const double* Q, int64_t i, in
     CellPolys P = fit_cell(m, st, (int)i, cfg);
     for (int64_t k = 0; k < np; ++k) {
       double v5[5], g[5][3];
-      weno_point(m, P, (int)i, {x[k * 3], x[k * 3 + 1], x[k * 3 + 2]}, v5, g);
+      weno_point(m, P, (int)i, {x[k * 3], x[k * 3 + 1], x[k * 3 + 2]}, v5, g, linear != 0);
       for (int v = 0; v < 5; ++v) {
         val[k * 5 + v] = v5[v];
         for (int a = 0; a < 3; ++a) grad[(k * 5 + v) * 3 + a] = g[v][a];
@@ -1402,6 +1459,8 @@ void ora_gp_flux(const double* cfgv, const double* ql, const double* dql, const 
     out[v] = o.I_half[v]; out[5 + v] = o.I_full[v]; out[10 + v] = o.F[v]; out[15 + v] = o.dF[v]; out[20 + v] = o.Q0[v];
   }
   out[25] = o.tau;
+  for (int j = 0; j < 3; ++j)
+    for (int v = 0; v < 5; ++v) out[26 + j * 5 + v] = o.dq0[j][v];
 }
 void ora_local_frame(const double* n, double* t1, double* t2) {
   Vec3 a, b;

@@ -63,7 +63,7 @@ def lib():
         L.ora_big_stencil.argtypes = [C.c_void_p, C.c_int64, _i64p, _dp]
         L.ora_sub_stencil.argtypes = [C.c_void_p, C.c_int64, C.c_int64, _i64p]
         L.ora_fit_cell.argtypes = [C.c_void_p, _dp, _dp, C.c_int64, _dp, _dp, _dp, _dp]
-        L.ora_weno_points.argtypes = [C.c_void_p, _dp, _dp, C.c_int64, C.c_int64, _dp, _dp, _dp]
+        L.ora_weno_points.argtypes = [C.c_void_p, _dp, _dp, C.c_int64, C.c_int64, _dp, _dp, _dp, C.c_int]
         L.ora_moments.argtypes = [_dp, C.c_double, C.c_int, _dp, _dp, _dp, _dp]
         L.ora_micro_slope.argtypes = [_dp, C.c_double, _dp, _dp]
         L.ora_slopes.argtypes = [_dp, C.c_double, _dp, _dp, _dp]
@@ -113,6 +113,7 @@ class OracleConfig:
     eps: float = 1e-10
     omega_pow: int = 1
     freestream: tuple = (1.0, 0.0, 0.0, 0.0, 1.0 / 1.4)  # rho, U, V, W, p
+    dq0_mode: int = 0          # equilibrium slopes: 0 average (R9), 1 kinetic (R9k), 2 gamma-weighted (R9s)
 
     @property
     def K(self):
@@ -120,7 +121,7 @@ class OracleConfig:
 
     def vec(self) -> np.ndarray:
         return np.array([self.gamma, self.cfl, self.fixed_dt, self.tau_mode, self.c1, self.mu_inf, self.t_inf,
-                         self.mu_exp, self.eps, self.omega_pow, *self.freestream], dtype=np.float64)
+                         self.mu_exp, self.eps, self.omega_pow, *self.freestream, self.dq0_mode], dtype=np.float64)
 
 
 class OracleMesh:
@@ -186,12 +187,15 @@ class OracleMesh:
             _check(-M)
         return dict(a=a, b=b[:M], beta=beta[:M + 1], wbar=wbar[:M + 1])
 
-    def weno_points(self, Q, i, x, cfg: OracleConfig | None = None):
+    def weno_points(self, Q, i, x, cfg: OracleConfig | None = None, linear: bool = False):
+        """Eq. (weno) value and gradient of cell i at points x; linear=True uses the linear
+        weights gamma in place of omega-bar (reading R9s)."""
         cfg = cfg or OracleConfig()
         Q = np.ascontiguousarray(Q, np.float64)
         x = np.ascontiguousarray(np.atleast_2d(x), np.float64)
         val = np.zeros((x.shape[0], 5)); grad = np.zeros((x.shape[0], 5, 3))
-        _check(lib().ora_weno_points(self.h, _p(cfg.vec()), _p(Q), i, x.shape[0], _p(x), _p(val), _p(grad)))
+        _check(lib().ora_weno_points(self.h, _p(cfg.vec()), _p(Q), i, x.shape[0], _p(x), _p(val), _p(grad),
+                                     1 if linear else 0))
         return val, grad
 
 
@@ -219,10 +223,10 @@ def gp_flux(ql, dql, qr, dqr, dt, cfg: OracleConfig | None = None):
     """One Gauss point in the local frame.  Returns dict of I_half, I_full, F, dF, Q0, tau."""
     cfg = cfg or OracleConfig()
     arr = [np.ascontiguousarray(a, np.float64) for a in (ql, dql, qr, dqr)]
-    out = np.zeros(26)
+    out = np.zeros(41)
     lib().ora_gp_flux(_p(cfg.vec()), *[_p(a) for a in arr], dt, _p(out))
     return dict(I_half=out[0:5].copy(), I_full=out[5:10].copy(), F=out[10:15].copy(), dF=out[15:20].copy(),
-                Q0=out[20:25].copy(), tau=float(out[25]))
+                Q0=out[20:25].copy(), tau=float(out[25]), dq0=out[26:41].reshape(3, 5).copy())
 
 
 def local_frame(n):

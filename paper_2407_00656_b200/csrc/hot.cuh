@@ -1311,8 +1311,9 @@ __global__ void __launch_bounds__((NV == 3 ? 3 : 4) * HGKS_FLUX_FPB,
       add_side<1>(ql, dql, K, gm1, ch, cf, Ih, If, gl, kShareHalves ? &hl : nullptr);
       add_side<2>(qr, dqr, K, gm1, ch, cf, Ih, If, gr, kShareHalves ? &hr : nullptr);
       add_side<0>(Q0, dq0, K, gm1, ch, cf, Ih, If, prim_of(Q0, K));
-      // 2x2 fit
-      const Real idt = Real(1.0) / dt;
+      // 2x2 fit; a step past t_stop has dt = 0 and must leave Q unchanged, so
+      // F and dF are 0 there (Ih = If = 0) instead of 0 * inf = NaN
+      const Real idt = dt > Real(0.0) ? Real(1.0) / dt : Real(0.0);
 #pragma unroll
       for (int v = 0; v < 5; ++v) {
         F[v] = (Real(4.0) * Ih[v] - If[v]) * idt;

@@ -895,6 +895,10 @@ hgks_status hgks_step(hgks_solver* s, int32_t n_steps, double t_stop, hgks_step_
     if (!s || n_steps < 0) throw Error(HGKS_E_ARG, "bad argument");
     if (s->transport == HGKS_TRANSPORT_P2P && s->n_ranks > 1 && !s->p2p_ready)
       throw Error(HGKS_E_STATE, "HGKS_TRANSPORT_P2P: call hgks_p2p_connect on every rank first");
+    if (s->transport == HGKS_TRANSPORT_LOOPBACK && s->n_ranks > 1 && n_steps > 0)
+      throw Error(HGKS_E_STATE,
+                  "HGKS_TRANSPORT_LOOPBACK solver of a multi-rank group: advance the group with hgks_group_step "
+                  "(hgks_step would run without a halo exchange or a global dt)");
     Ctrl before{};
     if (info) {
       CUDA_TRY(cudaMemcpyAsync(&before, s->d.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s->stream));

@@ -386,6 +386,16 @@ def density_step_ic(mesh: MeshInput, gamma: float = 1.4) -> np.ndarray:
     return Q
 
 
+def spike_state(mesh: MeshInput, amp: float = 30.0, cell: int = 100, gamma: float = 1.4) -> np.ndarray:
+    """Positivity-fallback stress input (R21): uniform flow (rho = p = 1, U = (0.5, 0.3, 0.2))
+    with one cell of density and pressure x amp; its neighbours' reconstructions overshoot
+    below zero at some Gauss points within a step."""
+    u = np.array([0.5, 0.3, 0.2])
+    Q = uniform_state(mesh.n_cells, 1.0, tuple(u), 1.0, gamma=gamma)
+    Q[cell] = [amp, *(amp * u), amp / (gamma - 1.0) + 0.5 * amp * float(u @ u)]
+    return Q
+
+
 def random_smooth_ic(mesh: MeshInput, seed: int = 118, gamma: float = 1.4,
                      base=(1.0, 0.3, 0.1, -0.2, 1.0 / 1.4), amp: float = 0.05) -> np.ndarray:
     """Smooth seeded perturbation of a uniform state (parity IC for C3/C4 and hex boxes).

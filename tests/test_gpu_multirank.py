@@ -40,6 +40,18 @@ def test_kuhn_multirank_bitwise(cuda_ok, world):
     assert mesh.info(0)["n_peers"] >= 1
 
 
+def test_loopback_solver_rejects_plain_step(cuda_ok):
+    """A loopback solver of a multi-rank group has no exchange of its own: hgks_step with
+    n_steps > 0 fails with HGKS_E_STATE (n_steps = 0, the sync/report call, is allowed)."""
+    mi = W.kuhn_box(8)
+    mesh = hgks.Mesh(mi, n_ranks=2)
+    s = hgks.Solver(mesh, W.advection_ic(mi), hgks.SolverConfig(cfl=0.3), rank=0, transport=hgks.TRANSPORT_LOOPBACK)
+    s.step(0)
+    with pytest.raises(hgks.HgksError) as e:
+        s.step(1)
+    assert e.value.code == 7
+
+
 def test_loopback_fused_put(cuda_ok):
     """f3: the loopback group moves its ghost rows with one k_put per sending rank
     (send rows written straight into the receivers' ghost rows), 2 per step, no

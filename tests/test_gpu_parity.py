@@ -100,6 +100,37 @@ def test_t_stop_clipping(cuda_ok):
     assert g.step(5, t_stop=0.05)["steps_done"] == 0
 
 
+def test_positivity_fallbacks_fire_and_match(cuda_ok):
+    """R21 with fallbacks > 0: one cell of density and pressure x1000 in a uniform flow on the
+    C1 mesh (tau = 0 and NS tau); 10 steps, the GPU's cumulative fallback count equals the
+    oracle's after every step and the state meets the bar."""
+    mi = W.kuhn_box(6)
+    for oc, gc in ((O.OracleConfig(cfl=0.3), hgks.SolverConfig(cfl=0.3)), ns_cfgs(mu=1e-3)):
+        errs, g, o = run_pair(mi, W.spike_state(mi), 10, ocfg=oc, gcfg=gc)
+        assert o.state()[3] > 0
+        assert errs.max() <= TOL, errs.max(axis=0)
+
+
+def test_t_stop_ns_tau_steps_after_stop(cuda_ok):
+    """NS tau (moment form, 1/dt in the time fit) with t_stop: the steps requested after
+    t reached t_stop have dt = 0 and leave the state unchanged (no 0 * inf)."""
+    mi = W.kuhn_box(6)
+    oc, gc = ns_cfgs(mu=1e-3)
+    Q0 = W.density_step_ic(mi)
+    g = hgks.Solver(hgks.Mesh(mi), Q0, gc)
+    o = O.OracleSolver(O.OracleMesh(mi), Q0, oc)
+    info = g.step(50, t_stop=0.02)
+    o.step(50, 0.02)
+    assert info["t"] == 0.02 and 0 < info["steps_done"] < 50
+    Qo, to, _, _ = o.state()
+    Qg, _, tg = g.get_state()
+    assert tg == to == 0.02
+    assert rel_err(Qg, Qo).max() <= TOL
+    assert g.step(3, t_stop=0.02)["steps_done"] == 0
+    Qg2, _, _ = g.get_state()
+    assert np.array_equal(Qg, Qg2)
+
+
 def test_bench_size_steps(cuda_ok):
     """configs[1] at the bench size N=48 (663,552 tets) in bench.py's launch configuration:
     one eager step, then one step replayed from the captured CUDA graph; every cell vs the

@@ -123,7 +123,20 @@ def slopes(q, dq):
     return a, A, au
 
 
-def brute_force_flux(ql, dql, qr, dqr, tau, delta, nt=24):
+def kinetic_dq0(ql, dql, qr, dqr):
+    """Reading R9k by numerical quadrature: d_j Q0 = rho_l <a^l_j psi>_{u>0} + rho_r <a^r_j psi>_{u<0},
+    the j-derivative of Q0 = int_{u>0} psi g_l + int_{u<0} psi g_r with d_j g_k = a^k_j g_k."""
+    rl, Ul, Vl, Wl, laml = prim(ql)
+    rr, Ur, Vr, Wr, lamr = prim(qr)
+    Tl_pos = Table(rl, Ul, Vl, Wl, laml, "pos")
+    Tr_neg = Table(rr, Ur, Vr, Wr, lamr, "neg")
+    al, _, _ = slopes(ql, dql)
+    ar, _, _ = slopes(qr, dqr)
+    return np.array([[rl * Tl_pos.mom(pmul(slope_poly(al[j]), PSI[i])) + rr * Tr_neg.mom(pmul(slope_poly(ar[j]), PSI[i]))
+                      for i in range(5)] for j in range(3)])
+
+
+def brute_force_flux(ql, dql, qr, dqr, tau, delta, nt=24, dq0_mode=0):
     """Numerical int_0^delta int psi u f dXi dt of Eq. (flux), local frame."""
     rl, Ul, Vl, Wl, laml = prim(ql)
     rr, Ur, Vr, Wr, lamr = prim(qr)
@@ -132,7 +145,10 @@ def brute_force_flux(ql, dql, qr, dqr, tau, delta, nt=24):
     Q0 = np.array([rl * Tl_pos.mom(PSI[i]) + rr * Tr_neg.mom(PSI[i]) for i in range(5)])
     r0, U0, V0, W0, lam0 = prim(Q0)
     T0 = Table(r0, U0, V0, W0, lam0, "full")
-    dq0 = 0.5 * (np.asarray(dql) + np.asarray(dqr))  # reading R9
+    if dq0_mode == 0:
+        dq0 = 0.5 * (np.asarray(dql) + np.asarray(dqr))  # reading R9
+    else:
+        dq0 = kinetic_dq0(ql, dql, qr, dqr)  # reading R9k
     a0, A0, au0 = slopes(Q0, dq0)
     al, Al, aul = slopes(ql, dql)
     ar, Ar, aur = slopes(qr, dqr)
@@ -225,6 +241,55 @@ def test_gp_flux_vs_brute_force(tau, delta):
         scale = np.abs(I_full).max()
         assert np.abs(o["I_half"] - I_half).max() <= 1e-10 * scale
         assert np.abs(o["I_full"] - I_full).max() <= 1e-10 * scale
+
+
+@pytest.mark.parametrize("tau,delta", [(0.07, 0.1), (0.0, 0.08)])
+def test_gp_flux_kinetic_dq0_vs_brute_force(tau, delta):
+    """Reading R9k (dq0_mode 1): the equilibrium slopes are the numerically integrated
+    half-range moments of the side slopes, and the whole Gauss-point flux matches the literal
+    velocity/time quadrature of Eq. (flux) with them."""
+    rng = np.random.default_rng(int(7000 * (tau + delta)))
+    for _ in range(3):
+        ql, dql, qr, dqr = random_gp(rng)
+        cfg = O.OracleConfig(dq0_mode=1)
+        if tau > 0:
+            o = O.gp_flux(ql, dql, qr, dqr, 2 * delta, O.OracleConfig())
+            r0, U0, V0, W0, lam0 = prim(o["Q0"])
+            p0 = r0 / (2 * lam0)
+            cfg = O.OracleConfig(tau_mode=1, c1=0.0, mu_inf=tau * p0, t_inf=p0 / r0, mu_exp=0.7, dq0_mode=1)
+        o = O.gp_flux(ql, dql, qr, dqr, 2 * delta, cfg)
+        ref = kinetic_dq0(ql, dql, qr, dqr)
+        assert np.abs(o["dq0"] - ref).max() <= 1e-11 * np.abs(ref).max()
+        I_half, _ = brute_force_flux(ql, dql, qr, dqr, tau, delta, dq0_mode=1)
+        I_full, _ = brute_force_flux(ql, dql, qr, dqr, tau, 2 * delta, dq0_mode=1)
+        scale = np.abs(I_full).max()
+        assert np.abs(o["I_half"] - I_half).max() <= 1e-10 * scale
+        assert np.abs(o["I_full"] - I_full).max() <= 1e-10 * scale
+        # R9 (mode 0) is the plain average; the two readings differ for unequal sides
+        assert np.allclose(O.gp_flux(ql, dql, qr, dqr, 2 * delta, O.OracleConfig())["dq0"], 0.5 * (dql + dqr),
+                           rtol=1e-14, atol=1e-14 * np.abs(dql).max())
+        assert np.abs(o["dq0"] - 0.5 * (dql + dqr)).max() > 1e-6 * np.abs(ref).max()
+
+
+def test_kinetic_dq0_special_cases():
+    """R9k limits: equal sides (q_l = q_r, dq_l = dq_r) give dQ0 = dQ (the half-range
+    moments add up to the full ones); a strongly supersonic flow to +n (U sqrt(lam) = 12)
+    takes dQ0 from the left side alone, and to -n from the right side."""
+    rng = np.random.default_rng(5)
+    ql, dql, qr, dqr = random_gp(rng)
+    o = O.gp_flux(ql, dql, ql, dql, 0.1, O.OracleConfig(dq0_mode=1))
+    assert np.abs(o["dq0"] - dql).max() <= 1e-13 * np.abs(dql).max()
+    for sgn, side in ((1.0, 0), (-1.0, 1)):
+        qa, qb = ql.copy(), qr.copy()
+        for q in (qa, qb):
+            rho, U, V, Wv, lam = prim(q)
+            p = rho / (2 * lam)
+            Un = sgn * 12.0 / np.sqrt(lam)
+            q[1] = rho * Un
+            q[4] = p / (GAMMA - 1) + 0.5 * rho * (Un * Un + V * V + Wv * Wv)
+        o = O.gp_flux(qa, dql, qb, dqr, 0.1, O.OracleConfig(dq0_mode=1))
+        exp = dql if side == 0 else dqr
+        assert np.abs(o["dq0"] - exp).max() <= 1e-9 * np.abs(exp).max()  # moments of |U| ~ 12/sqrt(lam): cancellation
 
 
 def euler_flux(q):
