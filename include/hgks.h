@@ -84,6 +84,16 @@ typedef struct {
   int32_t precision;   /* working precision of the hot path: 64 (fp64, the parity path) or 32
                           (the FP32 variant; the CFL bound, time and the caller's
                           state arrays stay fp64).  Anything else: HGKS_E_ARG from hgks_init. */
+  int32_t dq0_mode;    /* equilibrium slopes dQ0 (P:306-308 prints only <a-bar> = dQ0/dn):
+                          0 = average of the two reconstructed gradients (R9, default),
+                          1 = kinetic weighting rho_l<a^l psi>_{u>0} + rho_r<a^r psi>_{u<0} (R9k),
+                          2 = average of the two cells' linear-weight (P_0) gradients (R9s; adds a
+                              second 50-value record per cell to the workspace).
+                          1 and 2 need precision 64 (HGKS_E_ARG otherwise). */
+  double prandtl;      /* Prandtl number of the heat-flux correction (R29; P:1203-1210 runs the viscous
+                          sphere): the energy flux gains (1/Pr - 1) x the heat flux of the
+                          non-equilibrium part of Eq. (flux) (zero for tau_mode 0).  0 or 1 = no
+                          correction (BGK, Pr = 1); needs precision 64 and dq0_mode 0. */
 } hgks_config;
 
 #define HGKS_TRANSPORT_NCCL 0      /* one process per GPU, NCCL send/recv + allreduce */
@@ -116,9 +126,11 @@ typedef struct {
   int32_t n_sub;             /* sub-stencils per cell (4 tet, 8 hex) */
   int32_t n_peers;           /* ranks this rank exchanges ghosts with */
   int64_t send_cells, recv_cells;    /* per stage */
-  int64_t edge_cut;          /* faces between different ranks (global) */
+  int64_t edge_cut;          /* faces between different ranks (global; RCB + greedy boundary refinement) */
   int64_t n_early_cells;     /* owned cells reconstructed while the halo exchange is in flight */
   int64_t n_early_faces;     /* interior faces fluxed while the halo exchange is in flight */
+  int64_t edge_cut_rcb;      /* faces between different ranks of the plain RCB partition, before the
+                                boundary refinement (equal to edge_cut for a caller partition) */
 } hgks_mesh_stats;
 
 typedef struct {

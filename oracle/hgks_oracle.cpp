@@ -81,6 +81,7 @@ struct Config {
   int dq0_mode = 0;        // equilibrium slopes dQ0 (P:306-308 gives only <a-bar> = dQ0/dn):
                            // 0 average of the two reconstructed gradients (R9), 1 kinetic weighting
                            // (R9k), 2 linear-weight (gamma) recombination averaged (R9s)
+  double prandtl = 1.0;    // Pr; != 1: heat-flux (Prandtl-number) correction of the energy flux (R29)
   double K() const { return (5.0 - 3.0 * gamma) / (gamma - 1.0); }
 };
 
@@ -978,6 +979,38 @@ GpFluxOut gks_flux_local(const double ql[5], const double dql[3][5], const doubl
   };
   integral(0.5 * dt, out.I_half);
   integral(dt, out.I_full);
+  // Prandtl-number correction (R29; Xu's heat-flux fix, P:1203-1210 runs a viscous sphere but
+  // prints no Pr): the energy flux gains (1/Pr - 1) times the time integral of the heat flux
+  // q(t) = 1/2 int (u - U0)((u - U0)^2 + (v - V0)^2 + (w - W0)^2 + xi^2) f_neq dXi, U0 the
+  // velocity of Q0, of the non-equilibrium part f_neq = f - g0 (1 + A-bar t) of Eq. (flux)
+  // (zero at tau = 0; the Chapman-Enskog heat flux in the Navier-Stokes limit).
+  if (cfg.prandtl != 1.0) {
+    const Poly cu = {{1.0, 1, 0, 0, 0}, {-g0.U, 0, 0, 0, 0}}, cv = {{1.0, 0, 1, 0, 0}, {-g0.V, 0, 0, 0, 0}},
+               cw = {{1.0, 0, 0, 1, 0}, {-g0.W, 0, 0, 0, 0}};
+    Poly sq = addp(addp(addp(mul(cu, cu), mul(cv, cv)), mul(cw, cw)), Poly{{1.0, 0, 0, 0, 1}});
+    Poly qp = mul(Poly{{0.5, 0, 0, 0, 0}}, mul(cu, sq));
+    auto au_of = [](const Slopes& sk) {
+      return addp(addp(mul(slope_poly(sk.a[0]), kU), mul(slope_poly(sk.a[1]), kV)), mul(slope_poly(sk.a[2]), kW));
+    };
+    // heat-flux moments of each term of f_neq (rho-weighted)
+    const double q0a = g0.rho * moment2(qp, au_of(s0), M0), q0A = g0.rho * moment2(qp, slope_poly(s0.A), M0);
+    const double ql1 = gl.rho * moment(qp, Ml_pos), qla = gl.rho * moment2(qp, au_of(sl), Ml_pos),
+                 qlA = gl.rho * moment2(qp, slope_poly(sl.A), Ml_pos);
+    const double qr1 = gr.rho * moment(qp, Mr_neg), qra = gr.rho * moment2(qp, au_of(sr), Mr_neg),
+                 qrA = gr.rho * moment2(qp, slope_poly(sr.A), Mr_neg);
+    auto qint = [&](double delta) {
+      double e = std::exp(-delta / tau);
+      double c2 = 2 * tau * tau * (1 - e) - tau * delta * (1 + e);
+      double c3n = tau * tau * (1 - e) - tau * delta;  // A-bar g0 coefficient of f_neq: tau (e^{-t/tau} - 1)
+      double c4 = tau * (1 - e);
+      double c5 = -2 * tau * tau * (1 - e) + tau * delta * e;
+      double c6 = -tau * tau * (1 - e);
+      return c2 * q0a + c3n * q0A + c4 * (ql1 + qr1) + c5 * (qla + qra) + c6 * (qlA + qrA);
+    };
+    const double fac = 1.0 / cfg.prandtl - 1.0;
+    out.I_half[4] += fac * qint(0.5 * dt);
+    out.I_full[4] += fac * qint(dt);
+  }
   // 2x2 fit: F dt + 1/2 dF dt^2 = I_full ; 1/2 F dt + 1/8 dF dt^2 = I_half
   for (int i = 0; i < 5; ++i) {
     out.F[i] = (4.0 * out.I_half[i] - out.I_full[i]) / dt;
@@ -1286,12 +1319,14 @@ int guarded(F&& f) {
 }
 
 Config to_config(const double* c) {
-  // flat layout: gamma, cfl, fixed_dt, tau_mode, c1, mu_inf, t_inf, mu_exp, eps, omega_pow, fs[5], dq0_mode
+  // flat layout: gamma, cfl, fixed_dt, tau_mode, c1, mu_inf, t_inf, mu_exp, eps, omega_pow, fs[5], dq0_mode, prandtl
   Config k;
   k.gamma = c[0]; k.cfl = c[1]; k.fixed_dt = c[2]; k.tau_mode = (int)c[3]; k.c1 = c[4];
   k.mu_inf = c[5]; k.t_inf = c[6]; k.mu_exp = c[7]; k.eps = c[8]; k.omega_pow = (int)c[9];
   for (int i = 0; i < 5; ++i) k.fs[i] = c[10 + i];
   k.dq0_mode = (int)c[15];
+  k.prandtl = c[16];
+  if (!(k.prandtl > 0)) throw OracleError(E_ARG, "prandtl must be > 0");
   if (k.dq0_mode < 0 || k.dq0_mode > 2) throw OracleError(E_ARG, "dq0_mode must be 0, 1 or 2");
   return k;
 }

@@ -114,6 +114,7 @@ class OracleConfig:
     omega_pow: int = 1
     freestream: tuple = (1.0, 0.0, 0.0, 0.0, 1.0 / 1.4)  # rho, U, V, W, p
     dq0_mode: int = 0          # equilibrium slopes: 0 average (R9), 1 kinetic (R9k), 2 gamma-weighted (R9s)
+    prandtl: float = 1.0       # Pr != 1: heat-flux correction of the energy flux (R29)
 
     @property
     def K(self):
@@ -121,7 +122,7 @@ class OracleConfig:
 
     def vec(self) -> np.ndarray:
         return np.array([self.gamma, self.cfl, self.fixed_dt, self.tau_mode, self.c1, self.mu_inf, self.t_inf,
-                         self.mu_exp, self.eps, self.omega_pow, *self.freestream, self.dq0_mode], dtype=np.float64)
+                         self.mu_exp, self.eps, self.omega_pow, *self.freestream, self.dq0_mode, self.prandtl], dtype=np.float64)
 
 
 class OracleMesh:

@@ -16,7 +16,7 @@ DEPS = SOURCES + [os.path.join(PKG, "csrc", "kernels.cuh"), os.path.join(PKG, "c
                   os.path.join(PKG, "csrc", "moments_gen.cuh"), os.path.join(PKG, "csrc", "internal.h"),
                   os.path.join(ROOT, "include", "hgks.h")]
 
-NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+NVCC_FLAGS = ["-O3", "-std=c++17", "--split-compile=0", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
               "-Xcompiler", "-fPIC,-fopenmp,-O2", "-shared"]
 
 

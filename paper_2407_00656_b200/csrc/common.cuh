@@ -10,9 +10,10 @@ namespace hgks {
 
 // erfc(z) together with exp(-z^2), which the half-range Maxwellian moments need both
 // of.  fp64: erfcx(|z|) = P(t)/(|z| + K), t = (|z| - K)/(|z| + K), P a
-// degree-22 Chebyshev series (scripts/fit_erfc.py; absolute error of erfc <= 2e-15,
-// tests/test_erfc_fit.py), so one exp serves both and the branchy library erfc (about
-// 160 instructions per call in the flux kernels' SASS) is gone.  fp32: library calls.
+// degree-22 polynomial in t (Chebyshev fit emitted in the monomial basis, evaluated by
+// Horner's rule: one DFMA per degree; scripts/fit_erfc.py; absolute error of erfc
+// <= 2e-15, tests/test_erfc_fit.py), so one exp serves both and the branchy library erfc
+// (about 160 instructions per call in the flux kernels' SASS) is gone.  fp32: library calls.
 // exp(x) for x <= 0 (the Maxwellian tail exp(-z^2), exp(-dt/tau)): Cody-Waite
 // reduction x = k ln2 + r, |r| <= ln2/2 (two-part ln2), degree-12 Taylor series, 2^k
 // added to the exponent field; relative error <= 4e-16 on [-700, 0], 0 below -700
@@ -49,15 +50,9 @@ __device__ __forceinline__ void erfc_exp(double z, double& erfc_z, double& ez2) 
   const double a = fabs(z);
   const double r = 1.0 / (a + HGKS_ERFC_K);
   const double t = (a - HGKS_ERFC_K) * r;
-  const double t2 = t + t;
-  double b1 = 0.0, b2 = 0.0;
+  double P = c[HGKS_ERFC_DEG];
 #pragma unroll
-  for (int k = HGKS_ERFC_DEG; k >= 1; --k) {
-    const double b0 = fma(t2, b1, c[k] - b2);
-    b2 = b1;
-    b1 = b0;
-  }
-  const double P = fma(t, b1, c[0] - b2);
+  for (int k = HGKS_ERFC_DEG - 1; k >= 0; --k) P = fma(P, t, c[k]);
   ez2 = exp_neg(-z * z);
   const double v = P * r * ez2;  // erfc(|z|)
   erfc_z = z >= 0.0 ? v : 2.0 - v;
@@ -87,6 +82,7 @@ struct GasParams {
   int tau_mode;
   double c1, mu_inf, t_inf, mu_exp;
   double fs[5];
+  double pr_fac;  // 1/Pr - 1: heat-flux (Prandtl-number) correction of the energy flux (R29); 0 = none
 };
 
 

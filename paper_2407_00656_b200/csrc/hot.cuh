@@ -23,7 +23,7 @@ __device__ __forceinline__ R2 make_R2(Real x, Real y) {
 
 // gas constants in the working precision
 struct GasR {
-  Real gamma, K, c1, mu_inf, t_inf, mu_exp, fs[5];
+  Real gamma, K, c1, mu_inf, t_inf, mu_exp, fs[5], pr_fac;
 };
 inline GasR make_gas(const GasParams& g) {
   GasR r;
@@ -34,6 +34,7 @@ inline GasR make_gas(const GasParams& g) {
   r.t_inf = (Real)g.t_inf;
   r.mu_exp = (Real)g.mu_exp;
   for (int k = 0; k < 5; ++k) r.fs[k] = (Real)g.fs[k];
+  r.pr_fac = (Real)g.pr_fac;
   return r;
 }
 
@@ -120,6 +121,7 @@ struct ReconArgs {
   const Real* __restrict__ op;        // [E] per cell, tiled: LSQ operators in streaming order
   const Real* __restrict__ geo;       // [8] per cell, tiled: V^{2/3}, V^{4/3}, M2 (xx,yy,zz,xy,xz,yz)
   Real* __restrict__ ceff;            // [n_local][50]
+  Real* __restrict__ ceff0;           // [n_local][50] P_0 alone (linear weights, dq0 reading R9s), or null
   Real eps;
   int omega_pow;
 };
@@ -333,6 +335,19 @@ __global__ void __launch_bounds__(ReconShape<K>::BT, ReconShape<K>::MINB) k_reco
       for (int v = 0; v < 5; ++v) lin[d][v] = fma(alm[m][v], b[d][v], lin[d][v]);
   }
   if (!active) return;
+  if (a.ceff0) {  // R9s: P_0 itself (Eq. weno with the linear weights collapses to P_0)
+    R2* d0 = reinterpret_cast<R2*>(a.ceff0 + (size_t)ci * kRec);
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      const Real cst = qi[v] - (c[3][v] * m2[0] + c[4][v] * m2[1] + c[5][v] * m2[2] + c[6][v] * m2[3] +
+                                c[7][v] * m2[4] + c[8][v] * m2[5]);
+      d0[5 * v + 0] = make_R2(cst, c[0][v]);
+      d0[5 * v + 1] = make_R2(c[1][v], c[2][v]);
+      d0[5 * v + 2] = make_R2(c[3][v], c[4][v]);
+      d0[5 * v + 3] = make_R2(c[5][v], c[6][v]);
+      d0[5 * v + 4] = make_R2(c[7][v], c[8][v]);
+    }
+  }
   R2* dst = reinterpret_cast<R2*>(a.ceff + (size_t)ci * kRec);
 #pragma unroll
   for (int v = 0; v < 5; ++v) {
@@ -548,6 +563,20 @@ __global__ void __launch_bounds__(128, HGKS_RPAIR_MINB) k_recon_pair(ReconArgs a
       for (int v = 0; v < NS; ++v) lin[d][v] = fma(alm[m][v], b[d][v], lin[d][v]);
   }
   if (!active) return;
+  if (a.ceff0) {  // R9s: P_0 itself
+    R2* d0 = reinterpret_cast<R2*>(a.ceff0 + (size_t)ci * kRec) + 15 * part;
+#pragma unroll
+    for (int v = 0; v < NS; ++v) {
+      if (part && v == 2) break;
+      const Real cst = qi[v] - (c[3][v] * m2[0] + c[4][v] * m2[1] + c[5][v] * m2[2] + c[6][v] * m2[3] +
+                                c[7][v] * m2[4] + c[8][v] * m2[5]);
+      d0[5 * v + 0] = make_R2(cst, c[0][v]);
+      d0[5 * v + 1] = make_R2(c[1][v], c[2][v]);
+      d0[5 * v + 2] = make_R2(c[3][v], c[4][v]);
+      d0[5 * v + 3] = make_R2(c[5][v], c[6][v]);
+      d0[5 * v + 4] = make_R2(c[7][v], c[8][v]);
+    }
+  }
   // this lane's variables: part 0 writes v = 0, 1, 2; part 1 writes v = 3, 4
   R2* dst = reinterpret_cast<R2*>(a.ceff + (size_t)ci * kRec) + 15 * part;
 #pragma unroll
@@ -581,6 +610,7 @@ __global__ void __launch_bounds__(128, HGKS_RPAIR_MINB) k_recon_pair(ReconArgs a
 struct FluxArgs {
   const Real* __restrict__ Q;  // [n_local][QS]
   const Real* __restrict__ ceff;
+  const Real* __restrict__ ceff0;   // P_0 records (dq0 reading R9s only)
   const int* __restrict__ f_cells;  // [n][2]
   const Real* __restrict__ f_geo; // [n][stride]
   int f_stride;
@@ -596,21 +626,28 @@ struct FluxArgs {
 // evaluate the effective polynomial of a cell at X (relative to its centroid);
 // record layout rec[10 v + (const, x, y, z, xx, yy, zz, xy, xz, yz)], read as
 // 16-byte vectors (80 bytes per variable)
+template <bool GLOBAL = true>  // false: rec is in shared memory (plain loads)
 __device__ __forceinline__ void eval_poly(const Real* __restrict__ rec, const Real X[3], Real val[5],
                                           Real grad[5][3]) {
   const Real xx = X[0] * X[0], yy = X[1] * X[1], zz = X[2] * X[2];
   const Real xy = X[0] * X[1], xz = X[0] * X[2], yz = X[1] * X[2];
+  const Real x2[3] = {X[0] + X[0], X[1] + X[1], X[2] + X[2]};  // d/dx of q_xx x^2 = q_xx (2x)
   const R2* r2 = reinterpret_cast<const R2*>(rec);
 #pragma unroll
   for (int v = 0; v < 5; ++v) {
-    const R2 a0 = __ldg(r2 + 5 * v), a1 = __ldg(r2 + 5 * v + 1), a2 = __ldg(r2 + 5 * v + 2),
-                  a3 = __ldg(r2 + 5 * v + 3), a4 = __ldg(r2 + 5 * v + 4);
+    R2 a0, a1, a2, a3, a4;
+    if (GLOBAL) {
+      a0 = __ldg(r2 + 5 * v); a1 = __ldg(r2 + 5 * v + 1); a2 = __ldg(r2 + 5 * v + 2);
+      a3 = __ldg(r2 + 5 * v + 3); a4 = __ldg(r2 + 5 * v + 4);
+    } else {
+      a0 = r2[5 * v]; a1 = r2[5 * v + 1]; a2 = r2[5 * v + 2]; a3 = r2[5 * v + 3]; a4 = r2[5 * v + 4];
+    }
     const Real c0 = a0.x, lx = a0.y, ly = a1.x, lz = a1.y, qxx = a2.x, qyy = a2.y, qzz = a3.x, qxy = a3.y,
                  qxz = a4.x, qyz = a4.y;
     val[v] = c0 + lx * X[0] + ly * X[1] + lz * X[2] + qxx * xx + qyy * yy + qzz * zz + qxy * xy + qxz * xz + qyz * yz;
-    grad[v][0] = lx + Real(2.0) * qxx * X[0] + qxy * X[1] + qxz * X[2];
-    grad[v][1] = ly + Real(2.0) * qyy * X[1] + qxy * X[0] + qyz * X[2];
-    grad[v][2] = lz + Real(2.0) * qzz * X[2] + qxz * X[0] + qyz * X[1];
+    grad[v][0] = lx + qxx * x2[0] + qxy * X[1] + qxz * X[2];
+    grad[v][1] = ly + qyy * x2[1] + qxy * X[0] + qyz * X[2];
+    grad[v][2] = lz + qzz * x2[2] + qxz * X[0] + qyz * X[1];
   }
 }
 
@@ -736,6 +773,57 @@ __device__ __forceinline__ void euler_jvp(int j, const EulerState& e, const Real
   out[4] = du[j] * e.H + e.u[j] * (dq[4] + dp);
 }
 
+
+// the same along an arbitrary unit vector n (global components): d(F.n) = (dF_n/dQ) dq
+__device__ __forceinline__ void euler_jvp_dir(const EulerState& e, const Real n[3], const Real dq[5], Real gm1,
+                                              Real out[5]) {
+  const Real du[3] = {(dq[1] - e.u[0] * dq[0]) * e.inv, (dq[2] - e.u[1] * dq[0]) * e.inv,
+                      (dq[3] - e.u[2] * dq[0]) * e.inv};
+  const Real dp = gm1 * (dq[4] - (e.u[0] * dq[1] + e.u[1] * dq[2] + e.u[2] * dq[3]) + e.q2h * dq[0]);
+  const Real un = e.u[0] * n[0] + e.u[1] * n[1] + e.u[2] * n[2];
+  const Real dmn = dq[1] * n[0] + dq[2] * n[1] + dq[3] * n[2];
+  const Real dun = du[0] * n[0] + du[1] * n[1] + du[2] * n[2];
+  out[0] = dmn;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) out[1 + k] = dq[1 + k] * un + e.Q[1 + k] * dun + dp * n[k];
+  out[4] = dun * e.H + un * (dq[4] + dp);
+}
+
+// Q0 = int_{u.n>0} psi g_l + int_{u.n<0} psi g_r with the momentum in GLOBAL
+// components: each side's velocity splits into u_n n + u_t, and the half-range moments
+// along n give rho <1>, rho <u_n>, rho <u_n^2> while the tangential part rides along
+// (m0 u_t) -- no local frame is needed.
+__device__ __forceinline__ void equilibrium_state_n(const Real ql[5], const Real qr[5], const Real n[3], Real K,
+                                                    Real Q0[5]) {
+  const Real rpi = Real(0.56418958354775628);   // 1/sqrt(pi)
+  const Real c2k = Real(2.0) / (K + Real(3.0));  // = gamma - 1
+#pragma unroll
+  for (int v = 0; v < 5; ++v) Q0[v] = Real(0.0);
+#pragma unroll
+  for (int side = 0; side < 2; ++side) {
+    const Real* q = side ? qr : ql;
+    const Real sg = side ? Real(-1.0) : Real(1.0);
+    const Real inv = Real(1.0) / q[0];
+    const Real u[3] = {q[1] * inv, q[2] * inv, q[3] * inv};
+    const Real un = u[0] * n[0] + u[1] * n[1] + u[2] * n[2];
+    const Real uu = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+    const Real rhoe = q[4] - Real(0.5) * (q[1] * u[0] + q[2] * u[1] + q[3] * u[2]);
+    const Real h = c2k * rhoe * inv;          // p / rho = 1/(2 lambda)
+    const Real rs = rsqrt(h + h);             // sqrt(lambda)
+    const Real sq = (h + h) * rs;             // 1/sqrt(lambda)
+    Real ec, ex;
+    erfc_exp(-sg * un * rs, ec, ex);          // erfc(-sg sqrt(lambda) u_n), exp(-lambda u_n^2)
+    const Real m0 = Real(0.5) * ec;
+    const Real m1 = un * m0 + sg * (Real(0.5) * ex * rpi * sq);
+    const Real m2 = un * m1 + m0 * h;
+    const Real rm0 = q[0] * m0;
+    const Real a = q[0] * m1 - rm0 * un;      // rho (m1 - m0 u_n): the normal part beyond m0 u
+    Q0[0] += rm0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) Q0[1 + k] += rm0 * u[k] + a * n[k];  // rho (m1 n + m0 u_t)
+    Q0[4] += Real(0.5) * q[0] * (m2 + m0 * (uu - un * un + (K + Real(2.0)) * h));
+  }
+}
 
 // ---------------------------------------------------------------------------
 // Moment form (general tau).  Moments of a Maxwellian normalised by rho:
@@ -894,6 +982,7 @@ __device__ __forceinline__ void micro_slope(const Real b[5], Real U, Real V, Rea
 // closed-form time integrals of the Eq. (flux) coefficients over [0, delta]
 struct TimeCoef {
   Real c1, c2, c3, c4, c5, c6;
+  Real c3n;  // time integral of the A-bar g0 coefficient of f - g0 (1 + A-bar t): tau (e^{-t/tau} - 1) (R29)
 };
 __device__ __forceinline__ TimeCoef time_coef_e(Real delta, Real tau, Real e);
 __device__ __forceinline__ TimeCoef time_coef(Real delta, Real tau) {
@@ -909,6 +998,7 @@ __device__ __forceinline__ TimeCoef time_coef_e(Real delta, Real tau, Real e) {
   c.c4 = tau * om;
   c.c5 = -Real(2.0) * tau * tau * om + tau * delta * e;
   c.c6 = -tau * tau * om;
+  c.c3n = tau * tau * om - tau * delta;
   return c;
 }
 
@@ -946,6 +1036,16 @@ __device__ __forceinline__ void equilibrium_state(const Real ql[5], const Real q
           Real(0.5) * rr * (b[2] + b[0] * (Vr * Vr + Wr * Wr + (K + Real(2.0)) * hr));
 }
 
+// Heat flux about the interface velocity U0 (local frame) of a term h of f, from its flux-type
+// moments Fm = <u psi h> and state-type moments Wm = <psi h> (R29):
+//   1/2 <(u - U0)(|u - U0|^2 + xi^2) h> = <u psi_5 h> - U0.<u u h> + |U0|^2/2 <u h>
+//                                         - U0 <psi_5 h> + U0 (U0.<u h>) - U0 |U0|^2/2 <h>
+__device__ __forceinline__ Real heat_flux(const Real Fm[5], const Real Wm[5], const Real U0[3]) {
+  const Real uu = U0[0] * U0[0] + U0[1] * U0[1] + U0[2] * U0[2];
+  return Fm[4] - (U0[0] * Fm[1] + U0[1] * Fm[2] + U0[2] * Fm[3]) + Real(0.5) * uu * Fm[0] -
+         U0[0] * Wm[4] + U0[0] * (U0[0] * Wm[1] + U0[1] * Wm[2] + U0[2] * Wm[3]) - Real(0.5) * U0[0] * uu * Wm[0];
+}
+
 // One term group of Eq. (flux) for a Maxwellian with its slopes, accumulated into
 // I_half, I_full (rho-weighted).  Full-range Maxwellian moments of the slope
 // polynomials reduce to Euler-flux Jacobian-vector products (d_j g = a_j g, so
@@ -954,10 +1054,13 @@ __device__ __forceinline__ void equilibrium_state(const Real ql[5], const Real q
 // part rho<u psi> = F_n(Q), rho<A u psi> = A_n(Q) d_t Q.  Only <(a.u) u psi>
 // (full range for g0) and the half-range moments of g_l, g_r need the generic
 // moment sums.
-template <int RANGE>
+// PR: also accumulate the time integrals Qh, Qf of the heat flux about U0 of the group's
+// non-equilibrium terms (R29)
+template <int RANGE, bool PR = false>
 __device__ __forceinline__ void add_side(const Real q[5], const Real dq[3][5], Real K, Real gm1,
                                          const TimeCoef& ch, const TimeCoef& cf, Real Ih[5], Real If[5],
-                                         const Prim& g, const Half* hm = nullptr) {
+                                         const Prim& g, const Half* hm = nullptr, const Real* U0 = nullptr,
+                                         Real* Qh = nullptr, Real* Qf = nullptr) {
   const Real ir = Real(1.0) / g.rho;
   Real a[3][5];
 #pragma unroll
@@ -993,6 +1096,18 @@ __device__ __forceinline__ void add_side(const Real q[5], const Real dq[3][5], R
       Ih[v] += ch.c1 * m1[v] + ch.c2 * m2 + ch.c3 * m3[v];
       If[v] += cf.c1 * m1[v] + cf.c2 * m2 + cf.c3 * m3[v];
     }
+    if (PR) {
+      // (a-bar.u) g0 and A-bar g0: rho <(a.u) psi> = sum_j A_j d_j Q = -d_t Q, rho <A psi> = d_t Q
+      Real m2w[5], ndt[5];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        m2w[v] = g.rho * m2r[v];
+        ndt[v] = -dtq[v];
+      }
+      const Real qa = heat_flux(m2w, ndt, U0), qA = heat_flux(m3, dtq, U0);
+      *Qh += ch.c2 * qa + ch.c3n * qA;
+      *Qf += cf.c2 * qa + cf.c3n * qA;
+    }
   } else {
     Real A[5], b[5];
 #pragma unroll
@@ -1006,8 +1121,24 @@ __device__ __forceinline__ void add_side(const Real q[5], const Real dq[3][5], R
       Ih[v] += g.rho * (ch.c4 * m1[v] + ch.c6 * m3[v]) + ch.c5 * m2;
       If[v] += g.rho * (cf.c4 * m1[v] + cf.c6 * m3[v]) + cf.c5 * m2;
     }
+    if (PR) {
+      // state-type half-range moments <psi>, <(a.u) psi>, <A psi> (generic moment sums)
+      Real w1[5], w2[5], w3[5], t0[5], t1[5], t2[5];
+      psi_m<0, 0, 0>(mom, w1);
+      slope_m<1, 0, 0>(mom, a[0], t0);
+      slope_m<0, 1, 0>(mom, a[1], t1);
+      slope_m<0, 0, 1>(mom, a[2], t2);
+      slope_m<0, 0, 0>(mom, A, w3);
+#pragma unroll
+      for (int v = 0; v < 5; ++v) w2[v] = t0[v] + t1[v] + t2[v];
+      const Real q1 = g.rho * heat_flux(m1, w1, U0), qa = g.rho * heat_flux(m2r, w2, U0),
+                 qA = g.rho * heat_flux(m3, w3, U0);
+      *Qh += ch.c4 * q1 + ch.c5 * qa + ch.c6 * qA;
+      *Qf += cf.c4 * q1 + cf.c5 * qa + cf.c6 * qA;
+    }
   }
 #else
+  static_assert(!PR, "the Prandtl fix needs the generated moment contractions");
   Real m2[5];  // <(a.u) u psi> over the range
   {
     Real t0[5], t1[5], t2[5];
@@ -1073,7 +1204,131 @@ __device__ __forceinline__ void boundary_right(const Real ql[5], const Real dql[
   }
 }
 
-template <int NV, int STAGE, bool TAU0, int BC>
+#ifndef HGKS_FLUX_STAGE
+#define HGKS_FLUX_STAGE 1
+#endif
+__device__ __forceinline__ void cp_async_shared(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  if (sizeof(R2) == 16) asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+  else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+
+// tau = 0 interior faces with the R9 dQ0 (the C1/C2/C5 hot path), frame-free: f = g0 (1 + A t)
+// gives F = F_n(Q0) and d_t F = A_n(Q0) d_t Q0 with d_t Q0 = -sum_a A_a(Q0) d_a Q0
+// (SURVEY A.10).  Both are rotation invariant, so with Q0's momentum in global components
+// (equilibrium_state_n) the Jacobian-vector products run along the global axes on the global
+// gradients and along n for the flux: the same values as the local-frame form, without the
+// frame, the gradient rotation and the rotation back.  Only the average of the two gradients
+// enters (R9): the sum is used and the 1/2 folded into the output weight.
+// One warp = FPW faces x NGP Gauss points.  With HGKS_FLUX_STAGE the warp first copies its
+// 2 FPW effective-polynomial records global -> shared with cp.async (each record one
+// coalesced 400-byte row, no registers held), computes the Gauss-point geometry while they
+// are in flight, then evaluates the polynomials from shared memory.  Every lane runs the
+// arithmetic (lanes past the last face repeat it; masked lanes would not save issue slots);
+// only active lanes count fallbacks and write.
+template <int NV, int STAGE, int BLOCK>
+__device__ __forceinline__ void flux_tau0_interior(const FluxArgs& a, int lf, int g, int lane, bool active,
+                                                   Real* out) {
+  constexpr int NGP = NV == 3 ? 3 : 4, FPW = 32 / NGP;
+  const int lf0 = lf - lane / NGP;  // first face of this warp
+#if HGKS_FLUX_STAGE
+  __shared__ __align__(16) Real srec[BLOCK / 32][2 * FPW * kRec];
+  Real* sw = srec[threadIdx.x >> 5];
+  {
+    // lane r < 2 FPW: the cell of record r (face lf0 + r/2, owner / neighbour)
+    int rc = 0;
+    if (lane < 2 * FPW && lf0 + (lane >> 1) < a.n_faces) rc = __ldg(a.f_cells + 2 * (a.face0 + lf0 + (lane >> 1)) + (lane & 1));
+#pragma unroll 4
+    for (int r = 0; r < 2 * FPW; ++r) {
+      const int c = __shfl_sync(0xffffffffu, rc, r);
+      if (lane < kRec / 2) cp_async_shared(sw + r * kRec + 2 * lane, a.ceff + (size_t)c * kRec + 2 * lane);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+#endif
+  const int f = a.face0 + min(lf, a.n_faces - 1);
+  const int co = __ldg(a.f_cells + 2 * f), cn = __ldg(a.f_cells + 2 * f + 1);
+  const Real* fg = a.f_geo + (size_t)f * a.f_stride;
+  Real x[3], n[3], wS;
+  face_gp<NV>(fg, g, x, n, wS);
+  const Real xr[3] = {x[0] + __ldg(fg + 3 * NV), x[1] + __ldg(fg + 3 * NV + 1), x[2] + __ldg(fg + 3 * NV + 2)};
+  const Real K = a.gp.K;
+  const Real gm1 = a.gp.gamma - Real(1.0);
+  auto admissible = [](const Real q[5]) {
+    return q[0] > Real(0.0) && (q[0] * q[4] - Real(0.5) * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3])) > Real(0.0);
+  };
+#if HGKS_FLUX_STAGE
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncwarp();
+  const Real* rl = sw + (2 * (lane / NGP)) * kRec;
+  const Real* rr = rl + kRec;
+#else
+  const Real* rl = a.ceff + (size_t)co * kRec;
+  const Real* rr = a.ceff + (size_t)cn * kRec;
+#endif
+  constexpr bool kGlb = !HGKS_FLUX_STAGE;
+  Real vl[5], vr[5], gs[5][3];
+  eval_poly<kGlb>(rl, x, vl, gs);
+  if (!admissible(vl)) {  // R21 positivity fallback
+    if (active) atomicAdd((unsigned long long*)&a.ctrl->fallbacks, 1ull);
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      vl[v] = a.Q[(size_t)co * QS + v];
+      gs[v][0] = gs[v][1] = gs[v][2] = Real(0.0);
+    }
+  }
+  {
+    Real gr[5][3];
+    eval_poly<kGlb>(rr, xr, vr, gr);
+    if (!admissible(vr)) {
+      if (active) atomicAdd((unsigned long long*)&a.ctrl->fallbacks, 1ull);
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        vr[v] = a.Q[(size_t)cn * QS + v];
+        gr[v][0] = gr[v][1] = gr[v][2] = Real(0.0);
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < 5; ++v)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) gs[v][c] += gr[v][c];
+  }
+  Real Q0[5];
+  equilibrium_state_n(vl, vr, n, K, Q0);
+  const EulerState es = euler_state(Q0, gm1);
+  Real dtQ0[5] = {Real(0.0), Real(0.0), Real(0.0), Real(0.0), Real(0.0)};  // 2 d_t Q0 (gs = 2 dQ0)
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    Real jv[5], d[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) d[v] = gs[v][j];
+    euler_jvp(j, es, d, gm1, jv);
+#pragma unroll
+    for (int v = 0; v < 5; ++v) dtQ0[v] -= jv[v];
+  }
+  Real dF[5];
+  euler_jvp_dir(es, n, dtQ0, gm1, dF);  // 2 d_t F (global components)
+  const Real un = es.u[0] * n[0] + es.u[1] * n[1] + es.u[2] * n[2];
+  const Real hw = Real(0.5) * wS;
+  if (STAGE == 1) {
+    out[0] = wS * Q0[0] * un;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) out[1 + c] = wS * (Q0[1 + c] * un + es.p * n[c]);
+    out[4] = wS * un * es.H;
+#pragma unroll
+    for (int v = 0; v < 5; ++v) out[5 + v] = hw * dF[v];
+  } else {
+#pragma unroll
+    for (int v = 0; v < 5; ++v) out[v] = hw * dF[v];
+  }
+}
+
+//   DQ0 = equilibrium slopes dQ0 (P:306-308 gives only <a-bar> = dQ0/dn):
+//         0 average of the two reconstructed gradients (R9; the tau = 0 interior fast path),
+//         1 kinetic weighting rho_l<a^l psi>_{u>0} + rho_r<a^r psi>_{u<0} (R9k),
+//         2 average of the two cells' linear-weight (P_0) gradients (R9s, SPEC's recombination)
+//   PR  = heat-flux (Prandtl-number) correction of the energy flux, moment form only (R29)
+template <int NV, int STAGE, bool TAU0, int BC, int DQ0, bool PR>
 #ifndef HGKS_TAU0_MINB3
 #define HGKS_TAU0_MINB3 5
 #endif
@@ -1105,7 +1360,10 @@ __global__ void __launch_bounds__((NV == 3 ? 3 : 4) * HGKS_FLUX_FPB,
   Real out[NOUT];
 #pragma unroll
   for (int k = 0; k < NOUT; ++k) out[k] = Real(0.0);
-  if (active) {
+  constexpr bool FAST = TAU0 && BC == 0 && DQ0 == 0;  // tau = 0 interior faces, R9
+  if constexpr (FAST && WR) {
+    flux_tau0_interior<NV, STAGE, BLOCK>(a, lf, g, lane, active, out);
+  } else if (active) {
     const int f = a.face0 + lf;
     const int co = __ldg(a.f_cells + 2 * f);
     const Real* fg = a.f_geo + (size_t)f * a.f_stride;
@@ -1146,74 +1404,15 @@ __global__ void __launch_bounds__((NV == 3 ? 3 : 4) * HGKS_FLUX_FPB,
       q[3] = v5[1] * t2[0] + v5[2] * t2[1] + v5[3] * t2[2];
     };
     Real F[5], dF[5];
-    if (TAU0 && BC == 0) {
-      // tau = 0 interior face: only the average of the two gradients enters (R9),
-      // so it is summed in the global frame and rotated once
-      Real ql[5], qr[5], gs[5][3];
-      {
-        Real vl[5];
-        eval_poly(a.ceff + (size_t)co * kRec, x, vl, gs);
-        if (!admissible(vl)) {
-          atomicAdd((unsigned long long*)&a.ctrl->fallbacks, 1ull);
-#pragma unroll
-          for (int v = 0; v < 5; ++v) {
-            vl[v] = a.Q[(size_t)co * QS + v];
-            gs[v][0] = gs[v][1] = gs[v][2] = Real(0.0);
-          }
-        }
-        rotate_value(vl, ql);
-      }
-      {
-        const int cn = __ldg(a.f_cells + 2 * f + 1);
-        const Real xr[3] = {x[0] + __ldg(fg + 3 * NV), x[1] + __ldg(fg + 3 * NV + 1),
-                              x[2] + __ldg(fg + 3 * NV + 2)};
-        Real vr[5], gr[5][3];
-        eval_poly(a.ceff + (size_t)cn * kRec, xr, vr, gr);
-        if (!admissible(vr)) {
-          atomicAdd((unsigned long long*)&a.ctrl->fallbacks, 1ull);
-#pragma unroll
-          for (int v = 0; v < 5; ++v) {
-            vr[v] = a.Q[(size_t)cn * QS + v];
-            gr[v][0] = gr[v][1] = gr[v][2] = Real(0.0);
-          }
-        }
-        rotate_value(vr, qr);
-#pragma unroll
-        for (int v = 0; v < 5; ++v)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) gs[v][c] = Real(0.5) * (gs[v][c] + gr[v][c]);
-      }
-      Real dq0[3][5];
-      {
-        Real zero[5] = {0, 0, 0, 0, 0}, dummy[5];
-        to_local(zero, gs, n, t1, t2, dummy, dq0);
-      }
-      Real Q0[5];
-      equilibrium_state(ql, qr, K, Q0);
-      // f = g0 (1 + A t): F = Euler flux of Q0, d_t F = A_n(Q0) d_t Q0,
-      // d_t Q0 = -sum_j A_j(Q0) d_j Q0
-      const EulerState es = euler_state(Q0, gm1);
-      Real dtQ0[5] = {Real(0.0), Real(0.0), Real(0.0), Real(0.0), Real(0.0)};
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        Real jv[5];
-        euler_jvp(j, es, dq0[j], gm1, jv);
-#pragma unroll
-        for (int v = 0; v < 5; ++v) dtQ0[v] -= jv[v];
-      }
-      euler_jvp(0, es, dtQ0, gm1, dF);
-      F[0] = Q0[1];
-      F[1] = Q0[1] * es.u[0] + es.p;
-      F[2] = Q0[2] * es.u[0];
-      F[3] = Q0[3] * es.u[0];
-      F[4] = es.u[0] * es.H;
-    } else {
+    {
     Real ql[5], dql[3][5], qr[5], dqr[3][5];
     Real vl[5];
+    bool fell_l = false, fell_r = false;
     {
       Real grad[5][3];
       eval_poly(a.ceff + (size_t)co * kRec, x, vl, grad);
       if (!admissible(vl)) {  // R21 positivity fallback
+        fell_l = true;
         atomicAdd((unsigned long long*)&a.ctrl->fallbacks, 1ull);
 #pragma unroll
         for (int v = 0; v < 5; ++v) {
@@ -1229,6 +1428,7 @@ __global__ void __launch_bounds__((NV == 3 ? 3 : 4) * HGKS_FLUX_FPB,
       Real val[5], grad[5][3];
       eval_poly(a.ceff + (size_t)cn * kRec, xr, val, grad);
       if (!admissible(val)) {
+        fell_r = true;
         atomicAdd((unsigned long long*)&a.ctrl->fallbacks, 1ull);
 #pragma unroll
         for (int v = 0; v < 5; ++v) {
@@ -1245,7 +1445,8 @@ __global__ void __launch_bounds__((NV == 3 ? 3 : 4) * HGKS_FLUX_FPB,
     Half hl, hr;
     // fp32 measured faster recomputing the halves in the term groups (register allocation)
     constexpr bool kShareHalves = sizeof(Real) == 8;
-    if (TAU0 || !kShareHalves) {
+    constexpr bool kHalves = (kShareHalves && !TAU0) || DQ0 == 1;  // R9k needs the half-range moments
+    if (!kHalves) {
       equilibrium_state(ql, qr, K, Q0);
       if (!TAU0) {
         gl = prim_of(ql, K);
@@ -1266,15 +1467,74 @@ __global__ void __launch_bounds__((NV == 3 ? 3 : 4) * HGKS_FLUX_FPB,
       Q0[4] = Real(0.5) * gl.rho * (a2 + hl.m0 * (gl.V * gl.V + gl.W * gl.W + (K + Real(2.0)) * hL)) +
               Real(0.5) * gr.rho * (b2 + hr.m0 * (gr.V * gr.V + gr.W * gr.W + (K + Real(2.0)) * hR));
     }
+    // equilibrium slopes dQ0 (DQ0 reading, see above)
+    Real dq0[3][5];
+    if (DQ0 == 0) {
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int v = 0; v < 5; ++v) dq0[j][v] = Real(0.5) * (dql[j][v] + dqr[j][v]);
+    } else if (DQ0 == 1) {
+      // the j-derivative of Q0 = int_{u>0} psi g_l + int_{u<0} psi g_r with d_j g_k = a^k_j g_k
+      Mom ml, mr;
+      maxwell_moments<1>(gl, K, ml, &hl);
+      maxwell_moments<2>(gr, K, mr, &hr);
+      const Real il = Real(1.0) / gl.rho, ir = Real(1.0) / gr.rho;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        Real b[5], al[5], ar[5], ol[5], orr[5];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) b[v] = dql[j][v] * il;
+        micro_slope(b, gl.U, gl.V, gl.W, gl.lam, K, al);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) b[v] = dqr[j][v] * ir;
+        micro_slope(b, gr.U, gr.V, gr.W, gr.lam, K, ar);
+        slope_m<0, 0, 0>(ml, al, ol);
+        slope_m<0, 0, 0>(mr, ar, orr);
+#pragma unroll
+        for (int v = 0; v < 5; ++v) dq0[j][v] = gl.rho * ol[v] + gr.rho * orr[v];
+      }
+    } else {
+      // average of the two cells' P_0 gradients (a side that fell back contributes zero;
+      // wall: the mirror of the left one; farfield: zero)
+      Real dl0[3][5], dr0[3][5];
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int v = 0; v < 5; ++v) dl0[j][v] = dr0[j][v] = Real(0.0);
+      Real val[5], grad[5][3], q5[5];
+      if (!fell_l) {
+        eval_poly(a.ceff0 + (size_t)co * kRec, x, val, grad);
+        to_local(val, grad, n, t1, t2, q5, dl0);
+      }
+      if (BC == 0) {
+        if (!fell_r) {
+          const int cn = __ldg(a.f_cells + 2 * f + 1);
+          const Real xr[3] = {x[0] + __ldg(fg + 3 * NV), x[1] + __ldg(fg + 3 * NV + 1), x[2] + __ldg(fg + 3 * NV + 2)};
+          eval_poly(a.ceff0 + (size_t)cn * kRec, xr, val, grad);
+          to_local(val, grad, n, t1, t2, q5, dr0);
+        }
+      } else if (BC == 1) {
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+          const Real sv = (v >= 1 && v <= 3) ? -Real(1.0) : Real(1.0);
+          dr0[0][v] = -sv * dl0[0][v];
+          dr0[1][v] = sv * dl0[1][v];
+          dr0[2][v] = sv * dl0[2][v];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int v = 0; v < 5; ++v) dq0[j][v] = Real(0.5) * (dl0[j][v] + dr0[j][v]);
+    }
     if (TAU0) {
       Real dtQ0[5] = {Real(0.0), Real(0.0), Real(0.0), Real(0.0), Real(0.0)};
       const EulerState es = euler_state(Q0, gm1);
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
-        Real d0[5], jv[5];
-#pragma unroll
-        for (int v = 0; v < 5; ++v) d0[v] = Real(0.5) * (dql[j][v] + dqr[j][v]);
-        euler_jvp(j, es, d0, gm1, jv);
+        Real jv[5];
+        euler_jvp(j, es, dq0[j], gm1, jv);
 #pragma unroll
         for (int v = 0; v < 5; ++v) dtQ0[v] -= jv[v];
       }
@@ -1301,16 +1561,18 @@ __global__ void __launch_bounds__((NV == 3 ? 3 : 4) * HGKS_FLUX_FPB,
       const Real eh = exp_neg(-(Real(0.5) * dt) / tau);
       const TimeCoef ch = time_coef_e(Real(0.5) * dt, tau, eh), cf = time_coef_e(dt, tau, eh * eh);
       Real Ih[5] = {0, 0, 0, 0, 0}, If[5] = {0, 0, 0, 0, 0};
-      Real dq0[3][5];
-#pragma unroll
-      for (int j = 0; j < 3; ++j)
-#pragma unroll
-        for (int v = 0; v < 5; ++v) dq0[j][v] = Real(0.5) * (dql[j][v] + dqr[j][v]);
       // the two half-range groups first: each side's state dies after its group,
       // which keeps fewer values live (fewer spills) than starting with g0
-      add_side<1>(ql, dql, K, gm1, ch, cf, Ih, If, gl, kShareHalves ? &hl : nullptr);
-      add_side<2>(qr, dqr, K, gm1, ch, cf, Ih, If, gr, kShareHalves ? &hr : nullptr);
-      add_side<0>(Q0, dq0, K, gm1, ch, cf, Ih, If, prim_of(Q0, K));
+      const Prim g0 = prim_of(Q0, K);
+      const Real U0[3] = {g0.U, g0.V, g0.W};
+      Real Qh = Real(0.0), Qf = Real(0.0);  // heat-flux time integrals (R29)
+      add_side<1, PR>(ql, dql, K, gm1, ch, cf, Ih, If, gl, kHalves ? &hl : nullptr, U0, &Qh, &Qf);
+      add_side<2, PR>(qr, dqr, K, gm1, ch, cf, Ih, If, gr, kHalves ? &hr : nullptr, U0, &Qh, &Qf);
+      add_side<0, PR>(Q0, dq0, K, gm1, ch, cf, Ih, If, g0, nullptr, U0, &Qh, &Qf);
+      if (PR) {
+        Ih[4] += a.gp.pr_fac * Qh;
+        If[4] += a.gp.pr_fac * Qf;
+      }
       // 2x2 fit; a step past t_stop has dt = 0 and must leave Q unchanged, so
       // F and dF are 0 there (Ih = If = 0) instead of 0 * inf = NaN
       const Real idt = dt > Real(0.0) ? Real(1.0) / dt : Real(0.0);
@@ -1570,9 +1832,9 @@ struct Launch {
     using S = ReconShape<K>;
     k_recon<K, M, NM><<<n_tiles * S::SPLIT, S::BT, S::SMEM, st>>>(a);
   }
-  template <int NV, int STAGE, bool TAU0, int BC>
+  template <int NV, int STAGE, bool TAU0, int BC, int DQ0, bool PR>
   static void flux(int grid, cudaStream_t st, const FluxArgs& a) {
-    k_flux<NV, STAGE, TAU0, BC><<<grid, (NV == 3 ? 3 : 4) * HGKS_FLUX_FPB, 0, st>>>(a);
+    k_flux<NV, STAGE, TAU0, BC, DQ0, PR><<<grid, (NV == 3 ? 3 : 4) * HGKS_FLUX_FPB, 0, st>>>(a);
   }
   template <int NF>
   static void update1(int grid, cudaStream_t st, const UpdateArgs& u) {

@@ -63,7 +63,8 @@ struct GlobalMesh {
   // partition
   int32_t n_ranks = 1;
   std::vector<int32_t> part;
-  int64_t edge_cut = 0;
+  int64_t edge_cut = 0;       // faces between different ranks (after refinement)
+  int64_t edge_cut_rcb = 0;   // the same for the plain RCB partition (before refinement)
 };
 
 // One rank's device-ready arrays.  Local cell order:

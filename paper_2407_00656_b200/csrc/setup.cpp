@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <tuple>
 #include <unordered_map>
 
 #include "internal.h"
@@ -190,6 +191,96 @@ uint64_t spread21(uint64_t v) {
 }
 
 }  // namespace
+
+// Boundary refinement of a k-way partition on the face-adjacency (dual) graph (P:730-739:
+// balanced parts, few cut faces): Fiduccia-Mattheyses passes.  Each pass repeatedly moves the
+// unlocked boundary cell with the largest gain (cut faces removed minus added when it joins
+// the neighbouring part it shares most faces with), negative gains included, keeping every
+// part within 0.5 % of the mean size; each cell moves at most once per pass, and the pass is
+// rolled back to its best prefix.  Deterministic (ties by cell id, then lower rank).  The
+// solution does not depend on the partition (bitwise equal for any partition),
+// only the halo volume does.
+static void refine_partition(GlobalMesh& gm, int nfc) {
+  const int64_t nc = gm.nc;
+  const int nr = gm.n_ranks;
+  std::vector<int64_t> size(nr, 0);
+  for (int64_t i = 0; i < nc; ++i) ++size[gm.part[i]];
+  const double mean = (double)nc / nr;
+  // every part within 0.5 % of the mean, so the largest and smallest differ by <= 1 %
+  const int64_t hi = std::max((int64_t)std::floor(mean * 1.005), (int64_t)std::ceil(mean)),
+                lo = std::min((int64_t)std::ceil(mean * 0.995), (int64_t)std::floor(mean));
+  // best move of cell i: (gain, target part); target -1 if i is not on a part boundary
+  auto best_move = [&](int64_t i, int& target) {
+    const int p = gm.part[i];
+    int own = 0, nb_part[6], nb_cnt[6], nn = 0;
+    for (int q = 0; q < nfc; ++q) {
+      const int64_t j = gm.nbr_id[i * 6 + q];
+      if (j >= nc) continue;  // boundary ghost
+      const int r = gm.part[j];
+      if (r == p) { ++own; continue; }
+      int k = 0;
+      while (k < nn && nb_part[k] != r) ++k;
+      if (k == nn) { nb_part[nn] = r; nb_cnt[nn++] = 0; }
+      ++nb_cnt[k];
+    }
+    target = -1;
+    int best = -1;
+    for (int k = 0; k < nn; ++k)
+      if (nb_cnt[k] > best || (nb_cnt[k] == best && nb_part[k] < target)) { best = nb_cnt[k]; target = nb_part[k]; }
+    return target < 0 ? 0 : best - own;
+  };
+  std::vector<char> locked(nc, 0);
+  for (int pass = 0; pass < 8; ++pass) {
+    // max-heap of (gain, -cell) with lazy invalidation by a per-cell stamp
+    std::vector<std::tuple<int, int64_t, int64_t>> heap;  // gain, -cell, stamp
+    std::vector<int64_t> stamp(nc, 0);
+    auto push = [&](int64_t i) {
+      int t;
+      const int g = best_move(i, t);
+      if (t >= 0) {
+        heap.emplace_back(g, -i, ++stamp[i]);
+        std::push_heap(heap.begin(), heap.end());
+      }
+    };
+    for (int64_t i = 0; i < nc; ++i) push(i);
+    std::fill(locked.begin(), locked.end(), 0);
+    std::vector<std::pair<int64_t, int>> moves;  // (cell, previous part)
+    int64_t cum = 0, best_cum = 0;
+    size_t best_len = 0;
+    const size_t max_moves = heap.size();
+    while (!heap.empty() && moves.size() < max_moves) {
+      std::pop_heap(heap.begin(), heap.end());
+      auto [g, mi, st] = heap.back();
+      heap.pop_back();
+      const int64_t i = -mi;
+      if (locked[i] || st != stamp[i]) continue;
+      int t;
+      const int g2 = best_move(i, t);
+      if (t < 0 || g2 != g) continue;
+      const int p = gm.part[i];
+      if (size[t] + 1 > hi || size[p] - 1 < lo) continue;
+      gm.part[i] = t;
+      --size[p];
+      ++size[t];
+      locked[i] = 1;
+      moves.emplace_back(i, p);
+      cum += g;
+      if (cum > best_cum) { best_cum = cum; best_len = moves.size(); }
+      for (int q = 0; q < nfc; ++q) {
+        const int64_t j = gm.nbr_id[i * 6 + q];
+        if (j < nc && !locked[j]) push(j);
+      }
+      if (cum < best_cum - 64) break;  // a long losing streak: stop the pass early
+    }
+    for (size_t k = moves.size(); k > best_len; --k) {  // roll back to the best prefix
+      const auto [i, p] = moves[k - 1];
+      --size[gm.part[i]];
+      ++size[p];
+      gm.part[i] = p;
+    }
+    if (best_cum <= 0) break;
+  }
+}
 
 // ============================================================================
 GlobalMesh build_global_mesh(const double* xyz, int64_t n_nodes, const int8_t* type, const int64_t* cn,
@@ -627,6 +718,16 @@ GlobalMesh build_global_mesh(const double* xyz, int64_t n_nodes, const int8_t* t
         st.push_back({t.b, cut, t.r0, nl});
         st.push_back({cut, t.e, t.r0 + nl, t.nr - nl});
       }
+    }
+    if (!cell_part) {
+      auto cut = [&] {
+        int64_t c = 0;
+        for (int64_t f = 0; f < gm.nf; ++f)
+          if (gm.f_nb[f] >= 0 && gm.part[gm.f_owner[f]] != gm.part[gm.f_nb[f]]) ++c;
+        return c;
+      };
+      gm.edge_cut_rcb = cut();
+      refine_partition(gm, nfc);
     }
     for (int64_t f = 0; f < gm.nf; ++f)
       if (gm.f_nb[f] >= 0 && gm.part[gm.f_owner[f]] != gm.part[gm.f_nb[f]]) ++gm.edge_cut;

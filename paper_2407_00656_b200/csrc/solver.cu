@@ -146,7 +146,7 @@ int round32(int64_t n) { return (int)((n + 31) / 32 * 32); }
 
 struct DevArrays {
   // working-precision arrays (double for fp64, float for fp32)
-  void *Q, *Qtmp, *R, *ceff, *F1, *F2, *op, *geo, *f_geo, *inv_v, *h_dt, *bg_normal, *sendbuf;
+  void *Q, *Qtmp, *R, *ceff, *ceff0, *F1, *F2, *op, *geo, *f_geo, *inv_v, *h_dt, *bg_normal, *sendbuf;
   double *stage_in[2], *stage_out[2];  // caller-order staging (fp64), double-buffered for pipelining
   int *recon_cell, *st_id, *f_cells, *cf, *bg_cell, *bg_bc, *send_list, *out_local;
   int2* put_dst;  // fused halo put: (receiver rank, receiver row) per send row (f3)
@@ -156,8 +156,8 @@ struct DevArrays {
   Ctrl* ctrl;
 };
 
-// rs = bytes of the working precision
-size_t layout(const GlobalMesh& gm, const RankPlan& rp, size_t rs, Carve& c, DevArrays& d) {
+// rs = bytes of the working precision; dq0_mode 2 (R9s) adds the P_0 records
+size_t layout(const GlobalMesh& gm, const RankPlan& rp, size_t rs, int dq0_mode, Carve& c, DevArrays& d) {
   const Layout& L = gm.lay;
   const size_t nq = (size_t)QS * round32(rp.n_local());
   const int64_t ncl = rp.n_owned + rp.n_pghost;
@@ -167,6 +167,7 @@ size_t layout(const GlobalMesh& gm, const RankPlan& rp, size_t rs, Carve& c, Dev
   d.Qtmp = R(nq);
   d.R = R((size_t)QS * rp.n_owned);
   d.ceff = R((size_t)kRec * ncl);
+  d.ceff0 = dq0_mode == 2 ? R((size_t)kRec * ncl) : nullptr;
   d.F1 = R((size_t)10 * rp.n_faces);
   d.F2 = R((size_t)5 * rp.n_faces);
   d.recon_cell = c.take<int>(rp.n_recon);
@@ -223,6 +224,12 @@ struct hgks_solver {
   int recon_t1 = 0;  // end tile of the current reconstruction launch
   cudaStream_t comm_stream = nullptr;  // NCCL halo exchange (overlapped with the early work)
   cudaEvent_t ev_packed = nullptr, ev_halo = nullptr;
+  // min(dt) allreduce on the comm stream (n_ranks > 1): issued after k_update2, waited for
+  // only where the next step first needs dt (hidden behind stage-1 work)
+  cudaEvent_t ev_upd2 = nullptr, ev_dt = nullptr;
+  bool dt_pending = false;     // an allreduce is in flight on the comm stream
+  bool begin_pending = false;  // this step's k_step_begin is deferred until dt is needed
+  double cur_t_stop = 0.0;
   bool put_ready = false;  // put_dst uploaded (loopback group, first hgks_group_step)
   // HGKS_TRANSPORT_P2P: peers' workspaces mapped by CUDA IPC (hgks_p2p_connect)
   bool p2p_ready = false;
@@ -341,6 +348,7 @@ void run_recon(hgks_solver* s, const void* Q, int part) {
   a.op = as<L>(s->d.op);
   a.geo = as<L>(s->d.geo);
   a.ceff = as<L>(s->d.ceff);
+  a.ceff0 = s->d.ceff0 ? as<L>(s->d.ceff0) : nullptr;
   a.eps = (typename L::RealT)s->cfg.eps;
   a.omega_pow = s->cfg.omega_pow;
   if (LY.cell_type == 4) {
@@ -364,21 +372,33 @@ void run_recon(hgks_solver* s, const void* Q, int part) {
   }
 }
 
-template <class L, int NV, int BC>
-void launch_flux(hgks_solver* s, const typename L::FluxArgsT& a, int stage, bool tau0) {
+template <class L, int NV, int BC, int DQ0, bool PR = false>
+void launch_flux_q(hgks_solver* s, const typename L::FluxArgsT& a, int stage, bool tau0) {
   constexpr int NGP = NV == 3 ? 3 : 4, B = NGP * HGKS_FLUX_FPB;
   // faces per block: NGP lanes per face, or 10 faces per warp with the shuffle reduction
   constexpr int FPBk = HGKS_FLUX_WARPRED ? (B / 32) * (32 / NGP) : B / NGP;
   const int nb = (int)((a.n_faces + FPBk - 1) / FPBk);
   const char* names[2][2] = {{"k_flux_s1", "k_flux_s2"}, {"k_flux_tau0_s1", "k_flux_tau0_s2"}};
   const char* nm = BC == 0 ? names[tau0][stage - 1] : (BC == 1 ? "k_flux_wall" : "k_flux_farfield");
-  if (tau0) {
-    if (stage == 1) launch(s, nm, [&] { L::template flux<NV, 1, true, BC>(nb, s->stream, a); });
-    else launch(s, nm, [&] { L::template flux<NV, 2, true, BC>(nb, s->stream, a); });
+  if (tau0) {  // tau = 0: no non-equilibrium part, the Prandtl fix is identically zero (R29)
+    if (stage == 1) launch(s, nm, [&] { L::template flux<NV, 1, true, BC, DQ0, false>(nb, s->stream, a); });
+    else launch(s, nm, [&] { L::template flux<NV, 2, true, BC, DQ0, false>(nb, s->stream, a); });
   } else {
-    if (stage == 1) launch(s, nm, [&] { L::template flux<NV, 1, false, BC>(nb, s->stream, a); });
-    else launch(s, nm, [&] { L::template flux<NV, 2, false, BC>(nb, s->stream, a); });
+    if (stage == 1) launch(s, nm, [&] { L::template flux<NV, 1, false, BC, DQ0, PR>(nb, s->stream, a); });
+    else launch(s, nm, [&] { L::template flux<NV, 2, false, BC, DQ0, PR>(nb, s->stream, a); });
   }
+}
+
+// dq0 readings other than R9 and the Prandtl fix exist for the fp64 path only (hgks_init
+// rejects them for fp32); the Prandtl fix is built with the R9 reading
+template <class L, int NV, int BC>
+void launch_flux(hgks_solver* s, const typename L::FluxArgsT& a, int stage, bool tau0) {
+  if constexpr (sizeof(typename L::RealT) == 8) {
+    if (s->cfg.dq0_mode == 1) return launch_flux_q<L, NV, BC, 1>(s, a, stage, tau0);
+    if (s->cfg.dq0_mode == 2) return launch_flux_q<L, NV, BC, 2>(s, a, stage, tau0);
+    if (s->gp.pr_fac != 0.0) return launch_flux_q<L, NV, BC, 0, true>(s, a, stage, tau0);
+  }
+  launch_flux_q<L, NV, BC, 0>(s, a, stage, tau0);
 }
 
 template <class L, int NV>
@@ -406,6 +426,7 @@ void run_flux(hgks_solver* s, const void* Q, int stage, int part) {
   typename L::FluxArgsT a;
   a.Q = as<L>(Q);
   a.ceff = as<L>(s->d.ceff);
+  a.ceff0 = s->d.ceff0 ? as<L>(s->d.ceff0) : nullptr;
   a.f_cells = s->d.f_cells;
   a.f_geo = as<L>(s->d.f_geo);
   a.f_stride = rp.f_geo_stride;
@@ -519,11 +540,35 @@ void wait_halo(hgks_solver* s) {
   CUDA_TRY(cudaStreamWaitEvent(s->stream, s->ev_halo, 0));
 }
 
-// a4: global min of the CFL bound (exact, order independent)
+// a4: global min of the CFL bound (exact, order independent).  Enqueued on the comm stream
+// after the work that produced the local bound; the compute stream waits for it only in
+// begin_step (or before anything reads or resets the bound), so it overlaps the next step's
+// stage-1 reconstruction and flux.
 void allreduce_dt(hgks_solver* s) {
   if (s->n_ranks == 1 || s->transport == HGKS_TRANSPORT_LOOPBACK) return;
+  CUDA_TRY(cudaEventRecord(s->ev_upd2, s->stream));
+  CUDA_TRY(cudaStreamWaitEvent(s->comm_stream, s->ev_upd2, 0));
   NCCL_TRY(nccl().AllReduce(&s->d.ctrl->dtmin_bits, &s->d.ctrl->dtmin_bits, 1, ncclUint64, ncclMin, s->comm,
-                            s->stream));
+                            s->comm_stream));
+  CUDA_TRY(cudaEventRecord(s->ev_dt, s->comm_stream));
+  s->dt_pending = true;
+}
+
+// the compute stream waits for the last min(dt) allreduce (no-op if none is in flight)
+void wait_dt(hgks_solver* s) {
+  if (!s->dt_pending) return;
+  CUDA_TRY(cudaStreamWaitEvent(s->stream, s->ev_dt, 0));
+  s->dt_pending = false;
+}
+
+// this step's time bookkeeping (dt from the global min, t_stop clipping); deferred on
+// multi-rank solvers to the first point of stage 1 that needs dt
+void begin_step(hgks_solver* s) {
+  if (!s->begin_pending) return;
+  wait_dt(s);
+  launch(s, "k_step_begin",
+         [&] { k_step_begin<<<1, 1, 0, s->stream>>>(s->d.ctrl, s->cfg.cfl, s->cfg.fixed_dt, s->cur_t_stop); });
+  s->begin_pending = false;
 }
 
 template <class L>
@@ -542,6 +587,7 @@ template <class L>
 void stage_early(hgks_solver* s, int st) {
   bc_ghosts<L>(s, s->d.Q, 0);
   run_recon<L>(s, s->d.Q, 0);
+  if (s->cfg.tau_mode != 0) begin_step(s);  // the NS collision time needs dt (R7)
   run_flux<L>(s, s->d.Q, st, 0);
 }
 
@@ -551,6 +597,7 @@ void stage_late(hgks_solver* s, int st) {
   bc_ghosts<L>(s, s->d.Q, 1);
   run_recon<L>(s, s->d.Q, 1);
   run_flux<L>(s, s->d.Q, st, 1);
+  begin_step(s);  // tau = 0: dt is first needed by the stage-1 update
   const typename L::UpdateArgsT u = update_args<L>(s);
   const int n = (int)s->rp->n_owned;
   const int nf = s->lay.nfaces;
@@ -622,6 +669,7 @@ void init_dt(hgks_solver* s) {
 // rows, reset time, recompute the CFL bound
 template <class L>
 void upload_state(hgks_solver* s, const double* h_Q, double t) {
+  wait_dt(s);  // k_reset_ctrl rewrites the bound an allreduce may still be reducing
   const RankPlan& rp = *s->rp;
   const int n = (int)rp.n_owned;
   const int k = s->in_slot;
@@ -724,6 +772,7 @@ hgks_status hgks_mesh_info(const hgks_mesh* mc, int32_t rank, hgks_mesh_stats* s
     st->send_cells = (int64_t)rp.send_list.size();
     for (auto c : rp.recv_cnt) st->recv_cells += c;
     st->edge_cut = m->gm.edge_cut;
+    st->edge_cut_rcb = m->gm.edge_cut_rcb ? m->gm.edge_cut_rcb : m->gm.edge_cut;
     st->n_early_cells = rp.n_recon_early;
     st->n_early_faces = rp.n_if_early;
   });
@@ -738,7 +787,7 @@ hgks_status hgks_workspace_size(const hgks_mesh* mc, const hgks_config* cfg, int
     Carve c{nullptr, 0, 0};
     DevArrays d;
     const bool fp32 = cfg && cfg->precision == 32;
-    *bytes = layout(m->gm, rp, fp32 ? sizeof(float) : sizeof(double), c, d);
+    *bytes = layout(m->gm, rp, fp32 ? sizeof(float) : sizeof(double), cfg ? cfg->dq0_mode : 0, c, d);
   });
 }
 
@@ -782,13 +831,20 @@ hgks_status hgks_init(const hgks_mesh* mc, const hgks_config* cfg, const hgks_di
     g.t_inf = cfg->t_inf;
     g.mu_exp = cfg->mu_exp;
     for (int k = 0; k < 5; ++k) g.fs[k] = cfg->freestream[k];
+    if (cfg->prandtl < 0) throw Error(HGKS_E_ARG, "prandtl must be > 0 (0 = no correction)");
+    g.pr_fac = (cfg->prandtl > 0 && cfg->prandtl != 1.0) ? 1.0 / cfg->prandtl - 1.0 : 0.0;
     if (cfg->precision != 64 && cfg->precision != 32) throw Error(HGKS_E_ARG, "precision must be 64 or 32");
+    if (cfg->dq0_mode < 0 || cfg->dq0_mode > 2) throw Error(HGKS_E_ARG, "dq0_mode must be 0, 1 or 2");
+    if (cfg->dq0_mode != 0 && cfg->precision == 32)
+      throw Error(HGKS_E_ARG, "dq0_mode 1/2 (readings R9k/R9s) are built for the fp64 path only");
+    if (g.pr_fac != 0.0 && (cfg->precision == 32 || cfg->dq0_mode != 0))
+      throw Error(HGKS_E_ARG, "the Prandtl fix (R29) is built for the fp64 path with dq0_mode 0");
     s->fp32 = cfg->precision == 32;
     s->rs = s->fp32 ? sizeof(float) : sizeof(double);
     s->nq = (size_t)QS * round32(rp.n_local());
     Carve c{(char*)d_ws, 0, ws_bytes};
     if ((reinterpret_cast<uintptr_t>(d_ws) & 255) != 0) throw Error(HGKS_E_ARG, "workspace must be 256-byte aligned");
-    layout(m->gm, rp, s->rs, c, s->d);
+    layout(m->gm, rp, s->rs, cfg->dq0_mode, c, s->d);
     cudaStream_t st = s->stream;
     auto up = [&](void* dst, const void* src, size_t bytes) {
       if (bytes) CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
@@ -840,6 +896,8 @@ hgks_status hgks_init(const hgks_mesh* mc, const hgks_config* cfg, const hgks_di
       CUDA_TRY(cudaStreamCreateWithFlags(&s->comm_stream, cudaStreamNonBlocking));
       CUDA_TRY(cudaEventCreateWithFlags(&s->ev_packed, cudaEventDisableTiming));
       CUDA_TRY(cudaEventCreateWithFlags(&s->ev_halo, cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&s->ev_upd2, cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&s->ev_dt, cudaEventDisableTiming));
     }
     if (s->n_ranks > 1)
       for (int k = 0; k < 2; ++k)
@@ -871,10 +929,13 @@ hgks_status hgks_destroy(hgks_solver* s) {
     for (auto e : s->event_pool) cudaEventDestroy(e);
     for (int k = 0; k < kMaxGroup; ++k)
       if (s->peer_base[k]) cudaIpcCloseMemHandle(s->peer_base[k]);
+    if (s->comm_stream) cudaStreamSynchronize(s->comm_stream);  // a min(dt) allreduce may be in flight
     if (s->comm && nccl().CommDestroy) nccl().CommDestroy(s->comm);
     if (s->comm_stream) cudaStreamDestroy(s->comm_stream);
     if (s->ev_packed) cudaEventDestroy(s->ev_packed);
     if (s->ev_halo) cudaEventDestroy(s->ev_halo);
+    if (s->ev_upd2) cudaEventDestroy(s->ev_upd2);
+    if (s->ev_dt) cudaEventDestroy(s->ev_dt);
     cudaStreamSynchronize(s->h2d_stream);
     cudaStreamSynchronize(s->d2h_stream);
     for (int k = 0; k < 2; ++k) {
@@ -905,8 +966,10 @@ hgks_status hgks_step(hgks_solver* s, int32_t n_steps, double t_stop, hgks_step_
       CUDA_TRY(cudaStreamSynchronize(s->stream));
     }
     auto one_step = [&] {
-      launch(s, "k_step_begin",
-             [&] { k_step_begin<<<1, 1, 0, s->stream>>>(s->d.ctrl, s->cfg.cfl, s->cfg.fixed_dt, t_stop); });
+      s->begin_pending = true;
+      s->cur_t_stop = t_stop;
+      // one rank: begin at once (graph replays); several: where stage 1 first needs dt
+      if (s->n_ranks == 1 || s->transport == HGKS_TRANSPORT_LOOPBACK) begin_step(s);
       HGKS_DISPATCH(s, stage, s, 1);
       HGKS_DISPATCH(s, stage, s, 2);
     };
@@ -947,6 +1010,7 @@ hgks_status hgks_step(hgks_solver* s, int32_t n_steps, double t_stop, hgks_step_
       }
     }
     if (info) {
+      wait_dt(s);
       Ctrl h;
       CUDA_TRY(cudaMemcpyAsync(&h, s->d.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s->stream));
       CUDA_TRY(cudaStreamSynchronize(s->stream));

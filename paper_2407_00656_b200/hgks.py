@@ -45,7 +45,7 @@ class Config(C.Structure):
     _fields_ = [("gamma", C.c_double), ("cfl", C.c_double), ("fixed_dt", C.c_double), ("tau_mode", C.c_int32),
                 ("c1", C.c_double), ("mu_inf", C.c_double), ("t_inf", C.c_double), ("mu_exp", C.c_double),
                 ("eps", C.c_double), ("omega_pow", C.c_int32), ("freestream", C.c_double * 5),
-                ("precision", C.c_int32)]
+                ("precision", C.c_int32), ("dq0_mode", C.c_int32), ("prandtl", C.c_double)]
 
 
 class Dist(C.Structure):
@@ -58,7 +58,8 @@ class MeshStats(C.Structure):
                 ("ghost_layer", C.c_int64 * 3), ("n_bghost", C.c_int64), ("n_faces", C.c_int64),
                 ("n_faces_bc", C.c_int64), ("stencil_min", C.c_int32), ("stencil_max", C.c_int32),
                 ("n_sub", C.c_int32), ("n_peers", C.c_int32), ("send_cells", C.c_int64), ("recv_cells", C.c_int64),
-                ("edge_cut", C.c_int64), ("n_early_cells", C.c_int64), ("n_early_faces", C.c_int64)]
+                ("edge_cut", C.c_int64), ("n_early_cells", C.c_int64), ("n_early_faces", C.c_int64),
+                ("edge_cut_rcb", C.c_int64)]
 
     def as_dict(self):
         d = {}
@@ -140,6 +141,8 @@ class SolverConfig:
     omega_pow: int = 1
     freestream: tuple = (1.0, 0.0, 0.0, 0.0, 1.0 / 1.4)
     precision: int = 64  # 64: fp64 parity path; 32: FP32 variant
+    dq0_mode: int = 0    # equilibrium slopes: 0 average (R9), 1 kinetic (R9k), 2 gamma-weighted (R9s)
+    prandtl: float = 1.0  # Pr of the heat-flux correction (R29); 1 = none (BGK)
 
     def eps_value(self) -> float:
         if self.eps is not None:
@@ -148,7 +151,8 @@ class SolverConfig:
 
     def c(self) -> Config:
         return Config(self.gamma, self.cfl, self.fixed_dt, self.tau_mode, self.c1, self.mu_inf, self.t_inf,
-                      self.mu_exp, self.eps_value(), self.omega_pow, (C.c_double * 5)(*self.freestream), self.precision)
+                      self.mu_exp, self.eps_value(), self.omega_pow, (C.c_double * 5)(*self.freestream), self.precision,
+                      self.dq0_mode, self.prandtl)
 
 
 def p2p_selftest() -> None:

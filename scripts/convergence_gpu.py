@@ -14,6 +14,7 @@ ap.add_argument("--omega-pow", type=int, default=1)
 ap.add_argument("--cfl", type=float, default=0.3)
 ap.add_argument("--eps", type=float, default=None)
 ap.add_argument("--precision", type=int, default=64, choices=[64, 32])
+ap.add_argument("--dq0-mode", type=int, default=0, help="SURVEY Q9 reading: 0 R9, 1 R9k, 2 R9s")
 ap.add_argument("--jitter", type=float, default=0.0, help="interior node jitter (fraction of h), seed 656")
 args = ap.parse_args()
 prev = None
@@ -21,7 +22,7 @@ for N in args.N:
     mi = W.kuhn_box(N, jitter=args.jitter)
     Q0 = W.advection_ic(mi)
     s = hgks.Solver(hgks.Mesh(mi), Q0, hgks.SolverConfig(cfl=args.cfl, omega_pow=args.omega_pow, eps=args.eps,
-                                                            precision=args.precision))
+                                                            precision=args.precision, dq0_mode=args.dq0_mode))
     t0 = time.time()
     steps = 0
     while True:
@@ -39,6 +40,6 @@ for N in args.N:
     order = np.log2(prev / L1) if prev else None
     print(json.dumps(dict(N=N, steps=steps, t=t, L1=L1, L2=L2, order=order, paper_L1=T3.get(N),
                           ratio=L1 / T3[N] if N in T3 else None, fallbacks=info["fallbacks"],
-                          omega_pow=args.omega_pow, cfl=args.cfl, precision=args.precision, jitter=args.jitter, secs=time.time() - t0)), flush=True)
+                          omega_pow=args.omega_pow, cfl=args.cfl, dq0_mode=args.dq0_mode, precision=args.precision, jitter=args.jitter, secs=time.time() - t0)), flush=True)
     prev = L1
     s.close()

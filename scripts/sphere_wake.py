@@ -91,6 +91,7 @@ def main():
     ap.add_argument("--t-end", type=float, default=150.0)
     ap.add_argument("--chunk", type=int, default=2000)
     ap.add_argument("--precision", type=int, default=64)
+    ap.add_argument("--prandtl", type=float, default=1.0, help="Pr of the heat-flux correction (R29); 1 = none")
     ap.add_argument("--tol", type=float, default=1e-6, help="stop when the density residual falls below")
     ap.add_argument("--out", default=None, help="save the final state (.npy)")
     args = ap.parse_args()
@@ -102,6 +103,7 @@ def main():
     fs = (1.0, args.ma, 0.0, 0.0, 1.0 / gam)
     Q0 = W.uniform_state(mi.n_cells, 1.0, (args.ma, 0.0, 0.0), 1.0 / gam, gamma=gam)
     cfg = hgks.SolverConfig(gamma=gam, cfl=0.5, tau_mode=1, mu_inf=args.ma / args.re, c1=1.0, t_inf=1.0 / gam,
+                            prandtl=args.prandtl,
                             freestream=fs, precision=args.precision)
     s = hgks.Solver(hgks.Mesh(mi), Q0, cfg)
     Qp, _, tp = s.get_state()

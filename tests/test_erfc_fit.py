@@ -1,6 +1,6 @@
 """The fp64 erfc used by the flux kernels (csrc/common.cuh erfc_exp, coefficients in
-csrc/erfc_fit.h from scripts/fit_erfc.py): the same Clenshaw evaluation, done here
-in numpy, against the C library's erfc (math.erfc) over z in [-40, 40]."""
+csrc/erfc_fit.h from scripts/fit_erfc.py): the same Horner evaluation in the monomial
+basis, done here in numpy, against the C library's erfc (math.erfc) over z in [-40, 40]."""
 import json
 import math
 import os
@@ -15,10 +15,9 @@ def erfc_fit(z, K, c):
     a = np.abs(z)
     r = 1.0 / (a + K)
     t = (a - K) * r
-    b1 = np.zeros_like(t); b2 = np.zeros_like(t)
-    for ck in c[:0:-1]:
-        b1, b2 = 2 * t * b1 - b2 + ck, b1
-    P = t * b1 - b2 + c[0]
+    P = np.zeros_like(t)
+    for ck in c[::-1]:
+        P = P * t + ck
     v = P * r * np.exp(-z * z)
     return np.where(z >= 0, v, 2.0 - v)
 

@@ -18,14 +18,17 @@ def rel_err(a, b):
     return (np.abs(a - b).max(axis=0) / np.maximum(np.abs(b).max(axis=0), 1e-300))
 
 
-def run_pair(mi, Q0, steps, cfl=0.3, per_step=True, ocfg=None, gcfg=None):
+def run_pair(mi, Q0, steps, cfl=0.3, per_step=True, ocfg=None, gcfg=None, chunks=None):
+    """Advance the CUDA path and the oracle side by side and compare after every chunk of
+    steps (default: every step)."""
     ocfg = ocfg or O.OracleConfig(cfl=cfl)
     gcfg = gcfg or hgks.SolverConfig(cfl=cfl)
     g = hgks.Solver(hgks.Mesh(mi), Q0, gcfg)
     o = O.OracleSolver(O.OracleMesh(mi), Q0, ocfg)
     errs = []
-    for k in range(steps if per_step else 1):
-        n = 1 if per_step else steps
+    if chunks is None:
+        chunks = [1] * steps if per_step else [steps]
+    for n in chunks:
         gi = g.step(n)
         o.step(n)
         Qg, gid, tg = g.get_state()
@@ -35,6 +38,26 @@ def run_pair(mi, Q0, steps, cfl=0.3, per_step=True, ocfg=None, gcfg=None):
         assert gi["fallbacks"] == fbo
         errs.append(rel_err(Qg, Qo))
     return np.array(errs), g, o
+
+
+def gpu_and_oracle(mi, Q0, gcfg, ocfg, steps):
+    """Full-size runs: the oracle (mesh build + steps on all host cores) in a worker thread
+    while the CUDA path builds its mesh and steps (ctypes releases the GIL), so the test
+    takes about the oracle's time alone.  Returns (Q_gpu, t_gpu, oracle state)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    def oracle_run():
+        o = O.OracleSolver(O.OracleMesh(mi), Q0, ocfg)
+        o.step(steps)
+        return o.state()
+
+    with ThreadPoolExecutor(1) as ex:
+        fut = ex.submit(oracle_run)
+        g = hgks.Solver(hgks.Mesh(mi), Q0, gcfg)
+        g.step(steps)
+        Qg, _, tg = g.get_state()
+        del g
+        return Qg, tg, fut.result()
 
 
 def test_c1_residual_matches_oracle(cuda_ok):
@@ -132,13 +155,31 @@ def test_t_stop_ns_tau_steps_after_stop(cuda_ok):
 
 
 def test_bench_size_steps(cuda_ok):
-    """configs[1] at the bench size N=48 (663,552 tets) in bench.py's launch configuration:
-    one eager step, then one step replayed from the captured CUDA graph; every cell vs the
-    oracle after each."""
+    """configs[1] at its top size N=48 (663,552 tets) for 10 steps in bench.py's launch
+    configuration (one eager step, then CUDA-graph replays): every cell vs the oracle after
+    the first step and after the tenth."""
     mi = W.kuhn_box(48)
     Q0 = W.advection_ic(mi)
-    errs, _, _ = run_pair(mi, Q0, 2)
-    assert errs.max() <= TOL, errs.max(axis=0)
+    g = hgks.Solver(hgks.Mesh(mi), Q0, hgks.SolverConfig(cfl=0.3))
+    o = O.OracleSolver(O.OracleMesh(mi), Q0, O.OracleConfig(cfl=0.3))
+    for n in (1, 9):
+        gi = g.step(n)
+        o.step(n)
+        Qg, _, tg = g.get_state()
+        Qo, to, _, fbo = o.state()
+        assert abs(tg - to) <= 1e-13 and gi["fallbacks"] == fbo == 0
+        assert rel_err(Qg, Qo).max() <= TOL, rel_err(Qg, Qo)
+
+
+def test_c5_full_size_two_steps(cuda_ok):
+    """configs[4] at full size: the 110^3 Kuhn box (7,986,000 tets, bench.py's default
+    workload) for 2 steps in the bench launch configuration (eager step + graph replay),
+    every cell vs the oracle (all host cores; SURVEY 8(d) C5 allows >= 2 oracle steps)."""
+    mi = W.kuhn_box(110)
+    Q0 = W.advection_ic(mi)
+    Qg, tg, (Qo, to, _, fbo) = gpu_and_oracle(mi, Q0, hgks.SolverConfig(cfl=0.3), O.OracleConfig(cfl=0.3), 2)
+    assert abs(tg - to) <= 1e-13 and fbo == 0
+    assert rel_err(Qg, Qo).max() <= TOL, rel_err(Qg, Qo)
 
 
 def test_conservation_and_free_stream_gpu(cuda_ok):
@@ -280,10 +321,20 @@ def test_cuda_graph_steps_match_eager(cuda_ok, monkeypatch):
 
 def test_c3_size_steps(cuda_ok):
     """configs[2] at the bench size (sphere shell N = 35, 514,500 hexes; NS tau, wall +
-    farfield) with the parity IC: an eager and a graph-replayed step, every cell vs the oracle."""
+    farfield) with the parity IC for 10 steps (eager step + graph replays), every cell vs
+    the oracle after the first and the tenth step."""
     mi, Q0, oc, gc = sphere_case(35, 0.2535, 118.0)
-    errs, _, _ = run_pair(mi, Q0, 2, ocfg=oc, gcfg=gc)
+    errs, _, _ = run_pair(mi, Q0, 2, ocfg=oc, gcfg=gc, chunks=(1, 9))
     assert errs.max() <= TOL, errs.max(axis=0)
+
+
+def test_c4_full_size_two_steps(cuda_ok):
+    """configs[3] at full size (sphere shell N = 70, 4,116,000 hexes, Ma 1.5, Re 300: the
+    supersonic farfield states) with the parity IC, 2 steps, every cell vs the oracle."""
+    mi, Q0, oc, gc = sphere_case(70, 1.5, 300.0)
+    Qg, tg, (Qo, to, _, fbo) = gpu_and_oracle(mi, Q0, gc, oc, 2)
+    assert abs(tg - to) <= 1e-13 * max(1.0, to)
+    assert rel_err(Qg, Qo).max() <= TOL, rel_err(Qg, Qo)
 
 
 @pytest.mark.parametrize("pair", ["0", "1"])
@@ -297,3 +348,48 @@ def test_recon_lane_pair_variant(cuda_ok, monkeypatch, pair):
     mi, Q0, oc, gc = sphere_case(4, 0.2535, 118.0)
     errs, _, _ = run_pair(mi, Q0, 5, ocfg=oc, gcfg=gc)
     assert errs.max() <= TOL, errs.max(axis=0)
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_dq0_readings_match_oracle(cuda_ok, mode):
+    """SURVEY Q9 readings of dQ0 (R9k kinetic weighting, R9s linear-weight gradients) in both
+    flux forms: C1 (tau = 0), the fallback stress state (NS tau, fallbacks > 0) and the sphere
+    shell (wall + farfield faces, NS tau); 10 steps each within the bar."""
+    mi = W.kuhn_box(6)
+    errs, _, _ = run_pair(mi, W.advection_ic(mi), 10, ocfg=O.OracleConfig(dq0_mode=mode),
+                          gcfg=hgks.SolverConfig(dq0_mode=mode))
+    assert errs.max() <= TOL, errs.max(axis=0)
+    oc, gc = ns_cfgs(mu=1e-3)
+    oc.dq0_mode = gc.dq0_mode = mode
+    errs, _, o = run_pair(mi, W.spike_state(mi), 10, ocfg=oc, gcfg=gc)
+    assert o.state()[3] > 0
+    assert errs.max() <= TOL, errs.max(axis=0)
+    mi, Q0, oc, gc = sphere_case(4, 0.2535, 118.0)
+    oc.dq0_mode = gc.dq0_mode = mode
+    errs, _, _ = run_pair(mi, Q0, 10, ocfg=oc, gcfg=gc)
+    assert errs.max() <= TOL, errs.max(axis=0)
+    mi = W.walled_hex_box(6, h=0.4, jitter=0.1)  # tau = 0 with wall faces
+    Q0 = W.random_smooth_ic(mi, seed=7, base=(1.0, 0.3, 0.2, -0.25, 1 / 1.4), amp=0.05)
+    errs, _, _ = run_pair(mi, Q0, 10, ocfg=O.OracleConfig(cfl=0.5, dq0_mode=mode),
+                          gcfg=hgks.SolverConfig(cfl=0.5, dq0_mode=mode))
+    assert errs.max() <= TOL, errs.max(axis=0)
+
+
+def test_prandtl_fix_matches_oracle(cuda_ok):
+    """R29 heat-flux correction at Pr = 0.72 (moment form): the C1s stress state with NS tau
+    and the sphere shell (wall + farfield, the viscous sphere of P:1203-1210) for 10 steps
+    within the bar; tau = 0 is unaffected by construction (checked on the oracle side)."""
+    mi = W.kuhn_box(6)
+    oc, gc = ns_cfgs(mu=1e-3)
+    oc.prandtl = gc.prandtl = 0.72
+    errs, _, _ = run_pair(mi, W.density_step_ic(mi), 10, ocfg=oc, gcfg=gc)
+    assert errs.max() <= TOL, errs.max(axis=0)
+    mi, Q0, oc, gc = sphere_case(4, 0.2535, 118.0)
+    oc.prandtl = gc.prandtl = 0.72
+    errs, g, _ = run_pair(mi, Q0, 10, ocfg=oc, gcfg=gc)
+    assert errs.max() <= TOL, errs.max(axis=0)
+    # the fix changes the solution (it is not a no-op on this viscous case)
+    oc1, gc1 = sphere_case(4, 0.2535, 118.0)[2:]
+    g1 = hgks.Solver(hgks.Mesh(mi), Q0, gc1)
+    g1.step(10)
+    assert np.abs(g1.get_state()[0] - g.get_state()[0]).max() > 1e-9

@@ -447,3 +447,39 @@ def test_farfield_state_characteristics():
             assert np.allclose(ub - unb * n, up_u - (up_u @ n) * n, atol=1e-12)
             assert abs(pb / rb ** g - up_p / up_rho ** g) < 1e-11 * (up_p / up_rho ** g)
     assert seen == {"out", "in", "sub"}, seen
+
+
+@pytest.mark.parametrize("pr", [0.72, 2.0 / 3.0])
+def test_prandtl_heat_flux_ratio(pr):
+    """R29 (Prandtl-number fix, energy flux += (1/Pr - 1) x heat flux of the non-equilibrium
+    part): a resting gas (rho = p = 1) with a normal temperature gradient at uniform pressure,
+    tau << dt (Navier-Stokes regime).  The BGK energy flux is the Chapman-Enskog heat flux
+    q = -c_p mu dT/dn with mu = tau p, c_p = gamma/(gamma - 1) (Fourier's law at Pr = 1, a
+    textbook result independent of the kinetic code), and with the fix it is q / Pr."""
+    g = 0.3                                   # dT/dn; rho = p / T, so d rho/dn = -g at T = 1
+    q = np.array([1.0, 0.0, 0.0, 0.0, 1.0 / (GAMMA - 1)])
+    dq = np.zeros((3, 5))
+    dq[0, 0] = -g
+    tau, dt = 1e-6, 1e-3
+    base = dict(tau_mode=1, c1=0.0, mu_inf=tau * 1.0, t_inf=1.0, mu_exp=0.7)
+    F1 = O.gp_flux(q, dq, q, dq, dt, O.OracleConfig(**base))["F"]
+    Fp = O.gp_flux(q, dq, q, dq, dt, O.OracleConfig(prandtl=pr, **base))["F"]
+    q_ce = -GAMMA / (GAMMA - 1) * (tau * 1.0) * g
+    assert abs(F1[4] / q_ce - 1) < 1e-3, (F1[4], q_ce)
+    assert abs(Fp[4] / F1[4] - 1 / pr) < 1e-3, (Fp[4] / F1[4], 1 / pr)
+    assert np.allclose(Fp[:4], F1[:4], rtol=0, atol=1e-15)   # only the energy flux changes
+
+
+def test_prandtl_fix_inactive_without_nonequilibrium():
+    """Uniform state (no gradients): f = g0, no heat flux, so Pr changes nothing; tau = 0:
+    the non-equilibrium part vanishes identically (R29)."""
+    rng = np.random.default_rng(11)
+    ql, dql, qr, dqr = random_gp(rng)
+    z = np.zeros((3, 5))
+    cfg = dict(tau_mode=1, c1=0.0, mu_inf=0.01, t_inf=1.0)
+    a = O.gp_flux(ql, z, ql, z, 0.05, O.OracleConfig(**cfg))
+    b = O.gp_flux(ql, z, ql, z, 0.05, O.OracleConfig(prandtl=0.72, **cfg))
+    assert np.allclose(a["F"], b["F"], rtol=1e-13) and np.allclose(a["dF"], b["dF"], rtol=1e-12, atol=1e-14)
+    a = O.gp_flux(ql, dql, qr, dqr, 0.05, O.OracleConfig())
+    b = O.gp_flux(ql, dql, qr, dqr, 0.05, O.OracleConfig(prandtl=0.72))
+    assert np.array_equal(a["F"], b["F"]) and np.array_equal(a["dF"], b["dF"])

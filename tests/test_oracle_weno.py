@@ -80,6 +80,29 @@ def test_quadratic_field_reproduced_by_p0():
         assert np.allclose(a, expect, atol=1e-9), (a, expect)
 
 
+def test_linear_weight_gradients_exact_for_quadratics():
+    """Reading R9s (dq0_mode 2): Eq. (weno) with gamma in place of omega-bar collapses to P_0
+    (SURVEY A.6), so on quadratic data its gradient is the exact gradient at any point,
+    while the nonlinear weights (power 1) mix in the sub-stencil slopes."""
+    mi = W.kuhn_box(8, jitter=0.1)
+    m = O.OracleMesh(mi)
+    lin = np.array([0.3, -0.2, 0.1])
+    quad = np.array([[0.5, 0.1, 0.0], [0.1, -0.3, 0.2], [0.0, 0.2, 0.4]])
+    q = poly_means(mi, lin, quad, 2.0)
+    Q = np.repeat(q[:, None], 5, axis=1)
+    V, c, _ = m.geometry()
+    rng = np.random.default_rng(3)
+    worst_nl = 0.0
+    for i in interior_cells(m, mi, 0.6)[:8]:
+        x = c[i] + rng.uniform(-0.1, 0.1, size=(4, 3))
+        exact = lin[None, :] + 2 * x @ quad
+        _, g_lin = m.weno_points(Q, i, x, linear=True)
+        _, g_nl = m.weno_points(Q, i, x)
+        assert np.abs(g_lin[:, 0] - exact).max() <= 1e-10
+        worst_nl = max(worst_nl, np.abs(g_nl[:, 0] - exact).max())
+    assert worst_nl > 1e-6
+
+
 def test_constant_field_zero_coefficients():
     mi = W.kuhn_box(5)
     m = O.OracleMesh(mi)
