@@ -303,7 +303,7 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1 and "OMP_NUM_THREADS" not in os.environ:
-        # every rank builds the global mesh on the host (OpenMP): share the cores
+        # every rank builds its own region of the mesh on the host (OpenMP): share the cores
         os.environ["OMP_NUM_THREADS"] = str(max(1, len(os.sched_getaffinity(0)) // world))
     import torch
     import torch.distributed as dist
@@ -330,7 +330,8 @@ def main():
         Q0 = W.uniform_state(mi.n_cells, 1.0, (ma, 0.0, 0.0), 1.0 / GAMMA, gamma=GAMMA)  # free-stream IC
         cfg = hgks.SolverConfig(gamma=GAMMA, cfl=0.5, tau_mode=1, mu_inf=ma / re, c1=1.0, t_inf=1.0 / GAMMA,
                                 freestream=fs, precision=args.precision)
-    mesh = hgks.Mesh(mi, n_ranks=world)
+    # one process per GPU: each builds only its own region (O(owned + ghosts) host setup)
+    mesh = hgks.Mesh(mi, n_ranks=world, rank=rank if world > 1 else None)
     nid = None
     if world > 1:
         obj = [hgks.nccl_unique_id() if rank == 0 else None]
@@ -469,7 +470,7 @@ def main():
             "config": {**config, "cells": int(cells),
                        "parallelism": f"domain decomposition x{world} (RCB, 3 ghost layers, "
                                       f"{'NVLink put' if world > 1 and args.transport == 'p2p' else 'NCCL'})",
-                       "l2": "no flush: per-step working set %.2f GB > 126 MB L2" % (mesh.workspace_size(cfg) / 1e9)},
+                       "l2": "no flush: per-step working set %.2f GB > 126 MB L2" % (mesh.workspace_size(cfg, rank) / 1e9)},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "steps": e2e_steps, "pipelined": True},
             "gpu_launches": launches, "roofline": roof, "rooflines": rooflines, "cpu_baseline": cpu, "clocks": clocks,

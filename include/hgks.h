@@ -68,6 +68,15 @@ typedef struct {
   int64_t n_bfaces;
   int32_t n_ranks;            /* >= 1; > 1 builds the k-way partition + 3 ghost layers */
   const int32_t* cell_part;   /* optional [n_cells] rank of every cell (external partition), or NULL */
+  int32_t rank_only;          /* 0: build the whole mesh and the plans of every rank (one process per
+                                 group: loopback, tests, tools); r + 1 (n_ranks > 1): build only rank
+                                 r's region -- its owned cells and four node layers around them --
+                                 so host memory and time are O(owned + ghosts) per process, apart from
+                                 one pass over the cell list (centroids, partition: 28 B per cell).
+                                 Calls for other ranks then fail with HGKS_E_ARG; edge_cut is -1
+                                 (rank_cut_faces of each rank sum to twice the global cut); the
+                                 partition is plain RCB (the boundary refinement needs the whole
+                                 face graph), so it may differ from a rank_only = 0 build. */
 } hgks_mesh_desc;
 
 /* Solver configuration (readings R4, R6, R7, R13, R14, R24). */
@@ -104,7 +113,7 @@ typedef struct {
 #define HGKS_TRANSPORT_P2P 2       /* one process per GPU on one node: halo by the fused put k_put
                                       into the peers' ghost rows over NVLink (CUDA IPC, per-stage
                                       epoch flags; hgks_p2p_export/connect), dt by NCCL allreduce */
-#define HGKS_P2P_HANDLE_BYTES 96
+#define HGKS_P2P_HANDLE_BYTES 448
 
 /* Distributed context. */
 typedef struct {
@@ -126,11 +135,13 @@ typedef struct {
   int32_t n_sub;             /* sub-stencils per cell (4 tet, 8 hex) */
   int32_t n_peers;           /* ranks this rank exchanges ghosts with */
   int64_t send_cells, recv_cells;    /* per stage */
-  int64_t edge_cut;          /* faces between different ranks (global; RCB + greedy boundary refinement) */
+  int64_t edge_cut;          /* faces between different ranks (global; RCB + FM boundary refinement);
+                                -1 for a rank_only build */
   int64_t n_early_cells;     /* owned cells reconstructed while the halo exchange is in flight */
   int64_t n_early_faces;     /* interior faces fluxed while the halo exchange is in flight */
   int64_t edge_cut_rcb;      /* faces between different ranks of the plain RCB partition, before the
                                 boundary refinement (equal to edge_cut for a caller partition) */
+  int64_t rank_cut_faces;    /* faces of this rank's owned cells whose neighbour another rank owns */
 } hgks_mesh_stats;
 
 typedef struct {

@@ -1260,7 +1260,7 @@ __device__ __forceinline__ void flux_tau0_interior(const FluxArgs& a, int lf, in
 #if HGKS_FLUX_STAGE
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncwarp();
-  const Real* rl = sw + (2 * (lane / NGP)) * kRec;
+  const Real* rl = sw + (2 * min(lane / NGP, FPW - 1)) * kRec;  // lanes past the last face: any record
   const Real* rr = rl + kRec;
 #else
   const Real* rl = a.ceff + (size_t)co * kRec;

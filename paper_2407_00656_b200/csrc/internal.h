@@ -62,6 +62,12 @@ struct GlobalMesh {
   //  setup.cpp cell_operators; there is no global table)
   // partition
   int32_t n_ranks = 1;
+  // region builds (one rank per process, hgks_mesh_desc.rank_only): cells are the rank's
+  // region in ascending global id, gid[k] = global id of region cell k
+  int32_t only_rank = -1;
+  int64_t nc_global = 0;
+  std::vector<int64_t> gid;
+  double bbox_lo[3] = {0, 0, 0}, bbox_hi[3] = {0, 0, 0};  // centroid bounding box of the WHOLE mesh
   std::vector<int32_t> part;
   int64_t edge_cut = 0;       // faces between different ranks (after refinement)
   int64_t edge_cut_rcb = 0;   // the same for the plain RCB partition (before refinement)
@@ -102,6 +108,7 @@ struct RankPlan {
   std::vector<int32_t> send_list;           // local owned ids, grouped by peer, global-id order
   std::vector<int64_t> recv_off, recv_cnt;  // local ghost range [recv_off, recv_off + recv_cnt)
   int32_t stencil_min = 0, stencil_max = 0;
+  int64_t rank_cut_faces = 0;  // faces of owned cells whose neighbour another rank owns
 };
 
 struct MeshDescCopy;
@@ -109,7 +116,7 @@ struct MeshDescCopy;
 GlobalMesh build_global_mesh(const double* xyz, int64_t n_nodes, const int8_t* type, const int64_t* cell_nodes,
                              int64_t n_cells, const double* per_origin, const double* per_len,
                              const int64_t* bface_nodes, const int32_t* bface_tag, int64_t n_bf, int32_t n_ranks,
-                             const int32_t* cell_part);
+                             const int32_t* cell_part, int32_t rank_only);
 RankPlan build_rank_plan(const GlobalMesh& gm, int rank);
 
 }  // namespace hgks

@@ -283,12 +283,15 @@ static void refine_partition(GlobalMesh& gm, int nfc) {
 }
 
 // ============================================================================
-GlobalMesh build_global_mesh(const double* xyz, int64_t n_nodes, const int8_t* type, const int64_t* cn,
-                             int64_t n_cells, const double* per_origin, const double* per_len,
-                             const int64_t* bface_nodes, const int32_t* bface_tag, int64_t n_bf, int32_t n_ranks,
-                             const int32_t* cell_part) {
-  GlobalMesh gm;
-  PhaseTimer pt("global mesh");
+// Geometry, faces, periodic pairing, boundary ghosts, neighbours and Alg. 1 stencils of a
+// mesh (the whole mesh, or one rank's region of it).  open_ok[i]: cell i may keep faces
+// without a partner (the outer rim of a region; such faces are left out); stencil_ok[i]:
+// build cell i's stencils (cells without them are never reconstructed).  NULL = every cell.
+static void build_core(GlobalMesh& gm, const double* xyz, int64_t n_nodes, const int8_t* type, const int64_t* cn,
+                       int64_t n_cells, const double* per_origin, const double* per_len,
+                       const int64_t* bface_nodes, const int32_t* bface_tag, int64_t n_bf,
+                       const std::vector<char>* open_ok, const std::vector<char>* stencil_ok) {
+  PhaseTimer pt("mesh core");
   if (n_cells <= 0 || n_nodes <= 0 || !xyz || !type || !cn) throw Error(1, "empty mesh");
   gm.nc = n_cells;
   gm.type.assign(type, type + n_cells);
@@ -399,8 +402,13 @@ GlobalMesh build_global_mesh(const double* xyz, int64_t n_nodes, const int8_t* t
   }
   // periodic pairing (R23): canonical wrapped vertex coordinates
   if (!unmatched.empty()) {
+    // (region rims of a non-periodic mesh: handled by the check below)
     double Lm = std::max(gm.per_len[0], std::max(gm.per_len[1], gm.per_len[2]));
-    if (!(Lm > 0)) throw Error(2, "open boundary face at cell " + std::to_string(unmatched[0] / nfc));
+    if (!(Lm > 0)) {
+      for (int64_t h : unmatched)
+        if (!open_ok || !(*open_ok)[h / nfc]) throw Error(2, "open boundary face at cell " + std::to_string(h / nfc));
+      unmatched.clear();
+    }
     const double tol = 1e-7 * Lm;
     struct PK {
       std::array<int64_t, 12> k;
@@ -430,8 +438,14 @@ GlobalMesh build_global_mesh(const double* xyz, int64_t n_nodes, const int8_t* t
     }
     std::sort(pk.begin(), pk.end(), [](const PK& a, const PK& b) { return a.k != b.k ? a.k < b.k : a.h < b.h; });
     for (size_t u = 0; u < pk.size(); u += 2) {
-      if (u + 1 >= pk.size() || pk[u].k != pk[u + 1].k || (u + 2 < pk.size() && pk[u + 2].k == pk[u].k))
+      if (u + 1 >= pk.size() || pk[u].k != pk[u + 1].k || (u + 2 < pk.size() && pk[u + 2].k == pk[u].k)) {
+        // a region's rim: the partner lies outside the region (left open)
+        if (open_ok && (*open_ok)[pk[u].h / nfc] && (u + 1 >= pk.size() || pk[u].k != pk[u + 1].k)) {
+          --u;
+          continue;
+        }
         throw Error(2, "unmatched boundary face at cell " + std::to_string(pk[u].h / nfc));
+      }
       int64_t ha = pk[u].h, hb = pk[u + 1].h;
       if (hb / nfc < ha / nfc) std::swap(ha, hb);
       if (ha / nfc == hb / nfc) throw Error(2, "self-periodic cell " + std::to_string(ha / nfc));
@@ -499,7 +513,8 @@ GlobalMesh build_global_mesh(const double* xyz, int64_t n_nodes, const int8_t* t
   }
   for (int64_t i = 0; i < n_cells; ++i)
     for (int p = 0; p < nfc; ++p)
-      if (gm.cell_face[i * 6 + p] < 0) throw Error(2, "open face at cell " + std::to_string(i));
+      if (gm.cell_face[i * 6 + p] < 0 && !(open_ok && (*open_ok)[i]))
+        throw Error(2, "open face at cell " + std::to_string(i));
   pt.lap("faces + periodic pairing");
   // ---------------- boundary ghosts (R25) ----------------
   for (int64_t f = 0; f < gm.nf; ++f) {
@@ -550,6 +565,7 @@ GlobalMesh build_global_mesh(const double* xyz, int64_t n_nodes, const int8_t* t
     double smax = 0;
     for (int p = 0; p < nfc; ++p) {
       int64_t f = gm.cell_face[i * 6 + p];
+      if (f < 0) continue;  // region rim (open_ok): no neighbour, never used
       smax = std::max(smax, gm.f_area[f]);
       double sg = 1.0;
       int64_t other;
@@ -565,7 +581,7 @@ GlobalMesh build_global_mesh(const double* xyz, int64_t n_nodes, const int8_t* t
       gm.nbr_id[i * 6 + p] = other;
       for (int a = 0; a < 3; ++a) gm.nbr_shift[i * 18 + p * 3 + a] = sg * gm.f_shift[3 * f + a];
     }
-    gm.h_dt[i] = gm.V[i] / smax;
+    gm.h_dt[i] = smax > 0 ? gm.V[i] / smax : 0.0;
   }
   pt.lap("neighbours, h");
   // ---------------- Alg. 1 stencils + sub-stencils ----------------
@@ -578,6 +594,7 @@ GlobalMesh build_global_mesh(const double* xyz, int64_t n_nodes, const int8_t* t
   int bad_code = 0;
 #pragma omp parallel for schedule(dynamic, 256) reduction(max : max_k)
   for (int64_t i = 0; i < n_cells; ++i) {
+    if (stencil_ok && !(*stencil_ok)[i]) continue;
     std::vector<Member>& S = big[i];
     int err = 0;
     auto add = [&](int64_t id, P3 s) {
@@ -672,8 +689,200 @@ GlobalMesh build_global_mesh(const double* xyz, int64_t n_nodes, const int8_t* t
       }
   }
   pt.lap("stencils");
-  // least-squares operators (a2) are built per rank for the cells it reconstructs
-  // (cell_operators, called from build_rank_plan): no global [nc][E] table
+}
+
+// recursive coordinate bisection on centroids C [n][3] (P:730-739 objective: balance,
+// small interfaces); splits proportional to the rank counts on each side
+static void rcb_partition(const double* C, int64_t n, int nr, int32_t* part) {
+  std::vector<int64_t> ids(n);
+  std::iota(ids.begin(), ids.end(), 0);
+  struct Task {
+    int64_t b, e;
+    int r0, nr;
+  };
+  std::vector<Task> st{{0, n, 0, nr}};
+  while (!st.empty()) {
+    Task t = st.back();
+    st.pop_back();
+    if (t.nr == 1) {
+      for (int64_t k = t.b; k < t.e; ++k) part[ids[k]] = t.r0;
+      continue;
+    }
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (int64_t k = t.b; k < t.e; ++k)
+      for (int a = 0; a < 3; ++a) {
+        lo[a] = std::min(lo[a], C[3 * ids[k] + a]);
+        hi[a] = std::max(hi[a], C[3 * ids[k] + a]);
+      }
+    int ax = 0;
+    for (int a = 1; a < 3; ++a)
+      if (hi[a] - lo[a] > hi[ax] - lo[ax] + 1e-12) ax = a;
+    int nl = t.nr / 2;
+    int64_t cut = t.b + (t.e - t.b) * nl / t.nr;
+    std::nth_element(ids.begin() + t.b, ids.begin() + cut, ids.begin() + t.e, [&](int64_t a, int64_t b) {
+      double xa = C[3 * a + ax], xb = C[3 * b + ax];
+      return xa != xb ? xa < xb : a < b;
+    });
+    st.push_back({t.b, cut, t.r0, nl});
+    st.push_back({cut, t.e, t.r0 + nl, t.nr - nl});
+  }
+}
+
+static void check_cells(const int8_t* type, const int64_t* cn, int64_t n_cells, int64_t n_nodes) {
+  const int ct = type[0];
+  if (ct != 4 && ct != 8) throw Error(2, "unsupported element at cell 0");
+  for (int64_t i = 0; i < n_cells; ++i) {
+    if (type[i] != ct) throw Error(2, "mixed element kinds are not supported (cell " + std::to_string(i) + ")");
+    for (int k = 0; k < ct; ++k) {
+      int64_t v = cn[i * 8 + k];
+      if (v < 0 || v >= n_nodes) throw Error(2, "invalid node id in cell " + std::to_string(i));
+    }
+  }
+}
+
+static void centroid_bbox(GlobalMesh& gm, const double* C, int64_t n) {
+  for (int a = 0; a < 3; ++a) {
+    gm.bbox_lo[a] = 1e300;
+    gm.bbox_hi[a] = -1e300;
+  }
+  for (int64_t i = 0; i < n; ++i)
+    for (int a = 0; a < 3; ++a) {
+      gm.bbox_lo[a] = std::min(gm.bbox_lo[a], C[3 * i + a]);
+      gm.bbox_hi[a] = std::max(gm.bbox_hi[a], C[3 * i + a]);
+    }
+}
+
+// One rank's region of a partitioned mesh (rank_only > 0): the rank's owned cells and every
+// cell within four node-adjacency layers of them (a superset of the 3 face-adjacency ghost
+// layers, and of their face partners), found by streaming passes over the cell
+// list with a bitmap of (periodically identified) nodes.  Host memory is O(region): the
+// only per-global-cell arrays are the centroids and the partition (28 bytes per cell).
+static GlobalMesh build_region(const double* xyz, int64_t n_nodes, const int8_t* type, const int64_t* cn,
+                               int64_t n_cells, const double* per_origin, const double* per_len,
+                               const int64_t* bface_nodes, const int32_t* bface_tag, int64_t n_bf, int32_t n_ranks,
+                               const int32_t* cell_part, int rank) {
+  PhaseTimer pt("region");
+  const int ct = type[0];
+  // centroids of every cell (the partition input), the same numbers as the whole-mesh build
+  std::vector<double> C(3 * n_cells);
+  std::vector<int32_t> part(n_cells, 0);
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n_cells; ++i) {
+    P3 v[8];
+    for (int k = 0; k < ct; ++k) v[k] = {xyz[3 * cn[i * 8 + k]], xyz[3 * cn[i * 8 + k] + 1], xyz[3 * cn[i * 8 + k] + 2]};
+    double V, m2[6];
+    P3 c;
+    if (ct == 4) tet_geometry(v, V, c, m2);
+    else hex_geometry(v, V, c, m2);
+    C[3 * i] = c.x; C[3 * i + 1] = c.y; C[3 * i + 2] = c.z;
+  }
+  GlobalMesh gm;
+  centroid_bbox(gm, C.data(), n_cells);
+  if (cell_part) {
+    for (int64_t i = 0; i < n_cells; ++i) {
+      if (cell_part[i] < 0 || cell_part[i] >= n_ranks) throw Error(1, "cell_part out of range at cell " + std::to_string(i));
+      part[i] = cell_part[i];
+    }
+  } else {
+    rcb_partition(C.data(), n_cells, n_ranks, part.data());
+  }
+  pt.lap("centroids + partition");
+  // periodically identified node ids: wrapped coordinates quantised (R23)
+  std::vector<int64_t> canon(n_nodes);
+  {
+    double Lm = std::max(per_len ? per_len[0] : 0.0, std::max(per_len ? per_len[1] : 0.0, per_len ? per_len[2] : 0.0));
+    if (!(Lm > 0)) {
+      std::iota(canon.begin(), canon.end(), 0);
+    } else {
+      const double tol = 1e-7 * Lm;
+      std::vector<std::pair<std::array<int64_t, 3>, int64_t>> key(n_nodes);
+#pragma omp parallel for schedule(static)
+      for (int64_t nd = 0; nd < n_nodes; ++nd) {
+        std::array<int64_t, 3> q;
+        for (int a = 0; a < 3; ++a) {
+          double y = xyz[3 * nd + a] - (per_origin ? per_origin[a] : 0.0);
+          if (per_len[a] > 0) {
+            y -= per_len[a] * std::floor(y / per_len[a]);
+            if (per_len[a] - y < tol) y = 0.0;
+          }
+          q[a] = (int64_t)std::llround(y / tol);
+        }
+        key[nd] = {q, nd};
+      }
+      std::sort(key.begin(), key.end());
+      int64_t id = -1;
+      for (int64_t k = 0; k < n_nodes; ++k) {
+        if (k == 0 || key[k].first != key[k - 1].first) id = key[k].second;
+        canon[key[k].second] = id;
+      }
+    }
+  }
+  // region: owned cells, then four node-adjacency layers
+  std::vector<int8_t> lay(n_cells, -1);
+  for (int64_t i = 0; i < n_cells; ++i)
+    if (part[i] == rank) lay[i] = 0;
+  std::vector<char> mark(n_nodes, 0);
+  for (int l = 1; l <= 4; ++l) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n_cells; ++i)
+      if (lay[i] == l - 1)
+        for (int k = 0; k < ct; ++k) mark[canon[cn[i * 8 + k]]] = 1;
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n_cells; ++i) {
+      if (lay[i] >= 0) continue;
+      for (int k = 0; k < ct; ++k)
+        if (mark[canon[cn[i * 8 + k]]]) {
+          lay[i] = (int8_t)l;
+          break;
+        }
+    }
+  }
+  std::vector<int64_t> R;
+  for (int64_t i = 0; i < n_cells; ++i)
+    if (lay[i] >= 0) R.push_back(i);
+  if (R.empty() || std::none_of(R.begin(), R.end(), [&](int64_t i) { return lay[i] == 0; }))
+    throw Error(1, "rank " + std::to_string(rank) + " owns no cells");
+  pt.lap("region (4 node layers)");
+  const int64_t nr = (int64_t)R.size();
+  std::vector<int64_t> sub_cn((size_t)nr * 8);
+  std::vector<int8_t> sub_type(nr);
+  std::vector<char> open_ok(nr), stencil_ok(nr);
+  for (int64_t k = 0; k < nr; ++k) {
+    std::memcpy(&sub_cn[8 * k], cn + 8 * R[k], 8 * sizeof(int64_t));
+    sub_type[k] = type[R[k]];
+    open_ok[k] = lay[R[k]] == 4;       // every face of layers <= 3 has its partner in the region
+    stencil_ok[k] = lay[R[k]] <= 1;    // owned + face layer 1 (reconstructed cells)
+  }
+  build_core(gm, xyz, n_nodes, sub_type.data(), sub_cn.data(), nr, per_origin, per_len, bface_nodes, bface_tag,
+             n_bf, &open_ok, &stencil_ok);
+  gm.gid = R;
+  gm.nc_global = n_cells;
+  gm.n_ranks = n_ranks;
+  gm.only_rank = rank;
+  gm.part.resize(nr);
+  for (int64_t k = 0; k < nr; ++k) gm.part[k] = part[R[k]];
+  gm.edge_cut = -1;  // global cut unknown in a region build; rank_cut_faces in the plan
+  pt.lap("region mesh");
+  return gm;
+}
+
+GlobalMesh build_global_mesh(const double* xyz, int64_t n_nodes, const int8_t* type, const int64_t* cn,
+                             int64_t n_cells, const double* per_origin, const double* per_len,
+                             const int64_t* bface_nodes, const int32_t* bface_tag, int64_t n_bf, int32_t n_ranks,
+                             const int32_t* cell_part, int32_t rank_only) {
+  if (n_cells <= 0 || n_nodes <= 0 || !xyz || !type || !cn) throw Error(1, "empty mesh");
+  check_cells(type, cn, n_cells, n_nodes);
+  if (n_ranks > 1 && rank_only > 0) {
+    if (rank_only > n_ranks) throw Error(1, "rank_only out of range");
+    return build_region(xyz, n_nodes, type, cn, n_cells, per_origin, per_len, bface_nodes, bface_tag, n_bf, n_ranks,
+                        cell_part, rank_only - 1);
+  }
+  GlobalMesh gm;
+  PhaseTimer pt("global mesh");
+  build_core(gm, xyz, n_nodes, type, cn, n_cells, per_origin, per_len, bface_nodes, bface_tag, n_bf, nullptr, nullptr);
+  gm.nc_global = n_cells;
+  centroid_bbox(gm, gm.C.data(), n_cells);
+  const int nfc = gm.lay.nfaces;
   // ---------------- partition (a3) ----------------
   gm.n_ranks = std::max(1, n_ranks);
   gm.part.assign(n_cells, 0);
@@ -684,42 +893,7 @@ GlobalMesh build_global_mesh(const double* xyz, int64_t n_nodes, const int8_t* t
         gm.part[i] = cell_part[i];
       }
     } else {
-      // recursive coordinate bisection on centroids (P:730-739 objective: balance,
-      // small interfaces); splits proportional to the rank counts on each side
-      std::vector<int64_t> ids(n_cells);
-      std::iota(ids.begin(), ids.end(), 0);
-      struct Task {
-        int64_t b, e;
-        int r0, nr;
-      };
-      std::vector<Task> st{{0, n_cells, 0, gm.n_ranks}};
-      while (!st.empty()) {
-        Task t = st.back();
-        st.pop_back();
-        if (t.nr == 1) {
-          for (int64_t k = t.b; k < t.e; ++k) gm.part[ids[k]] = t.r0;
-          continue;
-        }
-        double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-        for (int64_t k = t.b; k < t.e; ++k)
-          for (int a = 0; a < 3; ++a) {
-            lo[a] = std::min(lo[a], gm.C[3 * ids[k] + a]);
-            hi[a] = std::max(hi[a], gm.C[3 * ids[k] + a]);
-          }
-        int ax = 0;
-        for (int a = 1; a < 3; ++a)
-          if (hi[a] - lo[a] > hi[ax] - lo[ax] + 1e-12) ax = a;
-        int nl = t.nr / 2;
-        int64_t cut = t.b + (t.e - t.b) * nl / t.nr;
-        std::nth_element(ids.begin() + t.b, ids.begin() + cut, ids.begin() + t.e, [&](int64_t a, int64_t b) {
-          double xa = gm.C[3 * a + ax], xb = gm.C[3 * b + ax];
-          return xa != xb ? xa < xb : a < b;
-        });
-        st.push_back({t.b, cut, t.r0, nl});
-        st.push_back({cut, t.e, t.r0 + nl, t.nr - nl});
-      }
-    }
-    if (!cell_part) {
+      rcb_partition(gm.C.data(), n_cells, gm.n_ranks, gm.part.data());
       auto cut = [&] {
         int64_t c = 0;
         for (int64_t f = 0; f < gm.nf; ++f)
@@ -813,13 +987,11 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
   for (int64_t i = 0; i < nc; ++i)
     if (gm.part[i] == rank) owned.push_back(i);
   if (owned.empty()) throw Error(1, "rank " + std::to_string(rank) + " owns no cells");
+  if (gm.only_rank >= 0 && rank != gm.only_rank)
+    throw Error(1, "this mesh holds rank " + std::to_string(gm.only_rank) + "'s region only");
   // Morton order over the global bounding box of centroids
-  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-  for (int64_t i = 0; i < nc; ++i)
-    for (int a = 0; a < 3; ++a) {
-      lo[a] = std::min(lo[a], gm.C[3 * i + a]);
-      hi[a] = std::max(hi[a], gm.C[3 * i + a]);
-    }
+  const double* lo = gm.bbox_lo;
+  const double* hi = gm.bbox_hi;
   auto morton = [&](int64_t i) {
     uint64_t k = 0;
     for (int a = 0; a < 3; ++a) {
@@ -844,7 +1016,7 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
     for (int64_t i : frontier)
       for (int p = 0; p < L.nfaces; ++p) {
         int64_t j = gm.nbr_id[i * 6 + p];
-        if (j < nc && layer[j] < 0) {
+        if (j >= 0 && j < nc && layer[j] < 0) {
           layer[j] = (int8_t)l;
           next.push_back(j);
         }
@@ -1098,7 +1270,7 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
         for (int64_t i : fr)
           for (int p = 0; p < L.nfaces; ++p) {
             int64_t j = gm.nbr_id[i * 6 + p];
-            if (j < nc && lay[j] < 0) {
+            if (j >= 0 && j < nc && lay[j] < 0) {
               lay[j] = (int8_t)l;
               nx.push_back(j);
             }
@@ -1128,6 +1300,15 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
       rp.recv_cnt.push_back(cnt);
     }
   }
+  // faces of owned cells whose other side another rank owns (this rank's share of the cut)
+  for (int64_t r = 0; r < rp.n_owned; ++r)
+    for (int p = 0; p < L.nfaces; ++p) {
+      const int64_t j = gm.nbr_id[owned[r] * 6 + p];
+      if (j >= 0 && j < nc && gm.part[j] != rank) ++rp.rank_cut_faces;
+    }
+  // region builds index cells by position in the region: report global ids
+  if (!gm.gid.empty())
+    for (auto& id : rp.l2g) id = gm.gid[id];
   pt.lap("update arrays, plans");
   return rp;
 }

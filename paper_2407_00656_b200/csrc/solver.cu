@@ -495,27 +495,60 @@ void exchange(hgks_solver* s, void* Q) {
 // rows straight into the receivers' ghost rows (replaces k_pack + one device copy per
 // peer pair).  The (receiver, row) map comes from the two ranks' plans (recv_off of the
 // receiver's range for this sender + position in the sender's range for that peer).
-// (receiver rank, receiver row) of every send row of rank q, from the two ranks' plans
-std::vector<int2> put_map(hgks_mesh* m, int q) {
-  const RankPlan& rq = m->plan(q);
+// What a sender needs to know about a receiver: where the receiver keeps the ghost rows
+// each of its peers sends (its recv_off / recv_cnt per peer).
+struct RecvTab {
+  int32_t n = 0;
+  int32_t peer[kMaxGroup];
+  int64_t off[kMaxGroup], cnt[kMaxGroup];
+};
+RecvTab recv_tab(const RankPlan& rp) {
+  RecvTab t;
+  if (rp.peers.size() > (size_t)kMaxGroup) throw Error(HGKS_E_ARG, "more than 16 exchange peers");
+  for (size_t k = 0; k < rp.peers.size(); ++k) {
+    t.peer[t.n] = rp.peers[k];
+    t.off[t.n] = rp.recv_off[k];
+    t.cnt[t.n++] = rp.recv_cnt[k];
+  }
+  return t;
+}
+
+// (receiver rank, receiver row) of every send row of rank q: the k-th row q sends to p lands
+// at p's recv_off for q plus k (both sides order these cells by global id)
+template <class TabOf>
+std::vector<int2> put_map(const RankPlan& rq, int q, TabOf&& tab_of) {
   std::vector<int2> dst(rq.send_list.size(), int2{-1, -1});
   for (size_t ip = 0; ip < rq.peers.size(); ++ip) {
     if (rq.send_cnt[ip] == 0) continue;
     const int p = rq.peers[ip];
-    const RankPlan& rpp = m->plan(p);
-    const size_t iq = std::find(rpp.peers.begin(), rpp.peers.end(), q) - rpp.peers.begin();
-    if (iq == rpp.peers.size() || rpp.recv_cnt[iq] != rq.send_cnt[ip])
+    const RecvTab& tp = tab_of(p);
+    int iq = 0;
+    while (iq < tp.n && tp.peer[iq] != q) ++iq;
+    if (iq == tp.n || tp.cnt[iq] != rq.send_cnt[ip])
       throw Error(HGKS_E_STATE, "inconsistent exchange plans between ranks");
-    for (int64_t k = 0; k < rq.send_cnt[ip]; ++k) dst[rq.send_off[ip] + k] = int2{p, (int)(rpp.recv_off[iq] + k)};
+    for (int64_t k = 0; k < rq.send_cnt[ip]; ++k) dst[rq.send_off[ip] + k] = int2{p, (int)(tp.off[iq] + k)};
   }
   return dst;
 }
 
+// the put map of rank q from the plans of one mesh object (whole-mesh builds)
+std::vector<int2> put_map_mesh(hgks_mesh* m, int q) {
+  std::map<int, RecvTab> tabs;
+  return put_map(m->plan(q), q, [&](int p) -> const RecvTab& {
+    auto it = tabs.find(p);
+    if (it == tabs.end()) it = tabs.emplace(p, recv_tab(m->plan(p))).first;
+    return it->second;
+  });
+}
+
+// loopback group: each solver's own plan (its mesh may be a region build)
 void build_put_map(hgks_solver* const* ss, int n) {
+  std::vector<RecvTab> tabs(n);
+  for (int p = 0; p < n; ++p) tabs[p] = recv_tab(*ss[p]->rp);
   for (int q = 0; q < n; ++q) {
     hgks_solver* s = ss[q];
     if (s->put_ready) continue;
-    std::vector<int2> dst = put_map(s->mesh, q);
+    std::vector<int2> dst = put_map(*s->rp, q, [&](int p) -> const RecvTab& { return tabs[p]; });
     if (!dst.empty())
       CUDA_TRY(cudaMemcpy(s->d.put_dst, dst.data(), dst.size() * sizeof(int2), cudaMemcpyHostToDevice));
     s->put_ready = true;
@@ -742,7 +775,8 @@ hgks_status hgks_mesh_create(const hgks_mesh_desc* d, hgks_mesh** out) {
     if (!d || !out) throw Error(HGKS_E_ARG, "null argument");
     auto m = std::make_unique<hgks_mesh>();
     m->gm = build_global_mesh(d->xyz, d->n_nodes, d->cell_type, d->cell_nodes, d->n_cells, d->periodic_origin,
-                              d->periodic_length, d->bface_nodes, d->bface_tag, d->n_bfaces, d->n_ranks, d->cell_part);
+                              d->periodic_length, d->bface_nodes, d->bface_tag, d->n_bfaces, d->n_ranks, d->cell_part,
+                              d->rank_only);
     *out = m.release();
   });
 }
@@ -758,7 +792,7 @@ hgks_status hgks_mesh_info(const hgks_mesh* mc, int32_t rank, hgks_mesh_stats* s
     hgks_mesh* m = const_cast<hgks_mesh*>(mc);
     const RankPlan& rp = m->plan(rank);
     std::memset(st, 0, sizeof(*st));
-    st->n_cells_global = m->gm.nc;
+    st->n_cells_global = m->gm.nc_global;
     st->n_owned = rp.n_owned;
     st->n_ghost = rp.n_pghost;
     for (int k = 0; k < 3; ++k) st->ghost_layer[k] = rp.ghost_layer[k];
@@ -773,6 +807,7 @@ hgks_status hgks_mesh_info(const hgks_mesh* mc, int32_t rank, hgks_mesh_stats* s
     for (auto c : rp.recv_cnt) st->recv_cells += c;
     st->edge_cut = m->gm.edge_cut;
     st->edge_cut_rcb = m->gm.edge_cut_rcb ? m->gm.edge_cut_rcb : m->gm.edge_cut;
+    st->rank_cut_faces = rp.rank_cut_faces;
     st->n_early_cells = rp.n_recon_early;
     st->n_early_faces = rp.n_if_early;
   });
@@ -1359,7 +1394,9 @@ struct P2PBlob {  // HGKS_P2P_HANDLE_BYTES
   cudaIpcMemHandle_t mem;  // the allocation holding this rank's workspace
   uint64_t off_Q, off_flags;  // byte offsets of Q and the flags from the allocation base
   int32_t rank, device;
-  uint8_t pad[8];
+  char bus_id[16];         // PCI bus id of the device (unique across processes, unlike the ordinal)
+  RecvTab recv;            // where this rank keeps each peer's ghost rows (the senders' put map)
+  uint8_t pad[HGKS_P2P_HANDLE_BYTES - sizeof(cudaIpcMemHandle_t) - 16 - 8 - 16 - sizeof(RecvTab)];
 };
 static_assert(sizeof(P2PBlob) == HGKS_P2P_HANDLE_BYTES, "blob size");
 
@@ -1390,6 +1427,8 @@ hgks_status hgks_p2p_export(const hgks_solver* s, uint8_t* out) {
     b.off_flags = (uint64_t)((char*)s->d.flags - base);
     b.rank = s->rank;
     b.device = s->device;
+    CUDA_TRY(cudaDeviceGetPCIBusId(b.bus_id, (int)sizeof(b.bus_id), s->device));
+    b.recv = recv_tab(*s->rp);
     std::memcpy(out, &b, sizeof(b));
   });
 }
@@ -1401,7 +1440,12 @@ hgks_status hgks_p2p_connect(hgks_solver* s, const uint8_t* blobs) {
     if (s->p2p_ready) throw Error(HGKS_E_STATE, "already connected");
     CUDA_TRY(cudaSetDevice(s->device));
     const RankPlan& rp = *s->rp;
-    std::vector<int2> dst = put_map(s->mesh, s->rank);
+    // the receivers' ghost ranges come with their blobs: no peer plan is built here
+    std::vector<P2PBlob> all_blobs(s->n_ranks);
+    for (int p = 0; p < s->n_ranks; ++p) std::memcpy(&all_blobs[p], blobs + (size_t)p * HGKS_P2P_HANDLE_BYTES, sizeof(P2PBlob));
+    std::vector<int2> dst = put_map(rp, s->rank, [&](int p) -> const RecvTab& { return all_blobs[p].recv; });
+    char my_bus[16];
+    CUDA_TRY(cudaDeviceGetPCIBusId(my_bus, (int)sizeof(my_bus), s->device));
     std::vector<int> to;
     for (const int2& d : dst) to.push_back(d.x);
     std::sort(to.begin(), to.end());
@@ -1417,7 +1461,14 @@ hgks_status hgks_p2p_connect(hgks_solver* s, const uint8_t* blobs) {
       P2PBlob b;
       std::memcpy(&b, blobs + (size_t)p * HGKS_P2P_HANDLE_BYTES, sizeof(b));
       if (b.rank != p) throw Error(HGKS_E_ARG, "blob " + std::to_string(p) + " belongs to rank " + std::to_string(b.rank));
-      if (b.device == s->device) throw Error(HGKS_E_ARG, "HGKS_TRANSPORT_P2P needs one GPU per rank");
+      if (std::strncmp(b.bus_id, my_bus, sizeof(my_bus)) == 0)
+        throw Error(HGKS_E_ARG, "HGKS_TRANSPORT_P2P needs one GPU per rank (rank " + std::to_string(p) +
+                                    " is on this rank's device " + std::string(my_bus) + ")");
+      int peer_dev = -1, can = 0;
+      if (cudaDeviceGetByPCIBusId(&peer_dev, b.bus_id) == cudaSuccess) {
+        CUDA_TRY(cudaDeviceCanAccessPeer(&can, s->device, peer_dev));
+        if (!can) throw Error(HGKS_E_ARG, "no peer access from " + std::string(my_bus) + " to " + b.bus_id);
+      }
       void* base = nullptr;
       CUDA_TRY(cudaIpcOpenMemHandle(&base, b.mem, cudaIpcMemLazyEnablePeerAccess));
       s->peer_base[p] = base;
@@ -1436,7 +1487,7 @@ hgks_status hgks_mesh_put_map(const hgks_mesh* mc, int32_t rank, int32_t* recv_r
   return guard([&] {
     if (!mc || !recv_rank || !recv_row) throw Error(HGKS_E_ARG, "null argument");
     hgks_mesh* m = const_cast<hgks_mesh*>(mc);
-    const std::vector<int2> dst = put_map(m, rank);
+    const std::vector<int2> dst = put_map_mesh(m, rank);
     for (size_t j = 0; j < dst.size(); ++j) {
       recv_rank[j] = dst[j].x;
       recv_row[j] = dst[j].y;

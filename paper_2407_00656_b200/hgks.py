@@ -31,14 +31,14 @@ EXPORTS = ["hgks_mesh_create", "hgks_mesh_destroy", "hgks_mesh_info", "hgks_work
            "hgks_set_profiling", "hgks_kernel_times", "hgks_launch_count", "hgks_nccl_unique_id", "hgks_nccl_selftest", "hgks_group_step", "hgks_mesh_plan", "hgks_mesh_put_map", "hgks_p2p_export", "hgks_p2p_connect", "hgks_p2p_selftest",
            "hgks_last_error", "hgks_version"]
 TRANSPORT_NCCL, TRANSPORT_LOOPBACK, TRANSPORT_P2P = 0, 1, 2
-P2P_HANDLE_BYTES = 96
+P2P_HANDLE_BYTES = 448
 
 
 class MeshDesc(C.Structure):
     _fields_ = [("xyz", _dp), ("n_nodes", C.c_int64), ("cell_type", _i8p), ("cell_nodes", _i64p),
                 ("n_cells", C.c_int64), ("periodic_origin", C.c_double * 3), ("periodic_length", C.c_double * 3),
                 ("bface_nodes", _i64p), ("bface_tag", _i32p), ("n_bfaces", C.c_int64), ("n_ranks", C.c_int32),
-                ("cell_part", _i32p)]
+                ("cell_part", _i32p), ("rank_only", C.c_int32)]
 
 
 class Config(C.Structure):
@@ -59,7 +59,7 @@ class MeshStats(C.Structure):
                 ("n_faces_bc", C.c_int64), ("stencil_min", C.c_int32), ("stencil_max", C.c_int32),
                 ("n_sub", C.c_int32), ("n_peers", C.c_int32), ("send_cells", C.c_int64), ("recv_cells", C.c_int64),
                 ("edge_cut", C.c_int64), ("n_early_cells", C.c_int64), ("n_early_faces", C.c_int64),
-                ("edge_cut_rcb", C.c_int64)]
+                ("edge_cut_rcb", C.c_int64), ("rank_cut_faces", C.c_int64)]
 
     def as_dict(self):
         d = {}
@@ -174,7 +174,9 @@ def nccl_unique_id() -> bytes:
 class Mesh:
     """hgks_mesh: host setup (geometry, faces, stencils, LSQ operators, partition)."""
 
-    def __init__(self, mi, n_ranks: int = 1, cell_part=None):
+    def __init__(self, mi, n_ranks: int = 1, cell_part=None, rank: int | None = None):
+        """rank: build only that rank's region (one process per GPU; O(owned + ghosts) host
+        memory); None: the whole mesh and every rank's plan."""
         L = lib()
         self._keep = [np.ascontiguousarray(mi.xyz, np.float64), np.ascontiguousarray(mi.cell_type, np.int8),
                       np.ascontiguousarray(mi.cell_nodes, np.int64),
@@ -188,7 +190,7 @@ class Mesh:
         d = MeshDesc(_p(xyz), xyz.shape[0], _p(ct, _i8p), _p(cn, _i64p), cn.shape[0],
                      (C.c_double * 3)(*mi.periodic_origin), (C.c_double * 3)(*mi.periodic_length),
                      _p(bf, _i64p), _p(bt, _i32p), bf.shape[0], n_ranks,
-                     _p(part, _i32p) if part is not None else None)
+                     _p(part, _i32p) if part is not None else None, 0 if rank is None else rank + 1)
         h = C.c_void_p()
         _check(L.hgks_mesh_create(C.byref(d), C.byref(h)))
         self.h = h

@@ -35,12 +35,30 @@ def make_mesh(kind):
     return W.sphere_shell(4)
 
 
-def _worker(rank, world, port, kind, out_q):
+def put_map_from_tables(plan, rank, tables):
+    """The fused-put destinations of rank's send rows from the receivers' (peers, recv_off,
+    recv_cnt) tables -- what hgks_p2p_connect does with the tables in the P2P blobs."""
+    rr = np.full(plan["send_list"].size, -1, np.int32)
+    row = np.full(plan["send_list"].size, -1, np.int32)
+    for p, peer in enumerate(plan["peers"]):
+        so, sc = int(plan["send_off"][p]), int(plan["send_cnt"][p])
+        if not sc:
+            continue
+        peers_p, off_p, cnt_p = tables[int(peer)]
+        k = list(peers_p).index(rank)
+        assert cnt_p[k] == sc
+        rr[so:so + sc] = peer
+        row[so:so + sc] = off_p[k] + np.arange(sc)
+    return rr, row
+
+
+def _worker(rank, world, port, kind, out_q, region=False):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=world)
         mi = make_mesh(kind)
-        mesh = hgks.Mesh(mi, n_ranks=world)
+        # region=True: this process builds only its own region (hgks_mesh_desc.rank_only)
+        mesh = hgks.Mesh(mi, n_ranks=world, rank=rank if region else None)
         plan = mesh.plan(rank)
         n_owned = plan["n_owned"]
         l2g = plan["l2g"]
@@ -72,7 +90,12 @@ def _worker(rank, world, port, kind, out_q):
         ghosts_ok = bool(np.array_equal(Q.T, Qg[l2g]))
         # fused put (f3): each send row goes to (receiver, ghost row) from hgks_mesh_put_map;
         # emulated as one (rows, values) message per receiver, scattered by the receiver
-        rr, row = mesh.put_map(rank)
+        if region:
+            tables = [None] * world
+            dist.all_gather_object(tables, (plan["peers"], plan["recv_off"], plan["recv_cnt"]))
+            rr, row = put_map_from_tables(plan, rank, tables)
+        else:
+            rr, row = mesh.put_map(rank)
         Qp = np.full((5, nl), np.nan)
         Qp[:, :n_owned] = Q[:, :n_owned]
         reqs, recv = [], []
@@ -102,11 +125,11 @@ def _worker(rank, world, port, kind, out_q):
         out_q.put((rank, dict(error=traceback.format_exc())))
 
 
-def run_world(world, kind):
+def run_world(world, kind, region=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, kind, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, kind, q, region)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in range(world))
@@ -183,3 +206,77 @@ def test_put_map_is_a_bijection_onto_ghost_rows(world):
     for p in range(world):
         n_owned = plans[p]["n_owned"]
         assert np.all(hits[p][:n_owned] == 0) and np.all(hits[p][n_owned:] == 1), p
+
+
+@pytest.mark.parametrize("world,kind", [(2, "kuhn"), (3, "sphere")])
+def test_region_build_exchange_gloo(world, kind):
+    """One process per rank, each building only its own region (rank_only, O(owned + ghosts)
+    host setup): the plain-RCB partition covers the mesh, every ghost
+    arrives bitwise over gloo with the region plans, and the fused-put map built from the
+    receivers' exchanged tables (as hgks_p2p_connect builds it) fills every ghost row."""
+    res = run_world(world, kind, region=True)
+    mi = make_mesh(kind)
+    owned = [set(res[r]["owned"]) for r in range(world)]
+    assert sum(len(o) for o in owned) == mi.n_cells and len(set().union(*owned)) == mi.n_cells
+    for r in range(world):
+        assert res[r]["ghosts_ok"], r
+        assert res[r]["info"]["edge_cut"] == -1
+    # each cut face is counted once on each side
+    cut = sum(res[r]["info"]["rank_cut_faces"] for r in range(world))
+    assert cut % 2 == 0 and cut > 0
+
+
+@pytest.mark.parametrize("mk,world", [(lambda: W.kuhn_box(9, jitter=0.1), 3), (lambda: W.sphere_shell(6), 4),
+                                      (lambda: W.walled_hex_box(7), 3)])
+def test_region_plans_equal_whole_mesh_plans(mk, world):
+    """A region build gives exactly the plan the whole-mesh build gives for that rank (same
+    partition passed in): local ids, peers, send lists, receive ranges and every count."""
+    mi = mk()
+    whole = hgks.Mesh(mi, n_ranks=world)
+    part = np.zeros(mi.n_cells, np.int32)
+    for r in range(world):
+        p = whole.plan(r)
+        part[p["l2g"][:p["n_owned"]]] = r
+    whole = hgks.Mesh(mi, n_ranks=world, cell_part=part)
+    for r in range(world):
+        reg = hgks.Mesh(mi, n_ranks=world, cell_part=part, rank=r)
+        a, b = whole.plan(r), reg.plan(r)
+        for k in a:
+            assert np.array_equal(a[k], b[k]), (r, k)
+        ia, ib = whole.info(r), reg.info(r)
+        for k in ia:
+            if k not in ("edge_cut", "edge_cut_rcb"):
+                assert ia[k] == ib[k], (r, k)
+        with pytest.raises(hgks.HgksError):
+            reg.info((r + 1) % world)
+
+
+_MEM_SCRIPT = """
+import resource, sys
+sys.path.insert(0, {root!r})
+from paper_2407_00656_b200 import hgks, workloads as W
+mi = W.kuhn_box({nx}, {ny}, {nz}, h=2.0 / {nb})
+base = resource.getrusage(resource.RUSAGE_SELF).ru_maxrss
+m = hgks.Mesh(mi, n_ranks={world}, rank={rank})
+m.info({r0})
+print(resource.getrusage(resource.RUSAGE_SELF).ru_maxrss - base, mi.n_cells)
+"""
+
+
+def test_region_build_host_memory_scales_with_the_rank():
+    """Host memory of one rank's setup for the C5 weak-scaling layout (one block per rank,
+    here 8 ranks of 24 x 24 x 12 cubes, 41,472 tets each): the region build of rank 0 needs a fraction
+    of the whole-mesh build (which holds connectivity for all 8 blocks); peak RSS measured in
+    a fresh process per build.  scripts/setup_memory.py reports the full-size C5@8 figures."""
+    import subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+    def peak(rank):
+        code = _MEM_SCRIPT.format(root=root, nx=48, ny=48, nz=24, nb=24, world=8, rank=rank,
+                                  r0=0)
+        out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr
+        kb, n = map(int, out.stdout.split())
+        return kb
+    whole, region = peak(None), peak(0)
+    assert region < 0.35 * whole, (region, whole)
