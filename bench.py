@@ -60,7 +60,8 @@ def peaks(precision=64):
     pk = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
     key = "fp64_tflops" if precision == 64 else "fp32_tflops"
     kind = "DFMA" if precision == 64 else "FFMA"
-    return (hbm or 6650.0), src, pk[key], f"profiles/fp64_peak.json {key} ({kind}-chain microbenchmark on this pool)"
+    return (hbm or 6650.0), src, pk[key], (f"builder-measured: profiles/fp64_peak.json {key} ({kind}-chain "
+                                           f"microbenchmark on this pool; not in MEASURED_PEAKS.json)")
 
 
 class ClockSampler:
@@ -149,11 +150,22 @@ class ClockSampler:
 
 
 # algorithmic bytes / flops per unit, tets
-def recon_bytes_per_cell(K=14, M=4, NM=6, rs=8):
-    """rs: bytes of the working precision (8 fp64, 4 for the FP32 variant)."""
-    op = (9 * K + M * 3 * NM) * rs     # LSQ operators
+RECON_NE = False  # csrc/internal.h HGKS_RECON_NE (default build 0: streamed pseudo-inverse)
+
+
+def recon_bytes_per_cell(K=14, M=4, NM=6, rs=8, ne=RECON_NE):
+    """Algorithmic bytes per reconstructed cell.  rs: bytes of the working
+    precision (8 fp64, 4 for the FP32 variant).  ne: P_0 by normal equations -- the 9x9 inverse
+    Cholesky factor (45 entries + 1 pad) instead of the 9 x K pseudo-inverse, one image code per
+    member, and the cell's own row of member geometry (centroid, M2: 10 values; each row is
+    read at least once per launch, its other uses hit L2)."""
+    op = ((46 if ne else 9 * K) + M * 3 * NM) * rs  # LSQ operators
     idx = K * 4 + M * NM * 1 + 4       # stencil ids, sub-stencil slots, recon cell id
+    if ne:
+        idx += K                       # periodic image codes of the members
     geo = 8 * rs                       # V^{2/3}, V^{4/3}, M2
+    if ne:
+        geo += 10 * rs                 # member geometry row (centroid, M2, pad)
     q = 5 * rs                         # the cell's own state (neighbours: each state read once overall)
     rec = 50 * rs                      # effective-polynomial record written
     return op + idx + geo + q + rec
@@ -293,7 +305,7 @@ def main():
     ap.add_argument("--jitter", type=float, default=0.0,
                     help="c2/c5: interior node jitter U[-j h, j h] (seed 656), SURVEY 8(d) benchmark rule")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
-                    help="halo exchange for --gpus > 1: NCCL send/recv (default) or the fused NVLink put (f3)")
+                    help="halo exchange for --gpus > 1: NCCL send/recv (default) or the fused NVLink put (f3; EXPERIMENTAL: its cross-process flag protocol has not run on a multi-GPU node yet)")
     ap.add_argument("--precision", type=int, default=64, choices=[64, 32],
                     help="64: the fp64 path BASELINE's metric names (default); 32: the FP32 variant (P:1098-1183)")
     args = ap.parse_args()
@@ -413,6 +425,7 @@ def main():
     # ---------------- roofline of the dominant kernel ----------------
     hbm_peak, hbm_src, alu_peak, alu_src = peaks(args.precision)
     flops = json.load(open(os.path.join(ROOT, "profiles", "flops_per_unit.json")))
+    flops_alg = json.load(open(os.path.join(ROOT, "profiles", "flops_algorithmic.json")))
 
     def roof_of(name):
         kt = ktimes[name]
@@ -429,15 +442,20 @@ def main():
                     "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,
                     "peak_source": hbm_src + " (burst copy)"}
         fkey = "c2" if args.workload == "c5" else args.workload  # same tet kernels and per-face work
-        fpf = flops.get(fkey, {}).get(name, {}).get(f"fp{args.precision}_flops_per_face")
         nf = info["n_faces"] - info["n_faces_bc"]  # interior faces (the counts are per interior face)
+        # algorithmic flops where counted (tau = 0 flux), else the executed SASS count (labelled)
+        fpf = flops_alg.get(args.workload, {}).get(name, {}).get(f"fp{args.precision}_flops_per_face")
+        src = ("algorithmic: plain evaluation of SURVEY A.10 with an op-counting scalar, "
+               "profiles/flops_algorithmic.json (tools/flop_count)")
+        if not fpf:
+            fpf = flops.get(fkey, {}).get(name, {}).get(f"fp{args.precision}_flops_per_face")
+            src = "executed: ncu sass op counts (2 fma + add + mul), profiles/flops_per_unit.json"
         if not fpf:
             return None
         achieved = fpf * nf / (avg_ms * 1e-3) / 1e12
         return {"kernel": name, "bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",
                 "frac": achieved / alu_peak, "traffic": None, "avg_launch_ms": avg_ms,
-                "flops_per_face": fpf, "flops_source": "ncu sass op counts (2 fma + add + mul), "
-                                                      "profiles/flops_per_unit.json", "peak_source": alu_src}
+                "flops_per_face": fpf, "flops_source": src, "peak_source": alu_src}
 
     top = max(ktimes.items(), key=lambda kv: kv[1]["ms"])
     roof = roof_of(top[0])

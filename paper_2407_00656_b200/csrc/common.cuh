@@ -143,6 +143,8 @@ struct GroupCtrl {
 struct P2PFlags {
   unsigned long long arrived[kMaxGroup];
   unsigned long long consumed[kMaxGroup];
+  unsigned int put_blocks;  // blocks of the current k_put_release done (the last one releases)
+  unsigned int pad[3];
 };
 struct P2PSignal {
   unsigned long long* dst[kMaxGroup];  // peer flag words (mapped peer memory)

@@ -118,6 +118,9 @@ struct ReconArgs {
   const int* __restrict__ recon_cell;   // [n_recon] local cell id
   const int* __restrict__ st_id;        // [K] per cell, tiled: stencil member local ids
   const uint8_t* __restrict__ sub_slot; // [M*NM] per cell, tiled: sub-stencil member -> big-stencil slot
+  const uint8_t* __restrict__ st_shift;  // [K] per cell, tiled: periodic image code of each member (NE)
+  const Real* __restrict__ cgeo;      // [n_local][10]: centroid, M2 of every local row (NE)
+  Real per_len[3];                    // periodic box lengths (member images, NE)
   const Real* __restrict__ op;        // [E] per cell, tiled: LSQ operators in streaming order
   const Real* __restrict__ geo;       // [8] per cell, tiled: V^{2/3}, V^{4/3}, M2 (xx,yy,zz,xy,xz,yz)
   Real* __restrict__ ceff;            // [n_local][50]
@@ -133,6 +136,88 @@ struct ReconArgs {
 // sub-stencils re-read them from shared memory.  The LSQ operators (1584 B per
 // tet cell, most of the kernel's HBM bytes) stream entry-major: each warp load
 // is 256 contiguous bytes.
+// P_0 by normal equations (HGKS_RECON_NE, P:432-442 with the scaled basis of R20):
+// b = A^T dq with the rows of A rebuilt here from member geometry (centroid offset of the
+// member's periodic image D and its second moments), then coefficients
+// c = diag(1/h, 1/h^2) W^T W b with W = L^{-1}, L L^T = A^T A (host, checked against QR).
+// NS variables per thread (5, or 3 for a lane of k_recon_pair); dq(k, v) reads the member
+// differences from shared memory.
+template <int K, int NS, class DQ>
+__device__ __forceinline__ void p0_normal_equations(const ReconArgs& a, int ci, const int* __restrict__ sid,
+                                                    const uint8_t* __restrict__ ssh, const R2* __restrict__ op2,
+                                                    Real V23, const Real m2[6], DQ&& dq, Real c[9][NS]) {
+  const Real ih = rsqrt(V23), ih2 = ih * ih;  // 1/h, 1/h^2, h = V^{1/3}
+  Real cix, ciy, ciz;
+  {
+    const R2* g = reinterpret_cast<const R2*>(a.cgeo + (size_t)ci * 10);
+    const R2 g0 = __ldg(g), g1 = __ldg(g + 1);
+    cix = g0.x; ciy = g0.y; ciz = g1.x;
+  }
+#pragma unroll
+  for (int d = 0; d < 9; ++d)
+#pragma unroll
+    for (int v = 0; v < NS; ++v) c[d][v] = Real(0.0);
+#ifndef HGKS_NE_UNROLL
+#define HGKS_NE_UNROLL 14  // measured: 2 / 4 / 7 / 14 -> 0.515 / 0.492 / 0.442 / 0.422 ms (C2)
+#endif
+  constexpr int kNeUnroll = HGKS_NE_UNROLL;
+#pragma unroll kNeUnroll
+  for (int k = 0; k < K; ++k) {
+    const int id = __ldg(sid + k * kTile);
+    const int code = __ldg(ssh + k * kTile);
+    const R2* g = reinterpret_cast<const R2*>(a.cgeo + (size_t)id * 10);
+    const R2 g0 = __ldg(g), g1 = __ldg(g + 1), g2 = __ldg(g + 2), g3 = __ldg(g + 3), g4 = __ldg(g + 4);
+    const Real sx = Real(code % 3 - 1) * a.per_len[0], sy = Real((code / 3) % 3 - 1) * a.per_len[1],
+               sz = Real(code / 9 - 1) * a.per_len[2];
+    const Real Dx = (g0.x + sx) - cix, Dy = (g0.y + sy) - ciy, Dz = (g1.x + sz) - ciz;
+    const Real r[9] = {Dx * ih, Dy * ih, Dz * ih,
+                       (g1.y + Dx * Dx - m2[0]) * ih2, (g2.x + Dy * Dy - m2[1]) * ih2, (g2.y + Dz * Dz - m2[2]) * ih2,
+                       (g3.x + Dx * Dy - m2[3]) * ih2, (g3.y + Dx * Dz - m2[4]) * ih2, (g4.x + Dy * Dz - m2[5]) * ih2};
+    Real q[NS];
+#pragma unroll
+    for (int v = 0; v < NS; ++v) q[v] = dq(k, v);
+#pragma unroll
+    for (int d = 0; d < 9; ++d)
+#pragma unroll
+      for (int v = 0; v < NS; ++v) c[d][v] = fma(r[d], q[v], c[d][v]);
+  }
+  // W (lower, row-major, 45 entries + pad) as 23 entry pairs
+  Real W[46];
+#pragma unroll
+  for (int p = 0; p < 23; ++p) {
+    const R2 w = __ldcs(op2 + p * kTile);
+    W[2 * p] = w.x;
+    W[2 * p + 1] = w.y;
+  }
+  // y = W b in place (row i uses b[0..i]: bottom row first)
+#pragma unroll
+  for (int i = 8; i >= 0; --i) {
+    Real t[NS];
+#pragma unroll
+    for (int v = 0; v < NS; ++v) t[v] = W[i * (i + 1) / 2] * c[0][v];
+#pragma unroll
+    for (int j = 1; j <= i; ++j)
+#pragma unroll
+      for (int v = 0; v < NS; ++v) t[v] = fma(W[i * (i + 1) / 2 + j], c[j][v], t[v]);
+#pragma unroll
+    for (int v = 0; v < NS; ++v) c[i][v] = t[v];
+  }
+  // c = W^T y in place (entry j uses y[j..8]: top entry first), then the basis scaling
+#pragma unroll
+  for (int j = 0; j < 9; ++j) {
+    Real t[NS];
+#pragma unroll
+    for (int v = 0; v < NS; ++v) t[v] = W[j * (j + 1) / 2 + j] * c[j][v];
+#pragma unroll
+    for (int i = j + 1; i < 9; ++i)
+#pragma unroll
+      for (int v = 0; v < NS; ++v) t[v] = fma(W[i * (i + 1) / 2 + j], c[i][v], t[v]);
+    const Real sc = j < 3 ? ih : ih2;
+#pragma unroll
+    for (int v = 0; v < NS; ++v) c[j][v] = t[v] * sc;
+  }
+}
+
 #ifndef HGKS_RECON_MINB
 #define HGKS_RECON_MINB 2
 #endif
@@ -151,7 +236,8 @@ template <int K, int M, int NM>
 __global__ void __launch_bounds__(ReconShape<K>::BT, ReconShape<K>::MINB) k_recon(ReconArgs a) {
   constexpr int BT = ReconShape<K>::BT, SPLIT = ReconShape<K>::SPLIT;
   constexpr int QP = 5 * BT;                         // values per member plane: [v][thread]
-  constexpr int E = 9 * K + 3 * M * NM;
+  constexpr int E0 = HGKS_RECON_NE ? 46 : 9 * K;     // P_0 operator entries (W, or the pseudo-inverse)
+  constexpr int E = E0 + 3 * M * NM;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Real* smem = reinterpret_cast<Real*>(smem_raw);
   Real* __restrict__ dqs = smem;                   // [K][5][BT] Q_k - Q_i
@@ -219,15 +305,20 @@ __global__ void __launch_bounds__(ReconShape<K>::BT, ReconShape<K>::MINB) k_reco
   Real m2[6];
 #pragma unroll
   for (int q = 0; q < 6; ++q) m2[q] = __ldg(geo + (2 + q) * kTile);
-  // ---- P_0: c[d][v] = sum_k A0+[d][k] (Q_k - Q_i)[v] ----
+  // ---- P_0 ----
   Real c[9][5];
+  // operators are tiled by entry pairs: pair p of this cell at op2[p * kTile]
+  const R2* __restrict__ op2 = reinterpret_cast<const R2*>(a.op + tb * E) + t;
+  static_assert(K % 2 == 0 && (3 * M * NM) % 2 == 0, "operator pairs");
+#if HGKS_RECON_NE
+  p0_normal_equations<K, 5>(a, ci, sid, a.st_shift + tb * K + t, op2, V23, m2,
+                            [&](int k, int v) { return dqs[k * QP + v * BT + tl]; }, c);
+#else
+  // c[d][v] = sum_k A0+[d][k] (Q_k - Q_i)[v]
 #pragma unroll
   for (int d = 0; d < 9; ++d)
 #pragma unroll
     for (int v = 0; v < 5; ++v) c[d][v] = Real(0.0);
-  // operators are tiled by entry pairs: pair p of this cell at op2[p * kTile]
-  const R2* __restrict__ op2 = reinterpret_cast<const R2*>(a.op + tb * E) + t;
-  static_assert(K % 2 == 0 && (3 * M * NM) % 2 == 0, "operator pairs");
   // measured unroll of the member-pair loop: tets (K = 14) 4, hexes (K = 24) 2
   // (C2 0.397 -> 0.388 ms, C3 0.484 -> 0.458 ms vs no unrolling)
   constexpr int kUnrollA0 = K <= 16 ? 4 : 2;
@@ -249,6 +340,7 @@ __global__ void __launch_bounds__(ReconShape<K>::BT, ReconShape<K>::MINB) k_reco
       for (int v = 0; v < 5; ++v) c[d][v] = fma(w, dq[h][v], c[d][v]);
     }
   }
+#endif
   // smoothness indicator of P_0 (closed form SURVEY A.5)
   Real beta0[5];
 #pragma unroll
@@ -264,7 +356,7 @@ __global__ void __launch_bounds__(ReconShape<K>::BT, ReconShape<K>::MINB) k_reco
                       c[7][v] * c[7][v] + c[8][v] * c[8][v];
     beta0[v] = V23 * s1 + V43 * s2;
   }
-  const R2* __restrict__ opm2 = op2 + (9 * K / 2) * kTile;
+  const R2* __restrict__ opm2 = op2 + (E0 / 2) * kTile;
   auto sub_slopes = [&](int m, Real b[3][5]) {  // P_m over sub-stencil m
 #pragma unroll
     for (int d = 0; d < 3; ++d)
@@ -378,7 +470,8 @@ __global__ void __launch_bounds__(128, HGKS_RPAIR_MINB) k_recon_pair(ReconArgs a
   constexpr int NS = 3;  // variable slots per lane
   constexpr int BT = 128, SPLIT = 2;                 // 64 cells per block, two blocks per tile
   constexpr int QP = NS * BT;                        // values per member plane: [slot][thread]
-  constexpr int E = 9 * K + 3 * M * NM;
+  constexpr int E0 = HGKS_RECON_NE ? 46 : 9 * K;
+  constexpr int E = E0 + 3 * M * NM;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Real* smem = reinterpret_cast<Real*>(smem_raw);
   Real* __restrict__ dqs = smem;                   // [K][NS][BT] Q_k - Q_i (this lane's slots)
@@ -447,15 +540,19 @@ __global__ void __launch_bounds__(128, HGKS_RPAIR_MINB) k_recon_pair(ReconArgs a
   Real m2[6];
 #pragma unroll
   for (int q = 0; q < 6; ++q) m2[q] = __ldg(geo + (2 + q) * kTile);
-  // ---- P_0: c[d][v] = sum_k A0+[d][k] (Q_k - Q_i)[v] ----
+  // ---- P_0 ----
   Real c[9][NS];
+  // operators are tiled by entry pairs: pair p of this cell at op2[p * kTile]
+  const R2* __restrict__ op2 = reinterpret_cast<const R2*>(a.op + tb * E) + t;
+  static_assert(K % 2 == 0 && (3 * M * NM) % 2 == 0, "operator pairs");
+#if HGKS_RECON_NE
+  p0_normal_equations<K, NS>(a, ci, sid, a.st_shift + tb * K + t, op2, V23, m2,
+                             [&](int k, int v) { return dqs[k * QP + v * BT + tl]; }, c);
+#else
 #pragma unroll
   for (int d = 0; d < 9; ++d)
 #pragma unroll
     for (int v = 0; v < NS; ++v) c[d][v] = Real(0.0);
-  // operators are tiled by entry pairs: pair p of this cell at op2[p * kTile]
-  const R2* __restrict__ op2 = reinterpret_cast<const R2*>(a.op + tb * E) + t;
-  static_assert(K % 2 == 0 && (3 * M * NM) % 2 == 0, "operator pairs");
   // measured unroll of the member-pair loop: tets (K = 14) 4, hexes (K = 24) 2
   // (C2 0.397 -> 0.388 ms, C3 0.484 -> 0.458 ms vs no unrolling)
   constexpr int kUnrollA0 = K <= 16 ? 4 : 2;
@@ -477,6 +574,7 @@ __global__ void __launch_bounds__(128, HGKS_RPAIR_MINB) k_recon_pair(ReconArgs a
       for (int v = 0; v < NS; ++v) c[d][v] = fma(w, dq[h][v], c[d][v]);
     }
   }
+#endif
   // smoothness indicator of P_0 (closed form SURVEY A.5)
   Real beta0[NS];
 #pragma unroll
@@ -492,7 +590,7 @@ __global__ void __launch_bounds__(128, HGKS_RPAIR_MINB) k_recon_pair(ReconArgs a
                       c[7][v] * c[7][v] + c[8][v] * c[8][v];
     beta0[v] = V23 * s1 + V43 * s2;
   }
-  const R2* __restrict__ opm2 = op2 + (9 * K / 2) * kTile;
+  const R2* __restrict__ opm2 = op2 + (E0 / 2) * kTile;
   auto sub_slopes = [&](int m, Real b[3][NS]) {  // P_m over sub-stencil m
 #pragma unroll
     for (int d = 0; d < 3; ++d)
@@ -1804,6 +1902,34 @@ __global__ void k_put(const Real* __restrict__ Q, const int* __restrict__ list, 
 
 
 
+// The same put for the cross-process transport, with the "stage e arrived" release fused in:
+// every thread fences its peer stores at system scope, the block counts itself done on an
+// atomic counter, and the last block releases the epoch to every receiver's flag.  The
+// ordering rests on the fence + atomic chain inside one kernel (the threadFenceReduction
+// pattern), not on kernel-boundary visibility of peer stores.
+__global__ void k_put_release(const Real* __restrict__ Q, const int* __restrict__ list,
+                              const int2* __restrict__ dst, int n, PeerQ peer, P2PSignal sig,
+                              unsigned long long epoch, unsigned int* __restrict__ done_blocks) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n * 3) {
+    const int j = k / 3, part = k - 3 * j;
+    const int2 d = __ldg(dst + j);
+    reinterpret_cast<R2*>(peer.q[d.x] + (size_t)d.y * QS)[part] =
+        reinterpret_cast<const R2*>(Q + (size_t)__ldg(list + j) * QS)[part];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int prev = atomicAdd(done_blocks, 1u);
+    if (prev == gridDim.x - 1) {  // every block's stores are fenced: release
+      __threadfence_system();
+      for (int q = 0; q < sig.n; ++q)
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(sig.dst[q]), "l"(epoch) : "memory");
+      *done_blocks = 0u;  // ready for the next stage (stream order)
+    }
+  }
+}
+
 // host-side launchers of this precision's kernels (solver.cu is templated on this struct)
 struct Launch {
   using RealT = Real;
@@ -1864,5 +1990,9 @@ struct Launch {
   static void put(int grid, cudaStream_t st, const Real* Q, const int* list, const int2* dst, int n,
                   const PeerQ& peer) {
     k_put<<<grid, 256, 0, st>>>(Q, list, dst, n, peer);
+  }
+  static void put_release(int grid, cudaStream_t st, const Real* Q, const int* list, const int2* dst, int n,
+                          const PeerQ& peer, const P2PSignal& sig, unsigned long long epoch, unsigned int* done) {
+    k_put_release<<<grid, 256, 0, st>>>(Q, list, dst, n, peer, sig, epoch, done);
   }
 };

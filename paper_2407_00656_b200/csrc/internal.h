@@ -11,6 +11,15 @@
 #include <string>
 #include <vector>
 
+// P_0 least squares by normal equations with the rows rebuilt on the device from member
+// geometry: 1584 -> 944 operator bytes per tet cell (-29 % DRAM bytes of k_recon), but the
+// member-geometry gathers make it latency bound: measured on C2 (same box) k_recon 0.422 vs
+// 0.433 ms and the step 1.518 vs 1.506 ms (profiles/r02/README.md), so it is built only on
+// request (-DHGKS_RECON_NE=1); 0 streams the 9 x K pseudo-inverse
+#ifndef HGKS_RECON_NE
+#define HGKS_RECON_NE 0
+#endif
+
 namespace hgks {
 
 struct Error : std::runtime_error {
@@ -29,7 +38,10 @@ struct Layout {
   int K = 14;          // padded big-stencil width
   int M = 4;           // sub-stencils per cell
   int NM = 6;          // padded members per sub-stencil
-  int op_entries() const { return 9 * K + M * 3 * NM; }
+  // P_0 part of the per-cell operators: the 9x9 inverse Cholesky factor W of the normal
+  // matrix (45 entries + 1 pad, HGKS_RECON_NE) or the K-column pseudo-inverse
+  int op0_entries() const { return HGKS_RECON_NE ? 46 : 9 * K; }
+  int op_entries() const { return op0_entries() + M * 3 * NM; }
 };
 
 struct GlobalMesh {
@@ -89,6 +101,8 @@ struct RankPlan {
   std::vector<int32_t> st_id;           // [K][ld] local ids (entry-major; host only)
   std::vector<int32_t> st_id_tiled;     // same, tiled entry-major (device)
   std::vector<uint8_t> sub_slot;        // [M*NM] per cell, tiled entry-major
+  std::vector<uint8_t> st_shift;        // [K] per cell, tiled: periodic image code of each member (HGKS_RECON_NE)
+  std::vector<double> cgeo;             // [n_local][10]: centroid (3), M2 (xx,yy,zz,xy,xz,yz), pad (HGKS_RECON_NE)
   std::vector<double> op;               // [op_entries] per cell, tiled entry-major (kernels.cuh k_recon)
   std::vector<double> geo;              // [8] per cell, tiled: V^{2/3}, V^{4/3}, M2 (xx,yy,zz,xy,xz,yz)
   // faces: interior [0, n_if), wall [n_if, n_if + n_wf), farfield after

@@ -955,8 +955,55 @@ static bool cell_operators(const GlobalMesh& gm, int64_t i, double* op) {
   }
   double P[9 * 64];
   if (!pinv_qr(K, 9, A, P)) return false;
+#if HGKS_RECON_NE
+  {
+    // normal equations of the scaled system: G = A^T A = L L^T, W = L^{-1} (lower), so the
+    // scaled coefficients are W^T W A^T dq; the device rebuilds the rows of A from member
+    // geometry and stores only W.  Checked against the QR pseudo-inverse (cond(G) =
+    // cond(A)^2 is ~1e2-2e3 on these stencils).
+    double G[9][9] = {}, Lc[9][9] = {}, Wm[9][9] = {};
+    for (int a = 0; a < 9; ++a)
+      for (int b = 0; b < 9; ++b)
+        for (int k = 0; k < K; ++k) G[a][b] += A[k * 9 + a] * A[k * 9 + b];
+    for (int j = 0; j < 9; ++j) {
+      double d = G[j][j];
+      for (int k = 0; k < j; ++k) d -= Lc[j][k] * Lc[j][k];
+      if (!(d > 0)) return false;
+      Lc[j][j] = std::sqrt(d);
+      for (int i = j + 1; i < 9; ++i) {
+        double v = G[i][j];
+        for (int k = 0; k < j; ++k) v -= Lc[i][k] * Lc[j][k];
+        Lc[i][j] = v / Lc[j][j];
+      }
+    }
+    for (int j = 0; j < 9; ++j) {  // W = L^{-1}, column by column
+      Wm[j][j] = 1.0 / Lc[j][j];
+      for (int i = j + 1; i < 9; ++i) {
+        double v = 0;
+        for (int k = j; k < i; ++k) v -= Lc[i][k] * Wm[k][j];
+        Wm[i][j] = v / Lc[i][i];
+      }
+    }
+    double pmax = 0, dmax = 0;
+    for (int d = 0; d < 9; ++d)
+      for (int k = 0; k < K; ++k) {
+        double s = 0;  // (W^T W A^T)[d][k]
+        for (int i = 0; i < 9; ++i) {
+          double wa = 0;
+          for (int j = 0; j <= i; ++j) wa += Wm[i][j] * A[k * 9 + j];
+          s += Wm[i][d] * wa;
+        }
+        pmax = std::max(pmax, std::fabs(P[d * K + k]));
+        dmax = std::max(dmax, std::fabs(s - P[d * K + k]));
+      }
+    if (!(dmax <= 1e-9 * pmax)) return false;
+    for (int i = 0, e = 0; i < 9; ++i)
+      for (int j = 0; j <= i; ++j) op[e++] = Wm[i][j];
+  }
+#else
   for (int d = 0; d < 9; ++d)
     for (int k = 0; k < K; ++k) op[d * L.K + k] = P[d * K + k] / (d < 3 ? h : h * h);
+#endif
   const int8_t* ss = &gm.sub_slot[i * L.M * L.NM];
   for (int m = 0; m < L.M; ++m) {
     int n = 0;
@@ -970,7 +1017,7 @@ static bool cell_operators(const GlobalMesh& gm, int64_t i, double* op) {
       }
     double Ps[3 * 8];
     if (n < 3 || !pinv_qr(n, 3, As, Ps)) return false;
-    double* om = op + 9 * L.K + m * 3 * L.NM;
+    double* om = op + L.op0_entries() + m * 3 * L.NM;
     for (int d = 0; d < 3; ++d)
       for (int j = 0; j < n; ++j) om[d * L.NM + j] = Ps[d * n + j] / h;
   }
@@ -1098,6 +1145,7 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
   rp.ld = R;
   rp.st_id.assign((size_t)K * R, 0);
   rp.sub_slot.assign((size_t)M * NM * R, 0);
+  rp.st_shift.assign((size_t)K * R, 13);
   rp.op.assign((size_t)E * R, 0.0);
   rp.geo.assign((size_t)8 * R, 0.0);
   // tiled entry-major layout: entry e of cell r at ((r/128)*NE + e)*128 + r%128, so one
@@ -1149,16 +1197,37 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
     }
     // streaming order of the operator entries (hot.cuh k_recon): A0+ member-major
     // (row k*9 + d), then the sub-stencil operators (row 9K + (m*NM + j)*3 + d)
-    double op[9 * 64 + 8 * 3 * 8];
+    double op[9 * 64 + 8 * 3 * 8] = {};
     if (!cell_operators(gm, gi, op)) {
 #pragma omp critical
       if (lsq_bad < 0 || gi < lsq_bad) lsq_bad = gi;
     }
+    const int E0 = L.op0_entries();
+#if HGKS_RECON_NE
+    for (int e = 0; e < E0; ++e) rp.op[tp(r, E, e)] = op[e];
+    for (int k = 0; k < K; ++k) {  // periodic image of member k: shift / box length per axis in {-1, 0, 1}
+      int code = 13;
+      if (k < kk) {
+        code = 0;
+        for (int a = 2; a >= 0; --a) {
+          const double sh = gm.big_shift[3 * (o0 + k) + a];
+          const int sa = gm.per_len[a] > 0 ? (int)std::lround(sh / gm.per_len[a]) : 0;
+          if (sa < -1 || sa > 1) {
+#pragma omp critical
+            lsq_bad = gi;
+          }
+          code = 3 * code + (sa + 1);
+        }
+      }
+      rp.st_shift[ti(r, K, k)] = (uint8_t)code;
+    }
+#else
     for (int d = 0; d < 9; ++d)
       for (int k = 0; k < K; ++k) rp.op[tp(r, E, k * 9 + d)] = op[d * K + k];
+#endif
     for (int m = 0; m < M; ++m)
       for (int d = 0; d < 3; ++d)
-        for (int j = 0; j < NM; ++j) rp.op[tp(r, E, 9 * K + (m * NM + j) * 3 + d)] = op[9 * K + (m * 3 + d) * NM + j];
+        for (int j = 0; j < NM; ++j) rp.op[tp(r, E, E0 + (m * NM + j) * 3 + d)] = op[E0 + (m * 3 + d) * NM + j];
     double V = gm.V[gi];
     rp.geo[ti(r, 8, 0)] = std::pow(V, 2.0 / 3.0);
     rp.geo[ti(r, 8, 1)] = std::pow(V, 4.0 / 3.0);
@@ -1250,6 +1319,24 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
   // resolve BC ghost interior cells (must be local)
   for (size_t k = 0; k < bg_used.size(); ++k) rp.bg_cell[k] = local_of(gm.g_cell[bg_used[k]]);
   rp.n_bghost = (int64_t)bg_used.size();
+#if HGKS_RECON_NE
+  // centroid and second moments of every local row (members of the rebuilt LSQ rows)
+  rp.cgeo.assign((size_t)10 * rp.n_local(), 0.0);
+  for (int64_t l = 0; l < rp.n_local(); ++l) {
+    const double *c, *m2;
+    if (l < rp.n_owned + rp.n_pghost) {
+      const int64_t gi = rp.l2g[l];
+      c = &gm.C[3 * gi];
+      m2 = &gm.M2[6 * gi];
+    } else {
+      const int64_t g = bg_used[l - rp.n_owned - rp.n_pghost];
+      c = &gm.gC[3 * g];
+      m2 = &gm.gM2[6 * g];
+    }
+    for (int a = 0; a < 3; ++a) rp.cgeo[10 * l + a] = c[a];
+    for (int a = 0; a < 6; ++a) rp.cgeo[10 * l + 3 + a] = m2[a];
+  }
+#endif
   // exchange plan: peers = owner ranks of my ghosts, and ranks that ghost my cells
   if (gm.n_ranks > 1) {
     std::vector<std::vector<int32_t>> sends(gm.n_ranks);

@@ -146,13 +146,14 @@ int round32(int64_t n) { return (int)((n + 31) / 32 * 32); }
 
 struct DevArrays {
   // working-precision arrays (double for fp64, float for fp32)
-  void *Q, *Qtmp, *R, *ceff, *ceff0, *F1, *F2, *op, *geo, *f_geo, *inv_v, *h_dt, *bg_normal, *sendbuf;
+  void *Q, *Qtmp, *R, *ceff, *ceff0, *F1, *F2, *op, *geo, *cgeo, *f_geo, *inv_v, *h_dt, *bg_normal, *sendbuf;
   double *stage_in[2], *stage_out[2];  // caller-order staging (fp64), double-buffered for pipelining
   int *recon_cell, *st_id, *f_cells, *cf, *bg_cell, *bg_bc, *send_list, *out_local;
   int2* put_dst;  // fused halo put: (receiver rank, receiver row) per send row (f3)
   P2PFlags* flags;  // cross-process put: epoch flags written by the peers (f3)
   int64_t* in_row;
   uint8_t* sub_slot;
+  uint8_t* st_shift;
   Ctrl* ctrl;
 };
 
@@ -175,6 +176,8 @@ size_t layout(const GlobalMesh& gm, const RankPlan& rp, size_t rs, int dq0_mode,
   d.sub_slot = c.take<uint8_t>((size_t)L.M * L.NM * rp.ld);
   d.op = R((size_t)L.op_entries() * rp.ld);
   d.geo = R((size_t)8 * rp.ld);
+  d.st_shift = c.take<uint8_t>(HGKS_RECON_NE ? (size_t)L.K * rp.ld : 1);
+  d.cgeo = R(HGKS_RECON_NE ? (size_t)10 * rp.n_local() : 1);
   d.f_cells = c.take<int>((size_t)2 * rp.n_faces);
   d.f_geo = R((size_t)rp.f_geo_stride * rp.n_faces);
   d.cf = c.take<int>((size_t)L.nfaces * rp.n_owned);
@@ -345,6 +348,9 @@ void run_recon(hgks_solver* s, const void* Q, int part) {
   a.recon_cell = s->d.recon_cell;
   a.st_id = s->d.st_id;
   a.sub_slot = s->d.sub_slot;
+  a.st_shift = s->d.st_shift;
+  a.cgeo = as<L>(s->d.cgeo);
+  for (int k = 0; k < 3; ++k) a.per_len[k] = (typename L::RealT)s->mesh->gm.per_len[k];
   a.op = as<L>(s->d.op);
   a.geo = as<L>(s->d.geo);
   a.ceff = as<L>(s->d.ceff);
@@ -646,7 +652,8 @@ void stage_late(hgks_solver* s, int st) {
 // f3 across processes (HGKS_TRANSPORT_P2P): the owner puts its send rows straight into
 // the receivers' ghost rows over NVLink (peer memory mapped by CUDA IPC), ordered by
 // per-stage epoch flags: (1) wait until every receiver has finished reading the ghost
-// rows of the previous stage, (2) k_put, (3) release "stage e arrived" to the receivers,
+// rows of the previous stage, (2)+(3) k_put_release: the puts, a system-scope fence by every
+// thread and, from the last block, the release of "stage e arrived" to the receivers,
 // (4) ghost-free work, (5) acquire "arrived" from every sender, (6) the rest of the
 // stage, (7) release "stage e consumed" to the senders.  Graph capture is off for
 // n_ranks > 1, so the host-side epoch values are baked into eager launches.
@@ -665,14 +672,16 @@ void stage_p2p(hgks_solver* s, int st) {
   }
   if (e > 1 && w_cons.n) launch(s, "k_p2p_wait", [&] { k_p2p_wait<<<1, 32, 0, s->stream>>>(w_cons, e - 1); });
   const int ns = (int)s->rp->send_list.size();
-  if (ns) {
+  if (ns) {  // put + system-scope release of "stage e arrived" in one kernel (k_put_release)
     typename L::PeerQT peer{};
     for (int p : s->put_to) peer.q[p] = as<L>(s->peer_Q[p]);
-    launch(s, "k_put", [&] {
-      L::put(blocks(3 * ns, 256), s->stream, as<L>(s->d.Q), s->d.send_list, s->d.put_dst, ns, peer);
+    launch(s, "k_put_release", [&] {
+      L::put_release(blocks(3 * ns, 256), s->stream, as<L>(s->d.Q), s->d.send_list, s->d.put_dst, ns, peer, s_arr, e,
+                     &s->d.flags->put_blocks);
     });
+  } else if (s_arr.n) {
+    launch(s, "k_p2p_signal", [&] { k_p2p_signal<<<1, 32, 0, s->stream>>>(s_arr, e); });
   }
-  if (s_arr.n) launch(s, "k_p2p_signal", [&] { k_p2p_signal<<<1, 32, 0, s->stream>>>(s_arr, e); });
   stage_early<L>(s, st);
   if (w_arr.n) launch(s, "k_p2p_wait", [&] { k_p2p_wait<<<1, 32, 0, s->stream>>>(w_arr, e); });
   stage_late<L>(s, st);
@@ -897,6 +906,8 @@ hgks_status hgks_init(const hgks_mesh* mc, const hgks_config* cfg, const hgks_di
     up(s->d.sub_slot, rp.sub_slot.data(), rp.sub_slot.size());
     upr(s->d.op, rp.op);
     upr(s->d.geo, rp.geo);
+    up(s->d.st_shift, rp.st_shift.data(), rp.st_shift.size());
+    upr(s->d.cgeo, rp.cgeo);
     up(s->d.f_cells, rp.f_cells.data(), rp.f_cells.size() * sizeof(int));
     upr(s->d.f_geo, rp.f_geo);
     up(s->d.cf, rp.cf.data(), rp.cf.size() * sizeof(int));
@@ -1248,6 +1259,14 @@ hgks_status hgks_p2p_selftest(void) {
       CUDA_TRY(cudaMemcpy(&h, fl, sizeof(P2PFlags), cudaMemcpyDeviceToHost));
       if (h.arrived[5] != 7 || h.consumed[2] != 7 || h.arrived[0] != 0)
         throw Error(HGKS_E_CUDA, "k_p2p_signal wrote wrong flags");
+      // the fused put + release: rows again, flags to epoch 9, block counter back to 0
+      P2PSignal sg2{};
+      sg2.dst[0] = &fl->arrived[6];
+      sg2.n = 1;
+      p64::Launch::put_release(blocks(3 * n, 256), 0, src, list, map, n, peer, sg2, 9ull, &fl->put_blocks);
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaMemcpy(&h, fl, sizeof(P2PFlags), cudaMemcpyDeviceToHost));
+      if (h.arrived[6] != 9 || h.put_blocks != 0) throw Error(HGKS_E_CUDA, "k_put_release wrote wrong flags");
       P2PWait w{};
       w.src[0] = &fl->arrived[5];
       w.src[1] = &fl->consumed[2];
