@@ -1449,7 +1449,6 @@ __global__ void __launch_bounds__((NV == 3 ? 3 : 4) * HGKS_FLUX_FPB,
   // stage-1 tau = 0 flux); otherwise a shared-memory reduction
   constexpr bool WR = HGKS_FLUX_WARPRED;
   constexpr int FPW = 32 / NGP;  // faces per warp: 10 or 8
-  __shared__ Real red[WR ? 1 : NOUT][WR ? 1 : BLOCK];
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * BLOCK + threadIdx.x;
   const int lf = WR ? (int)(blockIdx.x * (BLOCK / 32) * FPW + (threadIdx.x >> 5) * FPW + lane / NGP) : t / NGP;
@@ -1698,7 +1697,7 @@ __global__ void __launch_bounds__((NV == 3 ? 3 : 4) * HGKS_FLUX_FPB,
       out[4] = wS * dF[4];
     }
   }
-  if (WR) {
+  if constexpr (WR) {
     // face quadrature sum in Gauss-point order (((GP0 + GP1) + GP2) + GP3, as below)
 #pragma unroll
     for (int k = 0; k < NOUT; ++k) {
@@ -1712,8 +1711,8 @@ __global__ void __launch_bounds__((NV == 3 ? 3 : 4) * HGKS_FLUX_FPB,
 #pragma unroll
       for (int k = 0; k < NOUT; ++k) dst[k] = out[k];
     }
-    return;
-  }
+  } else {
+  __shared__ Real red[NOUT][BLOCK];
 #pragma unroll
   for (int k = 0; k < NOUT; ++k) red[k][threadIdx.x] = out[k];
   __syncthreads();
@@ -1729,6 +1728,7 @@ __global__ void __launch_bounds__((NV == 3 ? 3 : 4) * HGKS_FLUX_FPB,
       Real* dst = STAGE == 1 ? a.F1 : a.F2;
       dst[(size_t)(a.face0 + face) * NOUT + k] = s;
     }
+  }
   }
 }
 
