@@ -18,11 +18,11 @@ SRC = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "gpurun_out", "pr
 DST = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "profiles", "r01")
 
 N_BOX = 48
-CELLS = {"c2": 6 * N_BOX ** 3, "c3": 12 * 35 ** 3, "c4": 12 * 70 ** 3}
+CELLS = {"c2": 6 * N_BOX ** 3, "c3": 12 * 35 ** 3, "c4": 12 * 70 ** 3, "c5": 6 * 110 ** 3}
 IFACES = {"c2": 2 * CELLS["c2"], "c3": (6 * CELLS["c3"] - 2 * 6 * 35 ** 2) // 2,
           "c4": (6 * CELLS["c4"] - 2 * 6 * 70 ** 2) // 2}
-NAMES = {"k_flux<3, 1, 1, 0>": "k_flux_tau0_s1", "k_flux<3, 2, 1, 0>": "k_flux_tau0_s2",
-         "k_flux<4, 1, 0, 0>": "k_flux_s1", "k_flux<4, 2, 0, 0>": "k_flux_s2"}
+NAMES = {"k_flux<3, 1, 1, 0, 0, 0>": "k_flux_tau0_s1", "k_flux<3, 2, 1, 0, 0, 0>": "k_flux_tau0_s2",
+         "k_flux<4, 1, 0, 0, 0, 0>": "k_flux_s1", "k_flux<4, 2, 0, 0, 0, 0>": "k_flux_s2"}
 SCALE = {"": 1.0, "inst": 1.0, "K": 1e3, "M": 1e6, "G": 1e9, "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6,
          "Gbyte": 1e9, "ns": 1.0, "us": 1e3, "ms": 1e6}
 
@@ -63,27 +63,39 @@ def main():
     flops["c4"] = flops.get("c3", {})  # same kernels and per-face work (sphere shell, tau > 0)
     json.dump(flops, open(os.path.join(ROOT, "profiles", "flops_per_unit.json"), "w"), indent=1)
 
-    rep = os.path.join(SRC, "full_c2.ncu-rep")
-    if os.path.exists(rep):
-        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    for wl in ("c2", "c5"):
+        rep = os.path.join(SRC, f"full_{wl}.ncu-rep")
+        gz = os.path.join(SRC, f"ncu_full_{wl}.csv.gz")  # exported on the box (gpurun copies <= 64 MiB)
+        if os.path.exists(rep):
+            raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        elif os.path.exists(gz):
+            import gzip
+            raw = gzip.open(gz, "rt").read()
+        else:
+            continue
         rows = list(csv.reader(raw.splitlines()))
         h, units = rows[0], rows[1]
-        traffic = {}
+        tpath = os.path.join(ROOT, "profiles", "traffic.json")
+        traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
+        seen = set()
         for row in rows[2:]:
             d = {k: (v, u) for k, v, u in zip(h, row, units)}
             val = lambda k: float(d[k][0].replace(",", "")) * SCALE.get(d[k][1], 1.0)
             name = d["Kernel Name"][0].split("(")[0].replace("void ", "").strip()
             key = "k_recon" if name.startswith("k_recon") else NAMES.get(name, name)
-            traffic.setdefault(key, {"dram_bytes_per_launch": val("dram__bytes_read.sum") + val("dram__bytes_write.sum"),
-                                     "time_ns": val("gpu__time_duration.sum"), "cells": CELLS["c2"],
-                                     "source": "ncu --set full --clock-control none, 48^3 Kuhn box, "
-                                               "gpurun_out/prof/full_c2.ncu-rep (profiles/r01/ncu_full_c2.csv)"})
-        json.dump(traffic, open(os.path.join(ROOT, "profiles", "traffic.json"), "w"), indent=1)
-        open(os.path.join(DST, "ncu_full_c2.csv"), "w").write(raw)
+            if key in seen:
+                continue
+            seen.add(key)
+            traffic[key] = {"dram_bytes_per_launch": val("dram__bytes_read.sum") + val("dram__bytes_write.sum"),
+                            "time_ns": val("gpu__time_duration.sum"), "cells": CELLS[wl],
+                            "source": f"ncu --set full --clock-control none, {wl} Kuhn box, one launch "
+                                      f"({os.path.relpath(DST, ROOT)}/ncu_full_{wl}.csv)"}
+        json.dump(traffic, open(tpath, "w"), indent=1)
+        open(os.path.join(DST, f"ncu_full_{wl}.csv"), "w").write(raw)
     pk = os.path.join(SRC, "peaks.json")
     if os.path.exists(pk):
         shutil.copy(pk, os.path.join(ROOT, "profiles", "fp64_peak.json"))
-    for f in ("launches_c2.csv",):
+    for f in ("launches_c2.csv", "launches_c5.csv", "launches_c5.csv.gz"):
         if os.path.exists(os.path.join(SRC, f)):
             shutil.copy(os.path.join(SRC, f), os.path.join(DST, f))
     print(json.dumps(flops, indent=1))

@@ -40,6 +40,29 @@ def test_kuhn_multirank_bitwise(cuda_ok, world):
     assert mesh.info(0)["n_peers"] >= 1
 
 
+@pytest.mark.parametrize("world", [2, 4])
+def test_region_meshes_multirank_bitwise(cuda_ok, world):
+    """Per-rank region builds (hgks_mesh_desc.rank_only, what each process of a multi-GPU run
+    builds): one mesh object per rank, the loopback group's put map assembled from the ranks'
+    own plans; 10 steps bitwise equal to one rank (the partition is plain RCB here)."""
+    mi = W.kuhn_box(10, 8, 8, h=0.2)
+    Q0 = W.advection_ic(mi)
+    cfg = hgks.SolverConfig(cfl=0.3)
+    s1 = hgks.Solver(hgks.Mesh(mi), Q0, cfg)
+    s1.step(10)
+    Q1, _, t1 = s1.get_state()
+    meshes = [hgks.Mesh(mi, n_ranks=world, rank=r) for r in range(world)]
+    solvers = [hgks.Solver(meshes[r], Q0, cfg, rank=r, transport=hgks.TRANSPORT_LOOPBACK) for r in range(world)]
+    hgks.group_step(solvers, 10)
+    Q = np.empty_like(Q0)
+    for s in solvers:
+        s.step(0)
+        Qr, gid, tr = s.get_state()
+        Q[gid] = Qr
+        assert tr == t1
+    assert np.array_equal(Q, Q1), np.abs(Q - Q1).max()
+
+
 def test_loopback_solver_rejects_plain_step(cuda_ok):
     """A loopback solver of a multi-rank group has no exchange of its own: hgks_step with
     n_steps > 0 fails with HGKS_E_STATE (n_steps = 0, the sync/report call, is allowed)."""
