@@ -465,9 +465,6 @@ __global__ void __launch_bounds__(ReconShape<K>::BT, ReconShape<K>::MINB) k_reco
 #ifndef HGKS_RPAIR_MINB
 #define HGKS_RPAIR_MINB 3
 #endif
-#ifndef HGKS_RPAIR_DSPLIT
-#define HGKS_RPAIR_DSPLIT 1
-#endif
 template <int K, int M, int NM>
 __global__ void __launch_bounds__(128, HGKS_RPAIR_MINB) k_recon_pair(ReconArgs a) {
   constexpr int NS = 3;  // variable slots per lane
@@ -551,57 +548,6 @@ __global__ void __launch_bounds__(128, HGKS_RPAIR_MINB) k_recon_pair(ReconArgs a
 #if HGKS_RECON_NE
   p0_normal_equations<K, NS>(a, ci, sid, a.st_shift + tb * K + t, op2, V23, m2,
                              [&](int k, int v) { return dqs[k * QP + v * BT + tl]; }, c);
-#elif HGKS_RPAIR_DSPLIT
-  {
-    // P_0 split by COEFFICIENT between the two lanes of a cell: part 0 accumulates d = 0..4,
-    // part 1 d = 5..8, each for all five variables, so each lane streams (almost) only its
-    // own operator rows -- 11 of every 9 entry pairs per member pair are loaded in total
-    // instead of 18 -- then a shuffle transpose hands each lane its variable slots.
-    Real cp[5][5];
-#pragma unroll
-    for (int d = 0; d < 5; ++d)
-#pragma unroll
-      for (int v = 0; v < 5; ++v) cp[d][v] = Real(0.0);
-    // the five variables of member k from the two lanes' slot planes
-    const int tl0 = tl & ~1, tl1 = tl | 1;
-    __syncwarp();  // the partner lane's slot planes are written
-    auto dqf = [&](int k, int v) { return v < 3 ? dqs[k * QP + v * BT + tl0] : dqs[k * QP + (v - 3) * BT + tl1]; };
-    // member pair (k, k+1) = entry pairs 0..8 (entries k*9 + d): part 0 needs pairs 0, 1, 2.x,
-    // 4.y, 5, 6; part 1 needs 2.y, 3, 4.x, 7, 8
-    constexpr int kP0[6] = {0, 1, 2, 4, 5, 6}, kP1[6] = {2, 3, 4, 7, 8, 8};
-    constexpr int kUnrollD = K <= 16 ? 2 : 1;
-#pragma unroll kUnrollD
-    for (int k2 = 0; k2 < K; k2 += 2) {
-      Real dq[2][5];
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int v = 0; v < 5; ++v) dq[h][v] = dqf(k2 + h, v);
-      R2 w[6];
-#pragma unroll
-      for (int q = 0; q < 6; ++q) w[q] = __ldcs(op2 + (k2 * 9 / 2 + (part ? kP1[q] : kP0[q])) * kTile);
-      // entry j: coefficient d = j % 5 of this lane's range, member k2 + j / 5
-      const Real e0[10] = {w[0].x, w[0].y, w[1].x, w[1].y, w[2].x, w[3].y, w[4].x, w[4].y, w[5].x, w[5].y};
-      const Real e1[10] = {w[0].y, w[1].x, w[1].y, w[2].x, Real(0.0), w[3].x, w[3].y, w[4].x, w[4].y, Real(0.0)};
-#pragma unroll
-      for (int j = 0; j < 10; ++j) {
-        const Real wj = part ? e1[j] : e0[j];
-#pragma unroll
-        for (int v = 0; v < 5; ++v) cp[j % 5][v] = fma(wj, dq[j / 5][v], cp[j % 5][v]);
-      }
-    }
-    // transpose: part 0 keeps c[0..4][v0..2] and receives c[5..8][v0..2]; part 1 keeps
-    // c[5..8][v3, v4] and receives c[0..4][v3, v4] (slot 2 repeats v4)
-#pragma unroll
-    for (int d = 0; d < 9; ++d)
-#pragma unroll
-      for (int q = 0; q < NS; ++q) {
-        const int v1 = q == 0 ? 3 : 4;  // part 1's variable in slot q
-        const Real give = part ? (d >= 5 ? cp[d - 5][q] : Real(0.0)) : (d < 5 ? cp[d][v1] : Real(0.0));
-        const Real got = __shfl_xor_sync(0xffffffffu, give, 1);
-        c[d][q] = part ? (d >= 5 ? cp[d - 5][v1] : got) : (d < 5 ? cp[d][q] : got);
-      }
-  }
 #else
 #pragma unroll
   for (int d = 0; d < 9; ++d)
@@ -1995,8 +1941,14 @@ struct Launch {
   static GasR gas(const GasParams& g) { return make_gas(g); }
   template <int K, int M, int NM>
   static cudaError_t recon_smem() {
-    return cudaFuncSetAttribute(k_recon<K, M, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)ReconShape<K>::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(k_recon<K, M, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)ReconShape<K>::SMEM);
+#ifdef HGKS_RECON_CARVEOUT  // optional L1 / shared split hint (see HGKS_FLUX_CARVEOUT)
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_recon<K, M, NM>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               HGKS_RECON_CARVEOUT);
+#endif
+    return e;
   }
   template <int K, int M, int NM>
   static cudaError_t recon_pair_smem() {
@@ -2014,6 +1966,16 @@ struct Launch {
   }
   template <int NV, int STAGE, bool TAU0, int BC, int DQ0, bool PR>
   static void flux(int grid, cudaStream_t st, const FluxArgs& a) {
+#ifdef HGKS_FLUX_CARVEOUT
+    // optional L1 / shared-memory split hint for the flux kernels (percent of the unified
+    // capacity given to shared memory).  Not set by default: the driver's choice was as good
+    // as any pinned value in our A/B runs (profiles/r02/README.md, "L1 / shared split").
+    static bool carve = [] {
+      return cudaFuncSetAttribute(k_flux<NV, STAGE, TAU0, BC, DQ0, PR>,
+                                  cudaFuncAttributePreferredSharedMemoryCarveout, HGKS_FLUX_CARVEOUT) == cudaSuccess;
+    }();
+    (void)carve;
+#endif
     k_flux<NV, STAGE, TAU0, BC, DQ0, PR><<<grid, (NV == 3 ? 3 : 4) * HGKS_FLUX_FPB, 0, st>>>(a);
   }
   template <int NF>
