@@ -47,7 +47,7 @@ namespace {
 using Vec3 = std::array<double, 3>;
 using Mat3 = std::array<std::array<double, 3>, 3>;
 
-constexpr int kTet = 4, kHex = 8;
+constexpr int kTet = 4, kPrism = 6, kHex = 8;
 constexpr int kWall = 1, kFarfield = 2;
 
 Vec3 sub(const Vec3& a, const Vec3& b) { return {a[0] - b[0], a[1] - b[1], a[2] - b[2]}; }
@@ -92,6 +92,9 @@ struct Config {
 // VTK/Gmsh node order, 0 and 5 the opposed pair, 1..4 a ring (R17).
 const int kTetFace[4][3] = {{1, 2, 3}, {0, 2, 3}, {0, 1, 3}, {0, 1, 2}};
 const int kHexFace[6][4] = {{0, 1, 2, 3}, {0, 1, 5, 4}, {1, 2, 6, 5}, {2, 3, 7, 6}, {3, 0, 4, 7}, {4, 5, 6, 7}};
+// Triangular prism (VTK wedge order, reading R30): faces 0 / 1 the two triangles, 2..4 the
+// quadrilateral sides in ring order (side p joins triangle edges (p-2, p-1 mod 3)).
+const int kPrismFace[5][4] = {{0, 1, 2, -1}, {3, 4, 5, -1}, {0, 1, 4, 3}, {1, 2, 5, 4}, {2, 0, 3, 5}};
 
 struct CellGeom {
   double V = 0;
@@ -125,6 +128,35 @@ void cell_quadrature(int type, const std::vector<Vec3>& v, std::vector<Vec3>& pt
       pts.push_back(x);
       wts.push_back(V / 4.0);
     }
+  } else if (type == kPrism) {
+    // wedge map X = sum_a N_a v_a, N = (1-xi-eta, xi, eta) x (1-zeta, zeta): |J| is linear in
+    // (xi, eta) and quadratic in zeta, so Radon's 7-point degree-5 triangle rule x 3-point
+    // Gauss in zeta integrates (degree-2 poly) * |J| exactly
+    const double r15 = std::sqrt(15.0);
+    const double a1 = (9 - 2 * r15) / 21, b1 = (6 + r15) / 21, a2 = (9 + 2 * r15) / 21, b2 = (6 - r15) / 21;
+    const double w0 = 9.0 / 80, w1 = (155 + r15) / 2400, w2 = (155 - r15) / 2400;  // sum 1/2
+    const double tri[7][3] = {{1.0 / 3, 1.0 / 3, w0}, {a1, b1, w1}, {b1, a1, w1}, {b1, b1, w1},
+                              {a2, b2, w2}, {b2, a2, w2}, {b2, b2, w2}};
+    double g[3], gw[3];
+    gauss3(g, gw);
+    for (int q = 0; q < 7; ++q)
+      for (int k = 0; k < 3; ++k) {
+        const double xi = tri[q][0], et = tri[q][1], ze = g[k];
+        const double L[3] = {1 - xi - et, xi, et};
+        Vec3 X{0, 0, 0}, dxi{0, 0, 0}, det_{0, 0, 0}, dze{0, 0, 0};
+        for (int a = 0; a < 3; ++a) {
+          X = add(X, add(scale(v[a], L[a] * (1 - ze)), scale(v[a + 3], L[a] * ze)));
+          dze = add(dze, scale(sub(v[a + 3], v[a]), L[a]));
+        }
+        // d/dxi: L = (1-xi-eta, xi, eta) -> (-1, 1, 0); d/deta -> (-1, 0, 1)
+        const Vec3 b0 = add(scale(v[0], 1 - ze), scale(v[3], ze)), b1v = add(scale(v[1], 1 - ze), scale(v[4], ze)),
+                   b2v = add(scale(v[2], 1 - ze), scale(v[5], ze));
+        dxi = sub(b1v, b0);
+        det_ = sub(b2v, b0);
+        const double J = std::fabs(dot(dxi, cross(det_, dze)));
+        pts.push_back(X);
+        wts.push_back(tri[q][2] * gw[k] * J);
+      }
   } else {
     double g[3], gw[3];
     gauss3(g, gw);
@@ -256,10 +288,14 @@ struct Mesh {
   std::vector<double> h_dt;  // V_i / max_p S_ip (R6)
 };
 
-int n_faces_of(int t) { return t == kTet ? 4 : 6; }
+int n_faces_of(int t) { return t == kTet ? 4 : (t == kPrism ? 5 : 6); }
 
 std::vector<int> face_local_nodes(int t, int p) {
   if (t == kTet) return {kTetFace[p][0], kTetFace[p][1], kTetFace[p][2]};
+  if (t == kPrism) {
+    if (p < 2) return {kPrismFace[p][0], kPrismFace[p][1], kPrismFace[p][2]};
+    return {kPrismFace[p][0], kPrismFace[p][1], kPrismFace[p][2], kPrismFace[p][3]};
+  }
   return {kHexFace[p][0], kHexFace[p][1], kHexFace[p][2], kHexFace[p][3]};
 }
 
@@ -277,7 +313,8 @@ Mesh build_mesh(const MeshInputC& in) {
   m.cell_xyz.resize(m.n_cells);
   for (int i = 0; i < m.n_cells; ++i) {
     int t = in.type[i];
-    if (t != kTet && t != kHex) throw OracleError(E_MESH, "unsupported element at cell " + std::to_string(i));
+    if (t != kTet && t != kPrism && t != kHex)
+      throw OracleError(E_MESH, "unsupported element at cell " + std::to_string(i));
     m.type[i] = t;
     for (int k = 0; k < t; ++k) {
       int64_t nd = in.cell_nodes[(int64_t)i * 8 + k];
@@ -506,6 +543,15 @@ Mesh build_mesh(const MeshInputC& in) {
             if (nn.id >= m.n_cells) pushm({nn.id, im.s});
             else pushm({nn.id, add(im.s, nn.s)});
           }
+        m.subs[i].push_back(Sm);
+      }
+    } else if (m.type[i] == kPrism) {
+      // R30 (the paper gives no prism rule; the hex pattern of P:390-395 transferred): one
+      // triangle neighbour (face 0 or 1) with two ring-adjacent side neighbours, 2 x 3 = 6
+      const int ps[6][3] = {{0, 2, 3}, {0, 3, 4}, {0, 4, 2}, {1, 2, 3}, {1, 3, 4}, {1, 4, 2}};
+      for (int mm = 0; mm < 6; ++mm) {
+        std::vector<Member> Sm;
+        for (int k = 0; k < 3; ++k) Sm.push_back(F[ps[mm][k]]);
         m.subs[i].push_back(Sm);
       }
     } else {

@@ -15,6 +15,9 @@ Workloads:
     p = 1, U = V = W = 1, as EXACT cell averages (reading R5).
   * Cubed-sphere hexahedral shell (C3/C4): six blocks of
     N x N x 2N hexahedra (the grading and outer radius are readings R24).
+  * Hybrid tet/prism box (BASELINE configs[2] "mixed tet/prism cells"): the
+    Kuhn box with its lowest z-layers of cubes cut into two triangular prisms each instead of
+    six tets (conforming: both cut the cube's horizontal faces along the same diagonal).
 """
 from __future__ import annotations
 
@@ -24,6 +27,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 TET = 4
+PRISM = 6  # triangular prism (VTK wedge node order: 0-1-2 one triangle, 3-4-5 the other, i+3 above i)
 HEX = 8
 BC_WALL = 1
 BC_FARFIELD = 2
@@ -101,6 +105,56 @@ def kuhn_box(nx: int, ny: int | None = None, nz: int | None = None, h: float | N
         periodic_length=np.array([nx * h, ny * h, nz * h], dtype=np.float64),
         periodic_origin=np.zeros(3),
         name=f"kuhn_{nx}x{ny}x{nz}" + ("_jit" if jitter > 0 else ""),
+    )
+
+
+def hybrid_box(n: int, prism_layers: int | None = None, h: float | None = None, jitter: float = 0.0,
+               seed: int = 656) -> MeshInput:
+    """Periodic n^3 box of cubes (edge h = 2/n): the cubes of the lowest ``prism_layers``
+    z-layers (default n // 2) are cut along the x-y diagonal (0,0)-(1,1) into two triangular
+    prisms, the others into the six Kuhn tets of ``kuhn_box``.  The Kuhn split cuts a cube's
+    bottom and top faces along the same diagonal, so prism and tet layers meet conformingly
+    (also across the periodic z wrap).  ``jitter`` moves interior nodes as in ``kuhn_box``."""
+    prism_layers = n // 2 if prism_layers is None else prism_layers
+    h = 2.0 / n if h is None else h
+    ii, jj, kk = np.meshgrid(np.arange(n + 1), np.arange(n + 1), np.arange(n + 1), indexing="ij")
+    xyz = np.stack([ii, jj, kk], axis=-1).reshape(-1, 3).astype(np.float64) * h
+
+    def nid(i, j, k):
+        return (i * (n + 1) + j) * (n + 1) + k
+
+    ci, cj, ck = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
+    ci, cj, ck = ci.ravel(), cj.ravel(), ck.ravel()
+    cells, types = [], []
+    for c in range(ci.size):
+        i, j, k = int(ci[c]), int(cj[c]), int(ck[c])
+        v = lambda a, b, d: nid(i + a, j + b, k + d)  # noqa: E731
+        if k < prism_layers:
+            for tri in (((0, 0), (1, 0), (1, 1)), ((0, 0), (1, 1), (0, 1))):
+                cells.append([v(a, b, 0) for a, b in tri] + [v(a, b, 1) for a, b in tri] + [-1, -1])
+                types.append(PRISM)
+        else:
+            for perm in KUHN_PERMS:
+                pos = [i, j, k]
+                row = [nid(*pos)]
+                for axis in perm:
+                    pos[axis] += 1
+                    row.append(nid(*pos))
+                cells.append(row + [-1, -1, -1, -1])
+                types.append(TET)
+    if jitter > 0.0:
+        rng = np.random.default_rng(seed)
+        d = rng.uniform(-jitter * h, jitter * h, size=xyz.shape)
+        L = np.array([n, n, n]) * h
+        interior = np.all((xyz > 0.5 * h * 1e-6) & (xyz < L - 0.5 * h * 1e-6), axis=1)
+        xyz = xyz + d * interior[:, None]
+    return MeshInput(
+        xyz=xyz,
+        cell_type=np.array(types, dtype=np.int8),
+        cell_nodes=np.array(cells, dtype=np.int64),
+        periodic_length=np.array([n * h, n * h, n * h]),
+        periodic_origin=np.zeros(3),
+        name=f"hybrid_{n}_{prism_layers}" + ("_jit" if jitter > 0 else ""),
     )
 
 
@@ -365,9 +419,9 @@ def uniform_state(n_cells: int, rho: float, vel, p: float, gamma: float = 1.4) -
 
 def cell_centroids_simple(mesh: MeshInput) -> np.ndarray:
     """Vertex average (used only to place input patterns, never by the method)."""
-    k = np.where(mesh.cell_type == TET, 4, 8)
+    k = mesh.cell_type.astype(np.int64)  # node count = type code (TET 4, PRISM 6, HEX 8)
     out = np.zeros((mesh.n_cells, 3))
-    for nv in (4, 8):
+    for nv in (4, 6, 8):
         m = k == nv
         if m.any():
             out[m] = mesh.xyz[mesh.cell_nodes[m, :nv]].mean(axis=1)

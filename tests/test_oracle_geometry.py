@@ -166,3 +166,123 @@ def test_hex_box_stencil_24_and_substencils():
 def test_tiny_periodic_box_rejected():
     with pytest.raises(O.OracleError):
         O.OracleMesh(W.kuhn_box(2))
+
+
+# --------------------------------------------------------------------------- #
+# triangular prisms (reading R30)
+# --------------------------------------------------------------------------- #
+def single_prism(v):
+    xyz = np.asarray(v, float)
+    cn = np.full((1, 8), -1, np.int64)
+    cn[0, :6] = np.arange(6)
+    faces = [[0, 1, 2], [3, 4, 5], [0, 1, 4, 3], [1, 2, 5, 4], [2, 0, 3, 5]]
+    bf = np.full((5, 4), -1, np.int64)
+    for k, f in enumerate(faces):
+        bf[k, :len(f)] = f
+    return W.MeshInput(xyz=xyz, cell_type=np.array([W.PRISM], np.int8), cell_nodes=cn, bface_nodes=bf,
+                       bface_tag=np.full(5, W.BC_WALL, np.int32))
+
+
+def tet_moments(v):
+    """V, centroid, M2 of a tet from its vertices (closed forms, independent of the oracle)."""
+    v = np.asarray(v, float)
+    V = abs(np.linalg.det(v[1:] - v[0])) / 6.0
+    c = v.mean(0)
+    d = v - c
+    return V, c, (d.T @ d) / 20.0
+
+
+def test_right_prism_closed_forms():
+    """Unit right prism (triangle (0,0),(1,0),(0,1) x [0,1]): V = 1/2, centroid (1/3, 1/3, 1/2),
+    var x = var y = 1/18, cov xy = -1/36, var z = 1/12; five faces, two triangles + three quads."""
+    m = O.OracleMesh(single_prism([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1], [1, 0, 1], [0, 1, 1]]))
+    V, c, M2 = m.geometry()
+    assert abs(V[0] - 0.5) < 1e-15 and np.allclose(c[0], [1 / 3, 1 / 3, 0.5], atol=1e-15)
+    exp = np.array([[1 / 18, -1 / 36, 0], [-1 / 36, 1 / 18, 0], [0, 0, 1 / 12]])
+    assert np.allclose(M2[0], exp, atol=1e-15)
+    f = m.faces()
+    assert m.n_faces == 5 and sorted(f["ngp"].tolist()) == [3, 3, 4, 4, 4]
+
+
+def test_oblique_prism_vs_three_tets():
+    """A skewed straight prism (top = bottom + a shift, planar faces) is exactly the union of
+    the tets (A,B,C,D), (B,C,D,E), (C,D,E,F): V, centroid and M2 from their closed forms."""
+    A, B, C = np.array([0.1, 0.0, 0.2]), np.array([1.3, 0.2, 0.0]), np.array([0.4, 1.1, 0.3])
+    t = np.array([0.3, -0.2, 0.9])
+    v = [A, B, C, A + t, B + t, C + t]
+    m = O.OracleMesh(single_prism(v))
+    V, c, M2 = m.geometry()
+    parts = [tet_moments([v[0], v[1], v[2], v[3]]), tet_moments([v[1], v[2], v[3], v[4]]),
+             tet_moments([v[2], v[3], v[4], v[5]])]
+    Vt = sum(p[0] for p in parts)
+    ct = sum(p[0] * p[1] for p in parts) / Vt
+    St = sum(p[0] * (p[2] + np.outer(p[1] - ct, p[1] - ct)) for p in parts) / Vt
+    assert abs(V[0] - Vt) < 1e-14 and np.allclose(c[0], ct, atol=1e-14)
+    assert np.allclose(M2[0], St, atol=1e-14)
+
+
+def hybrid_adjacency(mi, N):
+    """Face neighbours of the periodic hybrid box from wrapped node keys (independent of the
+    oracle); faces of a prism in R30's order (0/1 triangles, 2..4 sides)."""
+    ijk = np.rint(mi.xyz / (2.0 / N)).astype(int) % N
+    wrapped = ijk[:, 0] * N * N + ijk[:, 1] * N + ijk[:, 2]
+    tet_f = [[1, 2, 3], [0, 2, 3], [0, 1, 3], [0, 1, 2]]
+    pri_f = [[0, 1, 2], [3, 4, 5], [0, 1, 4, 3], [1, 2, 5, 4], [2, 0, 3, 5]]
+    owners = {}
+    for c in range(mi.n_cells):
+        fl = tet_f if mi.cell_type[c] == W.TET else pri_f
+        for p, f in enumerate(fl):
+            owners.setdefault(tuple(sorted(wrapped[mi.cell_nodes[c, f]])), []).append((c, p))
+    nb = [[-1] * (4 if mi.cell_type[c] == W.TET else 5) for c in range(mi.n_cells)]
+    for key, cp in owners.items():
+        assert len(cp) == 2, key
+        (a, pa), (b, pb) = cp
+        nb[a][pa] = b
+        nb[b][pb] = a
+    return nb
+
+
+def test_hybrid_box_connectivity_and_closure():
+    """Hybrid tet/prism box: every face matched (conforming layers, periodic), sum V = V_D,
+    closed cells, big stencil = depth-2 BFS, prism sub-stencils = R30 (one triangle neighbour +
+    two ring-adjacent sides), tet sub-stencils = R16 with all the other face neighbours of a
+    prism neighbour (7 members)."""
+    N = 6
+    mi = W.hybrid_box(N)
+    nb = hybrid_adjacency(mi, N)
+    m = O.OracleMesh(mi)
+    V, c, _ = m.geometry()
+    assert abs(V[: m.n_cells].sum() - 8.0) < 1e-12
+    f = m.faces()
+    cf = m.cell_faces()
+    for i in range(0, m.n_cells, 5):
+        s = np.zeros(3)
+        for p in range(6):
+            fi = cf[i, p]
+            if fi < 0:
+                continue
+            sg = 1.0 if f["owner"][fi] == i else -1.0
+            ng = f["ngp"][fi]
+            s += sg * (f["gp_wS"][fi, :ng, None] * f["gp_n"][fi, :ng]).sum(0)
+        assert np.abs(s).max() < 1e-14
+    ps = [(0, 2, 3), (0, 3, 4), (0, 4, 2), (1, 2, 3), (1, 3, 4), (1, 4, 2)]
+    tri = [(0, 1, 2), (0, 1, 3), (1, 2, 3), (2, 0, 3)]
+    saw7 = False
+    for i in range(m.n_cells):
+        ids, _ = m.big_stencil(i)
+        bfs = set(nb[i]) | set().union(*[set(nb[j]) for j in nb[i]])
+        bfs.discard(i)
+        assert set(ids.tolist()) == bfs and list(ids[:len(nb[i])]) == nb[i]
+        if mi.cell_type[i] == W.PRISM:
+            for mm, t in enumerate(ps):
+                assert list(m.sub_stencil(i, mm)) == [nb[i][q] for q in t]
+        else:
+            for mm in range(4):
+                exp = [nb[i][q] for q in tri[mm]]
+                for x in nb[nb[i][mm]]:
+                    if x != i and x not in exp:
+                        exp.append(x)
+                sub = list(m.sub_stencil(i, mm))
+                assert sub == exp, (i, mm)
+                saw7 |= len(sub) == 7
+    assert saw7  # tets next to prism layers
