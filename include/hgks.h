@@ -2,13 +2,13 @@
  * hgks.h -- C-ABI of the B200-native HGKS hot path (libhgks.so).
  *
  * The library advances the high-order gas-kinetic scheme of Wang, Cao & Pan,
- * arXiv 2407.00656 (PAPER.md, cited "P:n"), on tetrahedral and hexahedral
- * unstructured meshes, on one CUDA device per process:
+ * arXiv 2407.00656 (PAPER.md, cited "P:n"), on tetrahedral, hexahedral and hybrid
+ * tetrahedral/prismatic unstructured meshes, on one CUDA device per process:
  *   - third-order WENO reconstruction per cell      (Eqs. polys/weno)
  *   - BGK gas-kinetic flux per face Gauss point      (Eqs. flux-G/flux)
  *   - two-stage fourth-order update + CFL minimum    (Alg. 2)
  *   - halo exchange of 3 ghost layers + min(dt), NCCL
- * Readings of points where the paper is silent are DESIGN.md R1-R28.
+ * Readings of points where the paper is silent are DESIGN.md R1-R30.
  *
  * Conventions for every call:
  *   - Return value: HGKS_OK (0) or an error code below; nothing throws or
@@ -46,6 +46,7 @@ typedef int32_t hgks_status;
 #define HGKS_E_STATE 7      /* dt <= 0 / non-finite state */
 
 #define HGKS_TET 4
+#define HGKS_PRISM 6        /* triangular prism (wedge); mixes with tets only (R30) */
 #define HGKS_HEX 8
 #define HGKS_BC_WALL 1      /* no-slip adiabatic wall (R25) */
 #define HGKS_BC_FARFIELD 2  /* Riemann-invariant inlet/outlet (R25) */
@@ -57,9 +58,12 @@ typedef struct hgks_solver hgks_solver;
 typedef struct {
   const double* xyz;          /* [n_nodes][3] node coordinates */
   int64_t n_nodes;
-  const int8_t* cell_type;    /* [n_cells] HGKS_TET or HGKS_HEX */
+  const int8_t* cell_type;    /* [n_cells] all HGKS_HEX, or any mix of HGKS_TET and HGKS_PRISM
+                                 (other mixes: HGKS_E_MESH) */
   const int64_t* cell_nodes;  /* [n_cells][8], -1 padded; tet: 4 nodes, face p opposite node p
-                                 (P:541-549); hex: VTK order, faces 0/5 = (0123)/(4567) (R17) */
+                                 (P:541-549); hex: VTK order, faces 0/5 = (0123)/(4567) (R17);
+                                 prism: VTK wedge order, triangles (012)/(345), sides (0143),
+                                 (1254), (2035) (R30) */
   int64_t n_cells;
   double periodic_origin[3];  /* periodic box; length 0 along an axis = not periodic (R23) */
   double periodic_length[3];
@@ -132,7 +136,8 @@ typedef struct {
   int64_t n_faces;           /* faces whose flux this rank computes */
   int64_t n_faces_bc;        /* ... of which wall/farfield faces */
   int32_t stencil_min, stencil_max;  /* big stencil sizes over owned cells (self excluded) */
-  int32_t n_sub;             /* sub-stencils per cell (4 tet, 8 hex) */
+  int32_t n_sub;             /* sub-stencils per cell (4 tet, 8 hex; hybrid meshes: 6, the most a
+                                 cell has -- prisms 6, tets 4) */
   int32_t n_peers;           /* ranks this rank exchanges ghosts with */
   int64_t send_cells, recv_cells;    /* per stage */
   int64_t edge_cut;          /* faces between different ranks (global; RCB + FM boundary refinement);

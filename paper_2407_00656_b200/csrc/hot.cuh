@@ -118,6 +118,7 @@ struct ReconArgs {
   const int* __restrict__ recon_cell;   // [n_recon] local cell id
   const int* __restrict__ st_id;        // [K] per cell, tiled: stencil member local ids
   const uint8_t* __restrict__ sub_slot; // [M*NM] per cell, tiled: sub-stencil member -> big-stencil slot
+  const uint8_t* __restrict__ n_sub;    // [ld] sub-stencils per cell (hybrid layouts, NM = 7), else null
   const uint8_t* __restrict__ st_shift;  // [K] per cell, tiled: periodic image code of each member (NE)
   const Real* __restrict__ cgeo;      // [n_local][10]: centroid, M2 of every local row (NE)
   Real per_len[3];                    // periodic box lengths (member images, NE)
@@ -379,12 +380,17 @@ __global__ void __launch_bounds__(ReconShape<K>::BT, ReconShape<K>::MINB) k_reco
     }
   };
   // ---- pass 1: beta_m and the nonlinear weights ----
-  const Real gm = Real(0.025), g0 = Real(1.0) - Real(0.025) * M;
+  // Hybrid layouts (NM = 7, f4): M is the capacity and this cell has mc of them (tets 4,
+  // prisms 6, R30), so gamma_0 = 1 - 0.025 mc; sub-stencils m >= mc get weight 0.
+  constexpr bool kVarM = NM == 7;
+  const int mc = kVarM ? (int)__ldg(a.n_sub + (size_t)tile * kTile + t) : M;
+  const Real gm = Real(0.025), g0 = Real(1.0) - Real(0.025) * mc;
   Real al0[5], alm[M][5];
   {
     Real tz[5] = {0, 0, 0, 0, 0};
 #pragma unroll
     for (int m = 0; m < M; ++m) {
+      if (kVarM && m >= mc) continue;
       Real b[3][5];
       sub_slopes(m, b);
 #pragma unroll
@@ -395,12 +401,13 @@ __global__ void __launch_bounds__(ReconShape<K>::BT, ReconShape<K>::MINB) k_reco
     }
 #pragma unroll
     for (int v = 0; v < 5; ++v) {
-      const Real tzv = tz[v] * (Real(1.0) / M);
+      const Real tzv = kVarM ? tz[v] / Real(mc) : tz[v] * (Real(1.0) / M);
       const Real r0 = tzv / (beta0[v] + a.eps);
       const Real w0 = g0 * (Real(1.0) + (a.omega_pow == 2 ? r0 * r0 : r0));
       Real sum = w0;
 #pragma unroll
       for (int m = 0; m < M; ++m) {
+        if (kVarM && m >= mc) continue;
         const Real rm = tzv / (alm[m][v] + a.eps);
         alm[m][v] = gm * (Real(1.0) + (a.omega_pow == 2 ? rm * rm : rm));  // omega_m
         sum += alm[m][v];
@@ -408,7 +415,8 @@ __global__ void __launch_bounds__(ReconShape<K>::BT, ReconShape<K>::MINB) k_reco
       const Real inv = Real(1.0) / sum;
       al0[v] = w0 * inv / g0;  // omega-bar_0 / gamma_0
 #pragma unroll
-      for (int m = 0; m < M; ++m) alm[m][v] = alm[m][v] * inv - al0[v] * gm;  // omega-bar_m - omega-bar_0 gamma_m/gamma_0
+      for (int m = 0; m < M; ++m)  // omega-bar_m - omega-bar_0 gamma_m/gamma_0
+        alm[m][v] = (kVarM && m >= mc) ? Real(0.0) : alm[m][v] * inv - al0[v] * gm;
     }
   }
   // ---- collapse to one quadratic ----
@@ -419,6 +427,7 @@ __global__ void __launch_bounds__(ReconShape<K>::BT, ReconShape<K>::MINB) k_reco
     for (int v = 0; v < 5; ++v) lin[d][v] = al0[v] * c[d][v];
 #pragma unroll
   for (int m = 0; m < M; ++m) {  // pass 2: weighted sum of the sub-stencil slopes
+    if (kVarM && m >= mc) continue;
     Real b[3][5];
     sub_slopes(m, b);
 #pragma unroll

@@ -31,7 +31,7 @@ constexpr int kMaxStencil = 40;  // big-stencil capacity (tet 14-16, hex interio
 
 // Sizes of the per-cell device records for one mesh kind.
 struct Layout {
-  int cell_type = 4;   // 4 tet, 8 hex (meshes are single-kind)
+  int cell_type = 4;   // 4 tet, 8 hex, 6 hybrid tet/prism (cells of several kinds, f4)
   int nfaces = 4;      // faces per cell
   int ngp = 3;         // Gauss points per face (R10)
   int nv = 3;          // vertices per face
@@ -57,6 +57,7 @@ struct GlobalMesh {
   std::vector<int32_t> f_bc, f_ghost;
   std::vector<double> f_shift;          // [nf][3] neighbour image = neighbour + shift
   std::vector<double> f_vert;           // [nf][4][3] vertices, oriented out of the owner
+  std::vector<int8_t> f_nv;             // [nf] vertex count (3 or 4)
   std::vector<double> f_area;
   std::vector<int64_t> cell_face;       // [nc][6]
   // boundary-condition ghosts (one per wall/farfield face)
@@ -85,6 +86,12 @@ struct GlobalMesh {
   int64_t edge_cut_rcb = 0;   // the same for the plain RCB partition (before refinement)
 };
 
+// One kind of face (triangles, quadrilaterals) of a rank's face list: its faces are
+// [base, base + n_if + n_wf + n_ff), interior (early ones first), wall, farfield.
+struct FaceClass {
+  int64_t base = 0, n_if_early = 0, n_if = 0, n_wf = 0, n_ff = 0;
+};
+
 // One rank's device-ready arrays.  Local cell order:
 //   [ owned (Morton order) | partition ghosts grouped by owner rank |
 //     boundary ghosts ]
@@ -106,12 +113,16 @@ struct RankPlan {
   std::vector<double> op;               // [op_entries] per cell, tiled entry-major (kernels.cuh k_recon)
   std::vector<double> geo;              // [8] per cell, tiled: V^{2/3}, V^{4/3}, M2 (xx,yy,zz,xy,xz,yz)
   // faces: interior [0, n_if), wall [n_if, n_if + n_wf), farfield after
-  int64_t n_faces = 0, n_if = 0, n_if_early = 0, n_wf = 0, n_ff = 0;  // interior faces [0, n_if_early) need no ghosts
+  // (totals over the face kinds; interior faces [base, base + n_if_early) of a kind need no ghosts)
+  int64_t n_faces = 0, n_if = 0, n_if_early = 0, n_wf = 0, n_ff = 0;
+  FaceClass fcls[2];                    // triangles, then quadrilaterals
   std::vector<int32_t> f_cells;         // [n_faces][2] local owner / neighbour (bc faces: ghost id)
   std::vector<double> f_geo;            // [n_faces][FG]: nv vertices rel. owner centroid, then d (3)
   int f_geo_stride = 12;
   // update: owned cells
   std::vector<int32_t> cf;              // [nfaces][n_owned] local face id, ~id when not the owner
+                                        // (n_faces: a zero row, for cells with fewer faces)
+  std::vector<uint8_t> n_sub;           // [ld] sub-stencils per reconstructed cell (hybrid layouts only)
   std::vector<double> inv_v, h_dt;      // [n_owned]
   // boundary ghosts
   std::vector<int32_t> bg_cell, bg_bc;  // [n_bghost]

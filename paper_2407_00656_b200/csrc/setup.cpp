@@ -46,9 +46,24 @@ inline double dotp(P3 a, P3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
 inline P3 crossp(P3 a, P3 b) { return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x}; }
 inline double len(P3 a) { return std::sqrt(dotp(a, a)); }
 
-// tet face p = nodes other than p; hex faces, VTK order (R17)
+// tet face p = nodes other than p; hex faces, VTK order (R17); prism (wedge)
+// faces: the two triangles, then the three sides, VTK order (R30)
 const int kTetF[4][3] = {{1, 2, 3}, {0, 2, 3}, {0, 1, 3}, {0, 1, 2}};
 const int kHexF[6][4] = {{0, 1, 2, 3}, {0, 1, 5, 4}, {1, 2, 6, 5}, {2, 3, 7, 6}, {3, 0, 4, 7}, {4, 5, 6, 7}};
+const int kPriF[5][4] = {{0, 1, 2, -1}, {3, 4, 5, -1}, {0, 1, 4, 3}, {1, 2, 5, 4}, {2, 0, 3, 5}};
+
+// cell kinds are coded by their node count: 4 tet, 6 prism, 8 hex
+inline int cell_nfaces(int t) { return t == 4 ? 4 : (t == 6 ? 5 : 6); }
+// node slots of face p of a cell of kind t; returns the face's vertex count
+inline int face_slots(int t, int p, int s[4]) {
+  if (t == 4) {
+    for (int q = 0; q < 3; ++q) s[q] = kTetF[p][q];
+    return 3;
+  }
+  const int* f = t == 6 ? kPriF[p] : kHexF[p];
+  for (int q = 0; q < 4; ++q) s[q] = f[q];
+  return (t == 6 && p < 2) ? 3 : 4;
+}
 
 // --- cell geometry (a0) ------------------------------------------------------
 void tet_geometry(const P3 v[4], double& V, P3& c, double m2[6]) {
@@ -104,6 +119,55 @@ void hex_geometry(const P3 v[8], double& V, P3& c, double m2[6]) {
     m2[0] += w * e.x * e.x; m2[1] += w * e.y * e.y; m2[2] += w * e.z * e.z;
     m2[3] += w * e.x * e.y; m2[4] += w * e.x * e.z; m2[5] += w * e.y * e.z;
   }
+}
+
+// Wedge map x = sum_a lam_a(r, s) ((1 - u) v_a + u v_{a+3}), lam = (1 - r - s, r, s): the
+// Jacobian is linear in (r, s) and quadratic in u, so V, the centroid and M2 need a rule exact
+// to degree 3 in (r, s) and 4 in u.  The triangle is collapsed from the unit square
+// (r = X, s = Y (1 - X), dr ds = (1 - X) dX dY: degree <= 4 in X, 3 in Y), so 3-point Gauss in
+// X, Y and u is exact.
+void prism_geometry(const P3 v[6], double& V, P3& c, double m2[6]) {
+  const double s = std::sqrt(0.15);
+  const double gx[3] = {0.5 - s, 0.5, 0.5 + s}, gw[3] = {5.0 / 18.0, 4.0 / 9.0, 5.0 / 18.0};
+  P3 X[27];
+  double W[27];
+  int q = 0;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      for (int k = 0; k < 3; ++k, ++q) {
+        const double r = gx[i], t = gx[j] * (1.0 - gx[i]), u = gx[k];
+        const double lam[3] = {1.0 - r - t, r, t};
+        P3 x{0, 0, 0}, du{0, 0, 0};
+        for (int a = 0; a < 3; ++a) {
+          x = x + lam[a] * ((1.0 - u) * v[a] + u * v[a + 3]);
+          du = du + lam[a] * (v[a + 3] - v[a]);
+        }
+        // d/dr and d/ds of the map: dlam/dr = (-1, 1, 0), dlam/ds = (-1, 0, 1)
+        const P3 b0 = (1.0 - u) * v[0] + u * v[3], b1 = (1.0 - u) * v[1] + u * v[4], b2 = (1.0 - u) * v[2] + u * v[5];
+        const P3 dr = b1 - b0, ds = b2 - b0;
+        X[q] = x;
+        W[q] = gw[i] * gw[j] * gw[k] * (1.0 - gx[i]) * std::fabs(dotp(dr, crossp(ds, du)));
+      }
+  V = 0;
+  P3 acc{0, 0, 0};
+  for (int k = 0; k < 27; ++k) {
+    V += W[k];
+    acc = acc + W[k] * X[k];
+  }
+  c = (1.0 / V) * acc;
+  for (int k = 0; k < 6; ++k) m2[k] = 0;
+  for (int k = 0; k < 27; ++k) {
+    P3 e = X[k] - c;
+    double w = W[k] / V;
+    m2[0] += w * e.x * e.x; m2[1] += w * e.y * e.y; m2[2] += w * e.z * e.z;
+    m2[3] += w * e.x * e.y; m2[4] += w * e.x * e.z; m2[5] += w * e.y * e.z;
+  }
+}
+
+void cell_geometry(int t, const P3* v, double& V, P3& c, double m2[6]) {
+  if (t == 4) tet_geometry(v, V, c, m2);
+  else if (t == 6) prism_geometry(v, V, c, m2);
+  else hex_geometry(v, V, c, m2);
 }
 
 // Face Gauss points (R10): positions, unit normals along the vertex order's
@@ -215,7 +279,7 @@ static void refine_partition(GlobalMesh& gm, int nfc) {
     int own = 0, nb_part[6], nb_cnt[6], nn = 0;
     for (int q = 0; q < nfc; ++q) {
       const int64_t j = gm.nbr_id[i * 6 + q];
-      if (j >= nc) continue;  // boundary ghost
+      if (j < 0 || j >= nc) continue;  // boundary ghost, or no face q (a tet of a hybrid mesh)
       const int r = gm.part[j];
       if (r == p) { ++own; continue; }
       int k = 0;
@@ -268,7 +332,7 @@ static void refine_partition(GlobalMesh& gm, int nfc) {
       if (cum > best_cum) { best_cum = cum; best_len = moves.size(); }
       for (int q = 0; q < nfc; ++q) {
         const int64_t j = gm.nbr_id[i * 6 + q];
-        if (j < nc && !locked[j]) push(j);
+        if (j >= 0 && j < nc && !locked[j]) push(j);
       }
       if (cum < best_cum - 64) break;  // a long losing streak: stop the pass early
     }
@@ -290,32 +354,38 @@ static void refine_partition(GlobalMesh& gm, int nfc) {
 static void build_core(GlobalMesh& gm, const double* xyz, int64_t n_nodes, const int8_t* type, const int64_t* cn,
                        int64_t n_cells, const double* per_origin, const double* per_len,
                        const int64_t* bface_nodes, const int32_t* bface_tag, int64_t n_bf,
-                       const std::vector<char>* open_ok, const std::vector<char>* stencil_ok) {
+                       const std::vector<char>* open_ok, const std::vector<char>* stencil_ok,
+                       bool hybrid = false) {
   PhaseTimer pt("mesh core");
   if (n_cells <= 0 || n_nodes <= 0 || !xyz || !type || !cn) throw Error(1, "empty mesh");
   gm.nc = n_cells;
   gm.type.assign(type, type + n_cells);
-  const int ct = type[0];
-  if (ct != 4 && ct != 8) throw Error(2, "unsupported element at cell 0");
-  for (int64_t i = 0; i < n_cells; ++i)
-    if (type[i] != ct) throw Error(2, "mixed element kinds are not supported (cell " + std::to_string(i) + ")");
+  // single-kind tet or hex meshes, or hybrid tet/prism meshes (f4, R30; hybrid: the whole
+  // mesh has prisms, so a region without any gets the same layout as the others)
+  bool any_prism = hybrid;
+  for (int64_t i = 0; i < n_cells; ++i) any_prism |= type[i] == 6;
+  const int ct = any_prism ? 6 : type[0];
   Layout& L = gm.lay;
   L.cell_type = ct;
-  L.nfaces = ct == 4 ? 4 : 6;
+  L.nfaces = cell_nfaces(ct);
   L.ngp = ct == 4 ? 3 : 4;
   L.nv = ct == 4 ? 3 : 4;
-  L.M = ct == 4 ? 4 : 8;
-  L.NM = ct == 4 ? 6 : 3;
+  // sub-stencils: tets 4 (R16, up to 6 members; 7 next to a prism), prisms 6 (R30), hexes 8
+  L.M = ct == 4 ? 4 : (ct == 6 ? 6 : 8);
+  L.NM = ct == 4 ? 6 : (ct == 6 ? 7 : 3);
   for (int a = 0; a < 3; ++a) gm.per_len[a] = per_len ? per_len[a] : 0.0;
   const double O[3] = {per_origin ? per_origin[0] : 0.0, per_origin ? per_origin[1] : 0.0,
                        per_origin ? per_origin[2] : 0.0};
   auto node = [&](int64_t id) { return P3{xyz[3 * id], xyz[3 * id + 1], xyz[3 * id + 2]}; };
-  const int nfc = L.nfaces, nvf = L.nv;
-  for (int64_t i = 0; i < n_cells; ++i)
-    for (int k = 0; k < ct; ++k) {
-      int64_t v = cn[i * 8 + k];
-      if (v < 0 || v >= n_nodes) throw Error(2, "invalid node id in cell " + std::to_string(i));
-    }
+  const int nfc = L.nfaces;  // half-face stride per cell (cells of a hybrid mesh use their first nf(i))
+  auto nf_of = [&](int64_t i) { return cell_nfaces(type[i]); };
+  // node ids of face p of cell i, returns its vertex count
+  auto fnodes = [&](int64_t i, int p, int64_t nd[4]) {
+    int sl[4];
+    const int nv = face_slots(type[i], p, sl);
+    for (int q = 0; q < nv; ++q) nd[q] = cn[i * 8 + sl[q]];
+    return nv;
+  };
   // ---------------- geometry ----------------
   gm.V.resize(n_cells);
   gm.C.resize(3 * n_cells);
@@ -323,11 +393,10 @@ static void build_core(GlobalMesh& gm, const double* xyz, int64_t n_nodes, const
 #pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n_cells; ++i) {
     P3 v[8];
-    for (int k = 0; k < ct; ++k) v[k] = node(cn[i * 8 + k]);
+    for (int k = 0; k < type[i]; ++k) v[k] = node(cn[i * 8 + k]);
     double V;
     P3 c;
-    if (ct == 4) tet_geometry(v, V, c, &gm.M2[6 * i]);
-    else hex_geometry(v, V, c, &gm.M2[6 * i]);
+    cell_geometry(type[i], v, V, c, &gm.M2[6 * i]);
     gm.V[i] = V;
     gm.C[3 * i] = c.x; gm.C[3 * i + 1] = c.y; gm.C[3 * i + 2] = c.z;
   }
@@ -337,21 +406,32 @@ static void build_core(GlobalMesh& gm, const double* xyz, int64_t n_nodes, const
 
   pt.lap("geometry");
   // ---------------- faces: bucket half-faces by their smallest node ----------
+  // half-face h = i * nfc + p; p >= nf(i) (a tet in a hybrid mesh) is no face (key -1)
   const int64_t nh = n_cells * nfc;
   std::vector<std::array<int64_t, 4>> hkey(nh);
+  int64_t nh_valid = 0;
   for (int64_t i = 0; i < n_cells; ++i)
     for (int p = 0; p < nfc; ++p) {
       std::array<int64_t, 4> k{INT64_MAX, INT64_MAX, INT64_MAX, INT64_MAX};
-      for (int q = 0; q < nvf; ++q) k[q] = cn[i * 8 + (ct == 4 ? kTetF[p][q] : kHexF[p][q])];
-      std::sort(k.begin(), k.end());
+      if (p < nf_of(i)) {
+        int64_t nd[4];
+        const int nv = fnodes(i, p, nd);
+        for (int q = 0; q < nv; ++q) k[q] = nd[q];
+        std::sort(k.begin(), k.end());
+        ++nh_valid;
+      } else {
+        k[0] = -1;
+      }
       hkey[i * nfc + p] = k;
     }
-  std::vector<int64_t> bstart(n_nodes + 1, 0), order(nh);
-  for (int64_t h = 0; h < nh; ++h) bstart[hkey[h][0] + 1]++;
+  std::vector<int64_t> bstart(n_nodes + 1, 0), order(nh_valid);
+  for (int64_t h = 0; h < nh; ++h)
+    if (hkey[h][0] >= 0) bstart[hkey[h][0] + 1]++;
   for (int64_t n = 0; n < n_nodes; ++n) bstart[n + 1] += bstart[n];
   {
     std::vector<int64_t> fill(bstart.begin(), bstart.end() - 1);
-    for (int64_t h = 0; h < nh; ++h) order[fill[hkey[h][0]]++] = h;  // stable: ascending h
+    for (int64_t h = 0; h < nh; ++h)
+      if (hkey[h][0] >= 0) order[fill[hkey[h][0]]++] = h;  // stable: ascending h
   }
   // boundary tags by key
   std::unordered_map<std::string, int32_t> btag;
@@ -419,8 +499,10 @@ static void build_core(GlobalMesh& gm, const double* xyz, int64_t n_nodes, const
       int64_t h = unmatched[u];
       std::array<std::array<int64_t, 3>, 4> q;
       for (int a = 0; a < 4; ++a) q[a] = {INT64_MAX, INT64_MAX, INT64_MAX};
-      for (int v = 0; v < nvf; ++v) {
-        int64_t nd = cn[(h / nfc) * 8 + (ct == 4 ? kTetF[h % nfc][v] : kHexF[h % nfc][v])];
+      int64_t fn[4];
+      const int nvh = fnodes(h / nfc, (int)(h % nfc), fn);
+      for (int v = 0; v < nvh; ++v) {
+        int64_t nd = fn[v];
         double c3[3] = {xyz[3 * nd] - O[0], xyz[3 * nd + 1] - O[1], xyz[3 * nd + 2] - O[2]};
         for (int a = 0; a < 3; ++a) {
           double y = c3[a];
@@ -451,9 +533,12 @@ static void build_core(GlobalMesh& gm, const double* xyz, int64_t n_nodes, const
       if (ha / nfc == hb / nfc) throw Error(2, "self-periodic cell " + std::to_string(ha / nfc));
       // shift = (owner face centroid) - (neighbour face centroid), snapped to the box lengths
       P3 ca{0, 0, 0}, cb{0, 0, 0};
-      for (int v = 0; v < nvf; ++v) {
-        ca = ca + (1.0 / nvf) * node(cn[(ha / nfc) * 8 + (ct == 4 ? kTetF[ha % nfc][v] : kHexF[ha % nfc][v])]);
-        cb = cb + (1.0 / nvf) * node(cn[(hb / nfc) * 8 + (ct == 4 ? kTetF[hb % nfc][v] : kHexF[hb % nfc][v])]);
+      int64_t fa[4], fb[4];
+      const int nva = fnodes(ha / nfc, (int)(ha % nfc), fa);
+      fnodes(hb / nfc, (int)(hb % nfc), fb);
+      for (int v = 0; v < nva; ++v) {
+        ca = ca + (1.0 / nva) * node(fa[v]);
+        cb = cb + (1.0 / nva) * node(fb[v]);
       }
       P3 d = ca - cb;
       double s[3] = {d.x, d.y, d.z};
@@ -483,6 +568,7 @@ static void build_core(GlobalMesh& gm, const double* xyz, int64_t n_nodes, const
   gm.f_ghost.assign(gm.nf, -1);
   gm.f_shift.resize(3 * gm.nf);
   gm.f_vert.assign(12 * gm.nf, 0.0);
+  gm.f_nv.resize(gm.nf);
   gm.f_area.resize(gm.nf);
   for (int64_t f = 0; f < gm.nf; ++f) {
     const FaceTmp& F = ft[f];
@@ -492,7 +578,10 @@ static void build_core(GlobalMesh& gm, const double* xyz, int64_t n_nodes, const
     gm.f_shift[3 * f] = F.shift.x; gm.f_shift[3 * f + 1] = F.shift.y; gm.f_shift[3 * f + 2] = F.shift.z;
     int p = (int)(F.hown % nfc);
     P3 v[4];
-    for (int q = 0; q < nvf; ++q) v[q] = node(cn[F.owner * 8 + (ct == 4 ? kTetF[p][q] : kHexF[p][q])]);
+    int64_t fn[4];
+    const int nvf = fnodes(F.owner, p, fn);
+    gm.f_nv[f] = (int8_t)nvf;
+    for (int q = 0; q < nvf; ++q) v[q] = node(fn[q]);
     // orient out of the owner
     P3 fc{0, 0, 0};
     for (int q = 0; q < nvf; ++q) fc = fc + (1.0 / nvf) * v[q];
@@ -512,7 +601,7 @@ static void build_core(GlobalMesh& gm, const double* xyz, int64_t n_nodes, const
     gm.f_area[f] = a;
   }
   for (int64_t i = 0; i < n_cells; ++i)
-    for (int p = 0; p < nfc; ++p)
+    for (int p = 0; p < nf_of(i); ++p)
       if (gm.cell_face[i * 6 + p] < 0 && !(open_ok && (*open_ok)[i]))
         throw Error(2, "open face at cell " + std::to_string(i));
   pt.lap("faces + periodic pairing");
@@ -525,6 +614,7 @@ static void build_core(GlobalMesh& gm, const double* xyz, int64_t n_nodes, const
     gm.g_face.push_back(f);
     gm.g_bc.push_back(gm.f_bc[f]);
     P3 v[4];
+    const int nvf = gm.f_nv[f];
     for (int q = 0; q < nvf; ++q) v[q] = {gm.f_vert[12 * f + 3 * q], gm.f_vert[12 * f + 3 * q + 1], gm.f_vert[12 * f + 3 * q + 2]};
     P3 gx[4], gn[4];
     double gw[4];
@@ -563,7 +653,7 @@ static void build_core(GlobalMesh& gm, const double* xyz, int64_t n_nodes, const
   gm.h_dt.resize(n_cells);
   for (int64_t i = 0; i < n_cells; ++i) {
     double smax = 0;
-    for (int p = 0; p < nfc; ++p) {
+    for (int p = 0; p < nf_of(i); ++p) {
       int64_t f = gm.cell_face[i * 6 + p];
       if (f < 0) continue;  // region rim (open_ok): no neighbour, never used
       smax = std::max(smax, gm.f_area[f]);
@@ -612,14 +702,14 @@ static void build_core(GlobalMesh& gm, const double* xyz, int64_t n_nodes, const
     auto nb = [&](int64_t c, int p) {
       return Member{gm.nbr_id[c * 6 + p], {gm.nbr_shift[c * 18 + 3 * p], gm.nbr_shift[c * 18 + 3 * p + 1], gm.nbr_shift[c * 18 + 3 * p + 2]}};
     };
-    for (int p = 0; p < nfc; ++p) {
+    for (int p = 0; p < nf_of(i); ++p) {
       Member m = nb(i, p);
       add(m.id, m.s);
     }
-    for (int p = 0; p < nfc; ++p) {
+    for (int p = 0; p < nf_of(i); ++p) {
       Member m = nb(i, p);
       if (m.id >= n_cells) continue;  // ghosts have no neighbours
-      for (int q = 0; q < nfc; ++q) {
+      for (int q = 0; q < nf_of(m.id); ++q) {
         Member m2 = nb(m.id, q);
         add(m2.id, m.s + m2.s);
       }
@@ -631,7 +721,7 @@ static void build_core(GlobalMesh& gm, const double* xyz, int64_t n_nodes, const
       return -1;
     };
     int8_t* ss = &gm.sub_slot[i * L.M * L.NM];
-    if (ct == 4) {
+    if (type[i] == 4) {
       // R16: sub m = three face neighbours {T_m} + neighbours of i_m
       const int tri[4][3] = {{0, 1, 2}, {0, 1, 3}, {1, 2, 3}, {2, 0, 3}};
       for (int m = 0; m < 4; ++m) {
@@ -647,8 +737,13 @@ static void build_core(GlobalMesh& gm, const double* xyz, int64_t n_nodes, const
         for (int k = 0; k < 3; ++k) put(gm.nbr_id[i * 6 + tri[m][k]]);
         int64_t im = gm.nbr_id[i * 6 + m];
         if (im < n_cells)
-          for (int q = 0; q < 4; ++q) put(gm.nbr_id[im * 6 + q]);
+          for (int q = 0; q < nf_of(im); ++q) put(gm.nbr_id[im * 6 + q]);
       }
+    } else if (type[i] == 6) {
+      // R30: the triangle-face neighbour (face 0 or 1) and two ring-adjacent side neighbours
+      const int ps[6][3] = {{0, 2, 3}, {0, 3, 4}, {0, 4, 2}, {1, 2, 3}, {1, 3, 4}, {1, 4, 2}};
+      for (int m = 0; m < 6; ++m)
+        for (int k = 0; k < 3; ++k) ss[m * L.NM + k] = (int8_t)slot_of(gm.nbr_id[i * 6 + ps[m][k]]);
     } else {
       const int hs[8][3] = {{0, 1, 2}, {0, 2, 3}, {0, 3, 4}, {0, 4, 1}, {5, 1, 2}, {5, 2, 3}, {5, 3, 4}, {5, 4, 1}};
       for (int m = 0; m < 8; ++m)
@@ -680,10 +775,11 @@ static void build_core(GlobalMesh& gm, const double* xyz, int64_t n_nodes, const
     }
   {
     // pad the stencil width to a capacity the reconstruction kernel is compiled for
+    // (hybrid meshes: 20 and up)
     const int caps[] = {14, 16, 20, 24, 32, 40};
     L.K = 40;
     for (int c : caps)
-      if (c >= max_k) {
+      if (c >= max_k && (ct != 6 || c >= 20)) {
         L.K = c;
         break;
       }
@@ -728,12 +824,15 @@ static void rcb_partition(const double* C, int64_t n, int nr, int32_t* part) {
   }
 }
 
+// accepted: tet-only, hex-only, or tets and prisms mixed (hybrid, f4)
 static void check_cells(const int8_t* type, const int64_t* cn, int64_t n_cells, int64_t n_nodes) {
-  const int ct = type[0];
-  if (ct != 4 && ct != 8) throw Error(2, "unsupported element at cell 0");
+  const bool hex = type[0] == 8;
   for (int64_t i = 0; i < n_cells; ++i) {
-    if (type[i] != ct) throw Error(2, "mixed element kinds are not supported (cell " + std::to_string(i) + ")");
-    for (int k = 0; k < ct; ++k) {
+    const int t = type[i];
+    if (t != 4 && t != 6 && t != 8) throw Error(2, "unsupported element at cell " + std::to_string(i));
+    if ((t == 8) != hex)
+      throw Error(2, "hexes cannot be mixed with other element kinds (cell " + std::to_string(i) + ")");
+    for (int k = 0; k < t; ++k) {
       int64_t v = cn[i * 8 + k];
       if (v < 0 || v >= n_nodes) throw Error(2, "invalid node id in cell " + std::to_string(i));
     }
@@ -762,18 +861,16 @@ static GlobalMesh build_region(const double* xyz, int64_t n_nodes, const int8_t*
                                const int64_t* bface_nodes, const int32_t* bface_tag, int64_t n_bf, int32_t n_ranks,
                                const int32_t* cell_part, int rank) {
   PhaseTimer pt("region");
-  const int ct = type[0];
   // centroids of every cell (the partition input), the same numbers as the whole-mesh build
   std::vector<double> C(3 * n_cells);
   std::vector<int32_t> part(n_cells, 0);
 #pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n_cells; ++i) {
     P3 v[8];
-    for (int k = 0; k < ct; ++k) v[k] = {xyz[3 * cn[i * 8 + k]], xyz[3 * cn[i * 8 + k] + 1], xyz[3 * cn[i * 8 + k] + 2]};
+    for (int k = 0; k < type[i]; ++k) v[k] = {xyz[3 * cn[i * 8 + k]], xyz[3 * cn[i * 8 + k] + 1], xyz[3 * cn[i * 8 + k] + 2]};
     double V, m2[6];
     P3 c;
-    if (ct == 4) tet_geometry(v, V, c, m2);
-    else hex_geometry(v, V, c, m2);
+    cell_geometry(type[i], v, V, c, m2);
     C[3 * i] = c.x; C[3 * i + 1] = c.y; C[3 * i + 2] = c.z;
   }
   GlobalMesh gm;
@@ -826,11 +923,11 @@ static GlobalMesh build_region(const double* xyz, int64_t n_nodes, const int8_t*
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n_cells; ++i)
       if (lay[i] == l - 1)
-        for (int k = 0; k < ct; ++k) mark[canon[cn[i * 8 + k]]] = 1;
+        for (int k = 0; k < type[i]; ++k) mark[canon[cn[i * 8 + k]]] = 1;
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n_cells; ++i) {
       if (lay[i] >= 0) continue;
-      for (int k = 0; k < ct; ++k)
+      for (int k = 0; k < type[i]; ++k)
         if (mark[canon[cn[i * 8 + k]]]) {
           lay[i] = (int8_t)l;
           break;
@@ -853,8 +950,9 @@ static GlobalMesh build_region(const double* xyz, int64_t n_nodes, const int8_t*
     open_ok[k] = lay[R[k]] == 4;       // every face of layers <= 3 has its partner in the region
     stencil_ok[k] = lay[R[k]] <= 1;    // owned + face layer 1 (reconstructed cells)
   }
+  const bool hybrid = std::any_of(type, type + n_cells, [](int8_t t) { return t == 6; });
   build_core(gm, xyz, n_nodes, sub_type.data(), sub_cn.data(), nr, per_origin, per_len, bface_nodes, bface_tag,
-             n_bf, &open_ok, &stencil_ok);
+             n_bf, &open_ok, &stencil_ok, hybrid);
   gm.gid = R;
   gm.nc_global = n_cells;
   gm.n_ranks = n_ranks;
@@ -1005,7 +1103,9 @@ static bool cell_operators(const GlobalMesh& gm, int64_t i, double* op) {
     for (int k = 0; k < K; ++k) op[d * L.K + k] = P[d * K + k] / (d < 3 ? h : h * h);
 #endif
   const int8_t* ss = &gm.sub_slot[i * L.M * L.NM];
-  for (int m = 0; m < L.M; ++m) {
+  // a tet of a hybrid mesh has 4 of the layout's 6 sub-stencils (the rest stay 0)
+  const int Mi = gm.type[i] == 4 ? 4 : L.M;
+  for (int m = 0; m < Mi; ++m) {
     int n = 0;
     double As[3 * 8];
     int slots[8];
@@ -1148,6 +1248,7 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
   rp.st_shift.assign((size_t)K * R, 13);
   rp.op.assign((size_t)E * R, 0.0);
   rp.geo.assign((size_t)8 * R, 0.0);
+  if (L.cell_type == 6) rp.n_sub.assign((size_t)R, 6);
   // tiled entry-major layout: entry e of cell r at ((r/128)*NE + e)*128 + r%128, so one
   // 128-cell block reads its operators from one contiguous range (DRAM page locality)
   auto ti = [](int64_t r, int ne, int e) { return (size_t)(((r >> 7) * ne + e) << 7) + (size_t)(r & 127); };
@@ -1195,6 +1296,7 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
       int8_t v = gm.sub_slot[gi * M * NM + s];
       rp.sub_slot[ti(r, M * NM, s)] = (uint8_t)(v < 0 ? 0 : v);
     }
+    if (L.cell_type == 6) rp.n_sub[r] = (uint8_t)(gm.type[gi] == 4 ? 4 : 6);
     // streaming order of the operator entries (hot.cuh k_recon): A0+ member-major
     // (row k*9 + d), then the sub-stencil operators (row 9K + (m*NM + j)*3 + d)
     double op[9 * 64 + 8 * 3 * 8] = {};
@@ -1245,7 +1347,7 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
     for (int64_t i : owned)
       for (int p = 0; p < L.nfaces; ++p) {
         int64_t f = gm.cell_face[i * 6 + p];
-        if (!seen[f]) {
+        if (f >= 0 && !seen[f]) {
           seen[f] = 1;
           fl.push_back(f);
         }
@@ -1253,8 +1355,9 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
   }
   for (int64_t f : fl)
     if (gm.f_nb[f] < 0) local_of(nc + gm.f_ghost[f]);
-  // order: early interior faces (both cells reconstructed before the exchange
-  // completes), late interior faces, wall, farfield; by min local endpoint within
+  // order: triangles before quadrilaterals (one flux instantiation per face kind), then
+  // early interior faces (both cells reconstructed before the exchange completes), late
+  // interior faces, wall, farfield; by min local endpoint within
   auto is_early = [&](int64_t gcell) {
     const int32_t l = g2l[gcell];
     return l < rp.n_owned && early_cell[l];
@@ -1264,7 +1367,7 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
                               : (gm.f_bc[f] == 1 ? 2 : 3);
     int64_t a = g2l[gm.f_owner[f]];
     int64_t b = gm.f_nb[f] >= 0 ? g2l[gm.f_nb[f]] : a;
-    return {cls, std::min(a, b)};
+    return {(gm.f_nv[f] == 4 ? 4 : 0) + cls, std::min(a, b)};
   };
   {
     // sort keys computed once: (class, min local endpoint, position) = a stable sort
@@ -1277,11 +1380,19 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
   }
   rp.n_faces = (int64_t)fl.size();
   for (int64_t f : fl) {
-    const int cls = fkey(f).first;
-    if (cls == 0) ++rp.n_if_early;
-    if (cls <= 1) ++rp.n_if;
-    else if (cls == 2) ++rp.n_wf;
-    else ++rp.n_ff;
+    const int kc = fkey(f).first, k = kc >> 2, cls = kc & 3;
+    FaceClass& F = rp.fcls[k];
+    if (cls == 0) ++F.n_if_early;
+    if (cls <= 1) ++F.n_if;
+    else if (cls == 2) ++F.n_wf;
+    else ++F.n_ff;
+  }
+  rp.fcls[1].base = rp.fcls[0].n_if + rp.fcls[0].n_wf + rp.fcls[0].n_ff;
+  for (const FaceClass& F : rp.fcls) {
+    rp.n_if_early += F.n_if_early;
+    rp.n_if += F.n_if;
+    rp.n_wf += F.n_wf;
+    rp.n_ff += F.n_ff;
   }
   pt.lap("face list + order");
   rp.f_geo_stride = 3 * L.nv + 3;
@@ -1295,11 +1406,12 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
     rp.f_cells[2 * k] = g2l[o];
     rp.f_cells[2 * k + 1] = gm.f_nb[f] >= 0 ? g2l[gm.f_nb[f]] : local_of(nc + gm.f_ghost[f]);
     double* fg = &rp.f_geo[(size_t)rp.f_geo_stride * k];
-    for (int q = 0; q < L.nv; ++q)
+    const int nv = gm.f_nv[f];
+    for (int q = 0; q < nv; ++q)
       for (int a = 0; a < 3; ++a) fg[3 * q + a] = gm.f_vert[12 * f + 3 * q + a] - gm.C[3 * o + a];
     // d = c_owner - (c_nb + shift): the neighbour evaluates at r_l + d
     if (gm.f_nb[f] >= 0)
-      for (int a = 0; a < 3; ++a) fg[3 * L.nv + a] = gm.C[3 * o + a] - (gm.C[3 * gm.f_nb[f] + a] + gm.f_shift[3 * f + a]);
+      for (int a = 0; a < 3; ++a) fg[3 * nv + a] = gm.C[3 * o + a] - (gm.C[3 * gm.f_nb[f] + a] + gm.f_shift[3 * f + a]);
   }
   pt.lap("face arrays");
   // update arrays
@@ -1310,6 +1422,10 @@ RankPlan build_rank_plan(const GlobalMesh& gm, int rank) {
     int64_t gi = owned[r];
     for (int p = 0; p < L.nfaces; ++p) {
       int64_t f = gm.cell_face[gi * 6 + p];
+      if (f < 0) {  // no face p (a tet of a hybrid mesh): the zero row past the last face
+        rp.cf[(size_t)p * rp.n_owned + r] = (int32_t)rp.n_faces;
+        continue;
+      }
       int32_t lf = f2l[f];
       rp.cf[(size_t)p * rp.n_owned + r] = gm.f_owner[f] == gi ? lf : ~lf;
     }

@@ -153,6 +153,7 @@ struct DevArrays {
   P2PFlags* flags;  // cross-process put: epoch flags written by the peers (f3)
   int64_t* in_row;
   uint8_t* sub_slot;
+  uint8_t* n_sub;  // sub-stencils per reconstructed cell (hybrid layouts), else null
   uint8_t* st_shift;
   Ctrl* ctrl;
 };
@@ -169,11 +170,13 @@ size_t layout(const GlobalMesh& gm, const RankPlan& rp, size_t rs, int dq0_mode,
   d.R = R((size_t)QS * rp.n_owned);
   d.ceff = R((size_t)kRec * ncl);
   d.ceff0 = dq0_mode == 2 ? R((size_t)kRec * ncl) : nullptr;
-  d.F1 = R((size_t)10 * rp.n_faces);
-  d.F2 = R((size_t)5 * rp.n_faces);
+  // one zero row past the last face: the update's entry for a face a cell does not have
+  d.F1 = R((size_t)10 * (rp.n_faces + 1));
+  d.F2 = R((size_t)5 * (rp.n_faces + 1));
   d.recon_cell = c.take<int>(rp.n_recon);
   d.st_id = c.take<int>((size_t)L.K * rp.ld);
   d.sub_slot = c.take<uint8_t>((size_t)L.M * L.NM * rp.ld);
+  d.n_sub = rp.n_sub.empty() ? nullptr : c.take<uint8_t>(rp.n_sub.size());
   d.op = R((size_t)L.op_entries() * rp.ld);
   d.geo = R((size_t)8 * rp.ld);
   d.st_shift = c.take<uint8_t>(HGKS_RECON_NE ? (size_t)L.K * rp.ld : 1);
@@ -320,17 +323,22 @@ typename L::RealT* as(T* p) {
 
 template <class L, int K, int M, int NM>
 void run_recon_k(hgks_solver* s, const typename L::ReconArgsT& a) {
+  // hybrid layouts (NM = 7, per-cell sub-stencil counts) have the one-lane kernel only
+  constexpr bool kPair = NM != 7;
   if (!s->recon_smem_set) {  // one reconstruction instantiation per solver (K, M, NM, precision fixed)
     CUDA_TRY((L::template recon_smem<K, M, NM>()));
-    CUDA_TRY((L::template recon_pair_smem<K, M, NM>()));
+    if constexpr (kPair) CUDA_TRY((L::template recon_pair_smem<K, M, NM>()));
     s->recon_smem_set = 1;
   }
   const int n_tiles = s->recon_t1 - a.tile0;
   if (n_tiles <= 0) return;
-  if (s->recon_pair == 1 || (s->recon_pair < 0 && s->fp32 && K <= 16))
-    launch(s, "k_recon", [&] { L::template recon_pair<K, M, NM>(n_tiles, s->stream, a); });
-  else
-    launch(s, "k_recon", [&] { L::template recon<K, M, NM>(n_tiles, s->stream, a); });
+  if constexpr (kPair) {
+    if (s->recon_pair == 1 || (s->recon_pair < 0 && s->fp32 && K <= 16)) {
+      launch(s, "k_recon", [&] { L::template recon_pair<K, M, NM>(n_tiles, s->stream, a); });
+      return;
+    }
+  }
+  launch(s, "k_recon", [&] { L::template recon<K, M, NM>(n_tiles, s->stream, a); });
 }
 
 // part 0: tiles of the early cells, 1: the rest, 2: all
@@ -348,6 +356,7 @@ void run_recon(hgks_solver* s, const void* Q, int part) {
   a.recon_cell = s->d.recon_cell;
   a.st_id = s->d.st_id;
   a.sub_slot = s->d.sub_slot;
+  a.n_sub = s->d.n_sub;
   a.st_shift = s->d.st_shift;
   a.cgeo = as<L>(s->d.cgeo);
   for (int k = 0; k < 3; ++k) a.per_len[k] = (typename L::RealT)s->mesh->gm.per_len[k];
@@ -357,7 +366,14 @@ void run_recon(hgks_solver* s, const void* Q, int part) {
   a.ceff0 = s->d.ceff0 ? as<L>(s->d.ceff0) : nullptr;
   a.eps = (typename L::RealT)s->cfg.eps;
   a.omega_pow = s->cfg.omega_pow;
-  if (LY.cell_type == 4) {
+  if (LY.cell_type == 6) {  // hybrid tet/prism (f4): 6 sub-stencils of up to 7 members, K >= 20
+    switch (LY.K) {
+      case 20: run_recon_k<L, 20, 6, 7>(s, a); break;
+      case 24: run_recon_k<L, 24, 6, 7>(s, a); break;
+      case 32: run_recon_k<L, 32, 6, 7>(s, a); break;
+      default: run_recon_k<L, 40, 6, 7>(s, a); break;
+    }
+  } else if (LY.cell_type == 4) {
     switch (LY.K) {
       case 14: run_recon_k<L, 14, 4, 6>(s, a); break;
       case 16: run_recon_k<L, 16, 4, 6>(s, a); break;
@@ -407,15 +423,17 @@ void launch_flux(hgks_solver* s, const typename L::FluxArgsT& a, int stage, bool
   launch_flux_q<L, NV, BC, 0>(s, a, stage, tau0);
 }
 
+// the faces of one kind (NV vertices)
 template <class L, int NV>
 void run_flux_nv(hgks_solver* s, typename L::FluxArgsT a, int stage, int part) {
-  const RankPlan& rp = *s->rp;
+  const FaceClass& F = s->rp->fcls[NV == 3 ? 0 : 1];
   const bool tau0 = s->cfg.tau_mode == 0;
   // part 0: early interior faces; 1: late interior + wall + farfield; 2: all
-  const int64_t i0 = part == 1 ? rp.n_if_early : 0, i1 = part == 0 ? rp.n_if_early : rp.n_if;
-  const int64_t ranges[3][2] = {{i0, i1 - i0},
-                                {rp.n_if, part == 0 ? 0 : rp.n_wf},
-                                {rp.n_if + rp.n_wf, part == 0 ? 0 : rp.n_ff}};
+  const int64_t b = F.base;
+  const int64_t i0 = part == 1 ? F.n_if_early : 0, i1 = part == 0 ? F.n_if_early : F.n_if;
+  const int64_t ranges[3][2] = {{b + i0, i1 - i0},
+                                {b + F.n_if, part == 0 ? 0 : F.n_wf},
+                                {b + F.n_if + F.n_wf, part == 0 ? 0 : F.n_ff}};
   for (int bc = 0; bc < 3; ++bc) {
     a.face0 = (int)ranges[bc][0];
     a.n_faces = (int)ranges[bc][1];
@@ -442,8 +460,9 @@ void run_flux(hgks_solver* s, const void* Q, int stage, int part) {
   a.F2 = as<L>(s->d.F2);
   a.ctrl = s->d.ctrl;
   a.gp = make_gas_for<L>(s->gp);
-  if (s->lay.nv == 3) run_flux_nv<L, 3>(s, a, stage, part);
-  else run_flux_nv<L, 4>(s, a, stage, part);
+  // triangles (tets, prism ends), then quadrilaterals (hexes, prism sides)
+  if (s->lay.cell_type != 8) run_flux_nv<L, 3>(s, a, stage, part);
+  if (s->lay.cell_type != 4) run_flux_nv<L, 4>(s, a, stage, part);
 }
 
 template <class L>
@@ -642,9 +661,11 @@ void stage_late(hgks_solver* s, int st) {
   const int nf = s->lay.nfaces;
   if (st == 1) {
     if (nf == 4) launch(s, "k_update1", [&] { L::template update1<4>(blocks(n, 256), s->stream, u); });
+    else if (nf == 5) launch(s, "k_update1", [&] { L::template update1<5>(blocks(n, 256), s->stream, u); });
     else launch(s, "k_update1", [&] { L::template update1<6>(blocks(n, 256), s->stream, u); });
   } else {
     if (nf == 4) launch(s, "k_update2", [&] { L::template update2<4>(blocks(n, 256), s->stream, u); });
+    else if (nf == 5) launch(s, "k_update2", [&] { L::template update2<5>(blocks(n, 256), s->stream, u); });
     else launch(s, "k_update2", [&] { L::template update2<6>(blocks(n, 256), s->stream, u); });
   }
 }
@@ -904,6 +925,7 @@ hgks_status hgks_init(const hgks_mesh* mc, const hgks_config* cfg, const hgks_di
     up(s->d.st_id, rp.st_id_tiled.data(), rp.st_id_tiled.size() * sizeof(int));
 
     up(s->d.sub_slot, rp.sub_slot.data(), rp.sub_slot.size());
+    if (s->d.n_sub) up(s->d.n_sub, rp.n_sub.data(), rp.n_sub.size());
     upr(s->d.op, rp.op);
     upr(s->d.geo, rp.geo);
     up(s->d.st_shift, rp.st_shift.data(), rp.st_shift.size());
@@ -928,6 +950,8 @@ hgks_status hgks_init(const hgks_mesh* mc, const hgks_config* cfg, const hgks_di
     up(s->d.in_row, in_row.data(), in_row.size() * sizeof(int64_t));
     up(s->d.out_local, out_local.data(), out_local.size() * sizeof(int));
     CUDA_TRY(cudaMemsetAsync(s->d.Q, 0, s->rs * s->nq, st));
+    CUDA_TRY(cudaMemsetAsync((char*)s->d.F1 + s->rs * 10 * rp.n_faces, 0, s->rs * 10, st));
+    CUDA_TRY(cudaMemsetAsync((char*)s->d.F2 + s->rs * 5 * rp.n_faces, 0, s->rs * 5, st));
     CUDA_TRY(cudaMemsetAsync(s->d.flags, 0, sizeof(P2PFlags), st));
     Ctrl h{};
     h.bad_cell = INT_MAX;
@@ -1153,6 +1177,7 @@ hgks_status hgks_debug_residual(hgks_solver* s, const double* h_Q, double dt, do
       for (int p = 0; p < NF; ++p) {
         int e = cf[(size_t)p * n + i];
         int f = e >= 0 ? e : ~e;
+        if (f >= s->rp->n_faces) continue;  // no face p (hybrid meshes)
         double sg = e >= 0 ? -1.0 : 1.0;
         for (int v = 0; v < 5; ++v) {
           L[v] += sg * F1[(size_t)f * 10 + v];

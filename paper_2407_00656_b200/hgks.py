@@ -20,7 +20,7 @@ _i64p = C.POINTER(C.c_int64)
 _i32p = C.POINTER(C.c_int32)
 _i8p = C.POINTER(C.c_int8)
 
-HGKS_TET, HGKS_HEX = 4, 8
+HGKS_TET, HGKS_PRISM, HGKS_HEX = 4, 6, 8
 ERRORS = {0: "OK", 1: "E_ARG", 2: "E_MESH", 3: "E_STENCIL", 4: "E_CUDA", 5: "E_NCCL", 6: "E_POSITIVITY",
           7: "E_STATE"}
 

@@ -211,6 +211,39 @@ def walled_hex_box(n: int, h: float | None = None, jitter: float = 0.0, seed: in
     return mi
 
 
+_CELL_FACES = {
+    TET: [[1, 2, 3], [0, 2, 3], [0, 1, 3], [0, 1, 2]],
+    PRISM: [[0, 1, 2], [3, 4, 5], [0, 1, 4, 3], [1, 2, 5, 4], [2, 0, 3, 5]],
+    8: [[0, 1, 2, 3], [0, 1, 5, 4], [1, 2, 6, 5], [2, 3, 7, 6], [3, 0, 4, 7], [4, 5, 6, 7]],
+}
+
+
+def close_with_walls(mi: MeshInput) -> MeshInput:
+    """Drop the periodicity of ``mi`` and tag every face without a partner (matched by node
+    ids) as a WALL boundary face."""
+    owners = {}
+    for c in range(mi.n_cells):
+        for f in _CELL_FACES[int(mi.cell_type[c])]:
+            nodes = mi.cell_nodes[c, f]
+            key = tuple(sorted(nodes.tolist()))
+            owners[key] = None if key in owners else nodes
+    faces = [nodes for nodes in owners.values() if nodes is not None]
+    bf = np.full((len(faces), 4), -1, np.int64)
+    for k, nodes in enumerate(faces):
+        bf[k, :len(nodes)] = nodes
+    mi.periodic_length = np.zeros(3)
+    mi.bface_nodes = bf
+    mi.bface_tag = np.full(len(faces), BC_WALL, np.int32)
+    mi.name += "_walled"
+    return mi
+
+
+def walled_hybrid_box(n: int, jitter: float = 0.0, seed: int = 656) -> MeshInput:
+    """``hybrid_box`` closed by walls on all six sides: wall faces of both kinds (prism
+    sides and tet faces on the x / y sides, prism bottoms at z = 0, tet faces at the top)."""
+    return close_with_walls(hybrid_box(n, jitter=jitter, seed=seed))
+
+
 # --------------------------------------------------------------------------- #
 # Cubed-sphere hexahedral shell (C3/C4)
 # --------------------------------------------------------------------------- #

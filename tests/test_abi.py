@@ -36,7 +36,8 @@ def test_library_contains_sm100a_cubin():
 
 
 @pytest.mark.parametrize("mk", [lambda: W.kuhn_box(6), lambda: W.kuhn_box(5, jitter=0.1),
-                                lambda: W.cartesian_hex_box(5, jitter=0.1)])
+                                lambda: W.cartesian_hex_box(5, jitter=0.1), lambda: W.hybrid_box(6, jitter=0.1),
+                                lambda: W.hybrid_box(5, prism_layers=5), lambda: W.walled_hybrid_box(5)])
 def test_host_setup_matches_oracle_counts(mk):
     mi = mk()
     m = hgks.Mesh(mi)
@@ -46,7 +47,7 @@ def test_host_setup_matches_oracle_counts(mk):
     assert info["n_faces"] == om.n_faces
     assert info["stencil_min"] == om.min_stencil and info["stencil_max"] == om.max_stencil
     assert info["n_sub"] == om.n_subs
-    assert info["n_ghost"] == 0 and info["n_peers"] == 0
+    assert info["n_ghost"] == 0 and info["n_peers"] == 0 and info["n_bghost"] == om.n_ghosts
     assert info["n_early_cells"] == info["n_owned"] and info["n_early_faces"] == info["n_faces"] - info["n_faces_bc"]
 
 

@@ -32,6 +32,8 @@ def make_mesh(kind):
         return W.kuhn_box(8, 8, 6, h=0.25)
     if kind == "kuhn_jit":
         return W.kuhn_box(7, jitter=0.1)
+    if kind == "hybrid":
+        return W.hybrid_box(8, jitter=0.1)
     return W.sphere_shell(4)
 
 
@@ -140,7 +142,7 @@ def run_world(world, kind, region=False):
     return res
 
 
-@pytest.mark.parametrize("world,kind", [(2, "kuhn"), (4, "kuhn_jit"), (2, "sphere")])
+@pytest.mark.parametrize("world,kind", [(2, "kuhn"), (4, "kuhn_jit"), (2, "sphere"), (3, "hybrid")])
 def test_partition_exchange_gloo(world, kind):
     res = run_world(world, kind)
     mi = make_mesh(kind)
@@ -175,7 +177,7 @@ def test_partition_exchange_gloo(world, kind):
     for r in range(world):
         local = owned[r] | set(res[r]["ghosts"])
         for c in list(owned[r])[::3]:
-            for p in range(6):
+            for p in range(cf.shape[1]):
                 fi = cf[c, p]
                 if fi < 0:
                     continue
@@ -227,7 +229,8 @@ def test_region_build_exchange_gloo(world, kind):
 
 
 @pytest.mark.parametrize("mk,world", [(lambda: W.kuhn_box(9, jitter=0.1), 3), (lambda: W.sphere_shell(6), 4),
-                                      (lambda: W.walled_hex_box(7), 3)])
+                                      (lambda: W.walled_hex_box(7), 3), (lambda: W.hybrid_box(8, jitter=0.1), 4),
+                                      (lambda: W.walled_hybrid_box(7), 3)])
 def test_region_plans_equal_whole_mesh_plans(mk, world):
     """A region build gives exactly the plan the whole-mesh build gives for that rank (same
     partition passed in): local ids, peers, send lists, receive ranges and every count."""
