@@ -161,6 +161,8 @@ def recon_bytes_per_cell(K=14, M=4, NM=6, rs=8, ne=RECON_NE):
     read at least once per launch, its other uses hit L2)."""
     op = ((46 if ne else 9 * K) + M * 3 * NM) * rs  # LSQ operators
     idx = K * 4 + M * NM * 1 + 4       # stencil ids, sub-stencil slots, recon cell id
+    if NM == 7:
+        idx += 1                       # hybrid layouts: the cell's sub-stencil count
     if ne:
         idx += K                       # periodic image codes of the members
     geo = 8 * rs                       # V^{2/3}, V^{4/3}, M2
@@ -191,11 +193,13 @@ def oracle_problem(workload: str, N: int):
         mi = W.kuhn_box(N)
         return mi, W.advection_ic(mi, gamma=GAMMA), O.OracleConfig(cfl=CFL), f"{N}^3 Kuhn box ({6 * N ** 3} tets)"
     ma, re, _ = SPHERE[workload]
-    mi = W.sphere_shell(N)
+    mi = sphere_mesh(workload, N)
     Q0 = W.uniform_state(mi.n_cells, 1.0, (ma, 0.0, 0.0), 1.0 / GAMMA, gamma=GAMMA)
-    cfg = O.OracleConfig(cfl=0.5, tau_mode=1, mu_inf=ma / re, c1=1.0, t_inf=1.0 / GAMMA,
+    cfg = O.OracleConfig(cfl=sphere_cfl(workload), tau_mode=1, mu_inf=ma / re, c1=1.0, t_inf=1.0 / GAMMA,
                          freestream=(1.0, ma, 0.0, 0.0, 1.0 / GAMMA))
-    return mi, Q0, cfg, f"sphere shell 12x{N}^3 ({12 * N ** 3} hexes, Ma {ma}, Re {re})"
+    what = (f"hybrid tet/prism sphere N = {N} ({mi.n_cells} cells, Ma {ma}, Re {re})" if workload == "c3h" else
+            f"sphere shell 12x{N}^3 ({12 * N ** 3} hexes, Ma {ma}, Re {re})")
+    return mi, Q0, cfg, what
 
 
 def cpu_oracle_rate(workload: str, N: int, steps: int, threads: int):
@@ -211,7 +215,7 @@ def cpu_oracle_rate(workload: str, N: int, steps: int, threads: int):
 
 # bounded oracle samples per workload family: (all cores N, one core N); the oracle's cost per
 # cell does not depend on the box size, so a smaller box of the same family is the same work
-CPU_SAMPLE = {"c2": (48, 12), "c5": (48, 12), "c3": (12, 5), "c4": (12, 5)}
+CPU_SAMPLE = {"c2": (48, 12), "c5": (48, 12), "c3": (12, 5), "c4": (12, 5), "c3h": (20, 6)}
 
 
 def cpu_baseline(workload: str):
@@ -227,7 +231,19 @@ def cpu_baseline(workload: str):
             "cpu_model": cpu_model()}
 
 
-SPHERE = {"c3": (0.2535, 118.0, 35), "c4": (1.5, 300.0, 70)}
+SPHERE = {"c3": (0.2535, 118.0, 35), "c4": (1.5, 300.0, 70), "c3h": (0.2535, 118.0, 20)}
+
+
+def sphere_mesh(workload: str, n: int):
+    """c3/c4: hex cubed-sphere shell 12 n^3; c3h: the hybrid tet/prism sphere of BASELINE.json
+    configs[2] ("~0.5M mixed tet/prism cells"): prisms in the first n/2 of 2n radial layers,
+    tets outside (n = 20: 480,000 cells)."""
+    from paper_2407_00656_b200 import workloads as W
+    return W.sphere_hybrid(n, prism_layers=n // 2) if workload == "c3h" else W.sphere_shell(n)
+
+
+def sphere_cfl(workload: str) -> float:
+    return 0.3 if workload == "c3h" else 0.5  # tets in the mesh: the tet CFL (R6)
 
 
 def workload_config(workload: str, world: int, box: int = 0, jitter: float = 0.0):
@@ -246,6 +262,12 @@ def workload_config(workload: str, world: int, box: int = 0, jitter: float = 0.0
             cfg["jitter"] = jitter
         return cfg, "weak", (14, 4, 6)
     ma, re, n = SPHERE[workload]
+    if workload == "c3h":
+        wl = (f"configs[2]: hybrid tet/prism sphere, cubed-sphere N = {n}, {n // 2} prism layers + "
+              f"{2 * n - n // 2} tet layers ({6 * n * n * (2 * (n // 2) + 6 * (2 * n - n // 2))} cells), Ma {ma}, "
+              f"Re {re}, NS collision time, wall + farfield, CFL 0.3, free-stream start")
+        return ({"workload": wl, "cells": 6 * n * n * (2 * (n // 2) + 6 * (2 * n - n // 2)), "sphere_N": n},
+                "strong", (24, 6, 7))
     wl = (f"configs[{2 if workload == 'c3' else 3}]: sphere shell 12x{n}^3 hexes, Ma {ma}, Re {re}, "
           f"NS collision time, wall + farfield, CFL 0.5, free-stream start")
     return {"workload": wl, "cells": 12 * n ** 3, "sphere_N": n}, "strong", (24, 8, 3)
@@ -266,7 +288,8 @@ def run_reference(args):
         Ns = int(max(8, min(24, (cells_budget / 6.0) ** (1.0 / 3.0))))
     else:
         cells_budget = 120.0 * 1.5e4 / max(1, args.steps + args.warmup)
-        Ns = int(max(4, min(10, (cells_budget / 12.0) ** (1.0 / 3.0))))
+        per_n3 = 60.0 if args.workload == "c3h" else 12.0  # cells per N^3 of the sphere family
+        Ns = int(max(4, min(10, (cells_budget / per_n3) ** (1.0 / 3.0))))
     mi, Q0, ocfg, what = oracle_problem(args.workload, Ns)
     m = O.OracleMesh(mi)
     s = O.OracleSolver(m, Q0, ocfg, threads=threads)
@@ -296,7 +319,7 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=50)
-    ap.add_argument("--workload", default="c5", choices=["c2", "c3", "c4", "c5"],
+    ap.add_argument("--workload", default="c5", choices=["c2", "c3", "c4", "c5", "c3h"],
                     help="c5: 110^3 Kuhn box (7,986,000 tets) per GPU (default: configs[4], the largest "
                          "single-GPU config, weak scaling); c2: 48^3 Kuhn box per GPU (configs[1]); c3: subsonic "
                          "sphere 12x35^3 hexes (configs[2]); c4: supersonic sphere 12x70^3 hexes (configs[3])")
@@ -337,10 +360,10 @@ def main():
         cfg = hgks.SolverConfig(gamma=GAMMA, cfl=CFL, precision=args.precision)
     else:
         ma, re, n = SPHERE[args.workload]
-        mi = W.sphere_shell(n)
+        mi = sphere_mesh(args.workload, n)
         fs = (1.0, ma, 0.0, 0.0, 1.0 / GAMMA)
         Q0 = W.uniform_state(mi.n_cells, 1.0, (ma, 0.0, 0.0), 1.0 / GAMMA, gamma=GAMMA)  # free-stream IC
-        cfg = hgks.SolverConfig(gamma=GAMMA, cfl=0.5, tau_mode=1, mu_inf=ma / re, c1=1.0, t_inf=1.0 / GAMMA,
+        cfg = hgks.SolverConfig(gamma=GAMMA, cfl=sphere_cfl(args.workload), tau_mode=1, mu_inf=ma / re, c1=1.0, t_inf=1.0 / GAMMA,
                                 freestream=fs, precision=args.precision)
     # one process per GPU: each builds only its own region (O(owned + ghosts) host setup)
     mesh = hgks.Mesh(mi, n_ranks=world, rank=rank if world > 1 else None)

@@ -348,6 +348,60 @@ def sphere_shell(n: int, r_in: float = 0.5, r_out: float = 10.0, first_cell: flo
     )
 
 
+def _prisms_to_tets(pr: np.ndarray) -> np.ndarray:
+    """Split prisms [n][6] (bottom 012, top 345, 3 over 0) into 3 tets each so that every quad
+    face is cut along the diagonal through its smallest node id (the neighbour's split of a
+    shared quad agrees, so the tet mesh stays conforming): rotate / flip the prism to put its
+    smallest node at slot 0, then the quad (1,2,5,4) decides between the two 3-tet splits."""
+    pr = pr.copy()
+    m = np.argmin(pr, axis=1)
+    flip = m >= 3
+    pr[flip] = pr[flip][:, [3, 4, 5, 0, 1, 2]]
+    m = np.where(flip, m - 3, m)
+    for r in (1, 2):  # rotate the triangles so slot m goes to slot 0
+        sel = m == r
+        rot = [r, (r + 1) % 3, (r + 2) % 3]
+        pr[sel] = pr[sel][:, rot + [x + 3 for x in rot]]
+    d15 = np.minimum(pr[:, 1], pr[:, 5]) < np.minimum(pr[:, 2], pr[:, 4])
+    a = np.where(d15[:, None], pr[:, [0, 1, 2, 5]], pr[:, [0, 1, 2, 4]])
+    b = np.where(d15[:, None], pr[:, [0, 1, 5, 4]], pr[:, [0, 4, 2, 5]])
+    c = pr[:, [0, 4, 5, 3]]
+    return np.stack([a, b, c], 1).reshape(-1, 4)
+
+
+def sphere_hybrid(n: int, prism_layers: int | None = None, **shell_kw) -> MeshInput:
+    """Hybrid tet/prism sphere mesh (BASELINE.json config 3: "mixed tet/prism cells"): the
+    cubed-sphere shell of ``sphere_shell`` with every hex cut into two prisms along the
+    (0,2)/(4,6) diagonal of its spherical faces; the first ``prism_layers`` radial layers
+    (default half) stay prisms (the boundary layer), the outer ones are split into tets
+    (``_prisms_to_tets``).  Wall faces on the sphere and farfield faces outside are triangles.
+    Cells: 6 n^2 per radial layer x (2 per prism layer + 6 per tet layer)."""
+    sh = sphere_shell(n, **shell_kw)
+    hx = sh.cell_nodes
+    nr = hx.shape[0] // (6 * n * n)
+    prism_layers = nr // 2 if prism_layers is None else prism_layers
+    r = np.arange(hx.shape[0]) % nr
+    pa = hx[:, [0, 1, 2, 4, 5, 6]]
+    pb = hx[:, [0, 2, 3, 4, 6, 7]]
+    prisms = np.stack([pa, pb], 1).reshape(-1, 6)
+    pr_r = np.repeat(r, 2)
+    keep = prisms[pr_r < prism_layers]
+    tets = _prisms_to_tets(prisms[pr_r >= prism_layers])
+    cells = np.full((keep.shape[0] + tets.shape[0], 8), -1, np.int64)
+    cells[:keep.shape[0], :6] = keep
+    cells[keep.shape[0]:, :4] = tets
+    types = np.concatenate([np.full(keep.shape[0], PRISM), np.full(tets.shape[0], TET)]).astype(np.int8)
+    inner, outer = hx[r == 0], hx[r == nr - 1]
+    wall = np.concatenate([inner[:, [0, 1, 2]], inner[:, [0, 2, 3]]], 0)
+    far = np.concatenate([outer[:, [4, 5, 6]], outer[:, [4, 6, 7]]], 0)
+    bf = np.full((wall.shape[0] + far.shape[0], 4), -1, np.int64)
+    bf[:wall.shape[0], :3] = wall
+    bf[wall.shape[0]:, :3] = far
+    tags = np.concatenate([np.full(wall.shape[0], BC_WALL), np.full(far.shape[0], BC_FARFIELD)]).astype(np.int32)
+    return MeshInput(xyz=sh.xyz, cell_type=types, cell_nodes=cells, bface_nodes=bf, bface_tag=tags,
+                     name=f"sphere_hybrid_{n}_{prism_layers}")
+
+
 # --------------------------------------------------------------------------- #
 # Initial conditions (inputs, not method arithmetic)
 # --------------------------------------------------------------------------- #

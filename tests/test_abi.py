@@ -138,3 +138,20 @@ def test_p2p_and_put_map_argument_errors():
     assert e.value.code == 1
     rr, row = mesh.put_map(1)
     assert rr.size == mesh.info(1)["send_cells"] and set(rr.tolist()) == {0}
+
+
+def test_hybrid_sphere_counts_and_volume():
+    """Hybrid sphere (f4): the prism/tet split of the cubed-sphere shell keeps its volume
+    (oracle geometry of both meshes), every wall / farfield face is a triangle, and the host
+    setup's counts equal the oracle's."""
+    mi = W.sphere_hybrid(4)
+    assert set(np.unique(mi.cell_type).tolist()) == {W.TET, W.PRISM}
+    assert np.all(mi.bface_nodes[:, 3] == -1)
+    info = hgks.Mesh(mi).info()
+    om = O.OracleMesh(mi)
+    assert info["n_faces"] == om.n_faces and info["n_bghost"] == om.n_ghosts == 2 * 2 * 6 * 16
+    assert info["stencil_min"] == om.min_stencil and info["stencil_max"] == om.max_stencil
+    hs = W.sphere_shell(4)
+    V = om.geometry()[0][: mi.n_cells].sum()
+    Vh = O.OracleMesh(hs).geometry()[0][: hs.n_cells].sum()
+    assert abs(V - Vh) <= 1e-12 * Vh

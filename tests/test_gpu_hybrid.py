@@ -115,3 +115,31 @@ def test_hybrid_fp32(cuda_ok):
     mi = W.hybrid_box(6, jitter=0.1)
     errs = run_pair32(mi, W.advection_ic(mi), 10)
     assert 0 < errs.max() <= TOL32, errs.max(axis=0)
+
+
+def hybrid_sphere_case(n, ma, re, prism_layers=None):
+    mi = W.sphere_hybrid(n, prism_layers=n // 2 if prism_layers is None else prism_layers)
+    gam = 1.4
+    fs = (1.0, ma, 0.0, 0.0, 1 / gam)
+    Q0 = W.random_smooth_ic(mi, seed=118, base=fs, amp=0.01)
+    oc, gc = ns_cfgs(mu=ma / re, c1=1.0, cfl=0.3, fs=fs, t_inf=1 / gam)
+    return mi, Q0, oc, gc
+
+
+@pytest.mark.parametrize("ma,re", [(0.2535, 118.0), (1.5, 300.0)])
+def test_hybrid_sphere_wall_farfield(cuda_ok, ma, re):
+    """Hybrid tet/prism sphere (prism boundary layer, tets outside; triangle wall and
+    farfield faces), NS tau, subsonic and supersonic, 10 steps."""
+    mi, Q0, oc, gc = hybrid_sphere_case(4, ma, re)
+    errs, _, _ = run_pair(mi, Q0, 10, ocfg=oc, gcfg=gc)
+    assert errs.max() <= TOL, errs.max(axis=0)
+
+
+def test_c3h_size_steps(cuda_ok):
+    """configs[2] as BASELINE.json words it ("~0.5M mixed tet/prism cells"): the hybrid sphere
+    at the bench size (N = 20, 10 prism + 30 tet layers, 480,000 cells), parity IC, 10 steps
+    (eager step + graph replays), every cell vs the oracle after the first and tenth step."""
+    mi, Q0, oc, gc = hybrid_sphere_case(20, 0.2535, 118.0)
+    assert mi.n_cells == 480000
+    errs, _, _ = run_pair(mi, Q0, 2, ocfg=oc, gcfg=gc, chunks=(1, 9))
+    assert errs.max() <= TOL, errs.max(axis=0)
