@@ -10,19 +10,42 @@ namespace hgks {
 
 // erfc(z) together with exp(-z^2), which the half-range Maxwellian moments need both
 // of.  fp64: erfcx(|z|) = P(t)/(|z| + K), t = (|z| - K)/(|z| + K), P a
-// degree-22 polynomial in t (Chebyshev fit emitted in the monomial basis, evaluated by
-// Horner's rule: one DFMA per degree; scripts/fit_erfc.py; absolute error of erfc
+// degree-22 polynomial in t (Chebyshev fit emitted in the monomial basis, evaluated as four
+// interleaved Horner chains in t^4; scripts/fit_erfc.py; absolute error of erfc
 // <= 2e-15, tests/test_erfc_fit.py), so one exp serves both and the branchy library erfc
 // (about 160 instructions per call in the flux kernels' SASS) is gone.  fp32: library calls.
 // exp(x) for x <= 0 (the Maxwellian tail exp(-z^2), exp(-dt/tau)): Cody-Waite
-// reduction x = k ln2 + r, |r| <= ln2/2 (two-part ln2), degree-12 Taylor series, 2^k
+// reduction x = k ln2 + r, |r| <= ln2/2 (two-part ln2), degree-12 Taylor series (even and
+// odd parts as two Horner chains in r^2), 2^k
 // added to the exponent field; relative error <= 4e-16 on [-700, 0], 0 below -700
 // (tests/test_exp_neg.py).  About half the instructions of the library exp, which
 // also handles positive arguments, overflow and NaN.
+#ifndef HGKS_POLY_SPLIT
+#define HGKS_POLY_SPLIT 1  // 0: single Horner chains (round-2 baseline, for A/B builds)
+#endif
 __device__ __forceinline__ double exp_neg(double x) {
   const double xc = fmax(x, -708.0);
   const double k = rint(xc * 1.4426950408889634);
   const double r = fma(-k, 1.90821492927058770002e-10, fma(-k, 6.93147180369123816490e-01, xc));
+#if HGKS_POLY_SPLIT
+  // sum_{j<=12} r^j / j! as even + r * odd parts in r^2: two independent Horner chains of
+  // depth 6 / 5 instead of one of depth 12 (the flux kernels stall on dependent DFMAs)
+  const double r2 = r * r;
+  double pe = 2.08767569878680989792e-09;  // 1/12!
+  double po = 2.50521083854417187751e-08;  // 1/11!
+  pe = fma(pe, r2, 2.75573192239858906526e-07);  // 1/10!
+  po = fma(po, r2, 2.75573192239858906526e-06);  // 1/9!
+  pe = fma(pe, r2, 2.48015873015873015873e-05);  // 1/8!
+  po = fma(po, r2, 1.98412698412698412698e-04);  // 1/7!
+  pe = fma(pe, r2, 1.38888888888888888889e-03);  // 1/6!
+  po = fma(po, r2, 8.33333333333333333333e-03);  // 1/5!
+  pe = fma(pe, r2, 4.16666666666666666667e-02);  // 1/4!
+  po = fma(po, r2, 1.66666666666666666667e-01);  // 1/3!
+  pe = fma(pe, r2, 0.5);                         // 1/2!
+  po = fma(po, r2, 1.0);                         // 1/1!
+  pe = fma(pe, r2, 1.0);                         // 1/0!
+  const double p = fma(po, r, pe);
+#else
   double p = 2.08767569878680989792e-09;  // 1/12!
   p = fma(p, r, 2.50521083854417187751e-08);
   p = fma(p, r, 2.75573192239858906526e-07);
@@ -36,6 +59,7 @@ __device__ __forceinline__ double exp_neg(double x) {
   p = fma(p, r, 0.5);
   p = fma(p, r, 1.0);
   p = fma(p, r, 1.0);
+#endif
   const int ki = (int)k;  // in [-1022, 0]
   const double v = __hiloint2double(__double2hiint(p) + ki * (1 << 20), __double2loint(p));
   return x < -700.0 ? 0.0 : v;
@@ -50,9 +74,26 @@ __device__ __forceinline__ void erfc_exp(double z, double& erfc_z, double& ez2) 
   const double a = fabs(z);
   const double r = 1.0 / (a + HGKS_ERFC_K);
   const double t = (a - HGKS_ERFC_K) * r;
+#if HGKS_POLY_SPLIT
+  // P(t) = P0(s) + t P1(s) + t^2 P2(s) + t^3 P3(s), s = t^4, P_i(s) = sum_j c_{4j+i} s^j:
+  // four independent Horner chains (depth 5) and a depth-3 combination instead of one
+  // chain of depth 22 (3 extra multiplies)
+  const double t2 = t * t, s4 = t2 * t2;
+  double Pi[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    constexpr int D = HGKS_ERFC_DEG;
+    const int top = D - ((D - i) % 4);  // highest degree k <= D with k = i (mod 4)
+    Pi[i] = c[top];
+#pragma unroll
+    for (int k = top - 4; k >= 0; k -= 4) Pi[i] = fma(Pi[i], s4, c[k]);
+  }
+  const double P = fma(fma(fma(Pi[3], t, Pi[2]), t, Pi[1]), t, Pi[0]);
+#else
   double P = c[HGKS_ERFC_DEG];
 #pragma unroll
   for (int k = HGKS_ERFC_DEG - 1; k >= 0; --k) P = fma(P, t, c[k]);
+#endif
   ez2 = exp_neg(-z * z);
   const double v = P * r * ez2;  // erfc(|z|)
   erfc_z = z >= 0.0 ? v : 2.0 - v;

@@ -233,19 +233,55 @@ struct ReconShape {
   static constexpr size_t SMEM = (size_t)K * 5 * BT * sizeof(Real);
 };
 
+// The operators of one 128-cell tile are one contiguous E*kTile*sizeof(Real)-byte range
+// (tiled layout): TMA bulk prefetches of it into L2 (8 chunks, from 8 threads).
+#ifndef HGKS_PF_CHUNKS
+#define HGKS_PF_CHUNKS 8
+#endif
+template <int E>
+__device__ __forceinline__ void prefetch_tile_ops(const ReconArgs& a, int tile, int lane) {
+  constexpr uint32_t bytes = (uint32_t)E * kTile * sizeof(Real);
+  constexpr uint32_t chunk = ((bytes / HGKS_PF_CHUNKS) + 15) / 16 * 16;
+  const uint32_t off = lane * chunk;
+  if (lane < HGKS_PF_CHUNKS && off < bytes) {
+    const uint32_t n = min(chunk, bytes - off);
+    const char* src = reinterpret_cast<const char*>(a.op + (size_t)tile * kTile * E) + off;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(n) : "memory");
+  }
+}
+
+template <int K, int M, int NM>
+__device__ __forceinline__ void recon_tile(const ReconArgs& a, int tile, int half, Real* __restrict__ dqs);
+
+// One block per tile (or SPLIT blocks per tile).  The first block of a tile starts TMA
+// bulk prefetches of the tile's whole operator range into L2, so the streamed operator loads
+// see L2 rather than DRAM latency (8 warps of 255 registers cannot keep enough loads in
+// flight).  A persistent variant that prefetched each unit's NEXT tile was slower (C2 0.479
+// vs 0.407 ms): two rounds of tiles (~150 MB) do not fit the 126 MB L2, so the early
+// prefetches were evicted before use (profiles/r02/experiments/p1_*).
 template <int K, int M, int NM>
 __global__ void __launch_bounds__(ReconShape<K>::BT, ReconShape<K>::MINB) k_recon(ReconArgs a) {
-  constexpr int BT = ReconShape<K>::BT, SPLIT = ReconShape<K>::SPLIT;
+  constexpr int SPLIT = ReconShape<K>::SPLIT;
+  constexpr int E0 = HGKS_RECON_NE ? 46 : 9 * K;
+  constexpr int E = E0 + 3 * M * NM;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Real* __restrict__ dqs = reinterpret_cast<Real*>(smem_raw);  // [K][5][BT] Q_k - Q_i
+  const int half = SPLIT == 1 ? 0 : (int)(blockIdx.x % SPLIT);
+  const int tile = a.tile0 + (int)(blockIdx.x / SPLIT);
+#ifndef HGKS_NO_L2_PREFETCH
+  if (half == 0) prefetch_tile_ops<E>(a, tile, threadIdx.x);
+#endif
+  recon_tile<K, M, NM>(a, tile, half, dqs);
+}
+
+template <int K, int M, int NM>
+__device__ __forceinline__ void recon_tile(const ReconArgs& a, int tile, int half, Real* __restrict__ dqs) {
+  constexpr int BT = ReconShape<K>::BT;
   constexpr int QP = 5 * BT;                         // values per member plane: [v][thread]
   constexpr int E0 = HGKS_RECON_NE ? 46 : 9 * K;     // P_0 operator entries (W, or the pseudo-inverse)
   constexpr int E = E0 + 3 * M * NM;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Real* smem = reinterpret_cast<Real*>(smem_raw);
-  Real* __restrict__ dqs = smem;                   // [K][5][BT] Q_k - Q_i
   const int tl = threadIdx.x;
-  const int half = SPLIT == 1 ? 0 : (int)(blockIdx.x % SPLIT);
   const int t = half * BT + tl;                      // position in the 128-cell tile
-  const int tile = a.tile0 + (int)(blockIdx.x / SPLIT);
   const int r = tile * kTile + t;
   int ci = r < a.n_recon ? __ldg(a.recon_cell + r) : -1;  // -1: padding
   const bool active = ci >= 0;
@@ -259,25 +295,6 @@ __global__ void __launch_bounds__(ReconShape<K>::BT, ReconShape<K>::MINB) k_reco
     const R2 x0 = __ldg(q2), x1 = __ldg(q2 + 1), x2 = __ldg(q2 + 2);
     qi[0] = x0.x; qi[1] = x0.y; qi[2] = x1.x; qi[3] = x1.y; qi[4] = x2.x;
   }
-#ifndef HGKS_NO_L2_PREFETCH
-  // The block's operators are one contiguous E*kTile*8-byte range (tiled layout):
-  // fire TMA bulk prefetches of it into L2 now, so the streamed operator loads
-  // below see L2 rather than DRAM latency (the warps cannot keep enough loads
-  // in flight at 255 registers).
-#ifndef HGKS_PF_CHUNKS
-#define HGKS_PF_CHUNKS 8
-#endif
-  if (t < HGKS_PF_CHUNKS) {  // first block of the tile
-    constexpr uint32_t bytes = (uint32_t)E * kTile * sizeof(Real);
-    constexpr uint32_t chunk = ((bytes / HGKS_PF_CHUNKS) + 15) / 16 * 16;
-    const uint32_t off = t * chunk;
-    if (off < bytes) {
-      const uint32_t n = min(chunk, bytes - off);
-      const char* src = reinterpret_cast<const char*>(a.op + tb * E) + off;
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(n) : "memory");
-    }
-  }
-#endif
   // gather the stencil members in groups (bounded registers, 7 x 3 loads in flight)
   constexpr int G = 7;
 #pragma unroll

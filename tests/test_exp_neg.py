@@ -11,29 +11,40 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def device_constants():
+    """ln2 split and the even / odd Horner coefficients of the HGKS_POLY_SPLIT branch."""
     src = open(os.path.join(ROOT, "paper_2407_00656_b200", "csrc", "common.cuh")).read()
     body = src[src.index("double exp_neg(double x)"):src.index("float exp_neg(float x)")]
     lo, hi = [float(v) for v in re.findall(r"fma\(-k, ([0-9.e+-]+)", body)]
-    coef = [float(re.search(r"double p = ([0-9.e+-]+);", body).group(1))]
-    coef += [float(v) for v in re.findall(r"p = fma\(p, r, ([0-9.e+-]+)\);", body)]
-    return lo, hi, coef
+    split = body[body.index("#if HGKS_POLY_SPLIT"):body.index("#else")]
+    ce = [float(re.search(r"double pe = ([0-9.e+-]+);", split).group(1))]
+    ce += [float(v) for v in re.findall(r"pe = fma\(pe, r2, ([0-9.e+-]+)\);", split)]
+    co = [float(re.search(r"double po = ([0-9.e+-]+);", split).group(1))]
+    co += [float(v) for v in re.findall(r"po = fma\(po, r2, ([0-9.e+-]+)\);", split)]
+    return lo, hi, ce, co
 
 
 def test_series_coefficients_are_inverse_factorials():
-    _, _, coef = device_constants()
-    assert len(coef) == 13
-    for k, c in enumerate(coef):
-        assert c == 1.0 / math.factorial(12 - k)
+    _, _, ce, co = device_constants()
+    assert len(ce) == 7 and len(co) == 6
+    for j, c in enumerate(ce):
+        assert c == 1.0 / math.factorial(12 - 2 * j)
+    for j, c in enumerate(co):
+        assert c == 1.0 / math.factorial(11 - 2 * j)
 
 
 def test_exp_neg_accuracy():
-    ln2_lo, ln2_hi, coef = device_constants()
+    ln2_lo, ln2_hi, ce, co = device_constants()
     assert ln2_hi + ln2_lo == math.log(2.0) or abs(ln2_hi + ln2_lo - math.log(2.0)) < 1e-17
     x = np.concatenate([-np.logspace(-20, np.log10(700), 100001), np.linspace(-700, 0, 100001), [0.0, -0.0]])
     k = np.rint(np.maximum(x, -708.0) * 1.4426950408889634)
     r = (x - k * ln2_hi) - k * ln2_lo
-    p = np.full_like(r, coef[0])
-    for c in coef[1:]:
-        p = p * r + c
+    r2 = r * r
+    pe = np.full_like(r, ce[0])
+    for c in ce[1:]:
+        pe = pe * r2 + c
+    po = np.full_like(r, co[0])
+    for c in co[1:]:
+        po = po * r2 + c
+    p = po * r + pe
     got = np.ldexp(p, k.astype(int))
     assert np.max(np.abs(got - np.exp(x)) / np.exp(x)) < 5e-16
