@@ -268,8 +268,17 @@ __global__ void __launch_bounds__(ReconShape<K>::BT, ReconShape<K>::MINB) k_reco
   Real* __restrict__ dqs = reinterpret_cast<Real*>(smem_raw);  // [K][5][BT] Q_k - Q_i
   const int half = SPLIT == 1 ? 0 : (int)(blockIdx.x % SPLIT);
   const int tile = a.tile0 + (int)(blockIdx.x / SPLIT);
+// (also prefetching the operators of tile + AHEAD, a block that starts later, was slower
+// for AHEAD = 37 / 74 / 148: C2 0.449 / 0.439 / 0.499 vs 0.402 ms -- L2 capacity again)
+#ifndef HGKS_RECON_PF_AHEAD
+#define HGKS_RECON_PF_AHEAD 0
+#endif
 #ifndef HGKS_NO_L2_PREFETCH
-  if (half == 0) prefetch_tile_ops<E>(a, tile, threadIdx.x);
+  if (half == 0) {
+    prefetch_tile_ops<E>(a, tile, threadIdx.x);
+    if (HGKS_RECON_PF_AHEAD > 0 && (tile + HGKS_RECON_PF_AHEAD) * kTile < a.n_recon)
+      prefetch_tile_ops<E>(a, tile + HGKS_RECON_PF_AHEAD, threadIdx.x);
+  }
 #endif
   recon_tile<K, M, NM>(a, tile, half, dqs);
 }
@@ -1355,6 +1364,27 @@ __device__ __forceinline__ void flux_tau0_interior(const FluxArgs& a, int lf, in
                                                    Real* out) {
   constexpr int NGP = NV == 3 ? 3 : 4, FPW = 32 / NGP;
   const int lf0 = lf - lane / NGP;  // first face of this warp
+// The first two threads of a block bulk-prefetch into L2 the face cells and face geometry
+// of the block HGKS_FLUX_PF_AHEAD blocks later (a block that has not started: ~2 us ahead
+// at ~740 resident 30-face blocks): that block's first loads then hit L2.  Measured
+// (profiles/r02/experiments/pf_*): C2 stage-1 flux 0.304 -> 0.297 ms, C5 3.55 -> 3.42 ms;
+// 1024 blocks ahead is the same, 0 the round-2 baseline.
+#ifndef HGKS_FLUX_PF_AHEAD
+#define HGKS_FLUX_PF_AHEAD 256
+#endif
+  if (HGKS_FLUX_PF_AHEAD > 0 && threadIdx.x < 2) {
+    constexpr int FB = (BLOCK / 32) * FPW;  // faces per block
+    const int f0 = ((int)blockIdx.x + HGKS_FLUX_PF_AHEAD) * FB;
+    if (f0 < a.n_faces) {
+      const int nf = min(FB, a.n_faces - f0);
+      const char* src = threadIdx.x == 0 ? reinterpret_cast<const char*>(a.f_geo + (size_t)(a.face0 + f0) * a.f_stride)
+                                         : reinterpret_cast<const char*>(a.f_cells + 2 * (size_t)(a.face0 + f0));
+      const uint32_t bytes = threadIdx.x == 0 ? (uint32_t)(nf * a.f_stride * sizeof(Real)) : (uint32_t)(nf * 8);
+      const char* s16 = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15));
+      const uint32_t n16 = (uint32_t)((src - s16) + bytes + 15) & ~15u;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(s16), "r"(n16) : "memory");
+    }
+  }
 #if HGKS_FLUX_STAGE
   __shared__ __align__(16) Real srec[BLOCK / 32][2 * FPW * kRec];
   Real* sw = srec[threadIdx.x >> 5];
