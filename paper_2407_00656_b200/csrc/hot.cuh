@@ -225,12 +225,28 @@ __device__ __forceinline__ void p0_normal_equations(const ReconArgs& a, int ci, 
 // Block shape: a 128-cell tile per block, or half a tile per 64-thread block when
 // the member planes would not leave room for two blocks per SM (fp64 hex, K >= 20:
 // 123 KB), so three blocks (6 warps) fit instead of one.
+// HGKS_RECON_RING = D > 0 (build option, off): for the tet layouts (K <= 16) the P_0
+// operator pairs stream through a per-thread D-stage cp.async ring in shared memory (loads
+// in flight hold no registers), in 64-thread blocks.  Measured (profiles/r02/experiments/
+// ring*/): D = 2 on one box C2 recon 0.403 -> 0.388 ms, C5 4.61 -> 4.39 ms, on another
+// 0.429 -> 0.447 ms, 4.94 -> 5.03 ms (the box-to-box L1 / shared mode spread is as large as
+// the effect); D = 3 / 4 slower (more shared memory, fewer blocks); hexes (K = 24) 0.482 ->
+// 0.618 ms, so they never use it.
+#ifndef HGKS_RECON_RING
+#define HGKS_RECON_RING 0
+#endif
+#ifndef HGKS_RECON_RING_MINB
+#define HGKS_RECON_RING_MINB 3
+#endif
 template <int K>
 struct ReconShape {
-  static constexpr int BT = (size_t)K * 5 * kTile * sizeof(Real) > 100 * 1024 ? 64 : 128;
+  static constexpr int RING = (HGKS_RECON_NE || K > 16) ? 0 : HGKS_RECON_RING;
+  static constexpr int BT = (RING > 0 || (size_t)K * 5 * kTile * sizeof(Real) > 100 * 1024) ? 64 : 128;
   static constexpr int SPLIT = kTile / BT;
-  static constexpr int MINB = BT == 64 ? 3 : HGKS_RECON_MINB;
-  static constexpr size_t SMEM = (size_t)K * 5 * BT * sizeof(Real);
+  static constexpr size_t SMEM = (size_t)K * 5 * BT * sizeof(Real) + (size_t)RING * 9 * BT * sizeof(R2);
+  static constexpr int MINB_FIT = (int)((227 * 1024) / (SMEM + 1024));
+  static constexpr int MINB_CAP = RING > 0 ? HGKS_RECON_RING_MINB : 3;
+  static constexpr int MINB = BT == 64 ? (MINB_FIT < MINB_CAP ? (MINB_FIT < 1 ? 1 : MINB_FIT) : MINB_CAP) : HGKS_RECON_MINB;
 };
 
 // The operators of one 128-cell tile are one contiguous E*kTile*sizeof(Real)-byte range
@@ -346,25 +362,70 @@ __device__ __forceinline__ void recon_tile(const ReconArgs& a, int tile, int hal
   for (int d = 0; d < 9; ++d)
 #pragma unroll
     for (int v = 0; v < 5; ++v) c[d][v] = Real(0.0);
-  // measured unroll of the member-pair loop: tets (K = 14) 4, hexes (K = 24) 2
-  // (C2 0.397 -> 0.388 ms, C3 0.484 -> 0.458 ms vs no unrolling)
-  constexpr int kUnrollA0 = K <= 16 ? 4 : 2;
+  if constexpr (ReconShape<K>::RING > 0) {
+    constexpr int D = ReconShape<K>::RING > 0 ? ReconShape<K>::RING : 1;
+    R2* __restrict__ ring = reinterpret_cast<R2*>(dqs + K * QP) + tl;  // [D][9][BT] entry pairs
+    // the 9 entry pairs of member pair k2 / 2 into ring stage (k2 / 2) % D; always one group
+    auto issue = [&](int k2) {
+      if (k2 < K) {
+        R2* dst = ring + ((k2 / 2) % D) * 9 * BT;
+#pragma unroll
+        for (int p = 0; p < 9; ++p) {
+          const unsigned d = (unsigned)__cvta_generic_to_shared(dst + p * BT);
+          if constexpr (sizeof(R2) == 16)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(op2 + (k2 * 9 / 2 + p) * kTile)
+                         : "memory");
+          else
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(op2 + (k2 * 9 / 2 + p) * kTile)
+                         : "memory");
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+#pragma unroll
+    for (int j = 0; j < D; ++j) issue(2 * j);
+#pragma unroll
+    for (int k2 = 0; k2 < K; k2 += 2) {
+      asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
+      Real dq[2][5];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int v = 0; v < 5; ++v) dq[h][v] = dqs[(k2 + h) * QP + v * BT + tl];
+      R2 w2[9];
+#pragma unroll
+      for (int p = 0; p < 9; ++p) w2[p] = ring[(((k2 / 2) % D) * 9 + p) * BT];
+#pragma unroll
+      for (int j = 0; j < 18; ++j) {
+        const Real w = (j & 1) ? w2[j >> 1].y : w2[j >> 1].x;
+        const int h = j / 9, d = j % 9;
+#pragma unroll
+        for (int v = 0; v < 5; ++v) c[d][v] = fma(w, dq[h][v], c[d][v]);
+      }
+      issue(k2 + 2 * D);  // refill the stage just consumed
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  } else {
+    // measured unroll of the member-pair loop: tets (K = 14) 4, hexes (K = 24) 2
+    // (C2 0.397 -> 0.388 ms, C3 0.484 -> 0.458 ms vs no unrolling)
+    constexpr int kUnrollA0 = K <= 16 ? 4 : 2;
 #pragma unroll kUnrollA0
-  for (int k2 = 0; k2 < K; k2 += 2) {  // two members = 18 entries = 9 pairs
-    Real dq[2][5];
+    for (int k2 = 0; k2 < K; k2 += 2) {  // two members = 18 entries = 9 pairs
+      Real dq[2][5];
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
+      for (int h = 0; h < 2; ++h)
 #pragma unroll
-      for (int v = 0; v < 5; ++v) dq[h][v] = dqs[(k2 + h) * QP + v * BT + tl];
-    R2 w2[9];
+        for (int v = 0; v < 5; ++v) dq[h][v] = dqs[(k2 + h) * QP + v * BT + tl];
+      R2 w2[9];
 #pragma unroll
-    for (int p = 0; p < 9; ++p) w2[p] = __ldcs(op2 + (k2 * 9 / 2 + p) * kTile);
+      for (int p = 0; p < 9; ++p) w2[p] = __ldcs(op2 + (k2 * 9 / 2 + p) * kTile);
 #pragma unroll
-    for (int j = 0; j < 18; ++j) {
-      const Real w = (j & 1) ? w2[j >> 1].y : w2[j >> 1].x;
-      const int h = j / 9, d = j % 9;
+      for (int j = 0; j < 18; ++j) {
+        const Real w = (j & 1) ? w2[j >> 1].y : w2[j >> 1].x;
+        const int h = j / 9, d = j % 9;
 #pragma unroll
-      for (int v = 0; v < 5; ++v) c[d][v] = fma(w, dq[h][v], c[d][v]);
+        for (int v = 0; v < 5; ++v) c[d][v] = fma(w, dq[h][v], c[d][v]);
+      }
     }
   }
 #endif
@@ -1385,6 +1446,15 @@ __device__ __forceinline__ void flux_tau0_interior(const FluxArgs& a, int lf, in
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(s16), "r"(n16) : "memory");
     }
   }
+#ifndef HGKS_FLUX_REC_PF_AHEAD
+#define HGKS_FLUX_REC_PF_AHEAD 0  // blocks ahead whose records this warp prefetches into L2 (at its end)
+#endif
+  int pf_cell = -1;  // lane r < 2 FPW: the cell of record r of this warp's batch in that block
+  if (HGKS_FLUX_REC_PF_AHEAD > 0) {
+    constexpr int FB = (BLOCK / 32) * FPW;
+    const int fa = lf0 + HGKS_FLUX_REC_PF_AHEAD * FB + (lane >> 1);
+    if (lane < 2 * FPW && fa < a.n_faces) pf_cell = __ldg(a.f_cells + 2 * (size_t)(a.face0 + fa) + (lane & 1));
+  }
 #if HGKS_FLUX_STAGE
   __shared__ __align__(16) Real srec[BLOCK / 32][2 * FPW * kRec];
   Real* sw = srec[threadIdx.x >> 5];
@@ -1462,6 +1532,12 @@ __device__ __forceinline__ void flux_tau0_interior(const FluxArgs& a, int lf, in
   }
   Real dF[5];
   euler_jvp_dir(es, n, dtQ0, gm1, dF);  // 2 d_t F (global components)
+  if (HGKS_FLUX_REC_PF_AHEAD > 0 && pf_cell >= 0) {
+    const char* p = reinterpret_cast<const char*>(a.ceff + (size_t)pf_cell * kRec);
+#pragma unroll
+    for (int o = 0; o < kRec * (int)sizeof(Real); o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + o));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p + kRec * sizeof(Real) - 1));
+  }
   const Real un = es.u[0] * n[0] + es.u[1] * n[1] + es.u[2] * n[2];
   const Real hw = Real(0.5) * wS;
   if (STAGE == 1) {
