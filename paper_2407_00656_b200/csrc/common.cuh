@@ -23,27 +23,30 @@ namespace hgks {
 #ifndef HGKS_POLY_SPLIT
 #define HGKS_POLY_SPLIT 1  // 0: single Horner chains (round-2 baseline, for A/B builds)
 #endif
+// 1/j! for even j = 12, 10, ..., 0 and odd j = 11, 9, ..., 1 (exp_neg's two Horner chains)
+__constant__ double kExpEven[7] = {2.08767569878680989792e-09, 2.75573192239858906526e-07,
+                                   2.48015873015873015873e-05, 1.38888888888888888889e-03,
+                                   4.16666666666666666667e-02, 0.5, 1.0};
+__constant__ double kExpOdd[6] = {2.50521083854417187751e-08, 2.75573192239858906526e-06,
+                                  1.98412698412698412698e-04, 8.33333333333333333333e-03,
+                                  1.66666666666666666667e-01, 1.0};
 __device__ __forceinline__ double exp_neg(double x) {
   const double xc = fmax(x, -708.0);
   const double k = rint(xc * 1.4426950408889634);
   const double r = fma(-k, 1.90821492927058770002e-10, fma(-k, 6.93147180369123816490e-01, xc));
 #if HGKS_POLY_SPLIT
   // sum_{j<=12} r^j / j! as even + r * odd parts in r^2: two independent Horner chains of
-  // depth 6 / 5 instead of one of depth 12 (the flux kernels stall on dependent DFMAs)
+  // depth 6 / 5 instead of one of depth 12 (the flux kernels stall on dependent DFMAs); the
+  // coefficients come from the constant bank (LDCU.128, two per load) instead of two UMOVs
+  // per literal
   const double r2 = r * r;
-  double pe = 2.08767569878680989792e-09;  // 1/12!
-  double po = 2.50521083854417187751e-08;  // 1/11!
-  pe = fma(pe, r2, 2.75573192239858906526e-07);  // 1/10!
-  po = fma(po, r2, 2.75573192239858906526e-06);  // 1/9!
-  pe = fma(pe, r2, 2.48015873015873015873e-05);  // 1/8!
-  po = fma(po, r2, 1.98412698412698412698e-04);  // 1/7!
-  pe = fma(pe, r2, 1.38888888888888888889e-03);  // 1/6!
-  po = fma(po, r2, 8.33333333333333333333e-03);  // 1/5!
-  pe = fma(pe, r2, 4.16666666666666666667e-02);  // 1/4!
-  po = fma(po, r2, 1.66666666666666666667e-01);  // 1/3!
-  pe = fma(pe, r2, 0.5);                         // 1/2!
-  po = fma(po, r2, 1.0);                         // 1/1!
-  pe = fma(pe, r2, 1.0);                         // 1/0!
+  double pe = kExpEven[0], po = kExpOdd[0];
+#pragma unroll
+  for (int j = 1; j < 6; ++j) {
+    pe = fma(pe, r2, kExpEven[j]);
+    po = fma(po, r2, kExpOdd[j]);
+  }
+  pe = fma(pe, r2, kExpEven[6]);
   const double p = fma(po, r, pe);
 #else
   double p = 2.08767569878680989792e-09;  // 1/12!

@@ -846,14 +846,15 @@ __device__ __forceinline__ void eval_poly(const Real* __restrict__ rec, const Re
 }
 
 // Gauss point g of a face from its vertices (relative to the owner centroid), R10
-template <int NV>
+// (GLB = false: fg is an array already loaded into registers)
+template <int NV, bool GLB = true>
 __device__ __forceinline__ void face_gp(const Real* __restrict__ fg, int g, Real x[3], Real n[3], Real& wS) {
   if (NV == 3) {
     Real p[3][3];
 #pragma unroll
     for (int q = 0; q < 3; ++q)
 #pragma unroll
-      for (int a = 0; a < 3; ++a) p[q][a] = __ldg(fg + 3 * q + a);
+      for (int a = 0; a < 3; ++a) p[q][a] = GLB ? __ldg(fg + 3 * q + a) : fg[3 * q + a];
     const Real e1[3] = {p[1][0] - p[0][0], p[1][1] - p[0][1], p[1][2] - p[0][2]};
     const Real e2[3] = {p[2][0] - p[0][0], p[2][1] - p[0][1], p[2][2] - p[0][2]};
     Real nn[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
@@ -872,7 +873,7 @@ __device__ __forceinline__ void face_gp(const Real* __restrict__ fg, int g, Real
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
-      for (int a = 0; a < 3; ++a) p[q][a] = __ldg(fg + 3 * q + a);
+      for (int a = 0; a < 3; ++a) p[q][a] = GLB ? __ldg(fg + 3 * q + a) : fg[3 * q + a];
     const Real h = Real(0.28867513459481287);  // 1/(2 sqrt 3)
     const Real s = (g & 1) ? Real(0.5) + h : Real(0.5) - h, t = (g >> 1) ? Real(0.5) + h : Real(0.5) - h;
     Real ds[3], dt[3];
@@ -1455,37 +1456,89 @@ __device__ __forceinline__ void flux_tau0_interior(const FluxArgs& a, int lf, in
     const int fa = lf0 + HGKS_FLUX_REC_PF_AHEAD * FB + (lane >> 1);
     if (lane < 2 * FPW && fa < a.n_faces) pf_cell = __ldg(a.f_cells + 2 * (size_t)(a.face0 + fa) + (lane & 1));
   }
+#ifndef HGKS_FLUX_TMA
+#define HGKS_FLUX_TMA 1
+#endif
+  // fp64: each of lanes 0 .. 2 FPW - 1 issues one TMA bulk copy (400 B) of its record,
+  // completing on a per-warp mbarrier (one instruction per lane instead of 2 FPW rounds of
+  // shuffle + address + cp.async); fp32 records (200 B) are not 16-byte multiples: cp.async
+  constexpr bool kTma = HGKS_FLUX_TMA && sizeof(Real) == 8;
+  // this lane's face geometry: loads issued before the staging waits on the face cells
+  const int f = a.face0 + min(lf, a.n_faces - 1);
+  Real fgr[3 * NV + 3];
+  {
+    const Real* fg = a.f_geo + (size_t)f * a.f_stride;
+#pragma unroll
+    for (int i = 0; i < 3 * NV + 3; ++i) fgr[i] = __ldg(fg + i);
+  }
+  int slot_l = 2 * min(lane / NGP, FPW - 1), slot_r = slot_l + 1;  // shared-memory record slots
 #if HGKS_FLUX_STAGE
   __shared__ __align__(16) Real srec[BLOCK / 32][2 * FPW * kRec];
+  __shared__ __align__(8) unsigned long long sbar[BLOCK / 32];
   Real* sw = srec[threadIdx.x >> 5];
+  const unsigned bar = (unsigned)__cvta_generic_to_shared(&sbar[threadIdx.x >> 5]);
   {
     // lane r < 2 FPW: the cell of record r (face lf0 + r/2, owner / neighbour)
     int rc = 0;
     if (lane < 2 * FPW && lf0 + (lane >> 1) < a.n_faces) rc = __ldg(a.f_cells + 2 * (a.face0 + lf0 + (lane >> 1)) + (lane & 1));
+    if constexpr (kTma) {
+      // a cell shared by several faces of the warp (owner of consecutive faces) is copied
+      // once, by the lowest lane holding it; the faces read the leader's slot
+#ifndef HGKS_FLUX_DEDUP
+#define HGKS_FLUX_DEDUP 1
+#endif
+      const unsigned same = HGKS_FLUX_DEDUP ? __match_any_sync(0xffffffffu, lane < 2 * FPW ? rc : -1 - lane) : 1u << lane;
+      const int lead = __ffs(same) - 1;
+      const unsigned leaders = __ballot_sync(0xffffffffu, lane < 2 * FPW && lead == lane);
+      slot_l = __shfl_sync(0xffffffffu, lead, slot_l);
+      slot_r = __shfl_sync(0xffffffffu, lead, slot_r);
+      if (lane == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "r"(__popc(leaders) * kRec * (int)sizeof(Real))
+                     : "memory");
+      }
+      __syncwarp();
+      if (lane < 2 * FPW && lead == lane) {
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(sw + lane * kRec);
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                     "l"(a.ceff + (size_t)rc * kRec), "r"(kRec * (int)sizeof(Real)), "r"(bar)
+                     : "memory");
+      }
+    } else {
 #pragma unroll 4
-    for (int r = 0; r < 2 * FPW; ++r) {
-      const int c = __shfl_sync(0xffffffffu, rc, r);
-      if (lane < kRec / 2) cp_async_shared(sw + r * kRec + 2 * lane, a.ceff + (size_t)c * kRec + 2 * lane);
+      for (int r = 0; r < 2 * FPW; ++r) {
+        const int c = __shfl_sync(0xffffffffu, rc, r);
+        if (lane < kRec / 2) cp_async_shared(sw + r * kRec + 2 * lane, a.ceff + (size_t)c * kRec + 2 * lane);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
   }
 #endif
-  const int f = a.face0 + min(lf, a.n_faces - 1);
   const int co = __ldg(a.f_cells + 2 * f), cn = __ldg(a.f_cells + 2 * f + 1);
-  const Real* fg = a.f_geo + (size_t)f * a.f_stride;
   Real x[3], n[3], wS;
-  face_gp<NV>(fg, g, x, n, wS);
-  const Real xr[3] = {x[0] + __ldg(fg + 3 * NV), x[1] + __ldg(fg + 3 * NV + 1), x[2] + __ldg(fg + 3 * NV + 2)};
+  face_gp<NV, false>(fgr, g, x, n, wS);
+  const Real xr[3] = {x[0] + fgr[3 * NV], x[1] + fgr[3 * NV + 1], x[2] + fgr[3 * NV + 2]};
   const Real K = a.gp.K;
   const Real gm1 = a.gp.gamma - Real(1.0);
   auto admissible = [](const Real q[5]) {
     return q[0] > Real(0.0) && (q[0] * q[4] - Real(0.5) * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3])) > Real(0.0);
   };
 #if HGKS_FLUX_STAGE
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  __syncwarp();
-  const Real* rl = sw + (2 * min(lane / NGP, FPW - 1)) * kRec;  // lanes past the last face: any record
-  const Real* rr = rl + kRec;
+  if constexpr (kTma) {
+    unsigned done = 0;
+    while (!done)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done)
+                   : "r"(bar)
+                   : "memory");
+  } else {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+  }
+  const Real* rl = sw + slot_l * kRec;  // lanes past the last face: any record
+  const Real* rr = sw + slot_r * kRec;
 #else
   const Real* rl = a.ceff + (size_t)co * kRec;
   const Real* rr = a.ceff + (size_t)cn * kRec;

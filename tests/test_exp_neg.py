@@ -11,15 +11,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def device_constants():
-    """ln2 split and the even / odd Horner coefficients of the HGKS_POLY_SPLIT branch."""
+    """ln2 split and the even / odd Horner coefficients (kExpEven / kExpOdd) of the split branch."""
     src = open(os.path.join(ROOT, "paper_2407_00656_b200", "csrc", "common.cuh")).read()
     body = src[src.index("double exp_neg(double x)"):src.index("float exp_neg(float x)")]
     lo, hi = [float(v) for v in re.findall(r"fma\(-k, ([0-9.e+-]+)", body)]
-    split = body[body.index("#if HGKS_POLY_SPLIT"):body.index("#else")]
-    ce = [float(re.search(r"double pe = ([0-9.e+-]+);", split).group(1))]
-    ce += [float(v) for v in re.findall(r"pe = fma\(pe, r2, ([0-9.e+-]+)\);", split)]
-    co = [float(re.search(r"double po = ([0-9.e+-]+);", split).group(1))]
-    co += [float(v) for v in re.findall(r"po = fma\(po, r2, ([0-9.e+-]+)\);", split)]
+    arr = lambda name: [float(v) for v in re.search(name + r"\[\d+\] = \{([^}]*)\}", src).group(1).replace("\n", " ").split(",")]
+    ce, co = arr("kExpEven"), arr("kExpOdd")
     return lo, hi, ce, co
 
 
