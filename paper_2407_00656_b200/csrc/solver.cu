@@ -164,10 +164,17 @@ size_t layout(const GlobalMesh& gm, const RankPlan& rp, size_t rs, int dq0_mode,
   const size_t nq = (size_t)QS * round32(rp.n_local());
   const int64_t ncl = rp.n_owned + rp.n_pghost;
   auto R = [&](size_t n) { return (void*)c.take<char>(n * rs); };
+  // experiment knobs (address-mapping study): extra bytes before the records and before the
+  // operators, in KiB (HGKS_PAD_REC, HGKS_PAD_OP; default 0)
+  auto pad_kib = [](const char* name) -> size_t {
+    const char* e = std::getenv(name);
+    return e ? (size_t)std::strtoull(e, nullptr, 10) * 1024 : 0;
+  };
   d.ctrl = c.take<Ctrl>(1);
   d.Q = R(nq);
   d.Qtmp = R(nq);
   d.R = R((size_t)QS * rp.n_owned);
+  c.off += pad_kib("HGKS_PAD_REC");
   d.ceff = R((size_t)kRec * ncl);
   d.ceff0 = dq0_mode == 2 ? R((size_t)kRec * ncl) : nullptr;
   // one zero row past the last face: the update's entry for a face a cell does not have
@@ -177,6 +184,7 @@ size_t layout(const GlobalMesh& gm, const RankPlan& rp, size_t rs, int dq0_mode,
   d.st_id = c.take<int>((size_t)L.K * rp.ld);
   d.sub_slot = c.take<uint8_t>((size_t)L.M * L.NM * rp.ld);
   d.n_sub = rp.n_sub.empty() ? nullptr : c.take<uint8_t>(rp.n_sub.size());
+  c.off += pad_kib("HGKS_PAD_OP");
   d.op = R((size_t)L.op_entries() * rp.ld);
   d.geo = R((size_t)8 * rp.ld);
   d.st_shift = c.take<uint8_t>(HGKS_RECON_NE ? (size_t)L.K * rp.ld : 1);
