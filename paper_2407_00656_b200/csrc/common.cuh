@@ -69,13 +69,48 @@ __device__ __forceinline__ double exp_neg(double x) {
 }
 __device__ __forceinline__ float exp_neg(float x) { return expf(x); }
 
+// 1/x for a positive normal x (densities, x + K, face areas): the MUFU reciprocal estimate
+// refined by two Newton steps (relative error ~1e-16, not correctly rounded), without the
+// IEEE division's special-case test and slow-path call (HGKS_FAST_RCP=0: plain division)
+#ifndef HGKS_FAST_RCP
+#define HGKS_FAST_RCP 1
+#endif
+__device__ __forceinline__ double rcp_pos(double x) {
+#if HGKS_FAST_RCP
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+#else
+  return 1.0 / x;
+#endif
+}
+__device__ __forceinline__ float rcp_pos(float x) { return 1.0f / x; }
+// 1/sqrt(x) for a positive normal x: MUFU estimate and two Newton steps y (3 - x y^2) / 2
+__device__ __forceinline__ double rsqrt_pos(double x) {
+#if HGKS_FAST_RCP
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  return y * fma(-hx * y, y, 1.5);
+#else
+  return rsqrt(x);
+#endif
+}
+__device__ __forceinline__ float rsqrt_pos(float x) { return rsqrtf(x); }
+
 // (coefficients in constant memory: the DFMA/DADD take them as c[][] operands, no
 // per-coefficient register moves)
 __constant__ double kErfcCoef[HGKS_ERFC_DEG + 1] = HGKS_ERFC_COEF;
+// FAST: 1/(|z| + K) by rcp_pos (the tau = 0 interior kernel; measured slower in the moment form)
+template <bool FAST = false>
 __device__ __forceinline__ void erfc_exp(double z, double& erfc_z, double& ez2) {
   const double* c = kErfcCoef;
   const double a = fabs(z);
-  const double r = 1.0 / (a + HGKS_ERFC_K);
+  const double r = FAST ? rcp_pos(a + HGKS_ERFC_K) : 1.0 / (a + HGKS_ERFC_K);
   const double t = (a - HGKS_ERFC_K) * r;
 #if HGKS_POLY_SPLIT
   // P(t) = P0(s) + t P1(s) + t^2 P2(s) + t^3 P3(s), s = t^4, P_i(s) = sum_j c_{4j+i} s^j:
@@ -101,6 +136,7 @@ __device__ __forceinline__ void erfc_exp(double z, double& erfc_z, double& ez2) 
   const double v = P * r * ez2;  // erfc(|z|)
   erfc_z = z >= 0.0 ? v : 2.0 - v;
 }
+template <bool FAST = false>
 __device__ __forceinline__ void erfc_exp(float z, float& erfc_z, float& ez2) {
   erfc_z = erfcf(z);
   ez2 = expf(-z * z);

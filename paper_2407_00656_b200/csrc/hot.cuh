@@ -858,10 +858,10 @@ __device__ __forceinline__ void face_gp(const Real* __restrict__ fg, int g, Real
     const Real e1[3] = {p[1][0] - p[0][0], p[1][1] - p[0][1], p[1][2] - p[0][2]};
     const Real e2[3] = {p[2][0] - p[0][0], p[2][1] - p[0][1], p[2][2] - p[0][2]};
     Real nn[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
-    const Real a2 = sqrt(nn[0] * nn[0] + nn[1] * nn[1] + nn[2] * nn[2]);
+    const Real nq = nn[0] * nn[0] + nn[1] * nn[1] + nn[2] * nn[2];
     const Real l0 = g == 0 ? Real(2.0) / Real(3.0) : Real(1.0) / Real(6.0), l1 = g == 1 ? Real(2.0) / Real(3.0) : Real(1.0) / Real(6.0),
                  l2 = g == 2 ? Real(2.0) / Real(3.0) : Real(1.0) / Real(6.0);
-    const Real ia = Real(1.0) / a2;
+    const Real ia = rsqrt_pos(nq), a2 = nq * ia;  // 1/|nn| and |nn| without a division or sqrt
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       x[a] = l0 * p[0][a] + l1 * p[1][a] + l2 * p[2][a];
@@ -944,11 +944,12 @@ __device__ __forceinline__ void to_local(const Real val[5], const Real grad[5][3
 struct EulerState {
   Real Q[5], inv, u[3], p, H, q2h;  // H = rhoE + p, q2h = |u|^2 / 2
 };
+template <bool FAST = false>  // FAST: 1/rho by rcp_pos (the tau = 0 interior kernel)
 __device__ __forceinline__ EulerState euler_state(const Real Q[5], Real gm1) {
   EulerState e;
 #pragma unroll
   for (int v = 0; v < 5; ++v) e.Q[v] = Q[v];
-  e.inv = Real(1.0) / Q[0];
+  e.inv = FAST ? rcp_pos(Q[0]) : Real(1.0) / Q[0];
   e.u[0] = Q[1] * e.inv;
   e.u[1] = Q[2] * e.inv;
   e.u[2] = Q[3] * e.inv;
@@ -998,16 +999,16 @@ __device__ __forceinline__ void equilibrium_state_n(const Real ql[5], const Real
   for (int side = 0; side < 2; ++side) {
     const Real* q = side ? qr : ql;
     const Real sg = side ? Real(-1.0) : Real(1.0);
-    const Real inv = Real(1.0) / q[0];
+    const Real inv = rcp_pos(q[0]);
     const Real u[3] = {q[1] * inv, q[2] * inv, q[3] * inv};
     const Real un = u[0] * n[0] + u[1] * n[1] + u[2] * n[2];
     const Real uu = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
     const Real rhoe = q[4] - Real(0.5) * (q[1] * u[0] + q[2] * u[1] + q[3] * u[2]);
     const Real h = c2k * rhoe * inv;          // p / rho = 1/(2 lambda)
-    const Real rs = rsqrt(h + h);             // sqrt(lambda)
+    const Real rs = rsqrt_pos(h + h);             // sqrt(lambda)
     const Real sq = (h + h) * rs;             // 1/sqrt(lambda)
     Real ec, ex;
-    erfc_exp(-sg * un * rs, ec, ex);          // erfc(-sg sqrt(lambda) u_n), exp(-lambda u_n^2)
+    erfc_exp<true>(-sg * un * rs, ec, ex);    // erfc(-sg sqrt(lambda) u_n), exp(-lambda u_n^2)
     const Real m0 = Real(0.5) * ec;
     const Real m1 = un * m0 + sg * (Real(0.5) * ex * rpi * sq);
     const Real m2 = un * m1 + m0 * h;
@@ -1572,7 +1573,7 @@ __device__ __forceinline__ void flux_tau0_interior(const FluxArgs& a, int lf, in
   }
   Real Q0[5];
   equilibrium_state_n(vl, vr, n, K, Q0);
-  const EulerState es = euler_state(Q0, gm1);
+  const EulerState es = euler_state<true>(Q0, gm1);
   Real dtQ0[5] = {Real(0.0), Real(0.0), Real(0.0), Real(0.0), Real(0.0)};  // 2 d_t Q0 (gs = 2 dQ0)
 #pragma unroll
   for (int j = 0; j < 3; ++j) {
