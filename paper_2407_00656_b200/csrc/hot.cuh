@@ -408,7 +408,10 @@ __device__ __forceinline__ void recon_tile(const ReconArgs& a, int tile, int hal
   } else {
     // measured unroll of the member-pair loop: tets (K = 14) 4, hexes (K = 24) 2
     // (C2 0.397 -> 0.388 ms, C3 0.484 -> 0.458 ms vs no unrolling)
-    constexpr int kUnrollA0 = K <= 16 ? 4 : 2;
+#ifndef HGKS_RECON_UNROLL_TET
+#define HGKS_RECON_UNROLL_TET 4
+#endif
+    constexpr int kUnrollA0 = K <= 16 ? HGKS_RECON_UNROLL_TET : 2;
 #pragma unroll kUnrollA0
     for (int k2 = 0; k2 < K; k2 += 2) {  // two members = 18 entries = 9 pairs
       Real dq[2][5];
