@@ -475,6 +475,8 @@ def main():
             src = "executed: ncu sass op counts (2 fma + add + mul), profiles/flops_per_unit.json"
         if not fpf:
             return None
+        if layout[2] == 7:  # hybrid layouts: one interior launch per face kind per stage
+            avg_ms *= 2
         achieved = fpf * nf / (avg_ms * 1e-3) / 1e12
         return {"kernel": name, "bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",
                 "frac": achieved / alu_peak, "traffic": None, "avg_launch_ms": avg_ms,

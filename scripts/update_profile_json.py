@@ -61,7 +61,11 @@ def main():
                 ent = flops.setdefault(w, {}).setdefault(key, {})
                 ent[f"fp{p}_flops_per_{unit}"] = round(per)
     flops["c4"] = flops.get("c3", {})  # same kernels and per-face work (sphere shell, tau > 0)
-    json.dump(flops, open(os.path.join(ROOT, "profiles", "flops_per_unit.json"), "w"), indent=1)
+    old_path = os.path.join(ROOT, "profiles", "flops_per_unit.json")
+    if os.path.exists(old_path):  # keep entries this capture does not regenerate (c3h)
+        for k, v in json.load(open(old_path)).items():
+            flops.setdefault(k, v)
+    json.dump(flops, open(old_path, "w"), indent=1)
 
     for wl in ("c2", "c5"):
         rep = os.path.join(SRC, f"full_{wl}.ncu-rep")
